@@ -1,0 +1,245 @@
+/*
+ * oserve_gpu.h — C-ABI of the B200-native OServe scheduling round.
+ *
+ * This is the drop-in boundary between the reference's C++ scheduler
+ * (/root/reference/proj, namespace oserve::) and the sm_100a kernels in
+ * paper_2602_12151_b200/csrc.  Plain C: POD structs, pointers + sizes,
+ * int status codes; no C++ or torch types cross it.
+ *
+ * Each entry point names the reference interface it replaces.  Results are
+ * bit-identical to the reference on the same inputs.
+ *
+ * Threading: one oserve_gpu_ctx is used by one host thread at a time
+ * (the reference functions are reentrant; contexts are independent).
+ * All calls are synchronous with respect to the host unless named
+ * "_async"; asynchronous calls run on the context's stream.
+ */
+#ifndef OSERVE_GPU_H
+#define OSERVE_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OSERVE_MAX_REPLICAS 128
+#define OSERVE_MAX_CLASSES 16
+#define OSERVE_MAX_DEVICES 1024
+
+/* Status codes.  Each maps to the exception the reference throws
+ * (proj/include/oserve/errors.hpp:9-82, std::invalid_argument, std::logic_error). */
+typedef enum {
+    OSERVE_OK = 0,
+    OSERVE_ERR_INVALID_ARGUMENT = 1,   /* std::invalid_argument                 */
+    OSERVE_ERR_INFEASIBLE_REPLICA = 2, /* oserve::InfeasibleReplica  errors.hpp:15 */
+    OSERVE_ERR_MODEL_TOO_LARGE = 3,    /* oserve::ModelTooLarge      errors.hpp:21 */
+    OSERVE_ERR_TOO_LARGE = 4,          /* oserve::TooLarge           errors.hpp:27 */
+    OSERVE_ERR_EMPTY_DEPLOYMENT = 5,   /* oserve::EmptyDeployment    errors.hpp:32 */
+    OSERVE_ERR_UNSOURCED_FRAGMENT = 6, /* oserve::UnsourcedFragment  errors.hpp:51 */
+    OSERVE_ERR_LOGIC = 7,              /* std::logic_error (check_constraints)    */
+    OSERVE_ERR_UNSUPPORTED = 8,        /* input outside the GPU path's limits     */
+    OSERVE_ERR_CUDA = 9,
+    OSERVE_ERR_NO_DEVICE = 10
+} oserve_status;
+
+/* ---- L0 types (proj/include/oserve/core.hpp:11-95) -------------------- */
+
+/* ClusterSpec (core.hpp:21-34): machines with device ids and per-device
+ * memory; two link classes. */
+typedef struct {
+    int num_machines;
+    const int *machine_num_devices; /* [num_machines]                       */
+    const int *device_ids;          /* concatenated per machine             */
+    const uint64_t *device_mem;     /* [num_machines] bytes per device      */
+    double intra_bw;                /* bytes/s within a machine             */
+    double inter_bw;                /* bytes/s across machines              */
+} oserve_cluster_desc;
+
+/* ModelSpec (core.hpp:36-45). */
+typedef struct {
+    uint64_t param_bytes;
+    uint32_t num_layers;
+    uint64_t bytes_per_token_kv;
+    uint64_t flops_per_token_prefill;
+    uint64_t min_mem_bytes;
+} oserve_model_desc;
+
+/* cost::ProfileParams (costmodel.hpp:14-22). */
+typedef struct {
+    double prefill_coeff;
+    double decode_coeff;
+    double tp_efficiency;
+    double pp_comm_cost;
+    double mem_bw_penalty;
+} oserve_profile;
+
+/* WorkloadType (core.hpp:73-79). */
+typedef struct {
+    int type_id;
+    double centroid_in;
+    double centroid_out;
+} oserve_class;
+
+/* flow::SolveOptions (flowassign.hpp:97-101). */
+typedef struct {
+    int64_t exact_demand_limit; /* default 400       */
+    int exact_cell_limit;       /* default 20        */
+    int64_t node_budget;        /* default 8'000'000 */
+} oserve_solve_options;
+
+/* Deployment (core.hpp:63-70) as flat arrays: replica r owns
+ * device_ids[off_r, off_r + replica_num_devices[r]) with its (tp, pp). */
+typedef struct {
+    int num_replicas;
+    const int *replica_num_devices; /* [R] */
+    const int *device_ids;          /* concatenated per replica */
+    const int *tp;                  /* [R] */
+    const int *pp;                  /* [R] */
+} oserve_deployment;
+
+/* A deployment returned by the GPU path (fixed-capacity, caller-owned). */
+typedef struct {
+    int num_replicas;
+    int num_devices;
+    int replica_num_devices[OSERVE_MAX_REPLICAS];
+    int tp[OSERVE_MAX_REPLICAS];
+    int pp[OSERVE_MAX_REPLICAS];
+    int device_ids[OSERVE_MAX_DEVICES]; /* concatenated per replica */
+} oserve_plan;
+
+/* Plan spaces enumerated by a scheduling round.
+ *  ORDERED   — the reference's own space: every partition of D into parts
+ *              >= g_min in partitions_desc order (deploysearch.cpp:421-432),
+ *              every ordered strategy combo of best_strategies
+ *              (deploysearch.cpp:153-229).
+ *  CANONICAL — symmetry-reduced space: parts restricted to
+ *              `sizes`, strategy picks non-decreasing within runs of equal
+ *              replicas.  Same order/tie-break restricted to that subset. */
+typedef enum { OSERVE_SPACE_ORDERED = 0, OSERVE_SPACE_CANONICAL = 1 } oserve_space_mode;
+
+typedef struct {
+    int mode;         /* oserve_space_mode                                   */
+    int num_sizes;    /* allowed part sizes (0 => every size >= g_min)       */
+    const int *sizes;
+    int max_devices;  /* >0: TooLarge when D > max_devices (exhaustive guard) */
+} oserve_space_desc;
+
+/* Result of a scheduling round (search::SearchState, deploysearch.hpp:86-92,
+ * plus the selection key). */
+typedef struct {
+    int64_t objective;       /* SearchState::throughput                        */
+    uint64_t key;            /* packed (obj desc, partition, sum_pp, rank) key */
+    int64_t partitions;      /* SearchState::iterations (partitions visited)   */
+    uint64_t plans;          /* plans in the space (evaluated by the kernel)   */
+    int64_t partition_index; /* winner's partition in enumeration order        */
+    uint64_t local_rank;     /* winner's rank inside its partition             */
+    int sum_pp;
+    oserve_plan plan;        /* SearchState::deployment                        */
+} oserve_round_result;
+
+/* switchplan::Transfer (switchplan.hpp:36-42). */
+typedef struct {
+    uint64_t begin;
+    uint64_t end;
+    int src;
+    int dst;
+} oserve_transfer;
+
+typedef struct oserve_gpu_ctx oserve_gpu_ctx;
+
+/* ---- context ---------------------------------------------------------- */
+
+/* Replaces the EvalContext construction (deploysearch.hpp:45-54): copies the
+ * cluster/model/profile (never retains caller pointers) and binds a CUDA
+ * device.  Validates like core.cpp:67-96 / costmodel.cpp:13-19. */
+int oserve_gpu_create(int cuda_device, const oserve_cluster_desc *cluster,
+                      const oserve_model_desc *model, const oserve_profile *profile,
+                      oserve_gpu_ctx **out);
+int oserve_gpu_destroy(oserve_gpu_ctx *ctx);
+const char *oserve_gpu_last_error(const oserve_gpu_ctx *ctx);
+const char *oserve_gpu_status_name(int status);
+
+/* Workload of one span: classes (the WorkloadType centroids), per-class
+ * demand lambda (TraceSpan::counts) and span length.  Runs the cost-table
+ * kernel (K0) on the device. */
+int oserve_gpu_set_workload(oserve_gpu_ctx *ctx, int num_classes, const oserve_class *classes,
+                            const int64_t *lambda, double span_seconds);
+int oserve_gpu_set_solve_options(oserve_gpu_ctx *ctx, const oserve_solve_options *opts);
+/* Multi-GPU: this context evaluates only the plans of shard `rank` of
+ * `world` (interleaved chunks of the global plan order). */
+int oserve_gpu_set_shard(oserve_gpu_ctx *ctx, int rank, int world);
+/* Launch stream (cudaStream_t as void*); NULL = the context's own stream. */
+int oserve_gpu_set_stream(oserve_gpu_ctx *ctx, void *stream);
+/* search::min_feasible_group (deploysearch.cpp:77-87). */
+int oserve_gpu_min_feasible_group(oserve_gpu_ctx *ctx, int *g_min);
+
+/* ---- scheduling round (enumerate -> cost -> assign -> argmin) --------- */
+
+/* Enumerate the space on the host and upload its tables. */
+int oserve_gpu_prepare_space(oserve_gpu_ctx *ctx, const oserve_space_desc *space,
+                             int64_t *partitions, uint64_t *plans);
+/* Asynchronously evaluate this shard's plans of the prepared space and write
+ * the shard-best packed key to device memory `d_key` (uint64, caller-owned;
+ * may be fed straight into an all-reduce(min)). */
+int oserve_gpu_launch_round_async(oserve_gpu_ctx *ctx, uint64_t *d_key);
+/* Decode a (global) key into the winning plan. */
+int oserve_gpu_decode_key(oserve_gpu_ctx *ctx, uint64_t key, oserve_round_result *out);
+/* Synchronous round over a space (single GPU or this shard). */
+int oserve_gpu_round(oserve_gpu_ctx *ctx, const oserve_space_desc *space,
+                     oserve_round_result *out);
+
+/* Drop-in for search::exhaustive (deploysearch.cpp:436-466): ordered space,
+ * D <= 16 guard, ModelTooLarge when nothing is feasible. */
+int oserve_gpu_exhaustive(oserve_gpu_ctx *ctx, oserve_round_result *out);
+/* Drop-in for search::best_strategies (deploysearch.cpp:153-229).  An
+ * infeasible partition returns OK with objective 0 and num_replicas 0. */
+int oserve_gpu_best_strategies(oserve_gpu_ctx *ctx, int num_replicas, const int *sizes,
+                               oserve_round_result *out);
+
+/* Per-plan objectives for ranks [first, first+count) of the prepared space
+ * (host output arrays; sum_pp may be NULL). */
+int oserve_gpu_evaluate_ranks(oserve_gpu_ctx *ctx, uint64_t first, uint64_t count,
+                              int64_t *objective, int32_t *sum_pp);
+/* search::evaluate_deployment (deploysearch.cpp:138-151) for a batch of
+ * explicit deployments.  Throws-equivalent InfeasibleReplica. */
+int oserve_gpu_evaluate_deployments(oserve_gpu_ctx *ctx, int count, const oserve_deployment *deps,
+                                    int64_t *objective);
+
+/* cost::build_capacity_table (costmodel.cpp:94-116) + flow::solve_assignment
+ * (flowassign.cpp:481-503) for one deployment: all outputs [R*J] row-major
+ * except M/used [R].  Any output pointer may be NULL. */
+int oserve_gpu_plan_detail(oserve_gpu_ctx *ctx, const oserve_deployment *dep, int64_t *n,
+                           int64_t *e, double *latency, int64_t *x, int64_t *M, int64_t *unit,
+                           int64_t *used, int64_t *objective);
+
+/* flow::solve_assignment over raw capacity tables (test_flowassign.cpp
+ * style): `count` independent instances, each R x J with its own lambda.
+ * n, e, x, unit: [count][R][J]; lambda: [count][J]; M, used: [count][R]. */
+int oserve_gpu_solve_batch(oserve_gpu_ctx *ctx, int count, int R, int J, const int64_t *n,
+                           const int64_t *e, const int64_t *lambda, int64_t *x, int64_t *objective,
+                           int64_t *M, int64_t *unit, int64_t *used);
+
+/* ---- workload-adaptive switching (switchplan.cpp:40-140) -------------- */
+
+/* est_seconds of layout()+greedy_plan()+estimate_time() from `src` to each of
+ * `count` candidate deployments (one CUDA block per pair).  max_link_bytes
+ * may be NULL. */
+int oserve_gpu_switch_cost_batch(oserve_gpu_ctx *ctx, const oserve_deployment *src, int count,
+                                 const oserve_deployment *dsts, double *est_seconds,
+                                 uint64_t *max_link_bytes);
+/* Full greedy_plan() for one pair: transfers in the reference's order
+ * (fragment-major, destination ascending).  `*num_transfers` returns the
+ * count (OSERVE_ERR_INVALID_ARGUMENT with the count set if > capacity). */
+int oserve_gpu_switch_plan(oserve_gpu_ctx *ctx, const oserve_deployment *src,
+                           const oserve_deployment *dst, int capacity, oserve_transfer *transfers,
+                           int *num_transfers, double *est_seconds);
+
+/* Kernel launches issued by this context since creation (evidence counter). */
+uint64_t oserve_gpu_launch_count(const oserve_gpu_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OSERVE_GPU_H */

@@ -1,0 +1,81 @@
+/*
+ * oracle_api.h — TEST INFRASTRUCTURE ONLY.
+ *
+ * The C-ABI exported by the two CPU oracles:
+ *   oracle/_ref/libref_oserve.so   the reference itself (/root/reference/proj/src,
+ *                                  compiled unmodified) behind ref_harness.cpp
+ *   oracle/liboserve_port.so       oserve_port.cpp, a CPU restatement of the
+ *                                  reference algorithm (each function cites
+ *                                  the reference file:line it follows)
+ * Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline leg may
+ * load these.  The product path (paper_2602_12151_b200) never does.
+ */
+#ifndef OSERVE_ORACLE_API_H
+#define OSERVE_ORACLE_API_H
+
+#include "../include/oserve_gpu.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+    oserve_cluster_desc cluster;
+    oserve_model_desc model;
+    oserve_profile profile;
+    int num_classes;
+    const oserve_class *classes;
+    const int64_t *lambda;
+    double span_seconds;
+} oracle_problem;
+
+const char *oracle_last_error(void);
+/* 1 for the reference build, 0 for the restatement. */
+int oracle_is_reference(void);
+
+int oracle_min_feasible_group(const oracle_problem *p, int *g_min);
+int oracle_capacity_table(const oracle_problem *p, const oserve_deployment *dep, int64_t *n,
+                          int64_t *e, double *latency);
+int oracle_normalize(int J, const int64_t *n_row, int strict, int64_t *M, int64_t *units,
+                     int *scaled);
+/* Default SolveOptions unless opts != NULL.  work (may be NULL) = greedy
+ * visits + exchange probes (port only; the reference returns 0). */
+int oracle_solve_assignment(int R, int J, const int64_t *n, const int64_t *e, const int64_t *lambda,
+                            const oserve_solve_options *opts, int64_t *x, int64_t *objective,
+                            int64_t *M, int64_t *unit, int64_t *used, uint64_t *work);
+int oracle_check_constraints(int R, int J, const int64_t *x, const int64_t *n, const int64_t *e,
+                             const int64_t *lambda);
+int oracle_evaluate_deployment(const oracle_problem *p, const oserve_deployment *dep,
+                               int64_t *objective);
+int oracle_best_strategies(const oracle_problem *p, int R, const int *sizes, int parallel,
+                           oserve_round_result *out);
+int oracle_exhaustive(const oracle_problem *p, int parallel, oserve_round_result *out);
+
+/* Plan spaces (same definition and order as the GPU path). */
+int oracle_space_info(const oracle_problem *p, const oserve_space_desc *s, int64_t *partitions,
+                      uint64_t *plans);
+int oracle_space_plan(const oracle_problem *p, const oserve_space_desc *s, uint64_t rank,
+                      oserve_plan *plan, int64_t *partition_index, uint64_t *local_rank);
+int oracle_evaluate_ranks(const oracle_problem *p, const oserve_space_desc *s, int64_t count,
+                          const uint64_t *ranks, int64_t *objective, int32_t *sum_pp,
+                          uint64_t *work, int threads);
+/* Full round: argmin over the space by (obj desc, partition asc, sum_pp asc,
+ * rank asc).  threads <= 1 => serial. */
+int oracle_round(const oracle_problem *p, const oserve_space_desc *s, int threads,
+                 oserve_round_result *out);
+
+int oracle_switch_plan(const oserve_cluster_desc *c, uint64_t param_bytes,
+                       const oserve_deployment *src, const oserve_deployment *dst, int capacity,
+                       oserve_transfer *transfers, int *num_transfers, double *est_seconds,
+                       uint64_t *max_link_bytes);
+
+/* Reference-only helpers used to generate the synthetic workloads. */
+int oracle_fit_types(int64_t n, const uint32_t *input_len, const uint32_t *output_len, int k,
+                     uint64_t seed, double *centroid_in, double *centroid_out);
+int oracle_holt_forecast(int J, int T, const int64_t *counts, int window, int64_t *lambda_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

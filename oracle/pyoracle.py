@@ -1,0 +1,191 @@
+"""TEST INFRASTRUCTURE ONLY — Python loader for the two CPU oracles.
+
+    Oracle("ref")   oracle/_ref/libref_oserve.so — the unmodified reference
+                    (/root/reference/proj/src) behind ref_harness.cpp
+    Oracle("port")  oracle/liboserve_port.so — oserve_port.cpp, the CPU
+                    restatement of the reference algorithm
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline leg may use
+this module; the product package never imports it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from paper_2602_12151_b200 import _abi as A
+from paper_2602_12151_b200 import core
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+PATHS = {"ref": os.path.join(HERE, "_ref", "libref_oserve.so"),
+         "port": os.path.join(HERE, "liboserve_port.so")}
+
+
+def available(kind: str) -> bool:
+    return os.path.exists(PATHS[kind])
+
+
+class Problem:
+    """Cluster + model + profile + workload of one span (an EvalContext)."""
+
+    def __init__(self, cluster: core.ClusterSpec, model: core.ModelSpec,
+                 types: Sequence[core.WorkloadType], lam: Sequence[int], span_s: float = 60.0,
+                 params: Optional[core.ProfileParams] = None):
+        self.cluster, self.model, self.types = cluster, model, list(types)
+        self.lam, self.span_s = [int(v) for v in lam], float(span_s)
+        self.params = params or core.ProfileParams()
+        self.keep = A.Keep()
+        self.desc = A.problem_desc(cluster, model, self.params, self.types, self.lam, span_s, self.keep)
+
+
+class Oracle:
+    def __init__(self, kind: str = "port"):
+        self.kind = kind
+        self.lib = C.CDLL(PATHS[kind], mode=C.RTLD_LOCAL)
+        L = self.lib
+        L.oracle_last_error.restype = C.c_char_p
+        P = C.POINTER
+        L.oracle_evaluate_ranks.argtypes = [P(A.ProblemDesc), P(A.SpaceDesc), C.c_int64, P(C.c_uint64),
+                                            P(C.c_int64), P(C.c_int32), P(C.c_uint64), C.c_int]
+        L.oracle_space_info.argtypes = [P(A.ProblemDesc), P(A.SpaceDesc), P(C.c_int64), P(C.c_uint64)]
+        L.oracle_space_plan.argtypes = [P(A.ProblemDesc), P(A.SpaceDesc), C.c_uint64, P(A.Plan),
+                                        P(C.c_int64), P(C.c_uint64)]
+        L.oracle_round.argtypes = [P(A.ProblemDesc), P(A.SpaceDesc), C.c_int, P(A.RoundResult)]
+
+    def _chk(self, st):
+        A.raise_for(st, self.lib.oracle_last_error().decode())
+
+    # -- L1/L2 --------------------------------------------------------------
+    def capacity_table(self, pr: Problem, dep: core.Deployment):
+        R, J = dep.replica_count(), len(pr.types)
+        keep = A.Keep()
+        d = A.deployment_desc(dep, keep)
+        n, e, lat = (C.c_int64 * (R * J))(), (C.c_int64 * (R * J))(), (C.c_double * (R * J))()
+        self._chk(self.lib.oracle_capacity_table(C.byref(pr.desc), C.byref(d), n, e, lat))
+        return core.CapacityTable(A.i64_rows(n, R, J), A.i64_rows(e, R, J),
+                                  [list(lat[k * J:(k + 1) * J]) for k in range(R)])
+
+    def normalize(self, row: Sequence[int], strict: bool = False):
+        J = len(row)
+        M, units, sc = C.c_int64(), (C.c_int64 * J)(), C.c_int()
+        self._chk(self.lib.oracle_normalize(J, A._arr(C.c_int64, row), int(strict), C.byref(M), units,
+                                            C.byref(sc)))
+        return M.value, list(units), bool(sc.value)
+
+    def solve_assignment(self, n, e, lam, opts: Optional[core.SolveOptions] = None):
+        R, J = len(n), len(lam)
+        x, M, unit, used = (C.c_int64 * (R * J))(), (C.c_int64 * R)(), (C.c_int64 * (R * J))(), (C.c_int64 * R)()
+        obj, work = C.c_int64(), C.c_uint64()
+        o = None
+        if opts is not None:
+            o = C.byref(A.SolveOptionsDesc(opts.exact_demand_limit, opts.exact_cell_limit, opts.node_budget))
+        self._chk(self.lib.oracle_solve_assignment(
+            R, J, A._arr(C.c_int64, [v for r in n for v in r]), A._arr(C.c_int64, [v for r in e for v in r]),
+            A._arr(C.c_int64, lam), o, x, C.byref(obj), M, unit, used, C.byref(work)))
+        ll = core.LowerLevel(core.AssignmentMatrix(A.i64_rows(x, R, J), obj.value), list(M),
+                             A.i64_rows(unit, R, J), list(used))
+        ll.work = work.value
+        return ll
+
+    def check_constraints(self, x, n, e, lam):
+        R, J = len(n), len(lam)
+        f = lambda m: A._arr(C.c_int64, [v for r in m for v in r])
+        self._chk(self.lib.oracle_check_constraints(R, J, f(x), f(n), f(e), A._arr(C.c_int64, lam)))
+
+    # -- L3 -----------------------------------------------------------------
+    def min_feasible_group(self, pr: Problem) -> int:
+        g = C.c_int()
+        self._chk(self.lib.oracle_min_feasible_group(C.byref(pr.desc), C.byref(g)))
+        return g.value
+
+    def evaluate_deployment(self, pr: Problem, dep: core.Deployment) -> int:
+        keep = A.Keep()
+        d = A.deployment_desc(dep, keep)
+        o = C.c_int64()
+        self._chk(self.lib.oracle_evaluate_deployment(C.byref(pr.desc), C.byref(d), C.byref(o)))
+        return o.value
+
+    def best_strategies(self, pr: Problem, sizes: Sequence[int], parallel: bool = False):
+        res = A.RoundResult()
+        self._chk(self.lib.oracle_best_strategies(C.byref(pr.desc), len(sizes), A._arr(C.c_int, sizes),
+                                                  int(parallel), C.byref(res)))
+        return core.StrategyChoice(A.plan_to_deployment(res.plan), res.objective)
+
+    def exhaustive(self, pr: Problem, parallel: bool = False) -> core.SearchState:
+        res = A.RoundResult()
+        self._chk(self.lib.oracle_exhaustive(C.byref(pr.desc), int(parallel), C.byref(res)))
+        return A.result_to_state(res)
+
+    def space_info(self, pr: Problem, mode: int, sizes: Sequence[int] = (), max_devices: int = 0):
+        keep = A.Keep()
+        s = A.space_desc(mode, sizes, max_devices, keep)
+        parts, plans = C.c_int64(), C.c_uint64()
+        self._chk(self.lib.oracle_space_info(C.byref(pr.desc), C.byref(s), C.byref(parts), C.byref(plans)))
+        return parts.value, plans.value
+
+    def space_plan(self, pr: Problem, mode: int, rank: int, sizes: Sequence[int] = ()):
+        keep = A.Keep()
+        s = A.space_desc(mode, sizes, 0, keep)
+        plan, pi, lr = A.Plan(), C.c_int64(), C.c_uint64()
+        self._chk(self.lib.oracle_space_plan(C.byref(pr.desc), C.byref(s), rank, C.byref(plan),
+                                             C.byref(pi), C.byref(lr)))
+        return A.plan_to_deployment(plan), pi.value, lr.value
+
+    def evaluate_ranks(self, pr: Problem, mode: int, ranks, sizes: Sequence[int] = (), threads: int = 1):
+        keep = A.Keep()
+        s = A.space_desc(mode, sizes, 0, keep)
+        ranks = np.ascontiguousarray(np.asarray(ranks, dtype=np.uint64))
+        n = len(ranks)
+        obj = np.zeros(n, np.int64)
+        spp = np.zeros(n, np.int32)
+        work = np.zeros(n, np.uint64)
+        P = lambda a, t: a.ctypes.data_as(C.POINTER(t))
+        self._chk(self.lib.oracle_evaluate_ranks(C.byref(pr.desc), C.byref(s), n, P(ranks, C.c_uint64),
+                                                 P(obj, C.c_int64), P(spp, C.c_int32), P(work, C.c_uint64),
+                                                 threads))
+        return obj, spp, work
+
+    def round(self, pr: Problem, mode: int, sizes: Sequence[int] = (), threads: int = 1,
+              max_devices: int = 0) -> core.SearchState:
+        keep = A.Keep()
+        s = A.space_desc(mode, sizes, max_devices, keep)
+        res = A.RoundResult()
+        self._chk(self.lib.oracle_round(C.byref(pr.desc), C.byref(s), threads, C.byref(res)))
+        return A.result_to_state(res)
+
+    # -- L3' ----------------------------------------------------------------
+    def switch_plan(self, cl: core.ClusterSpec, param_bytes: int, src: core.Deployment, dst: core.Deployment):
+        keep = A.Keep()
+        c = A.cluster_desc(cl, keep)
+        s, d = A.deployment_desc(src, keep), A.deployment_desc(dst, keep)
+        ntr = C.c_int()
+        est = C.c_double()
+        mx = C.c_uint64()
+        self._chk(self.lib.oracle_switch_plan(C.byref(c), param_bytes, C.byref(s), C.byref(d), 0, None,
+                                              C.byref(ntr), C.byref(est), C.byref(mx)))
+        cap = ntr.value
+        tr = (A.TransferDesc * max(1, cap))()
+        self._chk(self.lib.oracle_switch_plan(C.byref(c), param_bytes, C.byref(s), C.byref(d), cap, tr,
+                                              C.byref(ntr), C.byref(est), C.byref(mx)))
+        transfers = [core.Transfer(core.ByteRange(t.begin, t.end), t.src, t.dst) for t in tr[:cap]]
+        return core.SwitchPlan(transfers, est.value), mx.value
+
+    # -- workload (reference only) -------------------------------------------
+    def fit_types(self, input_len, output_len, k: int, seed: int = 0):
+        inp = np.ascontiguousarray(np.asarray(input_len, np.uint32))
+        out = np.ascontiguousarray(np.asarray(output_len, np.uint32))
+        ci, co = (C.c_double * k)(), (C.c_double * k)()
+        self._chk(self.lib.oracle_fit_types(C.c_int64(len(inp)), inp.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                            out.ctypes.data_as(C.POINTER(C.c_uint32)), k, C.c_uint64(seed),
+                                            ci, co))
+        return [core.WorkloadType(c, ci[c], co[c]) for c in range(k)]
+
+    def holt_forecast(self, counts: List[List[int]], window: int = 50) -> List[List[int]]:
+        T, J = len(counts), len(counts[0])
+        flat = A._arr(C.c_int64, [v for row in counts for v in row])
+        out = (C.c_int64 * (T * J))()
+        self._chk(self.lib.oracle_holt_forecast(J, T, flat, window, out))
+        return A.i64_rows(out, T, J)
