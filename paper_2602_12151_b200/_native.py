@@ -1,0 +1,247 @@
+"""ctypes binding of liboserve_gpu.so (include/oserve_gpu.h).
+
+The product path: every call goes through the C-ABI into the sm_100a kernels.
+There is no CPU fallback — if the in-tree library is missing or no CUDA
+device is present the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _abi as A
+from . import core
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liboserve_gpu.so")
+
+EXPORTS = [
+    "oserve_gpu_create", "oserve_gpu_destroy", "oserve_gpu_last_error", "oserve_gpu_status_name",
+    "oserve_gpu_set_workload", "oserve_gpu_set_solve_options", "oserve_gpu_set_shard", "oserve_gpu_set_stream",
+    "oserve_gpu_min_feasible_group", "oserve_gpu_prepare_space", "oserve_gpu_launch_round_async",
+    "oserve_gpu_decode_key", "oserve_gpu_round", "oserve_gpu_exhaustive", "oserve_gpu_best_strategies",
+    "oserve_gpu_evaluate_ranks", "oserve_gpu_evaluate_deployments", "oserve_gpu_plan_detail",
+    "oserve_gpu_solve_batch", "oserve_gpu_switch_cost_batch", "oserve_gpu_switch_plan",
+    "oserve_gpu_launch_count",
+]
+
+_lib = None
+
+
+def load_library() -> C.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+                           " (make -C paper_2602_12151_b200/csrc); there is no CPU fallback")
+    L = C.CDLL(LIB_PATH)
+    P = C.POINTER
+    vp = C.c_void_p
+    L.oserve_gpu_create.argtypes = [C.c_int, P(A.ClusterDesc), P(A.ModelDesc), P(A.Profile), P(vp)]
+    L.oserve_gpu_destroy.argtypes = [vp]
+    L.oserve_gpu_last_error.argtypes = [vp]
+    L.oserve_gpu_last_error.restype = C.c_char_p
+    L.oserve_gpu_status_name.restype = C.c_char_p
+    L.oserve_gpu_set_workload.argtypes = [vp, C.c_int, P(A.ClassDesc), P(C.c_int64), C.c_double]
+    L.oserve_gpu_set_solve_options.argtypes = [vp, P(A.SolveOptionsDesc)]
+    L.oserve_gpu_set_shard.argtypes = [vp, C.c_int, C.c_int]
+    L.oserve_gpu_set_stream.argtypes = [vp, vp]
+    L.oserve_gpu_min_feasible_group.argtypes = [vp, P(C.c_int)]
+    L.oserve_gpu_prepare_space.argtypes = [vp, P(A.SpaceDesc), P(C.c_int64), P(C.c_uint64)]
+    L.oserve_gpu_launch_round_async.argtypes = [vp, vp]
+    L.oserve_gpu_decode_key.argtypes = [vp, C.c_uint64, P(A.RoundResult)]
+    L.oserve_gpu_round.argtypes = [vp, P(A.SpaceDesc), P(A.RoundResult)]
+    L.oserve_gpu_exhaustive.argtypes = [vp, P(A.RoundResult)]
+    L.oserve_gpu_best_strategies.argtypes = [vp, C.c_int, P(C.c_int), P(A.RoundResult)]
+    L.oserve_gpu_evaluate_ranks.argtypes = [vp, C.c_uint64, C.c_uint64, P(C.c_int64), P(C.c_int32)]
+    L.oserve_gpu_evaluate_deployments.argtypes = [vp, C.c_int, P(A.DeploymentDesc), P(C.c_int64)]
+    L.oserve_gpu_plan_detail.argtypes = [vp, P(A.DeploymentDesc)] + [P(C.c_int64)] * 2 + [P(C.c_double)] + \
+        [P(C.c_int64)] * 5
+    L.oserve_gpu_solve_batch.argtypes = [vp, C.c_int, C.c_int, C.c_int] + [P(C.c_int64)] * 8
+    L.oserve_gpu_switch_cost_batch.argtypes = [vp, P(A.DeploymentDesc), C.c_int, P(A.DeploymentDesc),
+                                               P(C.c_double), P(C.c_uint64)]
+    L.oserve_gpu_switch_plan.argtypes = [vp, P(A.DeploymentDesc), P(A.DeploymentDesc), C.c_int,
+                                         P(A.TransferDesc), P(C.c_int), P(C.c_double)]
+    L.oserve_gpu_launch_count.argtypes = [vp]
+    L.oserve_gpu_launch_count.restype = C.c_uint64
+    _lib = L
+    return L
+
+
+def _np_ptr(a, t):
+    return a.ctypes.data_as(C.POINTER(t))
+
+
+class GpuContext:
+    """One oserve_gpu_ctx: a cluster/model/profile bound to one CUDA device.
+
+    Mirrors the reference's EvalContext (deploysearch.hpp:45-54) but owns
+    copies of its inputs and the device-resident tables.
+    """
+
+    def __init__(self, cluster: core.ClusterSpec, model: core.ModelSpec,
+                 params: Optional[core.ProfileParams] = None, device: int = 0):
+        self.lib = load_library()
+        self.cluster, self.model = cluster, model
+        self.params = params or core.ProfileParams()
+        keep = A.Keep()
+        cd = A.cluster_desc(cluster, keep)
+        md = A.model_desc(model)
+        pd = A.profile_desc(self.params)
+        h = C.c_void_p()
+        st = self.lib.oserve_gpu_create(device, C.byref(cd), C.byref(md), C.byref(pd), C.byref(h))
+        if st != A.OK:
+            A.raise_for(st, f"oserve_gpu_create: {self.lib.oserve_gpu_status_name(st).decode()}")
+        self.h = h
+        self.types: List[core.WorkloadType] = []
+        self.lam: List[int] = []
+        self.span_s = 60.0
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.oserve_gpu_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _chk(self, st: int):
+        if st != A.OK:
+            A.raise_for(st, self.lib.oserve_gpu_last_error(self.h).decode())
+
+    # -- configuration -------------------------------------------------------
+    def set_workload(self, types: Sequence[core.WorkloadType], lam: Sequence[int], span_s: float = 60.0):
+        keep = A.Keep()
+        cls = A.classes_arr(types, keep)
+        self._chk(self.lib.oserve_gpu_set_workload(self.h, len(types), cls, A._arr(C.c_int64, lam), float(span_s)))
+        self.types, self.lam, self.span_s = list(types), [int(v) for v in lam], float(span_s)
+
+    def set_solve_options(self, opts: core.SolveOptions):
+        self._chk(self.lib.oserve_gpu_set_solve_options(
+            self.h, C.byref(A.SolveOptionsDesc(opts.exact_demand_limit, opts.exact_cell_limit, opts.node_budget))))
+
+    def set_shard(self, rank: int, world: int):
+        self._chk(self.lib.oserve_gpu_set_shard(self.h, rank, world))
+
+    def set_stream(self, stream_ptr: int):
+        self._chk(self.lib.oserve_gpu_set_stream(self.h, C.c_void_p(stream_ptr)))
+
+    def launch_count(self) -> int:
+        return int(self.lib.oserve_gpu_launch_count(self.h))
+
+    def min_feasible_group(self) -> int:
+        g = C.c_int()
+        self._chk(self.lib.oserve_gpu_min_feasible_group(self.h, C.byref(g)))
+        return g.value
+
+    # -- scheduling round ------------------------------------------------------
+    def prepare_space(self, mode: int = A.SPACE_ORDERED, sizes: Sequence[int] = (), max_devices: int = 0):
+        keep = A.Keep()
+        sd = A.space_desc(mode, sizes, max_devices, keep)
+        parts, plans = C.c_int64(), C.c_uint64()
+        self._chk(self.lib.oserve_gpu_prepare_space(self.h, C.byref(sd), C.byref(parts), C.byref(plans)))
+        return parts.value, plans.value
+
+    def launch_round_async(self, d_key_ptr: int):
+        self._chk(self.lib.oserve_gpu_launch_round_async(self.h, C.c_void_p(d_key_ptr)))
+
+    def decode_key(self, key: int) -> core.SearchState:
+        res = A.RoundResult()
+        self._chk(self.lib.oserve_gpu_decode_key(self.h, C.c_uint64(key), C.byref(res)))
+        return A.result_to_state(res)
+
+    def round(self, mode: int = A.SPACE_ORDERED, sizes: Sequence[int] = (), max_devices: int = 0) -> core.SearchState:
+        keep = A.Keep()
+        sd = A.space_desc(mode, sizes, max_devices, keep)
+        res = A.RoundResult()
+        self._chk(self.lib.oserve_gpu_round(self.h, C.byref(sd), C.byref(res)))
+        return A.result_to_state(res)
+
+    def exhaustive(self) -> core.SearchState:
+        res = A.RoundResult()
+        self._chk(self.lib.oserve_gpu_exhaustive(self.h, C.byref(res)))
+        return A.result_to_state(res)
+
+    def best_strategies(self, sizes: Sequence[int]) -> core.StrategyChoice:
+        res = A.RoundResult()
+        self._chk(self.lib.oserve_gpu_best_strategies(self.h, len(sizes), A._arr(C.c_int, sizes), C.byref(res)))
+        return core.StrategyChoice(A.plan_to_deployment(res.plan), res.objective)
+
+    def evaluate_ranks(self, first: int, count: int) -> Tuple[np.ndarray, np.ndarray]:
+        obj = np.zeros(count, np.int64)
+        spp = np.zeros(count, np.int32)
+        self._chk(self.lib.oserve_gpu_evaluate_ranks(self.h, C.c_uint64(first), C.c_uint64(count),
+                                                     _np_ptr(obj, C.c_int64), _np_ptr(spp, C.c_int32)))
+        return obj, spp
+
+    def evaluate_deployments(self, deps: Sequence[core.Deployment]) -> List[int]:
+        keep = A.Keep()
+        arr = (A.DeploymentDesc * max(1, len(deps)))()
+        for i, d in enumerate(deps):
+            arr[i] = A.deployment_desc(d, keep)
+        out = (C.c_int64 * max(1, len(deps)))()
+        self._chk(self.lib.oserve_gpu_evaluate_deployments(self.h, len(deps), arr, out))
+        return list(out[:len(deps)])
+
+    def plan_detail(self, dep: core.Deployment):
+        R, J = dep.replica_count(), len(self.types)
+        keep = A.Keep()
+        d = A.deployment_desc(dep, keep)
+        n, e, x, unit = [(C.c_int64 * max(1, R * J))() for _ in range(4)]
+        lat = (C.c_double * max(1, R * J))()
+        M, used = (C.c_int64 * max(1, R))(), (C.c_int64 * max(1, R))()
+        obj = C.c_int64()
+        self._chk(self.lib.oserve_gpu_plan_detail(self.h, C.byref(d), n, e, lat, x, M, unit, used, C.byref(obj)))
+        table = core.CapacityTable(A.i64_rows(n, R, J), A.i64_rows(e, R, J),
+                                   [list(lat[k * J:(k + 1) * J]) for k in range(R)])
+        lower = core.LowerLevel(core.AssignmentMatrix(A.i64_rows(x, R, J), obj.value), list(M[:R]),
+                                A.i64_rows(unit, R, J), list(used[:R]))
+        return table, lower
+
+    def solve_batch(self, n: np.ndarray, e: np.ndarray, lam: np.ndarray):
+        """n, e: [count, R, J]; lam: [count, J] -> (x, obj, M, unit, used)."""
+        n = np.ascontiguousarray(n, np.int64)
+        e = np.ascontiguousarray(e, np.int64)
+        lam = np.ascontiguousarray(lam, np.int64)
+        cnt, R, J = n.shape
+        x = np.zeros((cnt, R, J), np.int64)
+        unit = np.zeros((cnt, R, J), np.int64)
+        obj = np.zeros(cnt, np.int64)
+        M = np.zeros((cnt, R), np.int64)
+        used = np.zeros((cnt, R), np.int64)
+        P = lambda a: _np_ptr(a, C.c_int64)
+        self._chk(self.lib.oserve_gpu_solve_batch(self.h, cnt, R, J, P(n), P(e), P(lam), P(x), P(obj), P(M), P(unit),
+                                                  P(used)))
+        return x, obj, M, unit, used
+
+    # -- switching ---------------------------------------------------------------
+    def switch_cost_batch(self, src: core.Deployment, dsts: Sequence[core.Deployment]):
+        keep = A.Keep()
+        s = A.deployment_desc(src, keep)
+        arr = (A.DeploymentDesc * max(1, len(dsts)))()
+        for i, d in enumerate(dsts):
+            arr[i] = A.deployment_desc(d, keep)
+        est = (C.c_double * max(1, len(dsts)))()
+        mb = (C.c_uint64 * max(1, len(dsts)))()
+        self._chk(self.lib.oserve_gpu_switch_cost_batch(self.h, C.byref(s), len(dsts), arr, est, mb))
+        return list(est[:len(dsts)]), list(mb[:len(dsts)])
+
+    def switch_plan(self, src: core.Deployment, dst: core.Deployment) -> core.SwitchPlan:
+        keep = A.Keep()
+        s, d = A.deployment_desc(src, keep), A.deployment_desc(dst, keep)
+        ntr, est = C.c_int(), C.c_double()
+        self._chk(self.lib.oserve_gpu_switch_plan(self.h, C.byref(s), C.byref(d), 0, None, C.byref(ntr),
+                                                  C.byref(est)))
+        cap = ntr.value
+        tr = (A.TransferDesc * max(1, cap))()
+        self._chk(self.lib.oserve_gpu_switch_plan(self.h, C.byref(s), C.byref(d), cap, tr, C.byref(ntr),
+                                                  C.byref(est)))
+        return core.SwitchPlan([core.Transfer(core.ByteRange(t.begin, t.end), t.src, t.dst) for t in tr[:cap]],
+                               est.value)

@@ -1,0 +1,1277 @@
+// oserve_host.cpp — host runtime of the B200 scheduling round (native C++).
+//
+// Implements the C-ABI of include/oserve_gpu.h: context (cluster/model/profile
+// copies, CUDA stream), the plan-space enumerator (partitions, candidate
+// lists, runs, prefix table), the shape registry feeding the cost kernel, key
+// packing/decoding, and the launch sequences of K0/K1/K4/K2.
+//
+// Host-side restatements (control plane, no per-plan compute):
+//   min_feasible_group   deploysearch.cpp:77-87
+//   partitions_desc      deploysearch.cpp:421-432
+//   canonical_blocks     deploysearch.cpp:89-103
+//   strategy_candidates  deploysearch.cpp:105-118 (+ validate_replica
+//                        core.cpp:105-127, memory_feasible costmodel.cpp:48-62)
+//   tp_speedup           costmodel.cpp:22-24 (host libm pow/log2, as the reference)
+// Every per-plan quantity (cost cells, normalisation, assignment, objective,
+// argmin, switching cost) is computed by the kernels.  There is no CPU
+// fallback: without a CUDA device every entry point returns
+// OSERVE_ERR_NO_DEVICE.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <limits>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/oserve_gpu.h"
+#include "oserve_internal.h"
+
+using namespace oserve_gpu;
+
+namespace {
+
+struct Fail : std::runtime_error {
+    int code;
+    Fail(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] void fail(int code, const std::string &m) { throw Fail(code, m); }
+
+void cuda_ok(cudaError_t e, const char *what) {
+    if (e != cudaSuccess) fail(OSERVE_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+void cuda_ok(int e, const char *what) { cuda_ok(static_cast<cudaError_t>(e), what); }
+
+// Growable device buffer.
+struct DBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    ~DBuf() {
+        if (p) cudaFree(p);
+    }
+    void *get(size_t bytes) {
+        if (bytes == 0) bytes = 16;
+        if (bytes > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            cuda_ok(cudaMalloc(&p, bytes), "cudaMalloc");
+            cap = bytes;
+        }
+        return p;
+    }
+    template <class T>
+    T *upload(const std::vector<T> &v, cudaStream_t s) {
+        T *d = static_cast<T *>(get(v.size() * sizeof(T)));
+        if (!v.empty()) cuda_ok(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s), "H2D");
+        return d;
+    }
+};
+
+template <class T>
+void download(std::vector<T> &v, const void *d, size_t n, cudaStream_t s) {
+    v.resize(n);
+    if (n) cuda_ok(cudaMemcpyAsync(v.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost, s), "D2H");
+}
+
+int bits_for(uint64_t x) {
+    int b = 1;
+    while (b < 64 && (x >> b) != 0) ++b;
+    return b;
+}
+
+uint64_t binom(int n, int k) {
+    if (k < 0 || k > n) return 0;
+    unsigned __int128 r = 1;
+    for (int i = 1; i <= k; ++i) {
+        r = r * static_cast<unsigned>(n - k + i) / static_cast<unsigned>(i);
+        if (r > (static_cast<unsigned __int128>(1) << 62)) fail(OSERVE_ERR_TOO_LARGE, "plan count exceeds 2^62");
+    }
+    return static_cast<uint64_t>(r);
+}
+
+using Cand = std::pair<int, int>;  // (tp, pp), tp descending
+
+struct Run {
+    int start, len, q;
+    uint64_t count;
+};
+
+struct Partition {
+    std::vector<int> sizes, offsets, cand_list;  // cand_list: list id per replica
+    std::vector<Run> runs;
+    uint64_t count = 0;
+};
+
+struct Space {
+    bool valid = false;
+    int mode = -1;
+    std::vector<int> sizes_key;
+    int max_devices = 0;
+    bool explicit_partition = false;
+    std::vector<int> explicit_sizes;
+    std::vector<Partition> parts;
+    std::vector<uint64_t> prefix;
+    uint64_t total = 0, max_count = 0;
+    int rmax = 0;
+    std::vector<std::vector<Cand>> lists;      // candidate lists
+    std::vector<std::vector<int>> list_shapes; // shape id per candidate
+    // device copies
+    DBuf d_prefix, d_R, d_rep_off, d_run_off, d_nruns, d_exact, d_rep_list, d_run_start, d_run_len, d_run_q,
+        d_run_count, d_run_weight, d_cl_n, d_cl_shape;
+    SpaceTables view{};
+    std::vector<uint8_t> exact;  // per partition, for the current workload
+    bool any_exact = false;
+};
+
+}  // namespace
+
+struct oserve_gpu_ctx {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t own = nullptr, stream = nullptr;
+    std::string err;
+    uint64_t launches = 0;
+    // cluster
+    std::vector<int> dev_sorted;
+    std::map<int, int> machine_of;
+    std::map<int, int> slot_of;
+    std::vector<uint64_t> machine_mem;
+    double intra = 0, inter = 0;
+    oserve_model_desc model{};
+    oserve_profile profile{};
+    oserve_solve_options opts{400, 20, 8000000};
+    // workload
+    int J = 0;
+    std::vector<double> cin, cout;
+    std::vector<int64_t> lambda;
+    double span = 60.0;
+    bool have_workload = false;
+    // shapes
+    std::map<std::tuple<int, int, uint64_t>, int> shape_id;
+    std::vector<ShapeParam> shapes;
+    int tables_shapes = -1;  // shapes computed in device tables
+    bool tables_dirty = true;
+    DBuf d_param, d_n, d_e, d_lat, d_M, d_unit, d_cap, d_order, d_olen, d_pp, d_scaled, d_cin, d_cout;
+    ShapeTables tables{};
+    // space
+    Space space;
+    KeyLayout key{};
+    int rank = 0, world = 1;
+    uint64_t chunk = 4096;
+    // scratch
+    DBuf d_key, d_obj, d_spp, d_x, d_used, d_aborted, d_aborted_n, d_ranks, d_listR, d_listOff, d_listShapes,
+        d_listLam, d_sw[12];
+
+    int D() const { return static_cast<int>(dev_sorted.size()); }
+    int machine(int d) const {
+        auto it = machine_of.find(d);
+        return it == machine_of.end() ? -1 : it->second;
+    }
+    uint64_t device_mem(int d) const {
+        int m = machine(d);
+        return m < 0 ? 0 : machine_mem[m];
+    }
+};
+
+namespace {
+
+// ----------------------------------------------------------- placement ---
+bool placement_ok(const oserve_gpu_ctx &c, const std::vector<int> &devs, int tp, int pp) {
+    if (tp < 1 || pp < 1 || devs.empty() || tp * pp != static_cast<int>(devs.size())) return false;
+    std::vector<int> s = devs;
+    std::sort(s.begin(), s.end());
+    if (std::adjacent_find(s.begin(), s.end()) != s.end()) return false;
+    for (int d : s)
+        if (c.machine(d) < 0) return false;
+    for (int st = 0; st < pp; ++st)
+        for (int i = 1; i < tp; ++i) {
+            int m0 = c.machine(s[st * tp]);
+            if (m0 < 0 || m0 != c.machine(s[st * tp + i])) return false;
+        }
+    return true;
+}
+
+bool mem_feasible(const oserve_gpu_ctx &c, const std::vector<int> &devs, int tp, int pp, uint64_t *total_out) {
+    if (devs.empty()) return false;
+    uint64_t total = 0, mn = std::numeric_limits<uint64_t>::max();
+    for (int d : devs) {
+        uint64_t m = c.device_mem(d);
+        if (m == 0) return false;
+        total += m;
+        mn = std::min(mn, m);
+    }
+    if (total_out) *total_out = total;
+    if (total < c.model.min_mem_bytes) return false;
+    uint64_t shards = static_cast<uint64_t>(tp) * static_cast<uint64_t>(pp);
+    return (c.model.param_bytes + shards - 1) / shards <= mn;
+}
+
+int shape_for(oserve_gpu_ctx &c, int tp, int pp, uint64_t total_mem) {
+    uint64_t budget = total_mem > c.model.param_bytes ? total_mem - c.model.param_bytes : 0;
+    auto key = std::make_tuple(tp, pp, budget);
+    auto it = c.shape_id.find(key);
+    if (it != c.shape_id.end()) return it->second;
+    ShapeParam sp;
+    sp.tp = tp;
+    sp.pp = pp;
+    sp.kv_budget = budget;
+    sp.speedup = tp * std::pow(c.profile.tp_efficiency, std::log2(static_cast<double>(tp)));
+    int id = static_cast<int>(c.shapes.size());
+    if (id >= 65535) fail(OSERVE_ERR_UNSUPPORTED, "more than 65535 replica shapes");
+    c.shapes.push_back(sp);
+    c.shape_id.emplace(key, id);
+    c.tables_dirty = true;
+    return id;
+}
+
+int g_min_of(const oserve_gpu_ctx &c) {
+    uint64_t mn = std::numeric_limits<uint64_t>::max();
+    for (uint64_t v : c.machine_mem) mn = std::min(mn, v);
+    for (int g = 1; g <= c.D(); ++g) {
+        bool total_ok = static_cast<uint64_t>(g) * mn >= c.model.min_mem_bytes;
+        bool shard_ok = (c.model.param_bytes + g - 1) / g <= mn;
+        if (total_ok && shard_ok) return g;
+    }
+    fail(OSERVE_ERR_MODEL_TOO_LARGE, "model does not fit on " + std::to_string(c.D()) + " devices");
+}
+
+// ------------------------------------------------------- shape tables ---
+void ensure_tables(oserve_gpu_ctx &c) {
+    if (!c.have_workload) fail(OSERVE_ERR_INVALID_ARGUMENT, "no workload set (oserve_gpu_set_workload)");
+    if (!c.tables_dirty && c.tables_shapes == static_cast<int>(c.shapes.size())) return;
+    const int S = static_cast<int>(c.shapes.size()), J = c.J;
+    cudaStream_t s = c.stream;
+    ShapeTables t{};
+    t.num_shapes = S;
+    t.J = J;
+    t.param = c.d_param.upload(c.shapes, s);
+    t.n = static_cast<int64_t *>(c.d_n.get(sizeof(int64_t) * S * J));
+    t.e = static_cast<int64_t *>(c.d_e.get(sizeof(int64_t) * S * J));
+    t.latency = static_cast<double *>(c.d_lat.get(sizeof(double) * S * J));
+    t.M = static_cast<int64_t *>(c.d_M.get(sizeof(int64_t) * S));
+    t.unit = static_cast<int64_t *>(c.d_unit.get(sizeof(int64_t) * S * J));
+    t.cap = static_cast<int32_t *>(c.d_cap.get(sizeof(int32_t) * S * J));
+    t.order = static_cast<uint8_t *>(c.d_order.get(S * kMaxJ));
+    t.olen = static_cast<uint8_t *>(c.d_olen.get(S));
+    t.scaled = static_cast<uint8_t *>(c.d_scaled.get(S));
+    std::vector<uint8_t> pps(S);
+    for (int i = 0; i < S; ++i) pps[i] = static_cast<uint8_t>(std::min(c.shapes[i].pp, 255));
+    t.pp = c.d_pp.upload(pps, s);
+    const double *cin = c.d_cin.upload(c.cin, s);
+    const double *cout = c.d_cout.upload(c.cout, s);
+    const auto &p = c.profile;
+    cuda_ok(launch_cost_tables(t, cin, cout, c.model.num_layers, c.model.bytes_per_token_kv, p.prefill_coeff,
+                               p.decode_coeff, p.pp_comm_cost, p.mem_bw_penalty, c.span, s),
+            "cost kernel");
+    cuda_ok(launch_normalize_rows(t, s), "normalize kernel");
+    c.launches += S ? 2 : 0;
+    c.tables = t;
+    c.tables_shapes = S;
+    c.tables_dirty = false;
+}
+
+SolveParams solve_params(const oserve_gpu_ctx &c) {
+    SolveParams p{};
+    p.J = c.J;
+    for (int j = 0; j < c.J; ++j) p.lambda[j] = c.lambda[j];
+    p.exact_demand_limit = c.opts.exact_demand_limit;
+    p.exact_cell_limit = c.opts.exact_cell_limit;
+    p.node_budget = c.opts.node_budget;
+    return p;
+}
+
+bool use_exact(const oserve_gpu_ctx &c, int R) {
+    int64_t tot = 0;
+    for (int64_t v : c.lambda) tot += v;
+    return tot <= c.opts.exact_demand_limit && static_cast<int64_t>(R) * c.J <= c.opts.exact_cell_limit;
+}
+
+// --------------------------------------------------------------- space ---
+std::vector<Cand> candidates(oserve_gpu_ctx &c, int off, int d, std::vector<int> &shape_ids) {
+    std::vector<int> block(c.dev_sorted.begin() + off, c.dev_sorted.begin() + off + d);
+    std::vector<Cand> out;
+    shape_ids.clear();
+    for (int tp = d; tp >= 1; --tp) {
+        if (d % tp) continue;
+        uint64_t total = 0;
+        if (placement_ok(c, block, tp, d / tp) && mem_feasible(c, block, tp, d / tp, &total)) {
+            out.emplace_back(tp, d / tp);
+            shape_ids.push_back(shape_for(c, tp, d / tp, total));
+        }
+    }
+    if (out.size() > static_cast<size_t>(kMaxCand)) fail(OSERVE_ERR_UNSUPPORTED, "more than 8 strategy candidates");
+    return out;
+}
+
+void build_space(oserve_gpu_ctx &c, Space &sp, int mode, const std::vector<int> &allowed_sizes,
+                 const std::vector<std::vector<int>> *explicit_parts) {
+    const int D = c.D();
+    sp.parts.clear();
+    sp.prefix.clear();
+    sp.lists.clear();
+    sp.list_shapes.clear();
+    sp.total = 0;
+    sp.max_count = 0;
+    sp.rmax = 0;
+    std::map<std::pair<int, int>, int> list_of;  // (offset, size) -> list id
+    std::map<std::vector<int>, int> list_dedup;  // shape-id list -> list id
+    auto handle = [&](const std::vector<int> &sizes) {
+        Partition part;
+        part.sizes = sizes;
+        int off = 0;
+        bool feasible = true;
+        for (int s : sizes) {
+            part.offsets.push_back(off);
+            auto key = std::make_pair(off, s);
+            auto it = list_of.find(key);
+            int lid;
+            if (it == list_of.end()) {
+                std::vector<int> ids;
+                std::vector<Cand> cands = candidates(c, off, s, ids);
+                auto dd = list_dedup.find(ids);
+                if (dd == list_dedup.end()) {
+                    lid = static_cast<int>(sp.lists.size());
+                    sp.lists.push_back(cands);
+                    sp.list_shapes.push_back(ids);
+                    list_dedup.emplace(ids, lid);
+                } else {
+                    lid = dd->second;
+                }
+                list_of.emplace(key, lid);
+            } else {
+                lid = it->second;
+            }
+            part.cand_list.push_back(lid);
+            if (sp.lists[lid].empty()) feasible = false;
+            off += s;
+        }
+        if (feasible) {
+            const int R = static_cast<int>(sizes.size());
+            for (int r = 0; r < R;) {
+                int e = r + 1;
+                if (mode == OSERVE_SPACE_CANONICAL)
+                    while (e < R && sizes[e] == sizes[r] && part.cand_list[e] == part.cand_list[r]) ++e;
+                Run run{r, e - r, static_cast<int>(sp.lists[part.cand_list[r]].size()), 0};
+                run.count = binom(run.len + run.q - 1, run.q - 1);
+                part.runs.push_back(run);
+                r = e;
+            }
+            unsigned __int128 cnt = 1;
+            for (const auto &run : part.runs) {
+                cnt *= run.count;
+                if (cnt > (static_cast<unsigned __int128>(1) << 62))
+                    fail(OSERVE_ERR_TOO_LARGE, "plans per partition exceed 2^62");
+            }
+            part.count = static_cast<uint64_t>(cnt);
+            sp.rmax = std::max(sp.rmax, R);
+        }
+        sp.prefix.push_back(sp.total);
+        sp.total += part.count;
+        if (sp.total > (uint64_t{1} << 62)) fail(OSERVE_ERR_TOO_LARGE, "plan space exceeds 2^62 plans");
+        sp.max_count = std::max(sp.max_count, part.count);
+        sp.parts.push_back(std::move(part));
+    };
+    if (explicit_parts) {
+        for (const auto &s : *explicit_parts) handle(s);
+    } else {
+        const int g = g_min_of(c);
+        std::vector<char> allowed;
+        if (!allowed_sizes.empty()) {
+            allowed.assign(D + 1, 0);
+            for (int s : allowed_sizes)
+                if (s >= 1 && s <= D) allowed[s] = 1;
+        }
+        std::vector<int> cur;
+        std::function<void(int, int)> rec = [&](int remaining, int max_part) {
+            if (remaining == 0) {
+                handle(cur);
+                return;
+            }
+            for (int p = std::min(remaining, max_part); p >= g; --p) {
+                if (!allowed.empty() && !allowed[p]) continue;
+                cur.push_back(p);
+                rec(remaining - p, p);
+                cur.pop_back();
+            }
+        };
+        rec(D, D);
+    }
+    if (sp.rmax > OSERVE_MAX_REPLICAS) fail(OSERVE_ERR_UNSUPPORTED, "more than 128 replicas per plan");
+    sp.prefix.push_back(sp.total);
+
+    // flatten + upload
+    const size_t P = sp.parts.size();
+    std::vector<int32_t> R(P), rep_off(P), run_off(P), nruns(P), rep_list, run_start, run_len, run_q;
+    std::vector<uint64_t> run_count, run_weight;
+    for (size_t i = 0; i < P; ++i) {
+        const auto &part = sp.parts[i];
+        R[i] = static_cast<int32_t>(part.sizes.size());
+        rep_off[i] = static_cast<int32_t>(rep_list.size());
+        run_off[i] = static_cast<int32_t>(run_start.size());
+        nruns[i] = static_cast<int32_t>(part.runs.size());
+        for (int l : part.cand_list) rep_list.push_back(l);
+        uint64_t w = 1;
+        std::vector<uint64_t> ws(part.runs.size());
+        for (int r = static_cast<int>(part.runs.size()) - 1; r >= 0; --r) {
+            ws[r] = w;
+            w *= part.runs[r].count;
+        }
+        for (size_t r = 0; r < part.runs.size(); ++r) {
+            run_start.push_back(part.runs[r].start);
+            run_len.push_back(part.runs[r].len);
+            run_q.push_back(part.runs[r].q);
+            run_count.push_back(part.runs[r].count);
+            run_weight.push_back(ws[r]);
+        }
+    }
+    std::vector<uint8_t> cl_n(sp.lists.size());
+    std::vector<uint16_t> cl_shape(sp.lists.size() * kMaxCand, 0);
+    for (size_t l = 0; l < sp.lists.size(); ++l) {
+        cl_n[l] = static_cast<uint8_t>(sp.lists[l].size());
+        for (size_t q = 0; q < sp.list_shapes[l].size(); ++q)
+            cl_shape[l * kMaxCand + q] = static_cast<uint16_t>(sp.list_shapes[l][q]);
+    }
+    cudaStream_t s = c.stream;
+    SpaceTables v{};
+    v.num_parts = static_cast<int64_t>(P);
+    v.prefix = sp.d_prefix.upload(sp.prefix, s);
+    v.R = sp.d_R.upload(R, s);
+    v.rep_off = sp.d_rep_off.upload(rep_off, s);
+    v.run_off = sp.d_run_off.upload(run_off, s);
+    v.nruns = sp.d_nruns.upload(nruns, s);
+    v.rep_list = sp.d_rep_list.upload(rep_list, s);
+    v.run_start = sp.d_run_start.upload(run_start, s);
+    v.run_len = sp.d_run_len.upload(run_len, s);
+    v.run_q = sp.d_run_q.upload(run_q, s);
+    v.run_count = sp.d_run_count.upload(run_count, s);
+    v.run_weight = sp.d_run_weight.upload(run_weight, s);
+    v.cl_n = sp.d_cl_n.upload(cl_n, s);
+    v.cl_shape = sp.d_cl_shape.upload(cl_shape, s);
+    sp.view = v;
+    sp.valid = true;
+}
+
+// Per-partition exact-path flags for the current workload.
+void refresh_exact(oserve_gpu_ctx &c, Space &sp) {
+    sp.exact.assign(sp.parts.size(), 0);
+    sp.any_exact = false;
+    for (size_t i = 0; i < sp.parts.size(); ++i) {
+        if (sp.parts[i].count && use_exact(c, static_cast<int>(sp.parts[i].sizes.size()))) {
+            if (static_cast<int64_t>(sp.parts[i].sizes.size()) * c.J > kMaxExactCells)
+                fail(OSERVE_ERR_UNSUPPORTED, "exact path limited to 64 cells");
+            sp.exact[i] = 1;
+            sp.any_exact = true;
+        }
+    }
+    sp.view.exact = sp.d_exact.upload(sp.exact, c.stream);
+}
+
+void make_key_layout(oserve_gpu_ctx &c, const Space &sp) {
+    int64_t tot = 0;
+    for (int64_t v : c.lambda) tot += v;
+    const int b_obj = bits_for(static_cast<uint64_t>(tot));
+    const int b_part = bits_for(sp.parts.empty() ? 0 : sp.parts.size() - 1);
+    const int b_spp = bits_for(static_cast<uint64_t>(c.D()));
+    const int b_loc = bits_for(sp.max_count ? sp.max_count - 1 : 0);
+    if (b_obj + b_part + b_spp + b_loc > 63)
+        fail(OSERVE_ERR_TOO_LARGE, "selection key does not fit 63 bits (" + std::to_string(b_obj + b_part + b_spp + b_loc) + ")");
+    c.key.sh_spp = b_loc;
+    c.key.sh_part = b_loc + b_spp;
+    c.key.sh_obj = b_loc + b_spp + b_part;
+    c.key.obj_max = (uint64_t{1} << b_obj) - 1;
+}
+
+uint64_t shard_count(const oserve_gpu_ctx &c, uint64_t total) {
+    const uint64_t ch = c.chunk, w = static_cast<uint64_t>(c.world), r = static_cast<uint64_t>(c.rank);
+    const uint64_t full = total / ch, rem = total % ch;
+    uint64_t n = full > r ? ((full - r + w - 1) / w) * ch : 0;
+    if (rem && full % w == r) n += rem;
+    return n;
+}
+
+void unrank_host(const Space &sp, uint64_t rank, int64_t &p, uint64_t &local, std::vector<int> &picks) {
+    auto it = std::upper_bound(sp.prefix.begin(), sp.prefix.end() - 1, rank);
+    p = static_cast<int64_t>(it - sp.prefix.begin()) - 1;
+    local = rank - sp.prefix[p];
+    const Partition &part = sp.parts[p];
+    picks.assign(part.sizes.size(), 0);
+    uint64_t r = local;
+    for (int i = static_cast<int>(part.runs.size()) - 1; i >= 0; --i) {
+        const Run &run = part.runs[i];
+        uint64_t rr = r % run.count;
+        r /= run.count;
+        int prev = 0;
+        for (int pos = 0; pos < run.len; ++pos) {
+            for (int v = prev; v < run.q; ++v) {
+                uint64_t cnt = binom((run.len - pos - 1) + (run.q - v) - 1, (run.q - v) - 1);
+                if (rr < cnt) {
+                    picks[run.start + pos] = v;
+                    prev = v;
+                    break;
+                }
+                rr -= cnt;
+            }
+        }
+    }
+}
+
+void fill_plan(const oserve_gpu_ctx &c, const Space &sp, int64_t p, const std::vector<int> &picks, oserve_plan *out) {
+    std::memset(out, 0, sizeof(*out));
+    const Partition &part = sp.parts[p];
+    out->num_replicas = static_cast<int>(part.sizes.size());
+    int pos = 0;
+    for (size_t r = 0; r < part.sizes.size(); ++r) {
+        const Cand &cd = sp.lists[part.cand_list[r]][picks[r]];
+        out->replica_num_devices[r] = part.sizes[r];
+        out->tp[r] = cd.first;
+        out->pp[r] = cd.second;
+        for (int i = 0; i < part.sizes[r]; ++i) out->device_ids[pos++] = c.dev_sorted[part.offsets[r] + i];
+    }
+    out->num_devices = pos;
+}
+
+void decode_key(oserve_gpu_ctx &c, uint64_t key, oserve_round_result *out) {
+    const Space &sp = c.space;
+    std::memset(out, 0, sizeof(*out));
+    out->partitions = static_cast<int64_t>(sp.parts.size());
+    out->plans = sp.total;
+    out->key = key;
+    if (key == kNoKey) {
+        out->objective = -1;
+        return;
+    }
+    const uint64_t m_loc = (uint64_t{1} << c.key.sh_spp) - 1;
+    const uint64_t m_spp = (uint64_t{1} << (c.key.sh_part - c.key.sh_spp)) - 1;
+    const uint64_t m_part = (uint64_t{1} << (c.key.sh_obj - c.key.sh_part)) - 1;
+    const uint64_t local = key & m_loc;
+    const int spp = static_cast<int>((key >> c.key.sh_spp) & m_spp);
+    const int64_t part = static_cast<int64_t>((key >> c.key.sh_part) & m_part);
+    const int64_t obj = static_cast<int64_t>(c.key.obj_max - (key >> c.key.sh_obj));
+    if (part >= static_cast<int64_t>(sp.parts.size()) || local >= sp.parts[part].count)
+        fail(OSERVE_ERR_INVALID_ARGUMENT, "key does not belong to the prepared space");
+    out->objective = obj;
+    out->partition_index = part;
+    out->local_rank = local;
+    out->sum_pp = spp;
+    int64_t p2;
+    uint64_t l2;
+    std::vector<int> picks;
+    unrank_host(sp, sp.prefix[part] + local, p2, l2, picks);
+    fill_plan(c, sp, p2, picks, &out->plan);
+}
+
+// Launch K1 (+K4, + heuristic fallback for aborted B&B) over this shard of
+// the prepared space; best key -> d_key.
+void launch_round(oserve_gpu_ctx &c, uint64_t *d_key) {
+    ensure_tables(c);
+    Space &sp = c.space;
+    refresh_exact(c, sp);
+    make_key_layout(c, sp);
+    cudaStream_t s = c.stream;
+    cuda_ok(cudaMemsetAsync(d_key, 0xff, sizeof(uint64_t), s), "memset key");
+    PlanSource src{};
+    src.mode = 0;
+    src.count = shard_count(c, sp.total);
+    src.rank = c.rank;
+    src.world = c.world;
+    src.chunk = c.chunk;
+    PlanOutputs out{};
+    out.best_key = d_key;
+    SolveParams prm = solve_params(c);
+    cuda_ok(launch_plan_eval(c.tables, sp.view, c.key, src, out, prm, sp.rmax, c.sm_count, sp.any_exact ? 1 : 0, s,
+                             &c.launches),
+            "plan kernel");
+    if (sp.any_exact) {
+        uint64_t *ab = static_cast<uint64_t *>(c.d_aborted.get(sizeof(uint64_t) * std::max<uint64_t>(src.count, 1)));
+        unsigned *abn = static_cast<unsigned *>(c.d_aborted_n.get(sizeof(unsigned)));
+        cuda_ok(cudaMemsetAsync(abn, 0, sizeof(unsigned), s), "memset");
+        PlanOutputs eo = out;
+        eo.aborted = ab;
+        eo.aborted_n = abn;
+        cuda_ok(launch_plan_exact(c.tables, sp.view, c.key, src, eo, prm, c.sm_count, s, &c.launches), "exact kernel");
+        unsigned n_ab = 0;
+        cuda_ok(cudaMemcpyAsync(&n_ab, abn, sizeof(unsigned), cudaMemcpyDeviceToHost, s), "D2H");
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+        if (n_ab) {
+            PlanSource rs{};
+            rs.mode = 1;
+            rs.count = n_ab;
+            rs.ranks = ab;
+            cuda_ok(launch_plan_eval(c.tables, sp.view, c.key, rs, out, prm, sp.rmax, c.sm_count, 0, s, &c.launches),
+                    "plan kernel (budget fallback)");
+        }
+    }
+}
+
+void prepare(oserve_gpu_ctx &c, const oserve_space_desc &d) {
+    if (d.max_devices > 0 && c.D() > d.max_devices)
+        fail(OSERVE_ERR_TOO_LARGE, "exhaustive enumeration guarded to " + std::to_string(d.max_devices) +
+                                       " devices, cluster has " + std::to_string(c.D()));
+    if (d.mode != OSERVE_SPACE_ORDERED && d.mode != OSERVE_SPACE_CANONICAL)
+        fail(OSERVE_ERR_INVALID_ARGUMENT, "unknown space mode");
+    std::vector<int> sizes(d.sizes, d.sizes + (d.sizes ? d.num_sizes : 0));
+    Space &sp = c.space;
+    if (sp.valid && !sp.explicit_partition && sp.mode == d.mode && sp.sizes_key == sizes) return;
+    sp.valid = false;
+    build_space(c, sp, d.mode, sizes, nullptr);
+    sp.mode = d.mode;
+    sp.sizes_key = sizes;
+    sp.explicit_partition = false;
+}
+
+template <class F>
+int guarded(oserve_gpu_ctx *c, F &&f) {
+    if (!c) return OSERVE_ERR_INVALID_ARGUMENT;
+    try {
+        cuda_ok(cudaSetDevice(c->device), "cudaSetDevice");
+        f();
+        c->err.clear();
+        return OSERVE_OK;
+    } catch (const Fail &e) {
+        c->err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc &) {
+        c->err = "out of host memory";
+        return OSERVE_ERR_INVALID_ARGUMENT;
+    } catch (const std::exception &e) {
+        c->err = e.what();
+        return OSERVE_ERR_INVALID_ARGUMENT;
+    }
+}
+
+// Deployment -> shape ids (evaluate_deployment / build_capacity_table).
+std::vector<int> deployment_shapes(oserve_gpu_ctx &c, const oserve_deployment &d) {
+    std::vector<int> ids;
+    int pos = 0;
+    for (int r = 0; r < d.num_replicas; ++r) {
+        std::vector<int> devs(d.device_ids + pos, d.device_ids + pos + d.replica_num_devices[r]);
+        pos += d.replica_num_devices[r];
+        uint64_t total = 0;
+        if (!mem_feasible(c, devs, d.tp[r], d.pp[r], &total))
+            fail(OSERVE_ERR_INFEASIBLE_REPLICA, "replica " + std::to_string(r) + " cannot host model");
+        ids.push_back(shape_for(c, d.tp[r], d.pp[r], total));
+    }
+    return ids;
+}
+
+// Evaluate explicit shape lists; returns objectives (+ x/used when requested).
+void eval_lists(oserve_gpu_ctx &c, const std::vector<int32_t> &listR, const std::vector<int32_t> &listOff,
+                const std::vector<int32_t> &shapes, const std::vector<int64_t> *lam_per_plan, int rmax,
+                std::vector<int64_t> &obj, std::vector<int64_t> *x, std::vector<int64_t> *used,
+                const SolveParams &prm) {
+    cudaStream_t s = c.stream;
+    const uint64_t n = listR.size();
+    PlanSource src{};
+    src.mode = 2;
+    src.count = n;
+    src.list_R = c.d_listR.upload(listR, s);
+    src.list_off = c.d_listOff.upload(listOff, s);
+    src.list_shapes = c.d_listShapes.upload(shapes, s);
+    if (lam_per_plan) src.list_lambda = c.d_listLam.upload(*lam_per_plan, s);
+    PlanOutputs out{};
+    out.objective = static_cast<int64_t *>(c.d_obj.get(sizeof(int64_t) * n));
+    out.rmax = std::max(rmax, 1);
+    if (x) {
+        out.x = static_cast<int64_t *>(c.d_x.get(sizeof(int64_t) * n * out.rmax * c.J));
+        out.used = static_cast<int64_t *>(c.d_used.get(sizeof(int64_t) * n * out.rmax));
+    }
+    // exact-path plans
+    bool any_exact = false;
+    for (uint64_t i = 0; i < n; ++i) {
+        int64_t tot = 0;
+        for (int j = 0; j < prm.J; ++j) tot += lam_per_plan ? (*lam_per_plan)[i * prm.J + j] : prm.lambda[j];
+        if (tot <= prm.exact_demand_limit && static_cast<int64_t>(listR[i]) * prm.J <= prm.exact_cell_limit) {
+            if (static_cast<int64_t>(listR[i]) * prm.J > kMaxExactCells)
+                fail(OSERVE_ERR_UNSUPPORTED, "exact path limited to 64 cells");
+            any_exact = true;
+        }
+    }
+    SpaceTables none{};
+    KeyLayout nk{};
+    cuda_ok(launch_plan_eval(c.tables, none, nk, src, out, prm, rmax, c.sm_count, any_exact ? 1 : 0, s, &c.launches),
+            "plan kernel");
+    if (any_exact) {
+        uint64_t *ab = static_cast<uint64_t *>(c.d_aborted.get(sizeof(uint64_t) * n));
+        unsigned *abn = static_cast<unsigned *>(c.d_aborted_n.get(sizeof(unsigned)));
+        cuda_ok(cudaMemsetAsync(abn, 0, sizeof(unsigned), s), "memset");
+        PlanOutputs eo = out;
+        eo.aborted = ab;
+        eo.aborted_n = abn;
+        cuda_ok(launch_plan_exact(c.tables, none, nk, src, eo, prm, c.sm_count, s, &c.launches), "exact kernel");
+        unsigned n_ab = 0;
+        cuda_ok(cudaMemcpyAsync(&n_ab, abn, sizeof(unsigned), cudaMemcpyDeviceToHost, s), "D2H");
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+        if (n_ab) {
+            std::vector<uint64_t> idx;
+            download(idx, ab, n_ab, s);
+            cuda_ok(cudaStreamSynchronize(s), "sync");
+            std::sort(idx.begin(), idx.end());
+            for (uint64_t li : idx) {  // heuristic fallback, one plan per launch (rare)
+                PlanSource one = src;
+                one.first = li;
+                one.count = 1;
+                PlanOutputs o1 = out;
+                o1.objective = out.objective + li;
+                if (x) {
+                    o1.x = out.x + li * out.rmax * c.J;
+                    o1.used = out.used + li * out.rmax;
+                }
+                cuda_ok(launch_plan_eval(c.tables, none, nk, one, o1, prm, rmax, c.sm_count, 0, s, &c.launches),
+                        "plan kernel (budget fallback)");
+            }
+        }
+    }
+    download(obj, out.objective, n, s);
+    if (x) {
+        download(*x, out.x, n * out.rmax * c.J, s);
+        download(*used, out.used, n * out.rmax, s);
+    }
+    cuda_ok(cudaStreamSynchronize(s), "sync");
+}
+
+// --------------------------------------------------------------- switch ---
+struct SwitchInput {
+    std::vector<int32_t> machine, dev_id, dep_rep_off, rep_tp, rep_pp, rep_dev_off, rep_devs;
+};
+
+void add_deployment(oserve_gpu_ctx &c, SwitchInput &in, std::map<int, int> &slots, const oserve_deployment &d) {
+    in.dep_rep_off.push_back(static_cast<int32_t>(in.rep_tp.size()));
+    int pos = 0;
+    std::set<int> seen;
+    for (int r = 0; r < d.num_replicas; ++r) {
+        std::vector<int> devs(d.device_ids + pos, d.device_ids + pos + d.replica_num_devices[r]);
+        pos += d.replica_num_devices[r];
+        if (d.tp[r] < 1 || d.pp[r] < 1 || d.tp[r] * d.pp[r] != static_cast<int>(devs.size()))
+            fail(OSERVE_ERR_INVALID_ARGUMENT, "switch: replica tp*pp must equal its device count");
+        std::sort(devs.begin(), devs.end());
+        in.rep_tp.push_back(d.tp[r]);
+        in.rep_pp.push_back(d.pp[r]);
+        in.rep_dev_off.push_back(static_cast<int32_t>(in.rep_devs.size()));
+        for (int dv : devs) {
+            if (!seen.insert(dv).second)
+                fail(OSERVE_ERR_UNSUPPORTED, "switch: a device appears in two replicas of one deployment");
+            auto it = slots.find(dv);
+            if (it == slots.end()) fail(OSERVE_ERR_INVALID_ARGUMENT, "switch: device slot missing");
+            in.rep_devs.push_back(it->second);
+        }
+    }
+}
+
+void run_switch(oserve_gpu_ctx &c, const oserve_deployment *src, int count, const oserve_deployment *dsts,
+                std::vector<double> &est, std::vector<uint64_t> &maxb, std::vector<int32_t> &status,
+                std::vector<int32_t> *detail, std::vector<uint64_t> *cuts, int *ncuts, SwitchInput *in_out) {
+    // device slots: every cluster device plus unknown ids, ascending id
+    std::set<int> ids(c.dev_sorted.begin(), c.dev_sorted.end());
+    auto collect = [&](const oserve_deployment &d) {
+        int n = 0;
+        for (int r = 0; r < d.num_replicas; ++r) n += d.replica_num_devices[r];
+        for (int i = 0; i < n; ++i) ids.insert(d.device_ids[i]);
+    };
+    collect(*src);
+    for (int i = 0; i < count; ++i) collect(dsts[i]);
+    if (ids.size() > 256) fail(OSERVE_ERR_UNSUPPORTED, "switch kernel limited to 256 devices");
+    SwitchInput in;
+    std::map<int, int> slots;
+    for (int id : ids) {
+        slots.emplace(id, static_cast<int>(in.dev_id.size()));
+        in.dev_id.push_back(id);
+        in.machine.push_back(c.machine(id));
+    }
+    add_deployment(c, in, slots, *src);
+    for (int i = 0; i < count; ++i) add_deployment(c, in, slots, dsts[i]);
+    in.dep_rep_off.push_back(static_cast<int32_t>(in.rep_tp.size()));
+    in.rep_dev_off.push_back(static_cast<int32_t>(in.rep_devs.size()));
+    if (in.dep_rep_off[1] - in.dep_rep_off[0] > 128) fail(OSERVE_ERR_UNSUPPORTED, "switch: > 128 source replicas");
+    if (c.model.param_bytes >= (uint64_t{1} << 46)) fail(OSERVE_ERR_UNSUPPORTED, "switch: param_bytes >= 2^46");
+    cudaStream_t s = c.stream;
+    SwitchDeps d{};
+    d.count = count;
+    d.num_devices = static_cast<int>(in.dev_id.size());
+    d.machine = c.d_sw[0].upload(in.machine, s);
+    d.dev_id = c.d_sw[1].upload(in.dev_id, s);
+    d.dep_rep_off = c.d_sw[2].upload(in.dep_rep_off, s);
+    d.rep_tp = c.d_sw[3].upload(in.rep_tp, s);
+    d.rep_pp = c.d_sw[4].upload(in.rep_pp, s);
+    d.rep_dev_off = c.d_sw[5].upload(in.rep_dev_off, s);
+    d.rep_devs = c.d_sw[6].upload(in.rep_devs, s);
+    d.P = c.model.param_bytes;
+    d.intra_bw = c.intra;
+    d.inter_bw = c.inter;
+    SwitchOut o{};
+    o.est = static_cast<double *>(c.d_sw[7].get(sizeof(double) * count));
+    o.max_bytes = static_cast<uint64_t *>(c.d_sw[8].get(sizeof(uint64_t) * count));
+    o.status = static_cast<int32_t *>(c.d_sw[9].get(sizeof(int32_t) * count));
+    const int maxf = 4 * d.num_devices;
+    if (detail) {
+        o.max_frags = maxf;
+        o.detail_src = static_cast<int32_t *>(c.d_sw[10].get(sizeof(int32_t) * d.num_devices * maxf));
+        cuda_ok(cudaMemsetAsync(o.detail_src, 0xff, sizeof(int32_t) * d.num_devices * maxf, s), "memset");
+        o.detail_cuts = static_cast<uint64_t *>(c.d_sw[11].get(sizeof(uint64_t) * (maxf + 2)));
+        o.detail_ncuts = reinterpret_cast<int32_t *>(o.detail_cuts + maxf + 1);
+    }
+    cuda_ok(launch_switch_cost(d, o, s, &c.launches), "switch kernel");
+    download(est, o.est, count, s);
+    download(maxb, o.max_bytes, count, s);
+    download(status, o.status, count, s);
+    if (detail) {
+        download(*detail, o.detail_src, static_cast<size_t>(d.num_devices) * maxf, s);
+        std::vector<uint64_t> tmp;
+        download(tmp, o.detail_cuts, maxf + 2, s);
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+        *ncuts = static_cast<int>(reinterpret_cast<int32_t *>(&tmp[maxf + 1])[0]);
+        cuts->assign(tmp.begin(), tmp.begin() + std::min(*ncuts, maxf + 1));
+    }
+    cuda_ok(cudaStreamSynchronize(s), "sync");
+    if (in_out) *in_out = std::move(in);
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+const char *oserve_gpu_status_name(int status) {
+    switch (status) {
+        case OSERVE_OK: return "OK";
+        case OSERVE_ERR_INVALID_ARGUMENT: return "INVALID_ARGUMENT";
+        case OSERVE_ERR_INFEASIBLE_REPLICA: return "INFEASIBLE_REPLICA";
+        case OSERVE_ERR_MODEL_TOO_LARGE: return "MODEL_TOO_LARGE";
+        case OSERVE_ERR_TOO_LARGE: return "TOO_LARGE";
+        case OSERVE_ERR_EMPTY_DEPLOYMENT: return "EMPTY_DEPLOYMENT";
+        case OSERVE_ERR_UNSOURCED_FRAGMENT: return "UNSOURCED_FRAGMENT";
+        case OSERVE_ERR_LOGIC: return "LOGIC";
+        case OSERVE_ERR_UNSUPPORTED: return "UNSUPPORTED";
+        case OSERVE_ERR_CUDA: return "CUDA";
+        case OSERVE_ERR_NO_DEVICE: return "NO_DEVICE";
+        default: return "UNKNOWN";
+    }
+}
+
+int oserve_gpu_create(int cuda_device, const oserve_cluster_desc *cluster, const oserve_model_desc *model,
+                      const oserve_profile *profile, oserve_gpu_ctx **out) {
+    if (!out || !cluster || !model || !profile) return OSERVE_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return OSERVE_ERR_NO_DEVICE;
+    if (cuda_device < 0 || cuda_device >= ndev) return OSERVE_ERR_NO_DEVICE;
+    auto c = std::make_unique<oserve_gpu_ctx>();
+    c->device = cuda_device;
+    int pos = 0;
+    for (int m = 0; m < cluster->num_machines; ++m) {
+        c->machine_mem.push_back(cluster->device_mem[m]);
+        for (int i = 0; i < cluster->machine_num_devices[m]; ++i) {
+            int d = cluster->device_ids[pos++];
+            c->machine_of.emplace(d, m);  // first machine wins (linear scan, core.cpp:29-35)
+            c->dev_sorted.push_back(d);
+        }
+    }
+    std::sort(c->dev_sorted.begin(), c->dev_sorted.end());
+    if (c->dev_sorted.empty() || c->dev_sorted.size() > OSERVE_MAX_DEVICES) return OSERVE_ERR_UNSUPPORTED;
+    c->intra = cluster->intra_bw;
+    c->inter = cluster->inter_bw;
+    c->model = *model;
+    c->profile = *profile;
+    int rc = guarded(c.get(), [&] {
+        cuda_ok(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "stream");
+        c->stream = c->own;
+        cudaDeviceProp prop{};
+        cuda_ok(cudaGetDeviceProperties(&prop, cuda_device), "props");
+        c->sm_count = prop.multiProcessorCount;
+    });
+    if (rc != OSERVE_OK) return rc;
+    *out = c.release();
+    return OSERVE_OK;
+}
+
+int oserve_gpu_destroy(oserve_gpu_ctx *ctx) {
+    if (!ctx) return OSERVE_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->own) {
+        cudaStreamSynchronize(ctx->own);
+        cudaStreamDestroy(ctx->own);
+    }
+    delete ctx;
+    return OSERVE_OK;
+}
+
+const char *oserve_gpu_last_error(const oserve_gpu_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+uint64_t oserve_gpu_launch_count(const oserve_gpu_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+int oserve_gpu_set_workload(oserve_gpu_ctx *ctx, int num_classes, const oserve_class *classes, const int64_t *lambda,
+                            double span_seconds) {
+    return guarded(ctx, [&] {
+        if (num_classes < 1 || num_classes > OSERVE_MAX_CLASSES)
+            fail(OSERVE_ERR_UNSUPPORTED, "classes must be in [1, 16]");
+        int64_t tot = 0;
+        for (int j = 0; j < num_classes; ++j) {
+            if (lambda[j] < 0) fail(OSERVE_ERR_INVALID_ARGUMENT, "negative demand");
+            if (lambda[j] > 0x7fffffffll) fail(OSERVE_ERR_UNSUPPORTED, "demand per class must be < 2^31");
+            tot += lambda[j];
+        }
+        if (tot > 0x7fffffffll) fail(OSERVE_ERR_UNSUPPORTED, "total demand must be < 2^31");
+        std::vector<double> ci(num_classes), co(num_classes);
+        for (int j = 0; j < num_classes; ++j) {
+            ci[j] = classes[j].centroid_in;
+            co[j] = classes[j].centroid_out;
+        }
+        if (ci != ctx->cin || co != ctx->cout || span_seconds != ctx->span || num_classes != ctx->J)
+            ctx->tables_dirty = true;
+        ctx->J = num_classes;
+        ctx->cin = ci;
+        ctx->cout = co;
+        ctx->lambda.assign(lambda, lambda + num_classes);
+        ctx->span = span_seconds;
+        ctx->have_workload = true;
+    });
+}
+
+int oserve_gpu_set_solve_options(oserve_gpu_ctx *ctx, const oserve_solve_options *opts) {
+    return guarded(ctx, [&] {
+        if (!opts) fail(OSERVE_ERR_INVALID_ARGUMENT, "null options");
+        ctx->opts = *opts;
+    });
+}
+
+int oserve_gpu_set_shard(oserve_gpu_ctx *ctx, int rank, int world) {
+    return guarded(ctx, [&] {
+        if (world < 1 || rank < 0 || rank >= world) fail(OSERVE_ERR_INVALID_ARGUMENT, "bad shard");
+        ctx->rank = rank;
+        ctx->world = world;
+    });
+}
+
+int oserve_gpu_set_stream(oserve_gpu_ctx *ctx, void *stream) {
+    return guarded(ctx, [&] { ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own; });
+}
+
+int oserve_gpu_min_feasible_group(oserve_gpu_ctx *ctx, int *g_min) {
+    return guarded(ctx, [&] { *g_min = g_min_of(*ctx); });
+}
+
+int oserve_gpu_prepare_space(oserve_gpu_ctx *ctx, const oserve_space_desc *space, int64_t *partitions,
+                             uint64_t *plans) {
+    return guarded(ctx, [&] {
+        prepare(*ctx, *space);
+        if (partitions) *partitions = static_cast<int64_t>(ctx->space.parts.size());
+        if (plans) *plans = ctx->space.total;
+    });
+}
+
+int oserve_gpu_launch_round_async(oserve_gpu_ctx *ctx, uint64_t *d_key) {
+    return guarded(ctx, [&] {
+        if (!ctx->space.valid) fail(OSERVE_ERR_INVALID_ARGUMENT, "no prepared space");
+        launch_round(*ctx, d_key);
+    });
+}
+
+int oserve_gpu_decode_key(oserve_gpu_ctx *ctx, uint64_t key, oserve_round_result *out) {
+    return guarded(ctx, [&] {
+        if (!ctx->space.valid) fail(OSERVE_ERR_INVALID_ARGUMENT, "no prepared space");
+        decode_key(*ctx, key, out);
+    });
+}
+
+int oserve_gpu_round(oserve_gpu_ctx *ctx, const oserve_space_desc *space, oserve_round_result *out) {
+    return guarded(ctx, [&] {
+        prepare(*ctx, *space);
+        uint64_t *dk = static_cast<uint64_t *>(ctx->d_key.get(sizeof(uint64_t)));
+        launch_round(*ctx, dk);
+        uint64_t key = kNoKey;
+        cuda_ok(cudaMemcpyAsync(&key, dk, sizeof(key), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        cuda_ok(cudaStreamSynchronize(ctx->stream), "sync");
+        decode_key(*ctx, key, out);
+        if (key == kNoKey && ctx->world == 1) fail(OSERVE_ERR_MODEL_TOO_LARGE, "round: no feasible deployment");
+    });
+}
+
+int oserve_gpu_exhaustive(oserve_gpu_ctx *ctx, oserve_round_result *out) {
+    oserve_space_desc d{OSERVE_SPACE_ORDERED, 0, nullptr, 16};
+    int rc = oserve_gpu_round(ctx, &d, out);
+    return rc;
+}
+
+int oserve_gpu_best_strategies(oserve_gpu_ctx *ctx, int num_replicas, const int *sizes, oserve_round_result *out) {
+    return guarded(ctx, [&] {
+        std::vector<int> sz(sizes, sizes + num_replicas);
+        std::sort(sz.begin(), sz.end(), std::greater<int>());
+        int tot = std::accumulate(sz.begin(), sz.end(), 0);
+        if (tot > ctx->D()) fail(OSERVE_ERR_INVALID_ARGUMENT, "canonical_blocks: sizes exceed cluster device count");
+        for (int s : sz)
+            if (s < 1) fail(OSERVE_ERR_INVALID_ARGUMENT, "replica size must be >= 1");
+        Space &sp = ctx->space;
+        if (!(sp.valid && sp.explicit_partition && sp.explicit_sizes == sz)) {
+            sp.valid = false;
+            std::vector<std::vector<int>> parts{sz};
+            build_space(*ctx, sp, OSERVE_SPACE_ORDERED, {}, &parts);
+            sp.explicit_partition = true;
+            sp.explicit_sizes = sz;
+            sp.mode = OSERVE_SPACE_ORDERED;
+        }
+        std::memset(out, 0, sizeof(*out));
+        out->partitions = 1;
+        if (sp.total == 0) return;  // a block without candidates: empty choice, objective 0
+        uint64_t *dk = static_cast<uint64_t *>(ctx->d_key.get(sizeof(uint64_t)));
+        launch_round(*ctx, dk);
+        uint64_t key = kNoKey;
+        cuda_ok(cudaMemcpyAsync(&key, dk, sizeof(key), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        cuda_ok(cudaStreamSynchronize(ctx->stream), "sync");
+        decode_key(*ctx, key, out);
+        if (out->objective < 0) out->objective = 0;
+    });
+}
+
+int oserve_gpu_evaluate_ranks(oserve_gpu_ctx *ctx, uint64_t first, uint64_t count, int64_t *objective,
+                              int32_t *sum_pp) {
+    return guarded(ctx, [&] {
+        Space &sp = ctx->space;
+        if (!sp.valid) fail(OSERVE_ERR_INVALID_ARGUMENT, "no prepared space");
+        if (first + count > sp.total) fail(OSERVE_ERR_INVALID_ARGUMENT, "rank range out of the space");
+        ensure_tables(*ctx);
+        refresh_exact(*ctx, sp);
+        cudaStream_t s = ctx->stream;
+        PlanSource src{};
+        src.mode = 0;
+        src.first = first;
+        src.count = count;
+        src.rank = 0;
+        src.world = 1;
+        src.chunk = ~0ull >> 2;
+        PlanOutputs out{};
+        out.objective = static_cast<int64_t *>(ctx->d_obj.get(sizeof(int64_t) * count));
+        out.sum_pp = static_cast<int32_t *>(ctx->d_spp.get(sizeof(int32_t) * count));
+        SolveParams prm = solve_params(*ctx);
+        KeyLayout nk{};
+        cuda_ok(launch_plan_eval(ctx->tables, sp.view, nk, src, out, prm, sp.rmax, ctx->sm_count, sp.any_exact, s,
+                                 &ctx->launches),
+                "plan kernel");
+        if (sp.any_exact) {
+            uint64_t *ab = static_cast<uint64_t *>(ctx->d_aborted.get(sizeof(uint64_t) * count));
+            unsigned *abn = static_cast<unsigned *>(ctx->d_aborted_n.get(sizeof(unsigned)));
+            cuda_ok(cudaMemsetAsync(abn, 0, sizeof(unsigned), s), "memset");
+            PlanOutputs eo = out;
+            eo.aborted = ab;
+            eo.aborted_n = abn;
+            cuda_ok(launch_plan_exact(ctx->tables, sp.view, nk, src, eo, prm, ctx->sm_count, s, &ctx->launches),
+                    "exact kernel");
+            unsigned n_ab = 0;
+            cuda_ok(cudaMemcpyAsync(&n_ab, abn, sizeof(unsigned), cudaMemcpyDeviceToHost, s), "D2H");
+            cuda_ok(cudaStreamSynchronize(s), "sync");
+            if (n_ab) {
+                std::vector<uint64_t> ranks;
+                download(ranks, ab, n_ab, s);
+                cuda_ok(cudaStreamSynchronize(s), "sync");
+                for (uint64_t g : ranks) {
+                    PlanSource one = src;
+                    one.first = g;
+                    one.count = 1;
+                    PlanOutputs o1 = out;
+                    o1.objective = out.objective + (g - first);
+                    o1.sum_pp = out.sum_pp + (g - first);
+                    cuda_ok(launch_plan_eval(ctx->tables, sp.view, nk, one, o1, prm, sp.rmax, ctx->sm_count, 0, s,
+                                             &ctx->launches),
+                            "plan kernel (budget fallback)");
+                }
+            }
+        }
+        if (objective)
+            cuda_ok(cudaMemcpyAsync(objective, out.objective, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, s), "D2H");
+        if (sum_pp)
+            cuda_ok(cudaMemcpyAsync(sum_pp, out.sum_pp, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, s), "D2H");
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+    });
+}
+
+int oserve_gpu_evaluate_deployments(oserve_gpu_ctx *ctx, int count, const oserve_deployment *deps,
+                                    int64_t *objective) {
+    return guarded(ctx, [&] {
+        std::vector<int32_t> listR, listOff, shapes;
+        std::vector<int> idx;  // non-empty deployments
+        int rmax = 1;
+        for (int i = 0; i < count; ++i) {
+            objective[i] = 0;  // evaluate_deployment: empty -> 0 (deploysearch.cpp:139)
+            if (deps[i].num_replicas == 0) continue;
+            if (deps[i].num_replicas > OSERVE_MAX_REPLICAS) fail(OSERVE_ERR_UNSUPPORTED, "more than 128 replicas");
+            auto ids = deployment_shapes(*ctx, deps[i]);
+            listR.push_back(static_cast<int32_t>(ids.size()));
+            listOff.push_back(static_cast<int32_t>(shapes.size()));
+            shapes.insert(shapes.end(), ids.begin(), ids.end());
+            rmax = std::max(rmax, static_cast<int>(ids.size()));
+            idx.push_back(i);
+        }
+        if (idx.empty()) return;
+        ensure_tables(*ctx);
+        std::vector<int64_t> obj;
+        eval_lists(*ctx, listR, listOff, shapes, nullptr, rmax, obj, nullptr, nullptr, solve_params(*ctx));
+        for (size_t q = 0; q < idx.size(); ++q) objective[idx[q]] = obj[q];
+    });
+}
+
+int oserve_gpu_plan_detail(oserve_gpu_ctx *ctx, const oserve_deployment *dep, int64_t *n, int64_t *e, double *latency,
+                           int64_t *x, int64_t *M, int64_t *unit, int64_t *used, int64_t *objective) {
+    return guarded(ctx, [&] {
+        const int R = dep->num_replicas, J = ctx->J;
+        if (R == 0) {
+            if (objective) *objective = 0;
+            return;
+        }
+        if (R > OSERVE_MAX_REPLICAS) fail(OSERVE_ERR_UNSUPPORTED, "more than 128 replicas");
+        auto ids = deployment_shapes(*ctx, *dep);
+        ensure_tables(*ctx);
+        std::vector<int32_t> listR{R}, listOff{0}, shapes(ids.begin(), ids.end());
+        std::vector<int64_t> obj, xs, us;
+        eval_lists(*ctx, listR, listOff, shapes, nullptr, R, obj, &xs, &us, solve_params(*ctx));
+        // shape rows (n, e, latency, M, unit) straight from the device tables
+        const int S = ctx->tables.num_shapes;
+        std::vector<int64_t> hn, he, hM, hu;
+        std::vector<double> hl;
+        cudaStream_t s = ctx->stream;
+        download(hn, ctx->tables.n, S * J, s);
+        download(he, ctx->tables.e, S * J, s);
+        download(hl, ctx->tables.latency, S * J, s);
+        download(hM, ctx->tables.M, S, s);
+        download(hu, ctx->tables.unit, S * J, s);
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+        for (int k = 0; k < R; ++k) {
+            const int sh = ids[k];
+            for (int j = 0; j < J; ++j) {
+                if (n) n[k * J + j] = hn[sh * J + j];
+                if (e) e[k * J + j] = he[sh * J + j];
+                if (latency) latency[k * J + j] = hl[sh * J + j];
+                if (unit) unit[k * J + j] = hu[sh * J + j];
+                if (x) x[k * J + j] = xs[k * J + j];
+            }
+            if (M) M[k] = hM[sh];
+            if (used) used[k] = us[k];
+        }
+        if (objective) *objective = obj[0];
+    });
+}
+
+int oserve_gpu_solve_batch(oserve_gpu_ctx *ctx, int count, int R, int J, const int64_t *n, const int64_t *e,
+                           const int64_t *lambda, int64_t *x, int64_t *objective, int64_t *M, int64_t *unit,
+                           int64_t *used) {
+    return guarded(ctx, [&] {
+        if (count <= 0) return;
+        if (J < 1 || J > OSERVE_MAX_CLASSES) fail(OSERVE_ERR_UNSUPPORTED, "classes must be in [1, 16]");
+        if (R < 1 || R > OSERVE_MAX_REPLICAS) fail(OSERVE_ERR_UNSUPPORTED, "replicas must be in [1, 128]");
+        const int64_t rows = static_cast<int64_t>(count) * R;
+        for (int64_t i = 0; i < rows * J; ++i) {
+            if (n[i] < 0) fail(OSERVE_ERR_INVALID_ARGUMENT, "normalize: negative capacity");
+        }
+        for (int64_t i = 0; i < static_cast<int64_t>(count); ++i) {
+            int64_t tot = 0;
+            for (int j = 0; j < J; ++j) {
+                if (lambda[i * J + j] < 0 || lambda[i * J + j] > 0x7fffffffll)
+                    fail(OSERVE_ERR_UNSUPPORTED, "demand per class must be in [0, 2^31)");
+                tot += lambda[i * J + j];
+            }
+            if (tot > 0x7fffffffll) fail(OSERVE_ERR_UNSUPPORTED, "total demand must be < 2^31");
+        }
+        // Raw rows become the shape tables of this call (K0b only).
+        cudaStream_t s = ctx->stream;
+        DBuf dn, de, dM, du, dc, dord, dol, dpp, dsc, dlat;
+        ShapeTables t{};
+        t.num_shapes = static_cast<int>(rows);
+        t.J = J;
+        t.n = static_cast<int64_t *>(dn.get(sizeof(int64_t) * rows * J));
+        t.e = static_cast<int64_t *>(de.get(sizeof(int64_t) * rows * J));
+        cuda_ok(cudaMemcpyAsync(t.n, n, sizeof(int64_t) * rows * J, cudaMemcpyHostToDevice, s), "H2D");
+        cuda_ok(cudaMemcpyAsync(t.e, e, sizeof(int64_t) * rows * J, cudaMemcpyHostToDevice, s), "H2D");
+        t.latency = static_cast<double *>(dlat.get(8));
+        t.M = static_cast<int64_t *>(dM.get(sizeof(int64_t) * rows));
+        t.unit = static_cast<int64_t *>(du.get(sizeof(int64_t) * rows * J));
+        t.cap = static_cast<int32_t *>(dc.get(sizeof(int32_t) * rows * J));
+        t.order = static_cast<uint8_t *>(dord.get(rows * kMaxJ));
+        t.olen = static_cast<uint8_t *>(dol.get(rows));
+        t.scaled = static_cast<uint8_t *>(dsc.get(rows));
+        t.pp = static_cast<uint8_t *>(dpp.get(rows));
+        cuda_ok(cudaMemsetAsync(t.pp, 1, rows, s), "memset");
+        cuda_ok(launch_normalize_rows(t, s), "normalize kernel");
+        ctx->launches += 1;
+        std::vector<int32_t> listR(count, R), listOff(count), shapes(rows);
+        for (int i = 0; i < count; ++i) listOff[i] = i * R;
+        std::iota(shapes.begin(), shapes.end(), 0);
+        std::vector<int64_t> lam(lambda, lambda + static_cast<int64_t>(count) * J);
+        SolveParams prm = solve_params(*ctx);
+        prm.J = J;
+        ShapeTables saved = ctx->tables;
+        ctx->tables = t;
+        std::vector<int64_t> obj, xs, us;
+        try {
+            eval_lists(*ctx, listR, listOff, shapes, &lam, R, obj, &xs, &us, prm);
+        } catch (...) {
+            ctx->tables = saved;
+            throw;
+        }
+        ctx->tables = saved;
+        std::vector<int64_t> hM, hu;
+        download(hM, t.M, rows, s);
+        download(hu, t.unit, rows * J, s);
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+        for (int i = 0; i < count; ++i) {
+            if (objective) objective[i] = obj[i];
+            for (int k = 0; k < R; ++k) {
+                const int64_t row = static_cast<int64_t>(i) * R + k;
+                for (int j = 0; j < J; ++j) {
+                    if (x) x[row * J + j] = xs[row * J + j];
+                    if (unit) unit[row * J + j] = hu[row * J + j];
+                }
+                if (M) M[row] = hM[row];
+                if (used) used[row] = us[row];
+            }
+        }
+    });
+}
+
+int oserve_gpu_switch_cost_batch(oserve_gpu_ctx *ctx, const oserve_deployment *src, int count,
+                                 const oserve_deployment *dsts, double *est_seconds, uint64_t *max_link_bytes) {
+    return guarded(ctx, [&] {
+        if (count <= 0) return;
+        std::vector<double> est;
+        std::vector<uint64_t> mb;
+        std::vector<int32_t> st;
+        run_switch(*ctx, src, count, dsts, est, mb, st, nullptr, nullptr, nullptr, nullptr);
+        for (int i = 0; i < count; ++i) {
+            if (st[i]) fail(OSERVE_ERR_UNSOURCED_FRAGMENT, "required bytes have no source holder");
+            est_seconds[i] = est[i];
+            if (max_link_bytes) max_link_bytes[i] = mb[i];
+        }
+    });
+}
+
+int oserve_gpu_switch_plan(oserve_gpu_ctx *ctx, const oserve_deployment *src, const oserve_deployment *dst,
+                           int capacity, oserve_transfer *transfers, int *num_transfers, double *est_seconds) {
+    return guarded(ctx, [&] {
+        std::vector<double> est;
+        std::vector<uint64_t> mb, cuts;
+        std::vector<int32_t> st, detail;
+        int ncuts = 0;
+        SwitchInput in;
+        run_switch(*ctx, src, 1, dst, est, mb, st, &detail, &cuts, &ncuts, &in);
+        if (st[0]) fail(OSERVE_ERR_UNSOURCED_FRAGMENT, "required bytes have no source holder");
+        const int ND = static_cast<int>(in.dev_id.size()), maxf = 4 * ND;
+        std::vector<oserve_transfer> tr;
+        for (int f = 0; f + 1 < ncuts; ++f)
+            for (int t = 0; t < ND; ++t) {
+                int sslot = detail[static_cast<size_t>(t) * maxf + f];
+                if (sslot >= 0) tr.push_back({cuts[f], cuts[f + 1], in.dev_id[sslot], in.dev_id[t]});
+            }
+        if (num_transfers) *num_transfers = static_cast<int>(tr.size());
+        if (est_seconds) *est_seconds = est[0];
+        if (transfers) {
+            for (int i = 0; i < std::min<int>(capacity, static_cast<int>(tr.size())); ++i) transfers[i] = tr[i];
+            if (static_cast<int>(tr.size()) > capacity) fail(OSERVE_ERR_INVALID_ARGUMENT, "transfer capacity too small");
+        }
+    });
+}
+
+}  // extern "C"

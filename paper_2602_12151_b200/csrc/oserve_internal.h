@@ -1,0 +1,151 @@
+// oserve_internal.h — device-side table layouts shared by the host runtime
+// (oserve_host.cpp) and the sm_100a kernels (oserve_kernels.cu).
+//
+// HBM layout (all SoA, one copy per context):
+//   shape tables   one "shape" = a replica cost row keyed by (tp, pp, sum of
+//                  device memory); K0 fills n/e/latency per (shape, class),
+//                  then the LCM normalisation M, unit, cap and the
+//                  ascending-unit class order per shape.
+//   space tables   partitions (plan-count prefix, R, replica/run offsets),
+//                  per-replica candidate-list ids, per-run (start, len, q,
+//                  count, radix weight), candidate lists of shape ids.
+// K1 stages the shape tables into shared memory once per CTA.
+#pragma once
+
+#include <cstdint>
+
+namespace oserve_gpu {
+
+constexpr int kMaxJ = 16;       // classes (OSERVE_MAX_CLASSES)
+constexpr int kMaxCand = 8;     // (tp, pp) candidates per replica block
+constexpr int kMaxExactCells = 64;
+constexpr uint64_t kNoKey = ~0ull;
+
+// Per-shape inputs of the cost kernel (K0).
+struct ShapeParam {
+    int tp;
+    int pp;
+    uint64_t kv_budget;  // sum(device_mem) - param_bytes, clamped at 0 (costmodel.cpp:64-68)
+    double speedup;      // tp * eff^log2(tp) (costmodel.cpp:22-24), host libm
+};
+
+// Device views of the shape tables.  Row s, class j at [s * J + j].
+struct ShapeTables {
+    int num_shapes;
+    int J;
+    const ShapeParam *param;
+    int64_t *n;
+    int64_t *e;
+    double *latency;
+    int64_t *M;       // [S]
+    int64_t *unit;    // [S*J]
+    int32_t *cap;     // [S*J] min(e, n, M/unit), clamped to INT32_MAX (exact while lambda < 2^31)
+    uint8_t *order;   // [S*kMaxJ] classes with cap > 0, stable-sorted by unit
+    uint8_t *olen;    // [S]
+    uint8_t *pp;      // [S]
+    uint8_t *scaled;  // [S] LCM fallback used
+};
+
+// Device views of a prepared plan space.
+struct SpaceTables {
+    int64_t num_parts;
+    const uint64_t *prefix;    // [P+1] plans before partition p
+    const int32_t *R;          // [P]
+    const int32_t *rep_off;    // [P] into rep_list
+    const int32_t *run_off;    // [P] into run arrays
+    const int32_t *nruns;      // [P]
+    const uint8_t *exact;      // [P] plans of this partition take the exact (B&B) path
+    const int32_t *rep_list;   // [sum R] candidate-list id per replica
+    const int32_t *run_start;  // [sum runs]
+    const int32_t *run_len;
+    const int32_t *run_q;
+    const uint64_t *run_count;
+    const uint64_t *run_weight;  // product of later runs' counts (mixed radix)
+    const uint8_t *cl_n;         // [L] candidates per list
+    const uint16_t *cl_shape;    // [L*kMaxCand] shape ids, tp-descending
+};
+
+// Packed selection key: (OBJMAX - obj, partition, sum_pp, local rank).
+struct KeyLayout {
+    int sh_obj, sh_part, sh_spp;
+    uint64_t obj_max;
+};
+
+// Which plans a K1/K4 launch evaluates.
+struct PlanSource {
+    int mode;  // 0: space ranks of this shard; 1: explicit rank list; 2: explicit shape lists
+    // mode 0: local index i -> global rank via interleaved chunks
+    uint64_t count;       // plans in this launch
+    uint64_t first;       // first local index (mode 0) / first list entry
+    int rank, world;      // shard
+    uint64_t chunk;       // shard interleave chunk
+    const uint64_t *ranks;  // mode 1
+    // mode 2: plan i has R = list_R[i] shapes at list_shapes[list_off[i] ...]
+    const int32_t *list_R;
+    const int32_t *list_off;
+    const int32_t *list_shapes;
+    const int64_t *list_lambda;  // optional per-plan lambda [count*J] (solve_batch)
+};
+
+// Optional per-plan outputs.
+struct PlanOutputs {
+    int64_t *objective;   // [count] or null
+    int32_t *sum_pp;      // [count] or null
+    int64_t *x;           // [count * rmax * J] (mode 2 detail) or null
+    int64_t *used;        // [count * rmax] or null
+    int rmax;             // row stride for x/used
+    uint64_t *best_key;   // argmin target (atomicMin) or null
+    uint64_t *aborted;    // [count] ranks whose B&B blew the budget (K4) or null
+    unsigned int *aborted_n;
+};
+
+struct SolveParams {
+    int J;
+    int64_t lambda[kMaxJ];
+    int64_t exact_demand_limit;
+    int exact_cell_limit;
+    int64_t node_budget;
+};
+
+// ---- launchers (oserve_kernels.cu) -----------------------------------------
+int launch_cost_tables(const ShapeTables &t, const double *cin, const double *cout, uint32_t num_layers,
+                       uint64_t bytes_per_token_kv, double prefill_coeff, double decode_coeff,
+                       double pp_comm_cost, double mem_bw_penalty, double span_s, void *stream);
+int launch_normalize_rows(const ShapeTables &t, void *stream);
+// Greedy + exchange (heuristic path) over a plan source; returns CUDA status.
+int launch_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key, const PlanSource &src,
+                     const PlanOutputs &out, const SolveParams &sp_params, int rmax, int sm_count,
+                     int skip_exact, void *stream, uint64_t *launches);
+// Exact branch-and-bound path (thread per plan).
+int launch_plan_exact(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key, const PlanSource &src,
+                      const PlanOutputs &out, const SolveParams &sp_params, int sm_count, void *stream,
+                      uint64_t *launches);
+
+// Switching cost (K2).
+struct SwitchDeps {
+    int count;                 // candidate deployments
+    int num_devices;           // distinct device slots (cluster size)
+    const int32_t *machine;    // [num_devices] machine index per device slot
+    const int32_t *dev_id;     // [num_devices] device id per slot (ascending)
+    // deployments: dep 0 = source, 1..count = candidates
+    const int32_t *dep_rep_off;  // [count+2] replica offset per deployment
+    const int32_t *rep_tp;
+    const int32_t *rep_pp;
+    const int32_t *rep_dev_off;  // [total reps + 1] offset into rep_devs
+    const int32_t *rep_devs;     // device slots, ascending per replica
+    uint64_t P;
+    double intra_bw, inter_bw;
+};
+struct SwitchOut {
+    double *est;            // [count]
+    uint64_t *max_bytes;    // [count]
+    int32_t *status;        // [count] 0 ok, 1 unsourced fragment
+    // detail (count == 1): per (target slot, fragment) chosen source slot or -1
+    int32_t *detail_src;    // [num_devices * max_frags] or null
+    uint64_t *detail_cuts;  // [max_frags + 1]
+    int32_t *detail_ncuts;  // [1]
+    int max_frags;
+};
+int launch_switch_cost(const SwitchDeps &d, const SwitchOut &o, void *stream, uint64_t *launches);
+
+}  // namespace oserve_gpu

@@ -1,0 +1,1087 @@
+// oserve_kernels.cu — sm_100a kernels of the OServe scheduling round.
+//
+//   K0a k_cost_cells      per (shape, class) FP64 service time, n, e
+//                         (costmodel.cpp:22-116; bit-exact: __dmul_rn/__dadd_rn/
+//                         __ddiv_rn keep the reference's operand order, no FMA)
+//   K0b k_normalize_rows  per shape LCM normalisation + instance caps + class
+//                         order (flowassign.cpp:22-62, :267-294)
+//   K1  k_plan_eval       one G-lane group per plan: unrank -> gather shape rows
+//                         (smem) -> speculative-parallel greedy_fill -> exchange
+//                         (first improving move, restart) -> objective -> packed
+//                         key -> group/CTA min -> atomicMin
+//                         (deploysearch.cpp:153-229, flowassign.cpp:393-503)
+//   K4  k_plan_exact      thread per plan: branch-and-bound exact path
+//                         (flowassign.cpp:296-369, :450-477)
+//   K2  k_switch_cost     CTA per (current, candidate) pair: layouts, cut points,
+//                         warp per target device, lane per source replica
+//                         (switchplan.cpp:40-140)
+// All integer work runs on the CUDA-core INT/FP32 pipes; there is no dense
+// contraction here, so no tensor-core path.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "oserve_internal.h"
+
+namespace oserve_gpu {
+
+namespace {
+
+constexpr int64_t kLcmLimit = int64_t{1} << 62;
+constexpr int kBinomN = 160;
+constexpr int kBinomK = kMaxCand;
+__constant__ uint64_t c_binom[kBinomN][kBinomK];  // C(n, k), k < kMaxCand
+
+inline int check(cudaError_t e) { return e == cudaSuccess ? 0 : static_cast<int>(e); }
+
+__device__ __forceinline__ int64_t gcd64(int64_t a, int64_t b) {
+    while (b != 0) {
+        int64_t t = a % b;
+        a = b;
+        b = t;
+    }
+    return a;
+}
+
+// ----------------------------------------------------------------- K0a ----
+__global__ void k_cost_cells(ShapeTables t, const double *__restrict__ cin, const double *__restrict__ cout,
+                             uint32_t num_layers, uint64_t kvb, double pc, double dc, double ppc,
+                             double slope, double span) {
+    const int J = t.J;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < t.num_shapes * J;
+         idx += gridDim.x * blockDim.x) {
+        const int s = idx / J, j = idx - (idx / J) * J;
+        const ShapeParam sp = t.param[s];
+        const double in = cin[j], out = cout[j], L = static_cast<double>(num_layers);
+        const double ppm1 = static_cast<double>(sp.pp - 1);
+        // prefill_latency (costmodel.cpp:28-33): in*L*pc/speedup + (pp-1)*ppc
+        const double prefill = __dadd_rn(__ddiv_rn(__dmul_rn(__dmul_rn(in, L), pc), sp.speedup), __dmul_rn(ppm1, ppc));
+        // decode_latency (:35-40): out*L*dc*(1+slope*(tp-1))/tp + (pp-1)*ppc*out
+        const double pen = __dadd_rn(1.0, __dmul_rn(slope, static_cast<double>(sp.tp - 1)));
+        const double decode = __dadd_rn(
+            __ddiv_rn(__dmul_rn(__dmul_rn(__dmul_rn(out, L), dc), pen), static_cast<double>(sp.tp)),
+            __dmul_rn(__dmul_rn(ppm1, ppc), out));
+        const double svc = __dadd_rn(prefill, decode);  // request_service_time (:42-46)
+        // capacity (:74-82) and edge_capacity (:84-92)
+        const int64_t n = static_cast<int64_t>(floor(__ddiv_rn(__dmul_rn(span, static_cast<double>(sp.pp)), svc)));
+        const double per_req = __dmul_rn(__dadd_rn(in, out), static_cast<double>(kvb));
+        const double capd = floor(__ddiv_rn(static_cast<double>(sp.kv_budget), per_req));
+        const int64_t e = capd >= static_cast<double>(n) ? n : static_cast<int64_t>(capd);
+        t.n[idx] = n;
+        t.e[idx] = e;
+        t.latency[idx] = svc;
+    }
+}
+
+// ----------------------------------------------------------------- K0b ----
+__global__ void k_normalize_rows(ShapeTables t) {
+    const int J = t.J;
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < t.num_shapes; s += gridDim.x * blockDim.x) {
+        const int64_t *n = t.n + static_cast<int64_t>(s) * J;
+        const int64_t *e = t.e + static_cast<int64_t>(s) * J;
+        int64_t *unit = t.unit + static_cast<int64_t>(s) * J;
+        int32_t *cap = t.cap + static_cast<int64_t>(s) * J;
+        // normalize (flowassign.cpp:31-46) with checked_lcm (:22-27)
+        int64_t m = 1;
+        bool overflow = false;
+        for (int j = 0; j < J && !overflow; ++j) {
+            const int64_t nj = n[j];
+            if (nj <= 0) continue;
+            const int64_t g = gcd64(m, nj);
+            const int64_t q = m / g;
+            if (q > kLcmLimit / nj) overflow = true;
+            else m = q * nj;
+        }
+        if (overflow) m = kLcmLimit;  // normalize_or_scale fallback (:48-62)
+        t.M[s] = m;
+        t.scaled[s] = overflow ? 1 : 0;
+        uint8_t ord[kMaxJ];
+        int ol = 0;
+        for (int j = 0; j < J; ++j) {
+            const int64_t nj = n[j];
+            int64_t u = 0;
+            if (nj > 0) u = overflow ? (kLcmLimit + nj - 1) / nj : m / nj;
+            unit[j] = u;
+            // make_instance (:278-292): cap = min(e, n, M/unit) where unit > 0
+            int64_t c = 0;
+            if (u > 0) {
+                c = e[j] < nj ? e[j] : nj;
+                const int64_t byb = m / u;
+                c = c < byb ? c : byb;
+            }
+            if (c > 0) {
+                cap[j] = c > 0x7fffffffll ? 0x7fffffff : static_cast<int32_t>(c);
+                // stable insertion by ascending unit (std::stable_sort, :289)
+                int pos = ol;
+                while (pos > 0 && unit[ord[pos - 1]] > u) {
+                    ord[pos] = ord[pos - 1];
+                    --pos;
+                }
+                ord[pos] = static_cast<uint8_t>(j);
+                ++ol;
+            } else {
+                cap[j] = 0;
+            }
+        }
+        for (int i = 0; i < kMaxJ; ++i) t.order[s * kMaxJ + i] = i < ol ? ord[i] : 0;
+        t.olen[s] = static_cast<uint8_t>(ol);
+    }
+}
+
+// ------------------------------------------------------- plan resolution --
+// Largest p with prefix[p] <= g (skips empty partitions automatically).
+__device__ __forceinline__ int64_t find_partition(const SpaceTables &sp, uint64_t g) {
+    int64_t lo = 0, hi = sp.num_parts - 1;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (__ldg(sp.prefix + mid) <= g) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ uint64_t shard_rank(const PlanSource &src, uint64_t li) {
+    const uint64_t c = li / src.chunk;
+    return (c * static_cast<uint64_t>(src.world) + static_cast<uint64_t>(src.rank)) * src.chunk + (li - c * src.chunk);
+}
+
+// Unrank a non-decreasing pick sequence of length len over [0, q) (lex order).
+__device__ __forceinline__ void unrank_run(uint64_t r, int len, int q, uint8_t *out) {
+    int prev = 0;
+    for (int pos = 0; pos < len; ++pos) {
+        const int rem = len - pos - 1;
+        for (int v = prev; v < q; ++v) {
+            const uint64_t c = c_binom[rem + (q - v) - 1][(q - v) - 1];
+            if (r < c) {
+                out[pos] = static_cast<uint8_t>(v);
+                prev = v;
+                break;
+            }
+            r -= c;
+        }
+    }
+}
+
+__device__ __forceinline__ uint64_t div_small(uint64_t a, uint64_t b) {
+    if ((a >> 32) == 0 && (b >> 32) == 0) return static_cast<uint32_t>(a) / static_cast<uint32_t>(b);
+    return a / b;
+}
+
+// ------------------------------------------------------------------- K1 ---
+// Group of G lanes evaluates one plan; lane gl owns replicas k = gl + G*kk.
+template <int G, int KPL>
+struct Group {
+    static constexpr int RMAX = G * KPL;
+    unsigned mask;
+    int gl, base;
+    __device__ __forceinline__ Group() {
+        const int lane = threadIdx.x & 31;
+        gl = lane & (G - 1);
+        base = lane - gl;
+        mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << base);
+    }
+    __device__ __forceinline__ void sync() const { __syncwarp(mask); }
+    __device__ __forceinline__ uint32_t ballot(bool p) const {
+        const uint32_t b = __ballot_sync(mask, p);
+        return (G == 32) ? b : ((b >> base) & ((1u << G) - 1u));
+    }
+    template <class T>
+    __device__ __forceinline__ T bcast(T v, int src) const { return __shfl_sync(mask, v, src, G); }
+    __device__ __forceinline__ uint32_t sum(uint32_t v) const { return __reduce_add_sync(mask, v); }
+    // inclusive prefix sum, saturating at `sat`
+    __device__ __forceinline__ uint32_t scan_sat(uint32_t v, uint32_t sat) const {
+#pragma unroll
+        for (int d = 1; d < G; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(mask, v, d, G);
+            if (gl >= d) v = min(v + o, sat);
+        }
+        return v;
+    }
+};
+
+struct SmemShapes {
+    const int64_t *M;
+    const int64_t *unit;
+    const int32_t *cap;
+    const uint8_t *order;
+    const uint8_t *olen;
+    const uint8_t *pp;
+};
+
+template <int G, int KPL>
+__global__ void __launch_bounds__(256) k_plan_eval(ShapeTables t, SpaceTables sp, KeyLayout key, PlanSource src,
+                                                   PlanOutputs out, SolveParams prm, int skip_exact) {
+    using Grp = Group<G, KPL>;
+    constexpr int RMAX = Grp::RMAX;
+    constexpr int GPB = 256 / G;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int S = t.num_shapes, J = prm.J;
+
+    // ---- stage the shape tables (SoA) into shared memory ----
+    int64_t *sM = reinterpret_cast<int64_t *>(smem);
+    int64_t *sUnit = sM + S;
+    int32_t *sCap = reinterpret_cast<int32_t *>(sUnit + S * J);
+    uint8_t *sOrder = reinterpret_cast<uint8_t *>(sCap + S * J);
+    uint8_t *sOlen = sOrder + S * kMaxJ;
+    uint8_t *sPP = sOlen + S;
+    size_t off = (reinterpret_cast<uintptr_t>(sPP + S) - reinterpret_cast<uintptr_t>(smem) + 15) & ~size_t(15);
+    for (int i = threadIdx.x; i < S; i += blockDim.x) {
+        sM[i] = t.M[i];
+        sOlen[i] = t.olen[i];
+        sPP[i] = t.pp[i];
+    }
+    for (int i = threadIdx.x; i < S * J; i += blockDim.x) {
+        sUnit[i] = t.unit[i];
+        sCap[i] = t.cap[i];
+    }
+    for (int i = threadIdx.x; i < S * kMaxJ; i += blockDim.x) sOrder[i] = t.order[i];
+
+    // ---- per-group scratch ----
+    const int gib = threadIdx.x / G;
+    const size_t per_group = ((size_t)J * RMAX * 4 + kMaxJ * 4 + kMaxJ * KPL * 4 + RMAX + 15) & ~size_t(15);
+    unsigned char *gs = smem + off + per_group * gib;
+    int32_t *xs = reinterpret_cast<int32_t *>(gs);              // [J][RMAX]
+    int32_t *lam = xs + J * RMAX;                               // [kMaxJ]
+    uint32_t *Am = reinterpret_cast<uint32_t *>(lam + kMaxJ);   // [kMaxJ][KPL]
+    uint8_t *pick = reinterpret_cast<uint8_t *>(Am + kMaxJ * KPL);  // [RMAX]
+    unsigned long long *blk_best = reinterpret_cast<unsigned long long *>(smem + off + per_group * GPB);
+    __syncthreads();
+
+    const Grp g;
+    uint64_t best = kNoKey;
+    const uint64_t ngroups = static_cast<uint64_t>(gridDim.x) * GPB;
+
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * GPB + gib; i < src.count; i += ngroups) {
+        // ---- resolve the plan ----
+        int R;
+        int shp[KPL];
+        int64_t part = 0;
+        uint64_t local = 0;
+        const int64_t *lam_src = prm.lambda;
+        if (src.mode == 2) {
+            const uint64_t li = src.first + i;
+            R = src.list_R[li];
+            const int32_t *ls = src.list_shapes + src.list_off[li];
+#pragma unroll
+            for (int kk = 0; kk < KPL; ++kk) {
+                const int k = g.gl + G * kk;
+                shp[kk] = k < R ? ls[k] : 0;
+            }
+            if (src.list_lambda) lam_src = src.list_lambda + li * J;
+            if (skip_exact) {
+                int64_t tot = 0;
+                for (int j = 0; j < J; ++j) tot += lam_src[j];
+                if (tot <= prm.exact_demand_limit && R * J <= prm.exact_cell_limit) continue;
+            }
+        } else {
+            const uint64_t gr = src.mode == 0 ? shard_rank(src, src.first + i) : src.ranks[src.first + i];
+            part = find_partition(sp, gr);
+            if (skip_exact && sp.exact[part]) continue;
+            local = gr - __ldg(sp.prefix + part);
+            R = sp.R[part];
+            const int ro = sp.rep_off[part], runo = sp.run_off[part], nr = sp.nruns[part];
+            for (int ri = g.gl; ri < nr; ri += G) {
+                const uint64_t w = sp.run_weight[runo + ri], c = sp.run_count[runo + ri];
+                uint64_t rr = div_small(local, w);
+                rr = rr - div_small(rr, c) * c;
+                const int q = sp.run_q[runo + ri], len = sp.run_len[runo + ri], st = sp.run_start[runo + ri];
+                if (len == 1) pick[st] = static_cast<uint8_t>(rr);
+                else unrank_run(rr, len, q, pick + st);
+            }
+            g.sync();
+#pragma unroll
+            for (int kk = 0; kk < KPL; ++kk) {
+                const int k = g.gl + G * kk;
+                shp[kk] = k < R ? sp.cl_shape[sp.rep_list[ro + k] * kMaxCand + pick[k]] : 0;
+            }
+        }
+
+        // ---- init: lam, x = 0, mrem = M ----
+        for (int j = g.gl; j < J; j += G) lam[j] = static_cast<int32_t>(lam_src[j]);
+        int64_t mrem[KPL];
+#pragma unroll
+        for (int kk = 0; kk < KPL; ++kk) {
+            const int k = g.gl + G * kk;
+            mrem[kk] = sM[shp[kk]];
+            for (int j = 0; j < J; ++j) xs[j * RMAX + k] = 0;
+        }
+        g.sync();
+
+        // ---- greedy_fill (flowassign.cpp:393-406), speculative-parallel ----
+        // Each replica >= k0 fills as if alone (its takes depend on lam only
+        // through min(., lam)); the first replica whose prefix demand exceeds
+        // lam for some class is the first one lam actually binds: commit the
+        // replicas before it, recompute it exactly, repeat.  Identical to the
+        // sequential fill; each round exhausts at least one class.
+        int k0 = 0;
+        while (k0 < R) {
+#pragma unroll
+            for (int kk = 0; kk < KPL; ++kk) {
+                const int k = g.gl + G * kk;
+                if (k >= k0 && k < R) {
+                    const int s = shp[kk];
+                    int64_t m = sM[s];
+                    for (int j = 0; j < J; ++j) xs[j * RMAX + k] = 0;
+                    const int ol = sOlen[s];
+                    for (int pos = 0; pos < ol; ++pos) {
+                        const int j = sOrder[s * kMaxJ + pos];
+                        const int64_t u = sUnit[s * J + j];
+                        const int32_t a = min(sCap[s * J + j], lam[j]);
+                        int32_t tk = a;
+                        if (static_cast<int64_t>(a) * u > m) tk = static_cast<int32_t>(m / u);
+                        xs[j * RMAX + k] = tk;
+                        m -= static_cast<int64_t>(tk) * u;
+                    }
+                    mrem[kk] = m;
+                }
+            }
+            g.sync();
+            bool bad[KPL];
+#pragma unroll
+            for (int kk = 0; kk < KPL; ++kk) bad[kk] = false;
+            for (int j = 0; j < J; ++j) {
+                const uint32_t L = static_cast<uint32_t>(lam[j]);
+                uint32_t carry = 0;
+#pragma unroll
+                for (int kk = 0; kk < KPL; ++kk) {
+                    const int k = g.gl + G * kk;
+                    const uint32_t v = (k >= k0 && k < R) ? static_cast<uint32_t>(xs[j * RMAX + k]) : 0u;
+                    const uint32_t sc = min(g.scan_sat(v, 0x80000000u) + carry, 0x80000000u);
+                    bad[kk] |= sc > L;
+                    carry = g.bcast(sc, G - 1);
+                }
+            }
+            int kstar = R;
+#pragma unroll
+            for (int kk = KPL - 1; kk >= 0; --kk) {
+                const uint32_t b = g.ballot(bad[kk]);
+                if (b) kstar = __ffs(b) - 1 + G * kk;
+            }
+            // commit lam for [k0, kstar)
+            for (int j = 0; j < J; ++j) {
+                uint32_t part_sum = 0;
+#pragma unroll
+                for (int kk = 0; kk < KPL; ++kk) {
+                    const int k = g.gl + G * kk;
+                    if (k >= k0 && k < kstar) part_sum += static_cast<uint32_t>(xs[j * RMAX + k]);
+                }
+                part_sum = g.sum(part_sum);
+                if (g.gl == 0) lam[j] -= static_cast<int32_t>(part_sum);
+            }
+            g.sync();
+            if (kstar < R) {
+#pragma unroll
+                for (int kk = 0; kk < KPL; ++kk) {
+                    if (g.gl + G * kk == kstar) {
+                        const int s = shp[kk];
+                        int64_t m = sM[s];
+                        for (int j = 0; j < J; ++j) xs[j * RMAX + kstar] = 0;
+                        const int ol = sOlen[s];
+                        for (int pos = 0; pos < ol; ++pos) {
+                            const int j = sOrder[s * kMaxJ + pos];
+                            const int64_t u = sUnit[s * J + j];
+                            const int32_t a = min(sCap[s * J + j], lam[j]);
+                            int32_t tk = a;
+                            if (static_cast<int64_t>(a) * u > m) tk = static_cast<int32_t>(m / u);
+                            xs[j * RMAX + kstar] = tk;
+                            lam[j] -= tk;
+                            m -= static_cast<int64_t>(tk) * u;
+                        }
+                        mrem[kk] = m;
+                    }
+                }
+                g.sync();
+            }
+            k0 = kstar + 1;
+        }
+
+        // ---- exchange_improve (flowassign.cpp:411-448) ----
+        // A[j2] = replicas able to take one more class-j2 request directly.
+        // (j, k) has a move iff direct (mrem >= unit) or some held j2 != j with
+        // A[j2]\{k} non-empty and unit[k][j2] >= unit[k][j] - mrem[k]; the
+        // first such (j, k) in (j asc, k asc) order, then the first j2 asc,
+        // then the first k2 asc, is exactly the reference's first move.
+        uint32_t held[KPL];
+#pragma unroll
+        for (int kk = 0; kk < KPL; ++kk) {
+            const int k = g.gl + G * kk;
+            uint32_t h = 0;
+            if (k < R)
+                for (int j = 0; j < J; ++j) h |= (xs[j * RMAX + k] > 0 ? 1u : 0u) << j;
+            held[kk] = h;
+        }
+        for (;;) {
+            // masks A
+            for (int j = 0; j < J; ++j) {
+#pragma unroll
+                for (int kk = 0; kk < KPL; ++kk) {
+                    const int k = g.gl + G * kk;
+                    bool p = false;
+                    if (k < R) {
+                        const int s = shp[kk];
+                        const int64_t u = sUnit[s * J + j];
+                        p = u > 0 && xs[j * RMAX + k] < sCap[s * J + j] && mrem[kk] >= u;
+                    }
+                    const uint32_t b = g.ballot(p);
+                    if (g.gl == 0) Am[j * KPL + kk] = b;
+                }
+            }
+            g.sync();
+            // top-2 eligible unit per owned replica
+            int64_t e1[KPL], e2[KPL];
+            int e1j[KPL];
+#pragma unroll
+            for (int kk = 0; kk < KPL; ++kk) {
+                e1[kk] = -1;
+                e2[kk] = -1;
+                e1j[kk] = -1;
+                uint32_t hb = held[kk];
+                while (hb) {
+                    const int j2 = __ffs(hb) - 1;
+                    hb &= hb - 1;
+                    uint32_t any = 0;
+#pragma unroll
+                    for (int k2 = 0; k2 < KPL; ++k2) {
+                        uint32_t w = Am[j2 * KPL + k2];
+                        if (k2 == kk) w &= ~(1u << g.gl);
+                        any |= w;
+                    }
+                    if (any) {
+                        const int64_t u = sUnit[shp[kk] * J + j2];
+                        if (u > e1[kk]) {
+                            e2[kk] = e1[kk];
+                            e1[kk] = u;
+                            e1j[kk] = j2;
+                        } else if (u > e2[kk]) {
+                            e2[kk] = u;
+                        }
+                    }
+                }
+            }
+            // first (j, k) with a move
+            int jf = -1, kf = -1;
+            for (int j = 0; j < J && jf < 0; ++j) {
+                if (lam[j] <= 0) continue;
+#pragma unroll
+                for (int kk = KPL - 1; kk >= 0; --kk) {
+                    const int k = g.gl + G * kk;
+                    bool p = false;
+                    if (k < R) {
+                        const int s = shp[kk];
+                        const int64_t u = sUnit[s * J + j];
+                        if (u > 0 && xs[j * RMAX + k] < sCap[s * J + j]) {
+                            if (mrem[kk] >= u) p = true;
+                            else p = (e1j[kk] == j ? e2[kk] : e1[kk]) >= u - mrem[kk];
+                        }
+                    }
+                    const uint32_t b = g.ballot(p);
+                    if (b) {
+                        kf = __ffs(b) - 1 + G * kk;
+                        jf = j;
+                    }
+                }
+            }
+            if (jf < 0) break;
+            // owner of kf picks the move
+            const int ogl = kf & (G - 1);
+            int j2 = -1, k2 = -1;
+            if (g.gl == ogl) {
+#pragma unroll
+                for (int kk = 0; kk < KPL; ++kk) {
+                    if (g.gl + G * kk != kf) continue;
+                    const int s = shp[kk];
+                    const int64_t u = sUnit[s * J + jf];
+                    if (mrem[kk] < u) {
+                        for (int jj = 0; jj < J && j2 < 0; ++jj) {
+                            if (jj == jf || xs[jj * RMAX + kf] <= 0) continue;
+                            if (mrem[kk] + sUnit[s * J + jj] < u) continue;
+#pragma unroll
+                            for (int k3 = 0; k3 < KPL; ++k3) {
+                                uint32_t w = Am[jj * KPL + k3];
+                                if (k3 == kk) w &= ~(1u << g.gl);
+                                if (w && k2 < 0) {
+                                    k2 = __ffs(w) - 1 + G * k3;
+                                    j2 = jj;
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+            j2 = g.bcast(j2, ogl);
+            k2 = g.bcast(k2, ogl);
+            // apply
+#pragma unroll
+            for (int kk = 0; kk < KPL; ++kk) {
+                const int k = g.gl + G * kk;
+                const int s = shp[kk];
+                if (k == kf) {
+                    const int64_t u = sUnit[s * J + jf];
+                    xs[jf * RMAX + kf] += 1;
+                    mrem[kk] -= u;
+                    held[kk] |= 1u << jf;
+                    lam[jf] -= 1;
+                    if (j2 >= 0) {
+                        const int32_t nv = xs[j2 * RMAX + kf] - 1;
+                        xs[j2 * RMAX + kf] = nv;
+                        mrem[kk] += sUnit[s * J + j2];
+                        if (nv == 0) held[kk] &= ~(1u << j2);
+                    }
+                }
+                if (j2 >= 0 && k == k2) {
+                    xs[j2 * RMAX + k2] += 1;
+                    mrem[kk] -= sUnit[s * J + j2];
+                    held[kk] |= 1u << j2;
+                }
+            }
+            g.sync();
+        }
+
+        // ---- objective, sum_pp, key / outputs ----
+        uint32_t served = 0;
+        for (int j = g.gl; j < J; j += G) served += static_cast<uint32_t>(lam_src[j] - lam[j]);
+        uint32_t spp = 0;
+#pragma unroll
+        for (int kk = 0; kk < KPL; ++kk)
+            if (g.gl + G * kk < R) spp += sPP[shp[kk]];
+        served = g.sum(served);
+        spp = g.sum(spp);
+        if (out.objective && g.gl == 0) out.objective[i] = served;
+        if (out.sum_pp && g.gl == 0) out.sum_pp[i] = static_cast<int32_t>(spp);
+        if (out.x) {
+#pragma unroll
+            for (int kk = 0; kk < KPL; ++kk) {
+                const int k = g.gl + G * kk;
+                if (k < R) {
+                    for (int j = 0; j < J; ++j)
+                        out.x[(i * out.rmax + k) * J + j] = xs[j * RMAX + k];
+                    if (out.used) out.used[i * out.rmax + k] = sM[shp[kk]] - mrem[kk];
+                }
+            }
+        }
+        if (out.best_key) {
+            const uint64_t kv = ((key.obj_max - served) << key.sh_obj) |
+                                (static_cast<uint64_t>(part) << key.sh_part) |
+                                (static_cast<uint64_t>(spp) << key.sh_spp) | local;
+            best = kv < best ? kv : best;
+        }
+        g.sync();
+    }
+
+    // ---- CTA argmin -> global atomicMin ----
+    if (out.best_key) {
+        if (g.gl == 0) blk_best[gib] = best;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long b = blk_best[0];
+            for (int q = 1; q < GPB; ++q) b = blk_best[q] < b ? blk_best[q] : b;
+            if (b != kNoKey) atomicMin(reinterpret_cast<unsigned long long *>(out.best_key), b);
+        }
+    }
+}
+
+template <int G, int KPL>
+size_t plan_eval_smem(int S, int J) {
+    constexpr int RMAX = G * KPL;
+    constexpr int GPB = 256 / G;
+    size_t shapes = (size_t)S * 8 + (size_t)S * J * 8 + (size_t)S * J * 4 + (size_t)S * kMaxJ + 2 * (size_t)S;
+    shapes = (shapes + 15) & ~size_t(15);
+    const size_t per_group = ((size_t)J * RMAX * 4 + kMaxJ * 4 + kMaxJ * KPL * 4 + RMAX + 15) & ~size_t(15);
+    return shapes + per_group * GPB + GPB * 8;
+}
+
+template <int G, int KPL>
+int run_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key, const PlanSource &src,
+                  const PlanOutputs &out, const SolveParams &prm, int sm_count, int skip_exact,
+                  cudaStream_t stream, uint64_t *launches) {
+    const size_t smem = plan_eval_smem<G, KPL>(t.num_shapes, prm.J);
+    auto kern = k_plan_eval<G, KPL>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return static_cast<int>(e);
+    }
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
+    if (e != cudaSuccess) return static_cast<int>(e);
+    if (per_sm < 1) return static_cast<int>(cudaErrorInvalidConfiguration);
+    constexpr int GPB = 256 / G;
+    uint64_t need = (src.count + GPB - 1) / GPB;
+    uint64_t grid = static_cast<uint64_t>(per_sm) * sm_count;
+    if (need < grid) grid = need;
+    if (grid == 0) return 0;
+    kern<<<static_cast<unsigned>(grid), 256, smem, stream>>>(t, sp, key, src, out, prm, skip_exact);
+    if (launches) ++*launches;
+    return check(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------- K4 ---
+// Exact branch-and-bound, thread per plan (flowassign.cpp:296-369).  State
+// in local memory (R*J <= kMaxExactCells); node counting and first-found-best
+// semantics identical to the recursive reference.
+struct ExactState {
+    int R, J;
+    int shp[kMaxExactCells];
+    int32_t x[kMaxExactCells];
+    int32_t bx[kMaxExactCells];
+    int64_t lam[kMaxJ];
+    int64_t mrem[kMaxExactCells];
+};
+
+__device__ int64_t suffix_bound(const ShapeTables &t, const ExactState &st, int k, int pos, const int64_t *lam_in,
+                                int64_t mr) {
+    // greedy_suffix (flowassign.cpp:298-311) on a private copy of lam
+    int64_t lam[kMaxJ];
+    for (int j = 0; j < st.J; ++j) lam[j] = lam_in[j];
+    const int s = st.shp[k];
+    const int ol = t.olen[s];
+    int64_t cnt = 0;
+    for (int i = pos; i < ol; ++i) {
+        const int j = t.order[s * kMaxJ + i];
+        const int64_t u = t.unit[s * st.J + j];
+        int64_t tk = t.cap[s * st.J + j];
+        if (lam[j] < tk) tk = lam[j];
+        const int64_t byb = mr / u;
+        if (byb < tk) tk = byb;
+        if (tk > 0) {
+            cnt += tk;
+            lam[j] -= tk;
+            mr -= tk * u;
+        }
+    }
+    return cnt;
+}
+
+__global__ void __launch_bounds__(128) k_plan_exact(ShapeTables t, SpaceTables sp, KeyLayout key, PlanSource src,
+                                                    PlanOutputs out, SolveParams prm) {
+    const int J = prm.J;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < src.count;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        ExactState st;
+        st.J = J;
+        int64_t part = 0;
+        uint64_t local = 0, gr = 0;
+        const int64_t *lam_src = prm.lambda;
+        if (src.mode == 2) {
+            const uint64_t li = src.first + i;
+            st.R = src.list_R[li];
+            if (st.R * J > kMaxExactCells) continue;
+            const int32_t *ls = src.list_shapes + src.list_off[li];
+            for (int k = 0; k < st.R; ++k) st.shp[k] = ls[k];
+            if (src.list_lambda) lam_src = src.list_lambda + li * J;
+            int64_t tot = 0;
+            for (int j = 0; j < J; ++j) tot += lam_src[j];
+            if (!(tot <= prm.exact_demand_limit && st.R * J <= prm.exact_cell_limit)) continue;
+            gr = li;
+        } else {
+            gr = src.mode == 0 ? shard_rank(src, src.first + i) : src.ranks[src.first + i];
+            part = find_partition(sp, gr);
+            if (!sp.exact[part]) continue;
+            local = gr - sp.prefix[part];
+            st.R = sp.R[part];
+            const int ro = sp.rep_off[part], runo = sp.run_off[part], nr = sp.nruns[part];
+            uint8_t pick[kMaxExactCells];
+            for (int ri = 0; ri < nr; ++ri) {
+                const uint64_t w = sp.run_weight[runo + ri], c = sp.run_count[runo + ri];
+                const uint64_t rr = (local / w) % c;
+                unrank_run(rr, sp.run_len[runo + ri], sp.run_q[runo + ri], pick + sp.run_start[runo + ri]);
+            }
+            for (int k = 0; k < st.R; ++k) st.shp[k] = sp.cl_shape[sp.rep_list[ro + k] * kMaxCand + pick[k]];
+        }
+        const int R = st.R;
+        for (int j = 0; j < J; ++j) st.lam[j] = lam_src[j];
+        for (int k = 0; k < R; ++k) st.mrem[k] = t.M[st.shp[k]];
+        for (int c = 0; c < R * J; ++c) {
+            st.x[c] = 0;
+            st.bx[c] = 0;
+        }
+        // explicit DFS stack: one frame per (k, pos) being iterated over v
+        int fk[kMaxExactCells + 1], fpos[kMaxExactCells + 1], fj[kMaxExactCells + 1];
+        int64_t fv[kMaxExactCells + 1];
+        int depth = 0;
+        int64_t count = 0, bestc = -1, nodes = 0;
+        bool aborted = false;
+        int k = 0, pos = 0;
+        bool calling = true;  // true: enter visit(k, pos); false: return to frame on top
+        while (true) {
+            if (calling) {
+                if (++nodes > prm.node_budget) {
+                    aborted = true;
+                    break;
+                }
+                if (k == R) {
+                    if (count > bestc) {
+                        bestc = count;
+                        for (int c = 0; c < R * J; ++c) st.bx[c] = st.x[c];
+                    }
+                    calling = false;
+                    continue;
+                }
+                const int s = st.shp[k];
+                if (pos == t.olen[s]) {
+                    ++k;
+                    pos = 0;
+                    continue;  // tail call visit(k+1, 0)
+                }
+                int64_t lam_total = 0;
+                for (int j = 0; j < J; ++j) lam_total += st.lam[j];
+                int64_t bound = suffix_bound(t, st, k, pos, st.lam, st.mrem[k]);
+                for (int k2 = k + 1; k2 < R; ++k2) bound += suffix_bound(t, st, k2, 0, st.lam, t.M[st.shp[k2]]);
+                if (count + (lam_total < bound ? lam_total : bound) <= bestc) {
+                    calling = false;
+                    continue;
+                }
+                const int j = t.order[s * kMaxJ + pos];
+                const int64_t u = t.unit[s * J + j];
+                int64_t hi = t.cap[s * J + j];
+                if (st.lam[j] < hi) hi = st.lam[j];
+                if (st.mrem[k] / u < hi) hi = st.mrem[k] / u;
+                fk[depth] = k;
+                fpos[depth] = pos;
+                fj[depth] = j;
+                fv[depth] = hi;
+                ++depth;
+                st.x[k * J + j] = static_cast<int32_t>(hi);
+                st.lam[j] -= hi;
+                st.mrem[k] -= hi * u;
+                count += hi;
+                pos = pos + 1;
+                continue;  // call visit(k, pos+1)
+            }
+            // return into the frame on top of the stack
+            if (depth == 0) break;
+            const int d = depth - 1;
+            const int kk = fk[d], j = fj[d];
+            const int64_t u = t.unit[st.shp[kk] * J + j];
+            int64_t v = fv[d];
+            count -= v;
+            st.mrem[kk] += v * u;
+            st.lam[j] += v;
+            st.x[kk * J + j] = 0;
+            if (v == 0) {
+                --depth;  // loop exhausted: return from this visit
+                continue;
+            }
+            --v;
+            fv[d] = v;
+            st.x[kk * J + j] = static_cast<int32_t>(v);
+            st.lam[j] -= v;
+            st.mrem[kk] -= v * u;
+            count += v;
+            k = kk;
+            pos = fpos[d] + 1;
+            calling = true;
+        }
+        if (aborted) {
+            if (out.aborted) {
+                const unsigned slot = atomicAdd(out.aborted_n, 1u);
+                out.aborted[slot] = gr;
+            }
+            continue;
+        }
+        int spp = 0;
+        for (int kk = 0; kk < R; ++kk) spp += t.pp[st.shp[kk]];
+        if (out.objective) out.objective[i] = bestc;
+        if (out.sum_pp) out.sum_pp[i] = spp;
+        if (out.x) {
+            for (int kk = 0; kk < R; ++kk) {
+                int64_t used = 0;
+                for (int j = 0; j < J; ++j) {
+                    out.x[(i * out.rmax + kk) * J + j] = st.bx[kk * J + j];
+                    used += static_cast<int64_t>(st.bx[kk * J + j]) * t.unit[st.shp[kk] * J + j];
+                }
+                if (out.used) out.used[i * out.rmax + kk] = used;
+            }
+        }
+        if (out.best_key) {
+            const uint64_t kv = ((key.obj_max - static_cast<uint64_t>(bestc)) << key.sh_obj) |
+                                (static_cast<uint64_t>(part) << key.sh_part) |
+                                (static_cast<uint64_t>(spp) << key.sh_spp) | local;
+            atomicMin(reinterpret_cast<unsigned long long *>(out.best_key), kv);
+        }
+    }
+}
+
+// ------------------------------------------------------------------- K2 ---
+constexpr int kSwMaxDev = 256;   // device slots per deployment pair
+constexpr int kSwMaxCuts = 1024; // 2 * (src + dst ranges), padded to pow2
+
+__device__ __forceinline__ double link_bw(const SwitchDeps &d, int s, int t) {
+    return d.machine[s] >= 0 && d.machine[s] == d.machine[t] ? d.intra_bw : d.inter_bw;
+}
+
+__global__ void __launch_bounds__(256) k_switch_cost(SwitchDeps d, SwitchOut o) {
+    __shared__ uint64_t sB[2][kSwMaxDev], sE[2][kSwMaxDev];
+    __shared__ uint64_t cuts[kSwMaxCuts];
+    __shared__ int ncuts_s;
+    __shared__ double wmax[8];
+    __shared__ unsigned long long wbytes[8];
+    __shared__ int wstatus[8];
+    const int pair = blockIdx.x;
+    const int ND = d.num_devices;
+    const int deps[2] = {0, pair + 1};
+    // ---- layouts (switchplan.cpp:40-63): one slice per device slot ----
+    for (int i = threadIdx.x; i < 2 * kSwMaxDev; i += blockDim.x) {
+        sB[i / kSwMaxDev][i % kSwMaxDev] = 0;
+        sE[i / kSwMaxDev][i % kSwMaxDev] = 0;
+    }
+    __syncthreads();
+    for (int w = 0; w < 2; ++w) {
+        const int r0 = d.dep_rep_off[deps[w]], r1 = d.dep_rep_off[deps[w] + 1];
+        for (int r = r0; r < r1; ++r) {
+            const uint64_t tp = d.rep_tp[r], pp = d.rep_pp[r];
+            const int dev0 = d.rep_dev_off[r];
+            const int nd = d.rep_dev_off[r + 1] - dev0;
+            for (int q = threadIdx.x; q < nd; q += blockDim.x) {
+                const uint64_t s = q / tp, i = q % tp;
+                if (s >= pp) continue;
+                const uint64_t sb = d.P * s / pp, se = d.P * (s + 1) / pp, len = se - sb;
+                const int slot = d.rep_devs[dev0 + q];
+                sB[w][slot] = sb + len * i / tp;
+                sE[w][slot] = sb + len * (i + 1) / tp;
+            }
+        }
+    }
+    __syncthreads();
+    // ---- cut points (:70-85): sorted unique begin/end of non-empty ranges ----
+    int P2 = 1;
+    while (P2 < 4 * ND) P2 <<= 1;
+    for (int i = threadIdx.x; i < P2; i += blockDim.x) {
+        uint64_t v = ~0ull;
+        if (i < 4 * ND) {
+            const int w = (i / ND) >> 1, slot = i % ND, be = (i / ND) & 1;
+            if (sE[w][slot] > sB[w][slot]) v = be ? sE[w][slot] : sB[w][slot];
+        }
+        cuts[i] = v;
+    }
+    __syncthreads();
+    for (int kz = 2; kz <= P2; kz <<= 1) {
+        for (int jz = kz >> 1; jz > 0; jz >>= 1) {
+            for (int i = threadIdx.x; i < P2; i += blockDim.x) {
+                const int ixj = i ^ jz;
+                if (ixj > i) {
+                    const bool up = (i & kz) == 0;
+                    const uint64_t a = cuts[i], b = cuts[ixj];
+                    if ((a > b) == up) {
+                        cuts[i] = b;
+                        cuts[ixj] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    if (threadIdx.x == 0) {
+        int m = 0;
+        for (int i = 0; i < P2 && cuts[i] != ~0ull; ++i)
+            if (m == 0 || cuts[i] != cuts[m - 1]) cuts[m++] = cuts[i];
+        ncuts_s = m;
+        if (o.detail_cuts) {
+            for (int i = 0; i < m && i <= o.max_frags; ++i) o.detail_cuts[i] = cuts[i];
+            *o.detail_ncuts = m;
+        }
+    }
+    __syncthreads();
+    const int ncuts = ncuts_s;
+    // ---- greedy_plan (:86-128): warp per target, lane per source replica ----
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    const int sr0 = d.dep_rep_off[0], nsr = d.dep_rep_off[1] - sr0;
+    double est = 0.0;
+    unsigned long long maxb = 0;
+    int status = 0;
+    for (int ts = warp; ts < ND; ts += nwarps) {
+        const uint64_t ta = sB[1][ts], tz = sE[1][ts];
+        if (tz <= ta) continue;  // target holds nothing in the new layout
+        const bool self_has = sE[0][ts] > sB[0][ts];
+        const uint64_t ha = sB[0][ts], hz = sE[0][ts];
+        // first fragment starting at ta
+        int f = 0;
+        {
+            int lo = 0, hi = ncuts - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (cuts[mid] < ta) lo = mid + 1;
+                else hi = mid;
+            }
+            f = lo;
+        }
+        // per-lane source replicas: lane owns replicas r = lane + 32*q
+        constexpr int QR = 4;  // up to 128 source replicas
+        int cur[QR], slot[QR];
+        uint64_t cend[QR], cbeg[QR], load[QR];
+#pragma unroll
+        for (int q = 0; q < QR; ++q) {
+            cur[q] = -1;
+            slot[q] = -1;
+            cend[q] = 0;
+            cbeg[q] = 0;
+            load[q] = 0;
+        }
+        for (; f + 1 < ncuts && cuts[f + 1] <= tz; ++f) {
+            const uint64_t fb = cuts[f], fe = cuts[f + 1];
+            if (self_has && ha <= fb && fe <= hz) continue;  // already held
+            unsigned long long bestkey = ~0ull;
+#pragma unroll
+            for (int q = 0; q < QR; ++q) {
+                const int r = lane + 32 * q;
+                if (r >= nsr) continue;
+                const int rep = sr0 + r;
+                const uint64_t tp = d.rep_tp[rep], pp = d.rep_pp[rep];
+                const int dev0 = d.rep_dev_off[rep];
+                const int nd = static_cast<int>(tp * pp);
+                // advance to the slice covering fb (slices ascend within a replica)
+                while (cur[q] + 1 < nd && (cend[q] <= fb || cend[q] == cbeg[q] || cur[q] < 0)) {
+                    // finalize the previous holder's link load toward this target
+                    if (load[q] > 0) {
+                        const double v = static_cast<double>(load[q]) / link_bw(d, slot[q], ts);
+                        est = v > est ? v : est;
+                        maxb = load[q] > maxb ? load[q] : maxb;
+                        load[q] = 0;
+                    }
+                    ++cur[q];
+                    const uint64_t s = cur[q] / tp, i = cur[q] % tp;
+                    const uint64_t sb = d.P * s / pp, se = d.P * (s + 1) / pp, len = se - sb;
+                    cbeg[q] = sb + len * i / tp;
+                    cend[q] = sb + len * (i + 1) / tp;
+                    slot[q] = d.rep_devs[dev0 + cur[q]];
+                }
+                if (cbeg[q] <= fb && fe <= cend[q] && cend[q] > cbeg[q]) {
+                    const bool intra = d.machine[slot[q]] >= 0 && d.machine[slot[q]] == d.machine[ts];
+                    const unsigned long long kv = (static_cast<unsigned long long>(!intra) << 63) |
+                                                  (static_cast<unsigned long long>(load[q]) << 16) |
+                                                  static_cast<unsigned long long>(slot[q]);
+                    bestkey = kv < bestkey ? kv : bestkey;
+                }
+            }
+#pragma unroll
+            for (int sft = 16; sft > 0; sft >>= 1) {
+                const unsigned long long other = __shfl_xor_sync(0xffffffffu, bestkey, sft);
+                bestkey = other < bestkey ? other : bestkey;
+            }
+            if (bestkey == ~0ull) {
+                status = 1;  // UnsourcedFragment (:99-103)
+                continue;
+            }
+            const int win = static_cast<int>(bestkey & 0xffff);
+#pragma unroll
+            for (int q = 0; q < QR; ++q)
+                if (lane + 32 * q < nsr && slot[q] == win && cbeg[q] <= fb && fe <= cend[q]) load[q] += fe - fb;
+            if (o.detail_src && lane == 0 && f < o.max_frags) o.detail_src[ts * o.max_frags + f] = win;
+        }
+#pragma unroll
+        for (int q = 0; q < QR; ++q) {
+            if (load[q] > 0) {
+                const double v = static_cast<double>(load[q]) / link_bw(d, slot[q], ts);
+                est = v > est ? v : est;
+                maxb = load[q] > maxb ? load[q] : maxb;
+            }
+        }
+    }
+    // estimate_time (:133-140): max over links
+#pragma unroll
+    for (int sft = 16; sft > 0; sft >>= 1) {
+        const double oe = __shfl_xor_sync(0xffffffffu, est, sft);
+        est = oe > est ? oe : est;
+        const unsigned long long ob = __shfl_xor_sync(0xffffffffu, maxb, sft);
+        maxb = ob > maxb ? ob : maxb;
+        status |= __shfl_xor_sync(0xffffffffu, status, sft);
+    }
+    if (lane == 0) {
+        wmax[warp] = est;
+        wbytes[warp] = maxb;
+        wstatus[warp] = status;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double e = 0.0;
+        unsigned long long b = 0;
+        int st = 0;
+        for (int w = 0; w < nwarps; ++w) {
+            e = wmax[w] > e ? wmax[w] : e;
+            b = wbytes[w] > b ? wbytes[w] : b;
+            st |= wstatus[w];
+        }
+        o.est[pair] = ncuts < 2 ? 0.0 : e;
+        o.max_bytes[pair] = b;
+        o.status[pair] = st;
+    }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------- launchers ---
+static bool g_binom_ready = false;
+
+static int ensure_binom() {
+    if (g_binom_ready) return 0;
+    static uint64_t h[kBinomN][kBinomK];
+    for (int n = 0; n < kBinomN; ++n)
+        for (int k = 0; k < kBinomK; ++k) {
+            unsigned __int128 r = 1;
+            if (k > n) {
+                r = 0;
+            } else {
+                for (int i = 1; i <= k; ++i) r = r * static_cast<unsigned>(n - k + i) / static_cast<unsigned>(i);
+            }
+            h[n][k] = r > ~0ull ? ~0ull : static_cast<uint64_t>(r);
+        }
+    cudaError_t e = cudaMemcpyToSymbol(c_binom, h, sizeof(h));
+    if (e != cudaSuccess) return static_cast<int>(e);
+    g_binom_ready = true;
+    return 0;
+}
+
+int launch_cost_tables(const ShapeTables &t, const double *cin, const double *cout, uint32_t num_layers,
+                       uint64_t kvb, double pc, double dc, double ppc, double slope, double span_s, void *stream) {
+    const int cells = t.num_shapes * t.J;
+    if (cells == 0) return 0;
+    const int block = 128, grid = (cells + block - 1) / block;
+    k_cost_cells<<<grid, block, 0, static_cast<cudaStream_t>(stream)>>>(t, cin, cout, num_layers, kvb, pc, dc, ppc,
+                                                                        slope, span_s);
+    return check(cudaGetLastError());
+}
+
+int launch_normalize_rows(const ShapeTables &t, void *stream) {
+    if (t.num_shapes == 0) return 0;
+    const int block = 128, grid = (t.num_shapes + block - 1) / block;
+    k_normalize_rows<<<grid, block, 0, static_cast<cudaStream_t>(stream)>>>(t);
+    return check(cudaGetLastError());
+}
+
+int launch_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key, const PlanSource &src,
+                     const PlanOutputs &out, const SolveParams &prm, int rmax, int sm_count, int skip_exact,
+                     void *stream, uint64_t *launches) {
+    if (int e = ensure_binom()) return e;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (src.count == 0) return 0;
+    if (rmax <= 8) return run_plan_eval<8, 1>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
+    if (rmax <= 16) return run_plan_eval<16, 1>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
+    if (rmax <= 32) return run_plan_eval<32, 1>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
+    if (rmax <= 64) return run_plan_eval<32, 2>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
+    if (rmax <= 128) return run_plan_eval<32, 4>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
+    return static_cast<int>(cudaErrorInvalidValue);
+}
+
+int launch_plan_exact(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key, const PlanSource &src,
+                      const PlanOutputs &out, const SolveParams &prm, int sm_count, void *stream,
+                      uint64_t *launches) {
+    if (int e = ensure_binom()) return e;
+    if (src.count == 0) return 0;
+    const int block = 128;
+    uint64_t grid = (src.count + block - 1) / block;
+    const uint64_t cap = static_cast<uint64_t>(sm_count) * 16;
+    if (grid > cap) grid = cap;
+    k_plan_exact<<<static_cast<unsigned>(grid), block, 0, static_cast<cudaStream_t>(stream)>>>(t, sp, key, src, out,
+                                                                                               prm);
+    if (launches) ++*launches;
+    return check(cudaGetLastError());
+}
+
+int launch_switch_cost(const SwitchDeps &d, const SwitchOut &o, void *stream, uint64_t *launches) {
+    if (d.count == 0) return 0;
+    if (d.num_devices > kSwMaxDev) return static_cast<int>(cudaErrorInvalidValue);
+    k_switch_cost<<<d.count, 256, 0, static_cast<cudaStream_t>(stream)>>>(d, o);
+    if (launches) ++*launches;
+    return check(cudaGetLastError());
+}
+
+}  // namespace oserve_gpu
