@@ -1,0 +1,367 @@
+"""bench.py — OServe scheduling round on B200 (BASELINE.json metric).
+
+Metric: candidate deployment plans evaluated/sec (+ end-to-end round latency)
+on config 5 (128-GPU cluster, 16 request classes, canonical plan space of
+13,090,221 plans) unless --config says otherwise.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1)
+
+One step = one full scheduling round over the whole plan space:
+  value : device-resident inputs; K1 (enumerate/unrank -> cost gather -> assign
+          -> objective -> argmin) on every rank's shard + NCCL all-reduce(min) of
+          the packed key; CUDA events on the launching stream, max over ranks;
+          L2 flushed (256 MiB write) between timed iterations.
+  e2e   : the public C-ABI from host buffers every step — enumerate + upload the
+          space tables, upload the workload, cost kernel K0, K1, all-reduce,
+          key D2H, decode, then the switching-cost plan (K2) from the current
+          (init_uniform) deployment to the winner, transfers D2H.
+The reference arm (--impl reference) times the reference's own CPU path
+(oracle/_ref: /root/reference/proj compiled unmodified; evaluate_deployment per
+plan, OpenMP over all host threads) on a bounded sample of the same space.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from paper_2602_12151_b200 import _abi as A  # noqa: E402
+from paper_2602_12151_b200 import core, workloads  # noqa: E402
+
+METRIC = "candidate deployment plans evaluated/sec and end-to-end scheduling-round latency"
+PEAK_LANE_OPS = None  # computed from the device: SMs x 128 lanes x max SM clock
+OPS_PER_CELL = 8      # lane-instructions per algorithmic cell-op (fixed)
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def init_dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    return rank, world, local
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+
+    def start(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx.append(float(p[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def load_work(name):
+    p = os.path.join(ROOT, "paper_2602_12151_b200", "configs", "work.json")
+    with open(p) as f:
+        return json.load(f)[name]
+
+
+def init_uniform(w: workloads.Workload, g_min: int) -> core.Deployment:
+    """init_uniform (deploysearch.cpp:120-136): D/g_min replicas of g_min
+    devices with the most tensor-parallel strategy (tp = g_min here)."""
+    R = w.cluster.device_count() // g_min
+    return core.canonical_deployment(w.cluster, [g_min] * R, [g_min] * R)
+
+
+def cpu_reference_sample(w: workloads.Workload, plans: int, target_s: float, threads: int):
+    """Time the reference CPU path (oracle/_ref; else the restatement) on a
+    bounded uniform sample of the same plan space.  Returns (plans/s, kind, n)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from pyoracle import Oracle, Problem, available
+    kind = "reference" if available("ref") else "port"
+    orc = Oracle("ref" if kind == "reference" else "port")
+    pr = Problem(w.cluster, w.model, w.types, w.lam, w.span_s, w.params)
+    rng = np.random.default_rng(2602)
+    n = 256
+    t = 0.0
+    while True:  # grow the sample until it takes ~target_s
+        ranks = rng.integers(0, plans, n).astype(np.uint64)
+        t0 = time.perf_counter()
+        orc.evaluate_ranks(pr, w.space_mode, ranks, w.space_sizes, threads=threads)
+        t = time.perf_counter() - t0
+        if t >= target_s / 4 or n >= plans:
+            break
+        n = min(plans, int(n * max(2.0, (target_s / 4) / max(t, 1e-3))))
+    # final timed sample ~ target_s
+    n2 = min(plans, max(n, int(n * target_s / max(t, 1e-3))))
+    ranks = rng.integers(0, plans, n2).astype(np.uint64)
+    t0 = time.perf_counter()
+    orc.evaluate_ranks(pr, w.space_mode, ranks, w.space_sizes, threads=threads)
+    t = time.perf_counter() - t0
+    return n2 / t, kind, n2, t
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    w = workloads.load(args.config)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from pyoracle import Oracle, Problem, available
+    threads = os.cpu_count() or 1
+    kind = "reference" if available("ref") else "port"
+    orc = Oracle("ref" if kind == "reference" else "port")
+    pr = Problem(w.cluster, w.model, w.types, w.lam, w.span_s, w.params)
+    parts, plans = orc.space_info(pr, w.space_mode, w.space_sizes)
+    # per-step sample sized to ~2 s of CPU work on this host
+    rate, _, _, _ = cpu_reference_sample(w, plans, 2.0, threads)
+    per_step = int(min(plans, max(64, rate * 2.0)))
+    rng = np.random.default_rng(7)
+    times = []
+    for i in range(args.warmup + args.steps):
+        ranks = rng.integers(0, plans, per_step).astype(np.uint64)
+        t0 = time.perf_counter()
+        orc.evaluate_ranks(pr, w.space_mode, ranks, w.space_sizes, threads=threads)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    value = per_step * len(times) / tot
+    ms = 1e3 * plans / value  # projected full-space round latency
+    line = {"metric": METRIC, "value": value, "unit": "plans/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+            "round_latency_ms_projected": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "int64", "data": "synthetic",
+            "config": {"workload": f"{w.name}: {w.description}", "plans_in_space": plans, "partitions": parts,
+                       "per_step_sample_plans": per_step},
+            "cpu_baseline": {"value": value, "unit": "plans/s", "cores": threads, "kind": kind,
+                             "sample": f"{per_step} uniform random plans of {plans} per step "
+                                       f"(evaluate_deployment each, OpenMP dynamic,4 over {threads} threads)"},
+            "e2e": {"value": value, "unit": "plans/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local):
+    from paper_2602_12151_b200._native import GpuContext
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    w = workloads.load(args.config)
+    stream = torch.cuda.current_stream(dev)
+    ctx = GpuContext(w.cluster, w.model, w.params, device=local)
+    ctx.set_stream(stream.cuda_stream)
+    ctx.set_shard(rank, world)
+    ctx.set_workload(w.types, w.lam, w.span_s)
+    parts, plans = ctx.prepare_space(w.space_mode, w.space_sizes)
+    g_min = ctx.min_feasible_group()
+    current = init_uniform(w, g_min)
+    d_key = torch.empty(1, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def device_step():
+        ctx.launch_round_async(d_key.data_ptr())
+        if world > 1:
+            dist.all_reduce(d_key, op=dist.ReduceOp.MIN)
+
+    # ---- value: device-resident round, per-step events, L2 flushed between ----
+    for _ in range(args.warmup):
+        device_step()
+    barrier()
+    launches0 = ctx.launch_count()
+    clocks = Clocks(local)
+    clocks.start()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier()
+    for i in range(args.steps):
+        flush.fill_(i)
+        starts[i].record(stream)
+        device_step()
+        ends[i].record(stream)
+    barrier()
+    clk = clocks.stop()
+    launches = ctx.launch_count() - launches0
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    t_local = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    total_ms = float(t_local.item())
+    ms_per_step = total_ms / args.steps
+    value = plans / (ms_per_step / 1e3)
+    key = int(d_key.item())
+    state = ctx.decode_key(key)
+
+    # ---- dominant kernel alone (K1 on this rank's shard), CUDA events ----
+    k_ms = []
+    for i in range(3):
+        flush.fill_(i)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        ctx.launch_round_async(d_key.data_ptr())
+        b.record(stream)
+        b.synchronize()
+        k_ms.append(a.elapsed_time(b))
+    k_ms = statistics.median(k_ms)
+    kt = torch.tensor([k_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(kt, op=dist.ReduceOp.MAX)
+    k_ms = float(kt.item())
+
+    # ---- e2e: public C-ABI from host buffers, every step ----
+    e2e_ms = []
+    bytes0 = None
+    for i in range(args.warmup + args.steps):
+        barrier()
+        if i == args.warmup:
+            bytes0 = ctx.copy_bytes()
+        t0 = time.perf_counter()
+        _, _ = ctx.prepare_space(w.space_mode, w.space_sizes)      # enumerate + H2D tables
+        ctx.set_workload(w.types, w.lam, w.span_s)                 # H2D workload (K0 runs in the round)
+        ctx.launch_round_async(d_key.data_ptr())                  # K0 + K1 (+K4) on this shard
+        if world > 1:
+            dist.all_reduce(d_key, op=dist.ReduceOp.MIN)
+        k = int(d_key.item())                                      # D2H result key
+        st = ctx.decode_key(k)
+        if rank == 0:
+            plan = ctx.switch_plan(current, st.deployment)         # K2 + transfers D2H
+        torch.cuda.synchronize(dev)
+        dt = (time.perf_counter() - t0) * 1e3
+        dtt = torch.tensor([dt], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(dtt, op=dist.ReduceOp.MAX)
+        if i >= args.warmup:
+            e2e_ms.append(float(dtt.item()))
+    e2e_step = statistics.mean(e2e_ms)
+    # bytes per step, counted by the C-ABI itself (every cudaMemcpy it issues)
+    bytes1 = ctx.copy_bytes()
+    h2d = (bytes1[0] - bytes0[0]) // args.steps
+    d2h = (bytes1[1] - bytes0[1]) // args.steps + 8  # + the key read through torch (.item())
+
+    if rank != 0:
+        return
+    # ---- roofline: issue-bound ----
+    work = load_work(args.config)
+    props = torch.cuda.get_device_properties(dev)
+    sm_max = clk.get("sm_max_mhz") or 1965.0
+    peak = props.multi_processor_count * 128 * sm_max * 1e6  # lane-ops/s per GPU
+    achieved = work["mean_work"] * OPS_PER_CELL * (plans / world) / (k_ms / 1e3)
+    traffic = profile_traffic(args.config)
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        rate, kind, n, t = cpu_reference_sample(w, plans, args.cpu_seconds, threads)
+        cpu = {"value": rate, "unit": "plans/s", "cores": threads, "kind": kind,
+               "sample": f"{n} uniform random plans of {plans} ({t:.1f} s; evaluate_deployment each, "
+                         f"OpenMP dynamic,4 over {threads} host threads)",
+               "round_latency_s_projected": plans / rate}
+    line = {
+        "metric": METRIC, "value": value, "unit": "plans/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "round_latency_ms": ms_per_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic",
+        "config": {"workload": f"{w.name}: {w.description}", "devices": w.cluster.device_count(),
+                   "classes": len(w.types), "plans_in_space": plans, "partitions": parts,
+                   "space": ("canonical sizes " + str(w.space_sizes)) if w.space_mode else "ordered (reference)",
+                   "parallelism": f"plan space sharded x{world} (interleaved 4096-plan chunks) + NCCL min",
+                   "l2": "flushed between timed iterations (256 MiB write outside the events)"},
+        "winner": {"objective": state.throughput, "key": key, "partition": state.partition_index,
+                   "local_rank": state.local_rank, "shapes": state.deployment.shapes()},
+        "e2e": {"value": plans / (e2e_step / 1e3), "unit": "plans/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "round_latency_ms": e2e_step,
+                "switch_est_seconds": plan.est_seconds, "switch_transfers": len(plan.transfers)},
+        "roofline": {"bound": "issue", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tlane-op/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "k_plan_eval (K1)", "kernel_ms": k_ms,
+                     "work_per_plan": work["mean_work"], "work_kind": work["kind"],
+                     "ops_per_cell": OPS_PER_CELL},
+        "cpu_baseline": cpu,
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def profile_traffic(name):
+    p = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(name)
+    return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg5")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warmup raised to 3 (timing rules)")
+        args.warmup = 3
+    rank, world, local = init_dist()
+    try:
+        if args.impl == "reference":
+            run_reference(args, rank, world)
+        else:
+            run_ours(args, rank, world, local)
+    finally:
+        if world > 1 and dist.is_initialized():
+            dist.barrier()
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

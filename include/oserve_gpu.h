@@ -237,6 +237,9 @@ int oserve_gpu_switch_plan(oserve_gpu_ctx *ctx, const oserve_deployment *src,
 
 /* Kernel launches issued by this context since creation (evidence counter). */
 uint64_t oserve_gpu_launch_count(const oserve_gpu_ctx *ctx);
+/* Host->device / device->host bytes copied by this context since creation
+ * (explicit copies plus the demand vector passed as kernel parameters). */
+int oserve_gpu_copy_bytes(const oserve_gpu_ctx *ctx, uint64_t *h2d_bytes, uint64_t *d2h_bytes);
 
 #ifdef __cplusplus
 }

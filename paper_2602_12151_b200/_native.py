@@ -25,7 +25,7 @@ EXPORTS = [
     "oserve_gpu_decode_key", "oserve_gpu_round", "oserve_gpu_exhaustive", "oserve_gpu_best_strategies",
     "oserve_gpu_evaluate_ranks", "oserve_gpu_evaluate_deployments", "oserve_gpu_plan_detail",
     "oserve_gpu_solve_batch", "oserve_gpu_switch_cost_batch", "oserve_gpu_switch_plan",
-    "oserve_gpu_launch_count",
+    "oserve_gpu_launch_count", "oserve_gpu_copy_bytes",
 ]
 
 _lib = None
@@ -68,6 +68,7 @@ def load_library() -> C.CDLL:
                                          P(A.TransferDesc), P(C.c_int), P(C.c_double)]
     L.oserve_gpu_launch_count.argtypes = [vp]
     L.oserve_gpu_launch_count.restype = C.c_uint64
+    L.oserve_gpu_copy_bytes.argtypes = [vp, P(C.c_uint64), P(C.c_uint64)]
     _lib = L
     return L
 
@@ -135,6 +136,12 @@ class GpuContext:
 
     def launch_count(self) -> int:
         return int(self.lib.oserve_gpu_launch_count(self.h))
+
+    def copy_bytes(self):
+        """(host->device, device->host) bytes this context has copied."""
+        a, b = C.c_uint64(), C.c_uint64()
+        self._chk(self.lib.oserve_gpu_copy_bytes(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def min_feasible_group(self) -> int:
         g = C.c_int()

@@ -50,6 +50,25 @@ void cuda_ok(cudaError_t e, const char *what) {
 }
 void cuda_ok(int e, const char *what) { cuda_ok(static_cast<cudaError_t>(e), what); }
 
+// Byte counters of the host<->device copies issued by the current call
+// (bound to the calling context by guarded()).
+thread_local uint64_t *t_h2d = nullptr;
+thread_local uint64_t *t_d2h = nullptr;
+inline void count_h2d(size_t b) {
+    if (t_h2d) *t_h2d += b;
+}
+inline void count_d2h(size_t b) {
+    if (t_d2h) *t_d2h += b;
+}
+cudaError_t h2d(void *dst, const void *src, size_t bytes, cudaStream_t s) {
+    count_h2d(bytes);
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+}
+cudaError_t d2h(void *dst, const void *src, size_t bytes, cudaStream_t s) {
+    count_d2h(bytes);
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s);
+}
+
 // Growable device buffer.
 struct DBuf {
     void *p = nullptr;
@@ -70,7 +89,7 @@ struct DBuf {
     template <class T>
     T *upload(const std::vector<T> &v, cudaStream_t s) {
         T *d = static_cast<T *>(get(v.size() * sizeof(T)));
-        if (!v.empty()) cuda_ok(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s), "H2D");
+        if (!v.empty()) cuda_ok(h2d(d, v.data(), v.size() * sizeof(T), s), "H2D");
         return d;
     }
 };
@@ -78,7 +97,7 @@ struct DBuf {
 template <class T>
 void download(std::vector<T> &v, const void *d, size_t n, cudaStream_t s) {
     v.resize(n);
-    if (n) cuda_ok(cudaMemcpyAsync(v.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost, s), "D2H");
+    if (n) cuda_ok(d2h(v.data(), d, n * sizeof(T), s), "D2H");
 }
 
 int bits_for(uint64_t x) {
@@ -139,6 +158,7 @@ struct oserve_gpu_ctx {
     cudaStream_t own = nullptr, stream = nullptr;
     std::string err;
     uint64_t launches = 0;
+    uint64_t h2d_bytes = 0, d2h_bytes = 0;
     // cluster
     std::vector<int> dev_sorted;
     std::map<int, int> machine_of;
@@ -586,6 +606,7 @@ void launch_round(oserve_gpu_ctx &c, uint64_t *d_key) {
     PlanOutputs out{};
     out.best_key = d_key;
     SolveParams prm = solve_params(c);
+    count_h2d(sizeof(int64_t) * c.J);  // the demand vector travels as a kernel parameter
     cuda_ok(launch_plan_eval(c.tables, sp.view, c.key, src, out, prm, sp.rmax, c.sm_count, sp.any_exact ? 1 : 0, s,
                              &c.launches),
             "plan kernel");
@@ -598,7 +619,7 @@ void launch_round(oserve_gpu_ctx &c, uint64_t *d_key) {
         eo.aborted_n = abn;
         cuda_ok(launch_plan_exact(c.tables, sp.view, c.key, src, eo, prm, c.sm_count, s, &c.launches), "exact kernel");
         unsigned n_ab = 0;
-        cuda_ok(cudaMemcpyAsync(&n_ab, abn, sizeof(unsigned), cudaMemcpyDeviceToHost, s), "D2H");
+        cuda_ok(d2h(&n_ab, abn, sizeof(unsigned), s), "D2H");
         cuda_ok(cudaStreamSynchronize(s), "sync");
         if (n_ab) {
             PlanSource rs{};
@@ -630,6 +651,8 @@ void prepare(oserve_gpu_ctx &c, const oserve_space_desc &d) {
 template <class F>
 int guarded(oserve_gpu_ctx *c, F &&f) {
     if (!c) return OSERVE_ERR_INVALID_ARGUMENT;
+    t_h2d = &c->h2d_bytes;
+    t_d2h = &c->d2h_bytes;
     try {
         cuda_ok(cudaSetDevice(c->device), "cudaSetDevice");
         f();
@@ -680,7 +703,7 @@ void eval_lists(oserve_gpu_ctx &c, const std::vector<int32_t> &listR, const std:
     out.objective = static_cast<int64_t *>(c.d_obj.get(sizeof(int64_t) * n));
     out.rmax = std::max(rmax, 1);
     if (x) {
-        out.x = static_cast<int64_t *>(c.d_x.get(sizeof(int64_t) * n * out.rmax * c.J));
+        out.x = static_cast<int64_t *>(c.d_x.get(sizeof(int64_t) * n * out.rmax * prm.J));
         out.used = static_cast<int64_t *>(c.d_used.get(sizeof(int64_t) * n * out.rmax));
     }
     // exact-path plans
@@ -707,7 +730,7 @@ void eval_lists(oserve_gpu_ctx &c, const std::vector<int32_t> &listR, const std:
         eo.aborted_n = abn;
         cuda_ok(launch_plan_exact(c.tables, none, nk, src, eo, prm, c.sm_count, s, &c.launches), "exact kernel");
         unsigned n_ab = 0;
-        cuda_ok(cudaMemcpyAsync(&n_ab, abn, sizeof(unsigned), cudaMemcpyDeviceToHost, s), "D2H");
+        cuda_ok(d2h(&n_ab, abn, sizeof(unsigned), s), "D2H");
         cuda_ok(cudaStreamSynchronize(s), "sync");
         if (n_ab) {
             std::vector<uint64_t> idx;
@@ -721,7 +744,7 @@ void eval_lists(oserve_gpu_ctx &c, const std::vector<int32_t> &listR, const std:
                 PlanOutputs o1 = out;
                 o1.objective = out.objective + li;
                 if (x) {
-                    o1.x = out.x + li * out.rmax * c.J;
+                    o1.x = out.x + li * out.rmax * prm.J;
                     o1.used = out.used + li * out.rmax;
                 }
                 cuda_ok(launch_plan_eval(c.tables, none, nk, one, o1, prm, rmax, c.sm_count, 0, s, &c.launches),
@@ -731,7 +754,7 @@ void eval_lists(oserve_gpu_ctx &c, const std::vector<int32_t> &listR, const std:
     }
     download(obj, out.objective, n, s);
     if (x) {
-        download(*x, out.x, n * out.rmax * c.J, s);
+        download(*x, out.x, n * out.rmax * prm.J, s);
         download(*used, out.used, n * out.rmax, s);
     }
     cuda_ok(cudaStreamSynchronize(s), "sync");
@@ -906,6 +929,13 @@ const char *oserve_gpu_last_error(const oserve_gpu_ctx *ctx) { return ctx ? ctx-
 
 uint64_t oserve_gpu_launch_count(const oserve_gpu_ctx *ctx) { return ctx ? ctx->launches : 0; }
 
+int oserve_gpu_copy_bytes(const oserve_gpu_ctx *ctx, uint64_t *h2d_bytes, uint64_t *d2h_bytes) {
+    if (!ctx) return OSERVE_ERR_INVALID_ARGUMENT;
+    if (h2d_bytes) *h2d_bytes = ctx->h2d_bytes;
+    if (d2h_bytes) *d2h_bytes = ctx->d2h_bytes;
+    return OSERVE_OK;
+}
+
 int oserve_gpu_set_workload(oserve_gpu_ctx *ctx, int num_classes, const oserve_class *classes, const int64_t *lambda,
                             double span_seconds) {
     return guarded(ctx, [&] {
@@ -923,8 +953,7 @@ int oserve_gpu_set_workload(oserve_gpu_ctx *ctx, int num_classes, const oserve_c
             ci[j] = classes[j].centroid_in;
             co[j] = classes[j].centroid_out;
         }
-        if (ci != ctx->cin || co != ctx->cout || span_seconds != ctx->span || num_classes != ctx->J)
-            ctx->tables_dirty = true;
+        ctx->tables_dirty = true;  // every round re-runs the cost kernel (K0) on its workload
         ctx->J = num_classes;
         ctx->cin = ci;
         ctx->cout = co;
@@ -960,6 +989,7 @@ int oserve_gpu_min_feasible_group(oserve_gpu_ctx *ctx, int *g_min) {
 int oserve_gpu_prepare_space(oserve_gpu_ctx *ctx, const oserve_space_desc *space, int64_t *partitions,
                              uint64_t *plans) {
     return guarded(ctx, [&] {
+        ctx->space.valid = false;  // explicit call: always re-enumerate and re-upload
         prepare(*ctx, *space);
         if (partitions) *partitions = static_cast<int64_t>(ctx->space.parts.size());
         if (plans) *plans = ctx->space.total;
@@ -986,7 +1016,7 @@ int oserve_gpu_round(oserve_gpu_ctx *ctx, const oserve_space_desc *space, oserve
         uint64_t *dk = static_cast<uint64_t *>(ctx->d_key.get(sizeof(uint64_t)));
         launch_round(*ctx, dk);
         uint64_t key = kNoKey;
-        cuda_ok(cudaMemcpyAsync(&key, dk, sizeof(key), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        cuda_ok(d2h(&key, dk, sizeof(key), ctx->stream), "D2H");
         cuda_ok(cudaStreamSynchronize(ctx->stream), "sync");
         decode_key(*ctx, key, out);
         if (key == kNoKey && ctx->world == 1) fail(OSERVE_ERR_MODEL_TOO_LARGE, "round: no feasible deployment");
@@ -1022,7 +1052,7 @@ int oserve_gpu_best_strategies(oserve_gpu_ctx *ctx, int num_replicas, const int 
         uint64_t *dk = static_cast<uint64_t *>(ctx->d_key.get(sizeof(uint64_t)));
         launch_round(*ctx, dk);
         uint64_t key = kNoKey;
-        cuda_ok(cudaMemcpyAsync(&key, dk, sizeof(key), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        cuda_ok(d2h(&key, dk, sizeof(key), ctx->stream), "D2H");
         cuda_ok(cudaStreamSynchronize(ctx->stream), "sync");
         decode_key(*ctx, key, out);
         if (out->objective < 0) out->objective = 0;
@@ -1063,7 +1093,7 @@ int oserve_gpu_evaluate_ranks(oserve_gpu_ctx *ctx, uint64_t first, uint64_t coun
             cuda_ok(launch_plan_exact(ctx->tables, sp.view, nk, src, eo, prm, ctx->sm_count, s, &ctx->launches),
                     "exact kernel");
             unsigned n_ab = 0;
-            cuda_ok(cudaMemcpyAsync(&n_ab, abn, sizeof(unsigned), cudaMemcpyDeviceToHost, s), "D2H");
+            cuda_ok(d2h(&n_ab, abn, sizeof(unsigned), s), "D2H");
             cuda_ok(cudaStreamSynchronize(s), "sync");
             if (n_ab) {
                 std::vector<uint64_t> ranks;
@@ -1083,9 +1113,9 @@ int oserve_gpu_evaluate_ranks(oserve_gpu_ctx *ctx, uint64_t first, uint64_t coun
             }
         }
         if (objective)
-            cuda_ok(cudaMemcpyAsync(objective, out.objective, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, s), "D2H");
+            cuda_ok(d2h(objective, out.objective, sizeof(int64_t) * count, s), "D2H");
         if (sum_pp)
-            cuda_ok(cudaMemcpyAsync(sum_pp, out.sum_pp, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, s), "D2H");
+            cuda_ok(d2h(sum_pp, out.sum_pp, sizeof(int32_t) * count, s), "D2H");
         cuda_ok(cudaStreamSynchronize(s), "sync");
     });
 }
@@ -1184,8 +1214,8 @@ int oserve_gpu_solve_batch(oserve_gpu_ctx *ctx, int count, int R, int J, const i
         t.J = J;
         t.n = static_cast<int64_t *>(dn.get(sizeof(int64_t) * rows * J));
         t.e = static_cast<int64_t *>(de.get(sizeof(int64_t) * rows * J));
-        cuda_ok(cudaMemcpyAsync(t.n, n, sizeof(int64_t) * rows * J, cudaMemcpyHostToDevice, s), "H2D");
-        cuda_ok(cudaMemcpyAsync(t.e, e, sizeof(int64_t) * rows * J, cudaMemcpyHostToDevice, s), "H2D");
+        cuda_ok(h2d(t.n, n, sizeof(int64_t) * rows * J, s), "H2D");
+        cuda_ok(h2d(t.e, e, sizeof(int64_t) * rows * J, s), "H2D");
         t.latency = static_cast<double *>(dlat.get(8));
         t.M = static_cast<int64_t *>(dM.get(sizeof(int64_t) * rows));
         t.unit = static_cast<int64_t *>(du.get(sizeof(int64_t) * rows * J));
