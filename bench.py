@@ -190,7 +190,8 @@ def run_ours(args, rank, world, local):
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
     w = workloads.load(args.config)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)  # the round, the collective and the events share this stream
+    torch.cuda.set_stream(stream)
     ctx = GpuContext(w.cluster, w.model, w.params, device=local)
     ctx.set_stream(stream.cuda_stream)
     ctx.set_shard(rank, world)

@@ -169,7 +169,8 @@ int oserve_gpu_set_solve_options(oserve_gpu_ctx *ctx, const oserve_solve_options
 /* Multi-GPU: this context evaluates only the plans of shard `rank` of
  * `world` (interleaved chunks of the global plan order). */
 int oserve_gpu_set_shard(oserve_gpu_ctx *ctx, int rank, int world);
-/* Launch stream (cudaStream_t as void*); NULL = the context's own stream. */
+/* Launch stream (cudaStream_t as void*), used exactly (NULL = the legacy
+ * default stream).  Until called, the context uses a stream of its own. */
 int oserve_gpu_set_stream(oserve_gpu_ctx *ctx, void *stream);
 /* search::min_feasible_group (deploysearch.cpp:77-87). */
 int oserve_gpu_min_feasible_group(oserve_gpu_ctx *ctx, int *g_min);

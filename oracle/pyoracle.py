@@ -54,6 +54,15 @@ class Oracle:
         L.oracle_space_plan.argtypes = [P(A.ProblemDesc), P(A.SpaceDesc), C.c_uint64, P(A.Plan),
                                         P(C.c_int64), P(C.c_uint64)]
         L.oracle_round.argtypes = [P(A.ProblemDesc), P(A.SpaceDesc), C.c_int, P(A.RoundResult)]
+        L.oracle_switch_plan.argtypes = [P(A.ClusterDesc), C.c_uint64, P(A.DeploymentDesc), P(A.DeploymentDesc),
+                                         C.c_int, P(A.TransferDesc), P(C.c_int), P(C.c_double), P(C.c_uint64)]
+        L.oracle_fit_types.argtypes = [C.c_int64, P(C.c_uint32), P(C.c_uint32), C.c_int, C.c_uint64,
+                                       P(C.c_double), P(C.c_double)]
+        L.oracle_holt_forecast.argtypes = [C.c_int, C.c_int, P(C.c_int64), C.c_int, P(C.c_int64)]
+        L.oracle_solve_assignment.argtypes = [C.c_int, C.c_int, P(C.c_int64), P(C.c_int64), P(C.c_int64),
+                                              P(A.SolveOptionsDesc), P(C.c_int64), P(C.c_int64), P(C.c_int64),
+                                              P(C.c_int64), P(C.c_int64), P(C.c_uint64)]
+        L.oracle_normalize.argtypes = [C.c_int, P(C.c_int64), C.c_int, P(C.c_int64), P(C.c_int64), P(C.c_int)]
 
     def _chk(self, st):
         A.raise_for(st, self.lib.oracle_last_error().decode())

@@ -16,7 +16,7 @@ from . import _abi as A
 from . import core
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liboserve_gpu.so")
+LIB_PATH = os.environ.get("OSERVE_GPU_LIB", os.path.join(HERE, "liboserve_gpu.so"))
 
 EXPORTS = [
     "oserve_gpu_create", "oserve_gpu_destroy", "oserve_gpu_last_error", "oserve_gpu_status_name",

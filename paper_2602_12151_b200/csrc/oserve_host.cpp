@@ -179,7 +179,7 @@ struct oserve_gpu_ctx {
     std::vector<ShapeParam> shapes;
     int tables_shapes = -1;  // shapes computed in device tables
     bool tables_dirty = true;
-    DBuf d_param, d_n, d_e, d_lat, d_M, d_unit, d_cap, d_order, d_olen, d_pp, d_scaled, d_cin, d_cout;
+    DBuf d_param, d_n, d_e, d_lat, d_M, d_unit, d_inv, d_cap, d_order, d_olen, d_pp, d_scaled, d_cin, d_cout;
     ShapeTables tables{};
     // space
     Space space;
@@ -278,6 +278,7 @@ void ensure_tables(oserve_gpu_ctx &c) {
     t.latency = static_cast<double *>(c.d_lat.get(sizeof(double) * S * J));
     t.M = static_cast<int64_t *>(c.d_M.get(sizeof(int64_t) * S));
     t.unit = static_cast<int64_t *>(c.d_unit.get(sizeof(int64_t) * S * J));
+    t.inv_unit = static_cast<double *>(c.d_inv.get(sizeof(double) * S * J));
     t.cap = static_cast<int32_t *>(c.d_cap.get(sizeof(int32_t) * S * J));
     t.order = static_cast<uint8_t *>(c.d_order.get(S * kMaxJ));
     t.olen = static_cast<uint8_t *>(c.d_olen.get(S));
@@ -979,7 +980,9 @@ int oserve_gpu_set_shard(oserve_gpu_ctx *ctx, int rank, int world) {
 }
 
 int oserve_gpu_set_stream(oserve_gpu_ctx *ctx, void *stream) {
-    return guarded(ctx, [&] { ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own; });
+    // Exactly the given stream (NULL = the legacy default stream), so callers
+    // can order the round with their own work and events.
+    return guarded(ctx, [&] { ctx->stream = static_cast<cudaStream_t>(stream); });
 }
 
 int oserve_gpu_min_feasible_group(oserve_gpu_ctx *ctx, int *g_min) {
@@ -1208,7 +1211,7 @@ int oserve_gpu_solve_batch(oserve_gpu_ctx *ctx, int count, int R, int J, const i
         }
         // Raw rows become the shape tables of this call (K0b only).
         cudaStream_t s = ctx->stream;
-        DBuf dn, de, dM, du, dc, dord, dol, dpp, dsc, dlat;
+        DBuf dn, de, dM, du, dc, dord, dol, dpp, dsc, dlat, dinv;
         ShapeTables t{};
         t.num_shapes = static_cast<int>(rows);
         t.J = J;
@@ -1219,6 +1222,7 @@ int oserve_gpu_solve_batch(oserve_gpu_ctx *ctx, int count, int R, int J, const i
         t.latency = static_cast<double *>(dlat.get(8));
         t.M = static_cast<int64_t *>(dM.get(sizeof(int64_t) * rows));
         t.unit = static_cast<int64_t *>(du.get(sizeof(int64_t) * rows * J));
+        t.inv_unit = static_cast<double *>(dinv.get(sizeof(double) * rows * J));
         t.cap = static_cast<int32_t *>(dc.get(sizeof(int32_t) * rows * J));
         t.order = static_cast<uint8_t *>(dord.get(rows * kMaxJ));
         t.olen = static_cast<uint8_t *>(dol.get(rows));

@@ -39,6 +39,7 @@ struct ShapeTables {
     double *latency;
     int64_t *M;       // [S]
     int64_t *unit;    // [S*J]
+    double *inv_unit; // [S*J] 1/unit (division-free quotient estimate, corrected exactly)
     int32_t *cap;     // [S*J] min(e, n, M/unit), clamped to INT32_MAX (exact while lambda < 2^31)
     uint8_t *order;   // [S*kMaxJ] classes with cap > 0, stable-sorted by unit
     uint8_t *olen;    // [S]

@@ -23,6 +23,10 @@
 
 #include "oserve_internal.h"
 
+#ifndef OSERVE_K1_MINB
+#define OSERVE_K1_MINB 3  // CTAs of 256 threads per SM the register budget must allow
+#endif
+
 namespace oserve_gpu {
 
 namespace {
@@ -102,6 +106,7 @@ __global__ void k_normalize_rows(ShapeTables t) {
             int64_t u = 0;
             if (nj > 0) u = overflow ? (kLcmLimit + nj - 1) / nj : m / nj;
             unit[j] = u;
+            t.inv_unit[static_cast<int64_t>(s) * J + j] = u > 0 ? __drcp_rn(static_cast<double>(u)) : 0.0;
             // make_instance (:278-292): cap = min(e, n, M/unit) where unit > 0
             int64_t c = 0;
             if (u > 0) {
@@ -162,6 +167,18 @@ __device__ __forceinline__ void unrank_run(uint64_t r, int len, int q, uint8_t *
     }
 }
 
+// floor(m / u) for 0 <= m < 2^63, u >= 1, when the quotient is known to be
+// < 2^31 (greedy: m < a*u with a <= INT32_MAX).  The FP64 estimate has
+// relative error < 2^-51, i.e. absolute error < 2^-20, so one correction
+// step in each direction makes it exact (no 64-bit integer division).
+__device__ __forceinline__ int32_t quot_small(int64_t m, int64_t u, double inv_u) {
+    int64_t q = static_cast<int64_t>(__dmul_rn(static_cast<double>(m), inv_u));
+    const int64_t r = m - q * u;
+    if (r < 0) --q;
+    else if (r >= u) ++q;
+    return static_cast<int32_t>(q);
+}
+
 __device__ __forceinline__ uint64_t div_small(uint64_t a, uint64_t b) {
     if ((a >> 32) == 0 && (b >> 32) == 0) return static_cast<uint32_t>(a) / static_cast<uint32_t>(b);
     return a / b;
@@ -208,33 +225,54 @@ struct SmemShapes {
     const uint8_t *pp;
 };
 
-template <int G, int KPL>
-__global__ void __launch_bounds__(256) k_plan_eval(ShapeTables t, SpaceTables sp, KeyLayout key, PlanSource src,
-                                                   PlanOutputs out, SolveParams prm, int skip_exact) {
+template <int G, int KPL, bool SMEM>
+__global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t, SpaceTables sp, KeyLayout key,
+                                                                   PlanSource src, PlanOutputs out, SolveParams prm,
+                                                                   int skip_exact) {
     using Grp = Group<G, KPL>;
     constexpr int RMAX = Grp::RMAX;
     constexpr int GPB = 256 / G;
     extern __shared__ __align__(16) unsigned char smem[];
     const int S = t.num_shapes, J = prm.J;
 
-    // ---- stage the shape tables (SoA) into shared memory ----
-    int64_t *sM = reinterpret_cast<int64_t *>(smem);
-    int64_t *sUnit = sM + S;
-    int32_t *sCap = reinterpret_cast<int32_t *>(sUnit + S * J);
-    uint8_t *sOrder = reinterpret_cast<uint8_t *>(sCap + S * J);
-    uint8_t *sOlen = sOrder + S * kMaxJ;
-    uint8_t *sPP = sOlen + S;
-    size_t off = (reinterpret_cast<uintptr_t>(sPP + S) - reinterpret_cast<uintptr_t>(smem) + 15) & ~size_t(15);
-    for (int i = threadIdx.x; i < S; i += blockDim.x) {
-        sM[i] = t.M[i];
-        sOlen[i] = t.olen[i];
-        sPP[i] = t.pp[i];
+    // ---- shape tables (SoA): staged in shared memory, or read from global
+    // (L1-cached) when they do not fit (solve_batch: one row per instance) ----
+    const int64_t *sM = t.M;
+    const int64_t *sUnit = t.unit;
+    const double *sInv = t.inv_unit;
+    const int32_t *sCap = t.cap;
+    const uint8_t *sOrder = t.order;
+    const uint8_t *sOlen = t.olen;
+    const uint8_t *sPP = t.pp;
+    size_t off = 0;
+    if constexpr (SMEM) {
+        int64_t *M_ = reinterpret_cast<int64_t *>(smem);
+        int64_t *U_ = M_ + S;
+        double *I_ = reinterpret_cast<double *>(U_ + S * J);
+        int32_t *C_ = reinterpret_cast<int32_t *>(I_ + S * J);
+        uint8_t *O_ = reinterpret_cast<uint8_t *>(C_ + S * J);
+        uint8_t *L_ = O_ + S * kMaxJ;
+        uint8_t *P_ = L_ + S;
+        off = (reinterpret_cast<uintptr_t>(P_ + S) - reinterpret_cast<uintptr_t>(smem) + 15) & ~size_t(15);
+        for (int i = threadIdx.x; i < S; i += blockDim.x) {
+            M_[i] = t.M[i];
+            L_[i] = t.olen[i];
+            P_[i] = t.pp[i];
+        }
+        for (int i = threadIdx.x; i < S * J; i += blockDim.x) {
+            U_[i] = t.unit[i];
+            I_[i] = t.inv_unit[i];
+            C_[i] = t.cap[i];
+        }
+        for (int i = threadIdx.x; i < S * kMaxJ; i += blockDim.x) O_[i] = t.order[i];
+        sM = M_;
+        sUnit = U_;
+        sInv = I_;
+        sCap = C_;
+        sOrder = O_;
+        sOlen = L_;
+        sPP = P_;
     }
-    for (int i = threadIdx.x; i < S * J; i += blockDim.x) {
-        sUnit[i] = t.unit[i];
-        sCap[i] = t.cap[i];
-    }
-    for (int i = threadIdx.x; i < S * kMaxJ; i += blockDim.x) sOrder[i] = t.order[i];
 
     // ---- per-group scratch ----
     const int gib = threadIdx.x / G;
@@ -328,7 +366,7 @@ __global__ void __launch_bounds__(256) k_plan_eval(ShapeTables t, SpaceTables sp
                         const int64_t u = sUnit[s * J + j];
                         const int32_t a = min(sCap[s * J + j], lam[j]);
                         int32_t tk = a;
-                        if (static_cast<int64_t>(a) * u > m) tk = static_cast<int32_t>(m / u);
+                        if (static_cast<int64_t>(a) * u > m) tk = quot_small(m, u, sInv[s * J + j]);
                         xs[j * RMAX + k] = tk;
                         m -= static_cast<int64_t>(tk) * u;
                     }
@@ -382,7 +420,7 @@ __global__ void __launch_bounds__(256) k_plan_eval(ShapeTables t, SpaceTables sp
                             const int64_t u = sUnit[s * J + j];
                             const int32_t a = min(sCap[s * J + j], lam[j]);
                             int32_t tk = a;
-                            if (static_cast<int64_t>(a) * u > m) tk = static_cast<int32_t>(m / u);
+                            if (static_cast<int64_t>(a) * u > m) tk = quot_small(m, u, sInv[s * J + j]);
                             xs[j * RMAX + kstar] = tk;
                             lam[j] -= tk;
                             m -= static_cast<int64_t>(tk) * u;
@@ -581,11 +619,11 @@ __global__ void __launch_bounds__(256) k_plan_eval(ShapeTables t, SpaceTables sp
 }
 
 template <int G, int KPL>
-size_t plan_eval_smem(int S, int J) {
+size_t plan_eval_smem(int S, int J, bool stage) {
     constexpr int RMAX = G * KPL;
     constexpr int GPB = 256 / G;
-    size_t shapes = (size_t)S * 8 + (size_t)S * J * 8 + (size_t)S * J * 4 + (size_t)S * kMaxJ + 2 * (size_t)S;
-    shapes = (shapes + 15) & ~size_t(15);
+    size_t shapes = (size_t)S * 8 + (size_t)S * J * 16 + (size_t)S * J * 4 + (size_t)S * kMaxJ + 2 * (size_t)S;
+    shapes = stage ? (shapes + 15) & ~size_t(15) : 0;
     const size_t per_group = ((size_t)J * RMAX * 4 + kMaxJ * 4 + kMaxJ * KPL * 4 + RMAX + 15) & ~size_t(15);
     return shapes + per_group * GPB + GPB * 8;
 }
@@ -594,8 +632,10 @@ template <int G, int KPL>
 int run_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key, const PlanSource &src,
                   const PlanOutputs &out, const SolveParams &prm, int sm_count, int skip_exact,
                   cudaStream_t stream, uint64_t *launches) {
-    const size_t smem = plan_eval_smem<G, KPL>(t.num_shapes, prm.J);
-    auto kern = k_plan_eval<G, KPL>;
+    cudaGetLastError();  // clear any stale (non-sticky) error before launching
+    const bool stage = plan_eval_smem<G, KPL>(t.num_shapes, prm.J, true) <= 160 * 1024;
+    const size_t smem = plan_eval_smem<G, KPL>(t.num_shapes, prm.J, stage);
+    auto kern = stage ? k_plan_eval<G, KPL, true> : k_plan_eval<G, KPL, false>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (e != cudaSuccess) return static_cast<int>(e);
@@ -1032,6 +1072,7 @@ static int ensure_binom() {
 
 int launch_cost_tables(const ShapeTables &t, const double *cin, const double *cout, uint32_t num_layers,
                        uint64_t kvb, double pc, double dc, double ppc, double slope, double span_s, void *stream) {
+    cudaGetLastError();
     const int cells = t.num_shapes * t.J;
     if (cells == 0) return 0;
     const int block = 128, grid = (cells + block - 1) / block;
@@ -1041,6 +1082,7 @@ int launch_cost_tables(const ShapeTables &t, const double *cin, const double *co
 }
 
 int launch_normalize_rows(const ShapeTables &t, void *stream) {
+    cudaGetLastError();
     if (t.num_shapes == 0) return 0;
     const int block = 128, grid = (t.num_shapes + block - 1) / block;
     k_normalize_rows<<<grid, block, 0, static_cast<cudaStream_t>(stream)>>>(t);
@@ -1064,6 +1106,7 @@ int launch_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayou
 int launch_plan_exact(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key, const PlanSource &src,
                       const PlanOutputs &out, const SolveParams &prm, int sm_count, void *stream,
                       uint64_t *launches) {
+    cudaGetLastError();
     if (int e = ensure_binom()) return e;
     if (src.count == 0) return 0;
     const int block = 128;
@@ -1077,6 +1120,7 @@ int launch_plan_exact(const ShapeTables &t, const SpaceTables &sp, const KeyLayo
 }
 
 int launch_switch_cost(const SwitchDeps &d, const SwitchOut &o, void *stream, uint64_t *launches) {
+    cudaGetLastError();
     if (d.count == 0) return 0;
     if (d.num_devices > kSwMaxDev) return static_cast<int>(cudaErrorInvalidValue);
     k_switch_cost<<<d.count, 256, 0, static_cast<cudaStream_t>(stream)>>>(d, o);
