@@ -179,7 +179,7 @@ struct oserve_gpu_ctx {
     std::vector<ShapeParam> shapes;
     int tables_shapes = -1;  // shapes computed in device tables
     bool tables_dirty = true;
-    DBuf d_param, d_n, d_e, d_lat, d_M, d_unit, d_inv, d_cap, d_order, d_olen, d_pp, d_scaled, d_cin, d_cout;
+    DBuf d_param, d_n, d_e, d_lat, d_M, d_unit, d_inv, d_rank, d_cap, d_order, d_olen, d_pp, d_scaled, d_cin, d_cout;
     ShapeTables tables{};
     // space
     Space space;
@@ -281,6 +281,7 @@ void ensure_tables(oserve_gpu_ctx &c) {
     t.inv_unit = static_cast<double *>(c.d_inv.get(sizeof(double) * S * J));
     t.cap = static_cast<int32_t *>(c.d_cap.get(sizeof(int32_t) * S * J));
     t.order = static_cast<uint8_t *>(c.d_order.get(S * kMaxJ));
+    t.rank = static_cast<uint8_t *>(c.d_rank.get(S * kMaxJ));
     t.olen = static_cast<uint8_t *>(c.d_olen.get(S));
     t.scaled = static_cast<uint8_t *>(c.d_scaled.get(S));
     std::vector<uint8_t> pps(S);
@@ -1211,7 +1212,7 @@ int oserve_gpu_solve_batch(oserve_gpu_ctx *ctx, int count, int R, int J, const i
         }
         // Raw rows become the shape tables of this call (K0b only).
         cudaStream_t s = ctx->stream;
-        DBuf dn, de, dM, du, dc, dord, dol, dpp, dsc, dlat, dinv;
+        DBuf dn, de, dM, du, dc, dord, dol, dpp, dsc, dlat, dinv, drank;
         ShapeTables t{};
         t.num_shapes = static_cast<int>(rows);
         t.J = J;
@@ -1225,6 +1226,7 @@ int oserve_gpu_solve_batch(oserve_gpu_ctx *ctx, int count, int R, int J, const i
         t.inv_unit = static_cast<double *>(dinv.get(sizeof(double) * rows * J));
         t.cap = static_cast<int32_t *>(dc.get(sizeof(int32_t) * rows * J));
         t.order = static_cast<uint8_t *>(dord.get(rows * kMaxJ));
+        t.rank = static_cast<uint8_t *>(drank.get(rows * kMaxJ));
         t.olen = static_cast<uint8_t *>(dol.get(rows));
         t.scaled = static_cast<uint8_t *>(dsc.get(rows));
         t.pp = static_cast<uint8_t *>(dpp.get(rows));

@@ -128,7 +128,11 @@ __global__ void k_normalize_rows(ShapeTables t) {
                 cap[j] = 0;
             }
         }
-        for (int i = 0; i < kMaxJ; ++i) t.order[s * kMaxJ + i] = i < ol ? ord[i] : 0;
+        for (int i = 0; i < kMaxJ; ++i) {
+            t.order[s * kMaxJ + i] = i < ol ? ord[i] : 0;
+            t.rank[s * kMaxJ + i] = 0xff;
+        }
+        for (int i = 0; i < ol; ++i) t.rank[s * kMaxJ + ord[i]] = static_cast<uint8_t>(i);
         t.olen[s] = static_cast<uint8_t>(ol);
     }
 }
@@ -205,6 +209,19 @@ struct Group {
     template <class T>
     __device__ __forceinline__ T bcast(T v, int src) const { return __shfl_sync(mask, v, src, G); }
     __device__ __forceinline__ uint32_t sum(uint32_t v) const { return __reduce_add_sync(mask, v); }
+    __device__ __forceinline__ uint32_t or_all(uint32_t v) const { return __reduce_or_sync(mask, v); }
+    // inclusive prefix sum of u64, saturating at `sat` (sat + sat must not overflow)
+    __device__ __forceinline__ uint64_t scan_sat64(uint64_t v, uint64_t sat) const {
+#pragma unroll
+        for (int d = 1; d < G; d <<= 1) {
+            const uint64_t o = __shfl_up_sync(mask, v, d, G);
+            if (gl >= d) {
+                v += o;
+                v = v < sat ? v : sat;
+            }
+        }
+        return v;
+    }
     // inclusive prefix sum, saturating at `sat`
     __device__ __forceinline__ uint32_t scan_sat(uint32_t v, uint32_t sat) const {
 #pragma unroll
@@ -216,14 +233,9 @@ struct Group {
     }
 };
 
-struct SmemShapes {
-    const int64_t *M;
-    const int64_t *unit;
-    const int32_t *cap;
-    const uint8_t *order;
-    const uint8_t *olen;
-    const uint8_t *pp;
-};
+__host__ __device__ constexpr size_t group_scratch_bytes(int J, int RMAX, int KPL) {
+    return ((size_t)J * RMAX * 4 + (size_t)kMaxJ * KPL * 4 + (size_t)RMAX * 2 + RMAX + 15) & ~size_t(15);
+}
 
 template <int G, int KPL, bool SMEM>
 __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t, SpaceTables sp, KeyLayout key,
@@ -242,6 +254,7 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
     const double *sInv = t.inv_unit;
     const int32_t *sCap = t.cap;
     const uint8_t *sOrder = t.order;
+    const uint8_t *sRank = t.rank;
     const uint8_t *sOlen = t.olen;
     const uint8_t *sPP = t.pp;
     size_t off = 0;
@@ -251,7 +264,8 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
         double *I_ = reinterpret_cast<double *>(U_ + S * J);
         int32_t *C_ = reinterpret_cast<int32_t *>(I_ + S * J);
         uint8_t *O_ = reinterpret_cast<uint8_t *>(C_ + S * J);
-        uint8_t *L_ = O_ + S * kMaxJ;
+        uint8_t *K_ = O_ + S * kMaxJ;
+        uint8_t *L_ = K_ + S * kMaxJ;
         uint8_t *P_ = L_ + S;
         off = (reinterpret_cast<uintptr_t>(P_ + S) - reinterpret_cast<uintptr_t>(smem) + 15) & ~size_t(15);
         for (int i = threadIdx.x; i < S; i += blockDim.x) {
@@ -264,8 +278,12 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
             I_[i] = t.inv_unit[i];
             C_[i] = t.cap[i];
         }
-        for (int i = threadIdx.x; i < S * kMaxJ; i += blockDim.x) O_[i] = t.order[i];
+        for (int i = threadIdx.x; i < S * kMaxJ; i += blockDim.x) {
+            O_[i] = t.order[i];
+            K_[i] = t.rank[i];
+        }
         sM = M_;
+        sRank = K_;
         sUnit = U_;
         sInv = I_;
         sCap = C_;
@@ -276,12 +294,12 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
 
     // ---- per-group scratch ----
     const int gib = threadIdx.x / G;
-    const size_t per_group = ((size_t)J * RMAX * 4 + kMaxJ * 4 + kMaxJ * KPL * 4 + RMAX + 15) & ~size_t(15);
+    const size_t per_group = group_scratch_bytes(J, RMAX, KPL);
     unsigned char *gs = smem + off + per_group * gib;
-    int32_t *xs = reinterpret_cast<int32_t *>(gs);              // [J][RMAX]
-    int32_t *lam = xs + J * RMAX;                               // [kMaxJ]
-    uint32_t *Am = reinterpret_cast<uint32_t *>(lam + kMaxJ);   // [kMaxJ][KPL]
-    uint8_t *pick = reinterpret_cast<uint8_t *>(Am + kMaxJ * KPL);  // [RMAX]
+    int32_t *xs = reinterpret_cast<int32_t *>(gs);                      // [J][RMAX] assignment x
+    uint32_t *Am = reinterpret_cast<uint32_t *>(xs + J * RMAX);         // [kMaxJ][KPL] direct-take masks
+    uint16_t *shpS = reinterpret_cast<uint16_t *>(Am + kMaxJ * KPL);    // [RMAX] shape per replica
+    uint8_t *pick = reinterpret_cast<uint8_t *>(shpS + RMAX);           // [RMAX] candidate pick per replica
     unsigned long long *blk_best = reinterpret_cast<unsigned long long *>(smem + off + per_group * GPB);
     __syncthreads();
 
@@ -334,145 +352,105 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
             }
         }
 
-        // ---- init: lam, x = 0, mrem = M ----
-        for (int j = g.gl; j < J; j += G) lam[j] = static_cast<int32_t>(lam_src[j]);
-        int64_t mrem[KPL];
+        // ---- init: lam (lane j holds class j), x = 0 ----
+        int32_t lamr = g.gl < J ? static_cast<int32_t>(lam_src[g.gl]) : 0;
 #pragma unroll
         for (int kk = 0; kk < KPL; ++kk) {
             const int k = g.gl + G * kk;
-            mrem[kk] = sM[shp[kk]];
+            if (k < R) shpS[k] = static_cast<uint16_t>(shp[kk]);
             for (int j = 0; j < J; ++j) xs[j * RMAX + k] = 0;
         }
         g.sync();
 
-        // ---- greedy_fill (flowassign.cpp:393-406), speculative-parallel ----
-        // Each replica >= k0 fills as if alone (its takes depend on lam only
-        // through min(., lam)); the first replica whose prefix demand exceeds
-        // lam for some class is the first one lam actually binds: commit the
-        // replicas before it, recompute it exactly, repeat.  Identical to the
-        // sequential fill; each round exhausts at least one class.
-        int k0 = 0;
-        while (k0 < R) {
-#pragma unroll
-            for (int kk = 0; kk < KPL; ++kk) {
-                const int k = g.gl + G * kk;
-                if (k >= k0 && k < R) {
-                    const int s = shp[kk];
-                    int64_t m = sM[s];
-                    for (int j = 0; j < J; ++j) xs[j * RMAX + k] = 0;
-                    const int ol = sOlen[s];
-                    for (int pos = 0; pos < ol; ++pos) {
-                        const int j = sOrder[s * kMaxJ + pos];
-                        const int64_t u = sUnit[s * J + j];
-                        const int32_t a = min(sCap[s * J + j], lam[j]);
-                        int32_t tk = a;
-                        if (static_cast<int64_t>(a) * u > m) tk = quot_small(m, u, sInv[s * J + j]);
-                        xs[j * RMAX + k] = tk;
-                        m -= static_cast<int64_t>(tk) * u;
-                    }
-                    mrem[kk] = m;
-                }
-            }
-            g.sync();
-            bool bad[KPL];
-#pragma unroll
-            for (int kk = 0; kk < KPL; ++kk) bad[kk] = false;
-            for (int j = 0; j < J; ++j) {
-                const uint32_t L = static_cast<uint32_t>(lam[j]);
-                uint32_t carry = 0;
-#pragma unroll
-                for (int kk = 0; kk < KPL; ++kk) {
-                    const int k = g.gl + G * kk;
-                    const uint32_t v = (k >= k0 && k < R) ? static_cast<uint32_t>(xs[j * RMAX + k]) : 0u;
-                    const uint32_t sc = min(g.scan_sat(v, 0x80000000u) + carry, 0x80000000u);
-                    bad[kk] |= sc > L;
-                    carry = g.bcast(sc, G - 1);
-                }
-            }
-            int kstar = R;
-#pragma unroll
-            for (int kk = KPL - 1; kk >= 0; --kk) {
-                const uint32_t b = g.ballot(bad[kk]);
-                if (b) kstar = __ffs(b) - 1 + G * kk;
-            }
-            // commit lam for [k0, kstar)
-            for (int j = 0; j < J; ++j) {
-                uint32_t part_sum = 0;
-#pragma unroll
-                for (int kk = 0; kk < KPL; ++kk) {
-                    const int k = g.gl + G * kk;
-                    if (k >= k0 && k < kstar) part_sum += static_cast<uint32_t>(xs[j * RMAX + k]);
-                }
-                part_sum = g.sum(part_sum);
-                if (g.gl == 0) lam[j] -= static_cast<int32_t>(part_sum);
-            }
-            g.sync();
-            if (kstar < R) {
-#pragma unroll
-                for (int kk = 0; kk < KPL; ++kk) {
-                    if (g.gl + G * kk == kstar) {
-                        const int s = shp[kk];
-                        int64_t m = sM[s];
-                        for (int j = 0; j < J; ++j) xs[j * RMAX + kstar] = 0;
-                        const int ol = sOlen[s];
-                        for (int pos = 0; pos < ol; ++pos) {
-                            const int j = sOrder[s * kMaxJ + pos];
-                            const int64_t u = sUnit[s * J + j];
-                            const int32_t a = min(sCap[s * J + j], lam[j]);
-                            int32_t tk = a;
-                            if (static_cast<int64_t>(a) * u > m) tk = quot_small(m, u, sInv[s * J + j]);
-                            xs[j * RMAX + kstar] = tk;
-                            lam[j] -= tk;
-                            m -= static_cast<int64_t>(tk) * u;
-                        }
-                        mrem[kk] = m;
-                    }
-                }
-                g.sync();
-            }
-            k0 = kstar + 1;
-        }
-
-        // ---- exchange_improve (flowassign.cpp:411-448) ----
-        // A[j2] = replicas able to take one more class-j2 request directly.
-        // (j, k) has a move iff direct (mrem >= unit) or some held j2 != j with
-        // A[j2]\{k} non-empty and unit[k][j2] >= unit[k][j] - mrem[k]; the
-        // first such (j, k) in (j asc, k asc) order, then the first j2 asc,
-        // then the first k2 asc, is exactly the reference's first move.
+        // ---- greedy_fill (flowassign.cpp:393-406) ----
+        // Replicas in order; inside one replica the reference takes
+        // min(cap, lam) for a prefix of its ascending-unit class order, one
+        // partial class where the budget binds, then nothing (every later
+        // class costs >= the binding unit > the budget left).  So one replica
+        // is one prefix scan of costs over its order positions (lane = position)
+        // plus a ballot for the binding position.  Bit-identical to the
+        // sequential fill; no 64-bit division.
+        int64_t mrem[KPL];
         uint32_t held[KPL];
 #pragma unroll
         for (int kk = 0; kk < KPL; ++kk) {
-            const int k = g.gl + G * kk;
-            uint32_t h = 0;
-            if (k < R)
-                for (int j = 0; j < J; ++j) h |= (xs[j * RMAX + k] > 0 ? 1u : 0u) << j;
-            held[kk] = h;
+            mrem[kk] = 0;
+            held[kk] = 0;
         }
-        for (;;) {
-            // masks A
-            for (int j = 0; j < J; ++j) {
-#pragma unroll
-                for (int kk = 0; kk < KPL; ++kk) {
-                    const int k = g.gl + G * kk;
-                    bool p = false;
-                    if (k < R) {
-                        const int s = shp[kk];
-                        const int64_t u = sUnit[s * J + j];
-                        p = u > 0 && xs[j * RMAX + k] < sCap[s * J + j] && mrem[kk] >= u;
-                    }
-                    const uint32_t b = g.ballot(p);
-                    if (g.gl == 0) Am[j * KPL + kk] = b;
-                }
+        for (int k = 0; k < R; ++k) {
+            const int s = shpS[k];
+            const int ol = sOlen[s];
+            const bool act = g.gl < ol;
+            const int j = act ? sOrder[s * kMaxJ + g.gl] : 0;
+            const int32_t lamp = g.bcast(lamr, j);
+            const int64_t Ms = sM[s];
+            int64_t u = 1;
+            int32_t a = 0;
+            if (act) {
+                u = sUnit[s * J + j];
+                a = min(sCap[s * J + j], lamp);
             }
-            g.sync();
-            // top-2 eligible unit per owned replica
-            int64_t e1[KPL], e2[KPL];
-            int e1j[KPL];
+            const uint64_t cost = static_cast<uint64_t>(a) * static_cast<uint64_t>(u);
+            const uint64_t csum = g.scan_sat64(cost, static_cast<uint64_t>(Ms) + 1);
+            const uint32_t ob = g.ballot(act && csum > static_cast<uint64_t>(Ms));
+            const int pb = ob ? __ffs(ob) - 1 : ol;
+            int32_t take = 0;
+            if (act) {
+                if (g.gl < pb) take = a;
+                else if (g.gl == pb) take = quot_small(Ms - static_cast<int64_t>(csum - cost), u, sInv[s * J + j]);
+                if (take) xs[j * RMAX + k] = take;
+            }
+            const uint64_t used_l = (g.gl == pb) ? (csum - cost) + static_cast<uint64_t>(take) * static_cast<uint64_t>(u) : csum;
+            const uint64_t used = ol ? g.bcast(used_l, pb < ol ? pb : ol - 1) : 0ull;
+            const uint32_t hb = g.or_all(take > 0 ? (1u << j) : 0u);
+            const int rp = g.gl < J ? sRank[s * kMaxJ + g.gl] : 0xff;
+            const int32_t tk = g.bcast(take, rp < G ? rp : 0);
+            if (rp != 0xff) lamr -= tk;
+#pragma unroll
+            for (int kk = 0; kk < KPL; ++kk)
+                if (g.gl + G * kk == k) {
+                    mrem[kk] = Ms - static_cast<int64_t>(used);
+                    held[kk] = hb;
+                }
+        }
+        g.sync();
+
+        // ---- exchange_improve (flowassign.cpp:411-448) ----
+        // A[j] = replicas able to take one more class-j request directly (one
+        // G-bit word per ownership slot kk).  (j, k) has a move iff lam_j > 0,
+        // unit > 0, x < cap and either mrem >= unit (direct) or some held
+        // class j2 != j has A[j2]\{k} non-empty and unit[k][j2] >= unit[k][j] -
+        // mrem[k].  The first such (j asc, k asc), then first j2 asc, first k2
+        // asc, is exactly the reference's first move; restart after each move.
+#pragma unroll
+        for (int kk = 0; kk < KPL; ++kk) {
+            const int k = g.gl + G * kk;
+            const int s = shp[kk];
+            for (int j = 0; j < J; ++j) {
+                bool p = false;
+                if (k < R) {
+                    const int64_t u = sUnit[s * J + j];
+                    p = u > 0 && xs[j * RMAX + k] < sCap[s * J + j] && mrem[kk] >= u;
+                }
+                const uint32_t b = g.ballot(p);
+                if (g.gl == 0) Am[j * KPL + kk] = b;
+            }
+        }
+        uint32_t lam_mask = g.ballot(g.gl < J && lamr > 0);
+        g.sync();
+        while (lam_mask) {
+            // feasible classes per owned replica
+            uint32_t F[KPL];
+            uint32_t anyF = 0;
 #pragma unroll
             for (int kk = 0; kk < KPL; ++kk) {
-                e1[kk] = -1;
-                e2[kk] = -1;
-                e1j[kk] = -1;
+                F[kk] = 0;
+                const int k = g.gl + G * kk;
+                if (k >= R) continue;
+                const int s = shp[kk];
+                // top-2 unit over eligible held classes
+                int64_t e1 = -1, e2 = -1;
+                int e1j = -1;
                 uint32_t hb = held[kk];
                 while (hb) {
                     const int j2 = __ffs(hb) - 1;
@@ -485,41 +463,35 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
                         any |= w;
                     }
                     if (any) {
-                        const int64_t u = sUnit[shp[kk] * J + j2];
-                        if (u > e1[kk]) {
-                            e2[kk] = e1[kk];
-                            e1[kk] = u;
-                            e1j[kk] = j2;
-                        } else if (u > e2[kk]) {
-                            e2[kk] = u;
+                        const int64_t u2 = sUnit[s * J + j2];
+                        if (u2 > e1) {
+                            e2 = e1;
+                            e1 = u2;
+                            e1j = j2;
+                        } else if (u2 > e2) {
+                            e2 = u2;
                         }
                     }
                 }
+                uint32_t lb = lam_mask;
+                while (lb) {
+                    const int j = __ffs(lb) - 1;
+                    lb &= lb - 1;
+                    const int64_t u = sUnit[s * J + j];
+                    if (u <= 0 || xs[j * RMAX + k] >= sCap[s * J + j]) continue;
+                    if (mrem[kk] >= u || (e1j == j ? e2 : e1) >= u - mrem[kk]) F[kk] |= 1u << j;
+                }
+                anyF |= F[kk];
             }
-            // first (j, k) with a move
-            int jf = -1, kf = -1;
-            for (int j = 0; j < J && jf < 0; ++j) {
-                if (lam[j] <= 0) continue;
+            anyF = g.or_all(anyF);
+            if (!anyF) break;
+            const int jf = __ffs(anyF) - 1;
+            int kf = -1;
 #pragma unroll
-                for (int kk = KPL - 1; kk >= 0; --kk) {
-                    const int k = g.gl + G * kk;
-                    bool p = false;
-                    if (k < R) {
-                        const int s = shp[kk];
-                        const int64_t u = sUnit[s * J + j];
-                        if (u > 0 && xs[j * RMAX + k] < sCap[s * J + j]) {
-                            if (mrem[kk] >= u) p = true;
-                            else p = (e1j[kk] == j ? e2[kk] : e1[kk]) >= u - mrem[kk];
-                        }
-                    }
-                    const uint32_t b = g.ballot(p);
-                    if (b) {
-                        kf = __ffs(b) - 1 + G * kk;
-                        jf = j;
-                    }
-                }
+            for (int kk = KPL - 1; kk >= 0; --kk) {
+                const uint32_t b = g.ballot((F[kk] >> jf) & 1u);
+                if (b) kf = __ffs(b) - 1 + G * kk;
             }
-            if (jf < 0) break;
             // owner of kf picks the move
             const int ogl = kf & (G - 1);
             int j2 = -1, k2 = -1;
@@ -530,8 +502,10 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
                     const int s = shp[kk];
                     const int64_t u = sUnit[s * J + jf];
                     if (mrem[kk] < u) {
-                        for (int jj = 0; jj < J && j2 < 0; ++jj) {
-                            if (jj == jf || xs[jj * RMAX + kf] <= 0) continue;
+                        uint32_t hb = held[kk] & ~(1u << jf);
+                        while (hb && j2 < 0) {
+                            const int jj = __ffs(hb) - 1;
+                            hb &= hb - 1;
                             if (mrem[kk] + sUnit[s * J + jj] < u) continue;
 #pragma unroll
                             for (int k3 = 0; k3 < KPL; ++k3) {
@@ -548,17 +522,15 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
             }
             j2 = g.bcast(j2, ogl);
             k2 = g.bcast(k2, ogl);
-            // apply
+            // apply the move
 #pragma unroll
             for (int kk = 0; kk < KPL; ++kk) {
                 const int k = g.gl + G * kk;
                 const int s = shp[kk];
                 if (k == kf) {
-                    const int64_t u = sUnit[s * J + jf];
                     xs[jf * RMAX + kf] += 1;
-                    mrem[kk] -= u;
+                    mrem[kk] -= sUnit[s * J + jf];
                     held[kk] |= 1u << jf;
-                    lam[jf] -= 1;
                     if (j2 >= 0) {
                         const int32_t nv = xs[j2 * RMAX + kf] - 1;
                         xs[j2 * RMAX + kf] = nv;
@@ -572,12 +544,28 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
                     held[kk] |= 1u << j2;
                 }
             }
+            if (g.gl == jf) lamr -= 1;
+            lam_mask = g.ballot(g.gl < J && lamr > 0);
+            g.sync();
+            // refresh the A bits of the two replicas that changed
+#pragma unroll
+            for (int kk = 0; kk < KPL; ++kk) {
+                const int k = g.gl + G * kk;
+                if (k == kf || (j2 >= 0 && k == k2)) {
+                    const int s = shp[kk];
+                    for (int j = 0; j < J; ++j) {
+                        const int64_t u = sUnit[s * J + j];
+                        const bool p = u > 0 && xs[j * RMAX + k] < sCap[s * J + j] && mrem[kk] >= u;
+                        if (p) atomicOr(&Am[j * KPL + kk], 1u << g.gl);
+                        else atomicAnd(&Am[j * KPL + kk], ~(1u << g.gl));
+                    }
+                }
+            }
             g.sync();
         }
 
         // ---- objective, sum_pp, key / outputs ----
-        uint32_t served = 0;
-        for (int j = g.gl; j < J; j += G) served += static_cast<uint32_t>(lam_src[j] - lam[j]);
+        uint32_t served = g.gl < J ? static_cast<uint32_t>(lam_src[g.gl] - lamr) : 0u;
         uint32_t spp = 0;
 #pragma unroll
         for (int kk = 0; kk < KPL; ++kk)
@@ -622,10 +610,9 @@ template <int G, int KPL>
 size_t plan_eval_smem(int S, int J, bool stage) {
     constexpr int RMAX = G * KPL;
     constexpr int GPB = 256 / G;
-    size_t shapes = (size_t)S * 8 + (size_t)S * J * 16 + (size_t)S * J * 4 + (size_t)S * kMaxJ + 2 * (size_t)S;
+    size_t shapes = (size_t)S * 8 + (size_t)S * J * 16 + (size_t)S * J * 4 + 2 * (size_t)S * kMaxJ + 2 * (size_t)S;
     shapes = stage ? (shapes + 15) & ~size_t(15) : 0;
-    const size_t per_group = ((size_t)J * RMAX * 4 + kMaxJ * 4 + kMaxJ * KPL * 4 + RMAX + 15) & ~size_t(15);
-    return shapes + per_group * GPB + GPB * 8;
+    return shapes + group_scratch_bytes(J, RMAX, KPL) * GPB + GPB * 8;
 }
 
 template <int G, int KPL>
@@ -1095,8 +1082,10 @@ int launch_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayou
     if (int e = ensure_binom()) return e;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (src.count == 0) return 0;
-    if (rmax <= 8) return run_plan_eval<8, 1>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
-    if (rmax <= 16) return run_plan_eval<16, 1>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
+    // lanes double as class positions in the greedy scan: G >= J
+    const int need = rmax > prm.J ? rmax : prm.J;
+    if (need <= 8) return run_plan_eval<8, 1>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
+    if (need <= 16) return run_plan_eval<16, 1>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
     if (rmax <= 32) return run_plan_eval<32, 1>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
     if (rmax <= 64) return run_plan_eval<32, 2>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
     if (rmax <= 128) return run_plan_eval<32, 4>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
