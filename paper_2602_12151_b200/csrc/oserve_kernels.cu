@@ -392,15 +392,19 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
             }
             const uint64_t cost = static_cast<uint64_t>(a) * static_cast<uint64_t>(u);
             const uint64_t csum = g.scan_sat64(cost, static_cast<uint64_t>(Ms) + 1);
+            // exclusive prefix from the previous lane: unsaturated up to the
+            // binding position (csum - cost is not, once saturated)
+            uint64_t excl = __shfl_up_sync(g.mask, csum, 1, G);
+            if (g.gl == 0) excl = 0;
             const uint32_t ob = g.ballot(act && csum > static_cast<uint64_t>(Ms));
             const int pb = ob ? __ffs(ob) - 1 : ol;
             int32_t take = 0;
             if (act) {
                 if (g.gl < pb) take = a;
-                else if (g.gl == pb) take = quot_small(Ms - static_cast<int64_t>(csum - cost), u, sInv[s * J + j]);
+                else if (g.gl == pb) take = quot_small(Ms - static_cast<int64_t>(excl), u, sInv[s * J + j]);
                 if (take) xs[j * RMAX + k] = take;
             }
-            const uint64_t used_l = (g.gl == pb) ? (csum - cost) + static_cast<uint64_t>(take) * static_cast<uint64_t>(u) : csum;
+            const uint64_t used_l = (g.gl == pb) ? excl + static_cast<uint64_t>(take) * static_cast<uint64_t>(u) : csum;
             const uint64_t used = ol ? g.bcast(used_l, pb < ol ? pb : ol - 1) : 0ull;
             const uint32_t hb = g.or_all(take > 0 ? (1u << j) : 0u);
             const int rp = g.gl < J ? sRank[s * kMaxJ + g.gl] : 0xff;
