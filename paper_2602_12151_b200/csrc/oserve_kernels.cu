@@ -211,9 +211,10 @@ struct Group {
     __device__ __forceinline__ uint32_t sum(uint32_t v) const { return __reduce_add_sync(mask, v); }
     __device__ __forceinline__ uint32_t or_all(uint32_t v) const { return __reduce_or_sync(mask, v); }
     // inclusive prefix sum of u64, saturating at `sat` (sat + sat must not overflow)
-    __device__ __forceinline__ uint64_t scan_sat64(uint64_t v, uint64_t sat) const {
+    __device__ __forceinline__ uint64_t scan_sat64(uint64_t v, uint64_t sat, int width) const {
 #pragma unroll
         for (int d = 1; d < G; d <<= 1) {
+            if (d >= width) break;
             const uint64_t o = __shfl_up_sync(mask, v, d, G);
             if (gl >= d) {
                 v += o;
@@ -304,6 +305,8 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
     __syncthreads();
 
     const Grp g;
+    int jw = 1;
+    while (jw < J) jw <<= 1;  // scan width over class positions
     uint64_t best = kNoKey;
     const uint64_t ngroups = static_cast<uint64_t>(gridDim.x) * GPB;
 
@@ -358,7 +361,11 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
         for (int kk = 0; kk < KPL; ++kk) {
             const int k = g.gl + G * kk;
             if (k < R) shpS[k] = static_cast<uint16_t>(shp[kk]);
-            for (int j = 0; j < J; ++j) xs[j * RMAX + k] = 0;
+        }
+        {
+            int4 *xz = reinterpret_cast<int4 *>(xs);
+            const int n4 = (J * RMAX) >> 2;  // RMAX is a multiple of 4
+            for (int q = g.gl; q < n4; q += G) xz[q] = make_int4(0, 0, 0, 0);
         }
         g.sync();
 
@@ -391,7 +398,7 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
                 a = min(sCap[s * J + j], lamp);
             }
             const uint64_t cost = static_cast<uint64_t>(a) * static_cast<uint64_t>(u);
-            const uint64_t csum = g.scan_sat64(cost, static_cast<uint64_t>(Ms) + 1);
+            const uint64_t csum = g.scan_sat64(cost, static_cast<uint64_t>(Ms) + 1, jw);
             // exclusive prefix from the previous lane: unsaturated up to the
             // binding position (csum - cost is not, once saturated)
             uint64_t excl = __shfl_up_sync(g.mask, csum, 1, G);
@@ -421,11 +428,16 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
 
         // ---- exchange_improve (flowassign.cpp:411-448) ----
         // A[j] = replicas able to take one more class-j request directly (one
-        // G-bit word per ownership slot kk).  (j, k) has a move iff lam_j > 0,
-        // unit > 0, x < cap and either mrem >= unit (direct) or some held
-        // class j2 != j has A[j2]\{k} non-empty and unit[k][j2] >= unit[k][j] -
-        // mrem[k].  The first such (j asc, k asc), then first j2 asc, first k2
-        // asc, is exactly the reference's first move; restart after each move.
+        // G-bit word per ownership slot kk; lane j is the only writer of class
+        // j's words).  (j, k) has a move iff lam_j > 0, unit > 0, x < cap and
+        // either mrem >= unit (direct) or some held class j2 != j has
+        // A[j2]\{k} non-empty and unit[k][j2] >= unit[k][j] - mrem[k].  The
+        // first such (j asc, k asc), then first j2 asc, first k2 asc, is the
+        // reference's first move.  F[kk] caches the feasible classes of each
+        // owned replica; a move changes only replicas kf, k2 (and lam_jf), so
+        // after it F is recomputed for those two and for replicas holding a
+        // class whose A set crossed size 2 (the only way A[j2]\{k} can change
+        // emptiness for a third replica).
 #pragma unroll
         for (int kk = 0; kk < KPL; ++kk) {
             const int k = g.gl + G * kk;
@@ -442,51 +454,52 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
         }
         uint32_t lam_mask = g.ballot(g.gl < J && lamr > 0);
         g.sync();
-        while (lam_mask) {
-            // feasible classes per owned replica
-            uint32_t F[KPL];
+        // feasible classes of owned replica kk (top-2 eligible held unit)
+        auto feasible_row = [&](int kk) -> uint32_t {
+            const int k = g.gl + G * kk;
+            if (k >= R) return 0u;
+            const int s = shp[kk];
+            int64_t e1 = -1, e2 = -1;
+            int e1j = -1;
+            uint32_t hb = held[kk];
+            while (hb) {
+                const int j2 = __ffs(hb) - 1;
+                hb &= hb - 1;
+                uint32_t any = 0;
+#pragma unroll
+                for (int k2 = 0; k2 < KPL; ++k2) {
+                    uint32_t w = Am[j2 * KPL + k2];
+                    if (k2 == kk) w &= ~(1u << g.gl);
+                    any |= w;
+                }
+                if (any) {
+                    const int64_t u2 = sUnit[s * J + j2];
+                    if (u2 > e1) {
+                        e2 = e1;
+                        e1 = u2;
+                        e1j = j2;
+                    } else if (u2 > e2) {
+                        e2 = u2;
+                    }
+                }
+            }
+            uint32_t f = 0, lb = lam_mask;
+            while (lb) {
+                const int j = __ffs(lb) - 1;
+                lb &= lb - 1;
+                const int64_t u = sUnit[s * J + j];
+                if (u <= 0 || xs[j * RMAX + k] >= sCap[s * J + j]) continue;
+                if (mrem[kk] >= u || (e1j == j ? e2 : e1) >= u - mrem[kk]) f |= 1u << j;
+            }
+            return f;
+        };
+        uint32_t F[KPL];
+#pragma unroll
+        for (int kk = 0; kk < KPL; ++kk) F[kk] = feasible_row(kk);
+        for (;;) {
             uint32_t anyF = 0;
 #pragma unroll
-            for (int kk = 0; kk < KPL; ++kk) {
-                F[kk] = 0;
-                const int k = g.gl + G * kk;
-                if (k >= R) continue;
-                const int s = shp[kk];
-                // top-2 unit over eligible held classes
-                int64_t e1 = -1, e2 = -1;
-                int e1j = -1;
-                uint32_t hb = held[kk];
-                while (hb) {
-                    const int j2 = __ffs(hb) - 1;
-                    hb &= hb - 1;
-                    uint32_t any = 0;
-#pragma unroll
-                    for (int k2 = 0; k2 < KPL; ++k2) {
-                        uint32_t w = Am[j2 * KPL + k2];
-                        if (k2 == kk) w &= ~(1u << g.gl);
-                        any |= w;
-                    }
-                    if (any) {
-                        const int64_t u2 = sUnit[s * J + j2];
-                        if (u2 > e1) {
-                            e2 = e1;
-                            e1 = u2;
-                            e1j = j2;
-                        } else if (u2 > e2) {
-                            e2 = u2;
-                        }
-                    }
-                }
-                uint32_t lb = lam_mask;
-                while (lb) {
-                    const int j = __ffs(lb) - 1;
-                    lb &= lb - 1;
-                    const int64_t u = sUnit[s * J + j];
-                    if (u <= 0 || xs[j * RMAX + k] >= sCap[s * J + j]) continue;
-                    if (mrem[kk] >= u || (e1j == j ? e2 : e1) >= u - mrem[kk]) F[kk] |= 1u << j;
-                }
-                anyF |= F[kk];
-            }
+            for (int kk = 0; kk < KPL; ++kk) anyF |= F[kk];
             anyF = g.or_all(anyF);
             if (!anyF) break;
             const int jf = __ffs(anyF) - 1;
@@ -551,21 +564,41 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
             if (g.gl == jf) lamr -= 1;
             lam_mask = g.ballot(g.gl < J && lamr > 0);
             g.sync();
-            // refresh the A bits of the two replicas that changed
+            // refresh the A bits of rows kf and k2 (lane j = class j)
+            uint32_t dirty = 0;
+            for (int q = 0; q < (j2 >= 0 ? 2 : 1); ++q) {
+                const int r = q == 0 ? kf : k2;
+                const int rgl = r & (G - 1), rkk = r / G;
+                int64_t mr = 0;
 #pragma unroll
-            for (int kk = 0; kk < KPL; ++kk) {
-                const int k = g.gl + G * kk;
-                if (k == kf || (j2 >= 0 && k == k2)) {
-                    const int s = shp[kk];
-                    for (int j = 0; j < J; ++j) {
-                        const int64_t u = sUnit[s * J + j];
-                        const bool p = u > 0 && xs[j * RMAX + k] < sCap[s * J + j] && mrem[kk] >= u;
-                        if (p) atomicOr(&Am[j * KPL + kk], 1u << g.gl);
-                        else atomicAnd(&Am[j * KPL + kk], ~(1u << g.gl));
+                for (int kk = 0; kk < KPL; ++kk)
+                    if (kk == rkk) mr = mrem[kk];
+                mr = g.bcast(mr, rgl);
+                if (g.gl < J) {
+                    const int j = g.gl;
+                    const int sr = shpS[r];
+                    const int64_t u = sUnit[sr * J + j];
+                    const bool p = u > 0 && xs[j * RMAX + r] < sCap[sr * J + j] && mr >= u;
+                    const uint32_t bit = 1u << rgl;
+                    const uint32_t old = Am[j * KPL + rkk];
+                    if (p != ((old & bit) != 0)) {
+                        int pc = 0;
+#pragma unroll
+                        for (int k3 = 0; k3 < KPL; ++k3) pc += __popc(Am[j * KPL + k3]);
+                        Am[j * KPL + rkk] = p ? (old | bit) : (old & ~bit);
+                        const int pn = pc + (p ? 1 : -1);
+                        if (pc < 2 || pn < 2) dirty |= 1u << j;
                     }
                 }
             }
+            dirty = g.or_all(dirty);
             g.sync();
+#pragma unroll
+            for (int kk = 0; kk < KPL; ++kk) {
+                const int k = g.gl + G * kk;
+                if (k == kf || k == k2 || (held[kk] & dirty)) F[kk] = feasible_row(kk);
+                else F[kk] &= lam_mask;
+            }
         }
 
         // ---- objective, sum_pp, key / outputs ----
