@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "oserve_internal.h"
 
@@ -1119,10 +1120,21 @@ int launch_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayou
     if (int e = ensure_binom()) return e;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (src.count == 0) return 0;
-    // lanes double as class positions in the greedy scan: G >= J
+    // lanes double as class positions in the greedy scan: G >= J.  Default:
+    // the narrowest group that covers the classes (more plans per warp,
+    // every lane busy in the class-parallel phases); OSERVE_K1_G=32 forces
+    // warp-wide groups (A/B experiments).
     const int need = rmax > prm.J ? rmax : prm.J;
+    static const int force32 = [] {
+        const char *e = getenv("OSERVE_K1_G");
+        return e && atoi(e) == 32;
+    }();
     if (need <= 8) return run_plan_eval<8, 1>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
     if (need <= 16) return run_plan_eval<16, 1>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
+    if (prm.J <= 16 && !force32) {
+        if (rmax <= 32) return run_plan_eval<16, 2>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
+        if (rmax <= 64) return run_plan_eval<16, 4>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
+    }
     if (rmax <= 32) return run_plan_eval<32, 1>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
     if (rmax <= 64) return run_plan_eval<32, 2>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
     if (rmax <= 128) return run_plan_eval<32, 4>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
