@@ -236,6 +236,21 @@ int oserve_gpu_switch_plan(oserve_gpu_ctx *ctx, const oserve_deployment *src,
                            const oserve_deployment *dst, int capacity, oserve_transfer *transfers,
                            int *num_transfers, double *est_seconds);
 
+/* ---- device-free helpers (host protocol of the multi-GPU round) ------- */
+
+/* Plans of shard `rank` of `world` when the global plan order is dealt out
+ * in interleaved chunks of `chunk` plans. */
+uint64_t oserve_shard_count(uint64_t total, uint64_t chunk, int rank, int world);
+/* Global plan rank of this shard's local index. */
+uint64_t oserve_shard_global_rank(uint64_t local, uint64_t chunk, int rank, int world);
+/* Bit layout of the packed selection key for a space: key =
+ * ((obj_max - objective) << sh_obj) | (partition << sh_part) |
+ * (sum_pp << sh_spp) | local_rank.  OSERVE_ERR_TOO_LARGE if > 63 bits. */
+int oserve_key_layout(int64_t total_demand, int64_t partitions, int devices, uint64_t max_plans_per_partition,
+                      int *sh_obj, int *sh_part, int *sh_spp, uint64_t *obj_max);
+/* Default interleave chunk of oserve_gpu_set_shard. */
+#define OSERVE_SHARD_CHUNK 4096
+
 /* Kernel launches issued by this context since creation (evidence counter). */
 uint64_t oserve_gpu_launch_count(const oserve_gpu_ctx *ctx);
 /* Host->device / device->host bytes copied by this context since creation

@@ -1,0 +1,165 @@
+"""Generate tests/golden/*.json from the REFERENCE itself (oracle/_ref).
+
+TEST INFRASTRUCTURE — runs in the build container (needs oracle/_ref built
+from /root/reference).  The committed fixtures pin the CPU restatement and
+the GPU path on machines without the reference:
+
+  kats.json        the reference tests' known answers (test_costmodel.cpp,
+                   test_flowassign.cpp) recomputed through the reference API
+  solve.json       solve_assignment on seeded random instances (incl. B&B)
+  rounds.json      per-config round winners (exhaustive / ordered / canonical)
+  plans_<cfg>.json per-plan objectives: every plan of cfg1 / cfg1_bnb, a
+                   seeded sample elsewhere, plus an all-plan checksum for cfg2
+  switch.json      greedy_plan/estimate_time on seeded deployment pairs
+"""
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+sys.path.insert(0, ROOT)
+sys.path.insert(0, HERE)
+
+from paper_2602_12151_b200 import core, workloads  # noqa: E402
+from pyoracle import Oracle, Problem  # noqa: E402
+
+OUT = os.path.join(ROOT, "tests", "golden")
+THREADS = os.cpu_count() or 1
+
+
+def problem(w):
+    return Problem(w.cluster, w.model, w.types, w.lam, w.span_s, w.params)
+
+
+def dep_json(d: core.Deployment):
+    return [[r.device_ids, r.tp, r.pp] for r in d.replicas]
+
+
+def objective_digest(obj: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(obj, dtype="<i8").tobytes()).hexdigest()
+
+
+def random_instances(seed, count, max_r, max_j, max_lam, max_n=100):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(count):
+        R, J = int(rng.integers(1, max_r + 1)), int(rng.integers(1, max_j + 1))
+        n = rng.integers(1, max_n + 1, (R, J))
+        n[rng.random((R, J)) < 0.125] = 0
+        e = (rng.random((R, J)) * (n + 1)).astype(np.int64)
+        lam = rng.integers(0, max_lam + 1, J)
+        out.append((n.tolist(), e.tolist(), lam.tolist()))
+    return out
+
+
+def main():
+    os.makedirs(OUT, exist_ok=True)
+    ref = Oracle("ref")
+
+    # ---- KATs (test_costmodel.cpp / test_flowassign.cpp) ----
+    kats = {"normalize": [], "capacity": [], "assignment": []}
+    for row in ([80, 50], [7], [12, 18, 30], [80, 0, 50],
+                [(1 << 31) - 1, (1 << 31) - 99, (1 << 31) - 365]):
+        M, units, scaled = ref.normalize(row)
+        kats["normalize"].append({"n": row, "M": M, "units": units, "scaled": scaled})
+    # lcm_80_50_fixture (fixtures.hpp:85-101) and appendix_d_fixture (:113-129)
+    lcm = dict(params=core.ProfileParams(1.0 / 256.0, 1.0 / 512.0, 1.0, 1e-9, 0.0),
+               model=core.ModelSpec("lcm-fixture", core.KGB, 1, 1, 1, core.KGB),
+               types=[core.WorkloadType(0, 128.0, 64.0), core.WorkloadType(1, 128.0, 256.0)], span=50.0,
+               cluster=core.cluster(1, 4), deps=[[([0], 1, 1)], [([0], 1, 1), ([1], 1, 1)]])
+    appd = dict(params=core.ProfileParams(0.002, 0.002, 1.0, 0.0004, 0.0),
+                model=core.ModelSpec("appendix-d", core.KGB, 1, 1, 1, core.KGB),
+                types=[core.WorkloadType(0, 131.0, 48.0), core.WorkloadType(1, 121.0, 196.0)], span=1.0,
+                cluster=core.cluster(2, 4), deps=[[([0, 1, 2, 3], 2, 2), ([4, 5], 2, 1), ([6, 7], 2, 1)]])
+    for name, f in (("lcm_80_50", lcm), ("appendix_d", appd)):
+        pr = Problem(f["cluster"], f["model"], f["types"], [0, 0], f["span"], f["params"])
+        for d in f["deps"]:
+            dep = core.Deployment([core.ReplicaConfig(ids, tp, pp) for ids, tp, pp in d])
+            t = ref.capacity_table(pr, dep)
+            kats["capacity"].append({"fixture": name, "deployment": d, "n": t.n, "e": t.e, "latency": t.latency,
+                                     "cluster": [len(f["cluster"].machines), len(f["cluster"].machines[0].device_ids)],
+                                     "params": f["params"].__dict__, "model": f["model"].__dict__,
+                                     "types": [t_.__dict__ for t_ in f["types"]], "span": f["span"]})
+    for n, e, lam, expect in (([[80, 50], [80, 50]], [[80, 50], [80, 50]], [7, 4], 11),
+                              ([[200, 100], [200, 100]], [[200, 100], [200, 100]], [50, 100], 150),
+                              ([[10, 5], [5, 3], [5, 3]], [[10, 5], [5, 3], [5, 3]], [5, 60], None)):
+        ll = ref.solve_assignment(n, e, lam)
+        kats["assignment"].append({"n": n, "e": e, "lambda": lam, "objective": ll.assignment.objective,
+                                   "x": ll.assignment.x, "expect": expect})
+    json.dump(kats, open(os.path.join(OUT, "kats.json"), "w"), indent=0)
+
+    # ---- solve_assignment on seeded random instances ----
+    solve = []
+    for seed, cnt, mr, mj, ml in ((7, 80, 3, 3, 60), (11, 120, 6, 5, 500), (13, 60, 12, 8, 3000)):
+        for n, e, lam in random_instances(seed, cnt, mr, mj, ml):
+            ll = ref.solve_assignment(n, e, lam)
+            solve.append({"seed": seed, "n": n, "e": e, "lambda": lam, "objective": ll.assignment.objective,
+                          "x": ll.assignment.x, "M": ll.M, "unit": ll.unit, "used": ll.used})
+    json.dump(solve, open(os.path.join(OUT, "solve.json"), "w"))
+
+    # ---- rounds and per-plan objectives ----
+    rounds = {}
+    for name in ("cfg1", "cfg1_bnb"):
+        w = workloads.load(name)
+        pr = problem(w)
+        s = ref.exhaustive(pr, parallel=True)
+        rounds[name] = {"kind": "search::exhaustive", "objective": s.throughput, "iterations": s.iterations,
+                        "deployment": dep_json(s.deployment)}
+        parts, plans = ref.space_info(pr, w.space_mode, w.space_sizes)
+        obj, spp, _ = ref.evaluate_ranks(pr, w.space_mode, np.arange(plans, dtype=np.uint64), w.space_sizes,
+                                         threads=THREADS)
+        json.dump({"partitions": parts, "plans": plans, "ranks": list(range(plans)), "objective": obj.tolist(),
+                   "sum_pp": spp.tolist()}, open(os.path.join(OUT, f"plans_{name}.json"), "w"))
+    for name in ("cfg2", "cfg2_low"):
+        w = workloads.load(name)
+        pr = problem(w)
+        s = ref.round(pr, w.space_mode, w.space_sizes, threads=THREADS)
+        rounds[name] = {"kind": "partitions_desc + search::best_strategies, first wins", "objective": s.throughput,
+                        "partitions": s.iterations, "plans": s.plans, "partition_index": s.partition_index,
+                        "local_rank": s.local_rank, "sum_pp": s.sum_pp, "deployment": dep_json(s.deployment)}
+        parts, plans = ref.space_info(pr, w.space_mode, w.space_sizes)
+        ranks = np.arange(plans, dtype=np.uint64)
+        obj, spp, _ = ref.evaluate_ranks(pr, w.space_mode, ranks, w.space_sizes, threads=THREADS)
+        sample = np.random.default_rng(12151).integers(0, plans, 2000)
+        json.dump({"partitions": parts, "plans": plans, "all_objective_sha256": objective_digest(obj),
+                   "objective_sum": int(obj.sum()), "ranks": sample.tolist(), "objective": obj[sample].tolist(),
+                   "sum_pp": spp[sample].tolist()}, open(os.path.join(OUT, f"plans_{name}.json"), "w"))
+    for name in ("cfg3_70b", "cfg3_7b", "cfg5", "cfg5_low"):
+        w = workloads.load(name)
+        pr = problem(w)
+        parts, plans = ref.space_info(pr, w.space_mode, w.space_sizes)
+        sample = np.unique(np.random.default_rng(12151).integers(0, plans, 3000)).astype(np.uint64)
+        obj, spp, _ = ref.evaluate_ranks(pr, w.space_mode, sample, w.space_sizes, threads=THREADS)
+        json.dump({"partitions": parts, "plans": plans, "ranks": sample.tolist(), "objective": obj.tolist(),
+                   "sum_pp": spp.tolist()}, open(os.path.join(OUT, f"plans_{name}.json"), "w"))
+        if name == "cfg3_70b":
+            s = ref.round(pr, w.space_mode, w.space_sizes, threads=THREADS)
+            rounds[name] = {"kind": "canonical space through search::evaluate_deployment", "objective": s.throughput,
+                            "partitions": s.iterations, "plans": s.plans, "partition_index": s.partition_index,
+                            "local_rank": s.local_rank, "sum_pp": s.sum_pp, "deployment": dep_json(s.deployment)}
+    json.dump(rounds, open(os.path.join(OUT, "rounds.json"), "w"), indent=1)
+
+    # ---- switching: greedy_plan + estimate_time on seeded pairs ----
+    sw = []
+    for name in ("cfg1", "cfg2", "cfg5"):
+        w = workloads.load(name)
+        pr = problem(w)
+        parts, plans = ref.space_info(pr, w.space_mode, w.space_sizes)
+        rng = np.random.default_rng(99)
+        deps = [ref.space_plan(pr, w.space_mode, int(r), w.space_sizes)[0] for r in rng.integers(0, plans, 12)]
+        for a in range(0, len(deps) - 1, 2):
+            src, dst = deps[a], deps[a + 1]
+            plan, mx = ref.switch_plan(w.cluster, w.model.param_bytes, src, dst)
+            sw.append({"config": name, "src": dep_json(src), "dst": dep_json(dst), "est_seconds": plan.est_seconds,
+                       "max_link_bytes": mx, "transfers": [[t.range.begin, t.range.end, t.src, t.dst]
+                                                           for t in plan.transfers]})
+    json.dump(sw, open(os.path.join(OUT, "switch.json"), "w"))
+    print("golden fixtures written to", OUT)
+
+
+if __name__ == "__main__":
+    main()

@@ -26,6 +26,7 @@ EXPORTS = [
     "oserve_gpu_evaluate_ranks", "oserve_gpu_evaluate_deployments", "oserve_gpu_plan_detail",
     "oserve_gpu_solve_batch", "oserve_gpu_switch_cost_batch", "oserve_gpu_switch_plan",
     "oserve_gpu_launch_count", "oserve_gpu_copy_bytes",
+    "oserve_shard_count", "oserve_shard_global_rank", "oserve_key_layout",
 ]
 
 _lib = None
@@ -69,8 +70,40 @@ def load_library() -> C.CDLL:
     L.oserve_gpu_launch_count.argtypes = [vp]
     L.oserve_gpu_launch_count.restype = C.c_uint64
     L.oserve_gpu_copy_bytes.argtypes = [vp, P(C.c_uint64), P(C.c_uint64)]
+    L.oserve_shard_count.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.c_int]
+    L.oserve_shard_count.restype = C.c_uint64
+    L.oserve_shard_global_rank.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.c_int]
+    L.oserve_shard_global_rank.restype = C.c_uint64
+    L.oserve_key_layout.argtypes = [C.c_int64, C.c_int64, C.c_int, C.c_uint64, P(C.c_int), P(C.c_int), P(C.c_int),
+                                    P(C.c_uint64)]
     _lib = L
     return L
+
+
+SHARD_CHUNK = 4096
+
+
+def shard_count(total: int, rank: int, world: int, chunk: int = SHARD_CHUNK) -> int:
+    """Plans of shard `rank` (C++ host logic, no device needed)."""
+    return int(load_library().oserve_shard_count(total, chunk, rank, world))
+
+
+def shard_global_rank(local: int, rank: int, world: int, chunk: int = SHARD_CHUNK) -> int:
+    return int(load_library().oserve_shard_global_rank(local, chunk, rank, world))
+
+
+def key_layout(total_demand: int, partitions: int, devices: int, max_plans: int):
+    """(sh_obj, sh_part, sh_spp, obj_max) of the packed selection key."""
+    a, b, c, m = C.c_int(), C.c_int(), C.c_int(), C.c_uint64()
+    st = load_library().oserve_key_layout(total_demand, partitions, devices, max_plans, C.byref(a), C.byref(b),
+                                          C.byref(c), C.byref(m))
+    A.raise_for(st, "selection key does not fit 63 bits")
+    return a.value, b.value, c.value, m.value
+
+
+def pack_key(layout, objective: int, partition: int, sum_pp: int, local_rank: int) -> int:
+    sh_obj, sh_part, sh_spp, obj_max = layout
+    return ((obj_max - objective) << sh_obj) | (partition << sh_part) | (sum_pp << sh_spp) | local_rank
 
 
 def _np_ptr(a, t):

@@ -185,7 +185,7 @@ struct oserve_gpu_ctx {
     Space space;
     KeyLayout key{};
     int rank = 0, world = 1;
-    uint64_t chunk = 4096;
+    uint64_t chunk = OSERVE_SHARD_CHUNK;
     // scratch
     DBuf d_key, d_obj, d_spp, d_x, d_used, d_aborted, d_aborted_n, d_ranks, d_listR, d_listOff, d_listShapes,
         d_listLam, d_sw[12];
@@ -496,27 +496,36 @@ void refresh_exact(oserve_gpu_ctx &c, Space &sp) {
     sp.view.exact = sp.d_exact.upload(sp.exact, c.stream);
 }
 
+// Key bit layout: objective (descending) above partition, sum_pp, rank.
+bool key_layout(int64_t total_demand, int64_t parts, int devices, uint64_t max_count, KeyLayout &k) {
+    const int b_obj = bits_for(static_cast<uint64_t>(total_demand));
+    const int b_part = bits_for(parts > 0 ? static_cast<uint64_t>(parts - 1) : 0);
+    const int b_spp = bits_for(static_cast<uint64_t>(devices));
+    const int b_loc = bits_for(max_count ? max_count - 1 : 0);
+    if (b_obj + b_part + b_spp + b_loc > 63) return false;
+    k.sh_spp = b_loc;
+    k.sh_part = b_loc + b_spp;
+    k.sh_obj = b_loc + b_spp + b_part;
+    k.obj_max = (uint64_t{1} << b_obj) - 1;
+    return true;
+}
+
 void make_key_layout(oserve_gpu_ctx &c, const Space &sp) {
     int64_t tot = 0;
     for (int64_t v : c.lambda) tot += v;
-    const int b_obj = bits_for(static_cast<uint64_t>(tot));
-    const int b_part = bits_for(sp.parts.empty() ? 0 : sp.parts.size() - 1);
-    const int b_spp = bits_for(static_cast<uint64_t>(c.D()));
-    const int b_loc = bits_for(sp.max_count ? sp.max_count - 1 : 0);
-    if (b_obj + b_part + b_spp + b_loc > 63)
-        fail(OSERVE_ERR_TOO_LARGE, "selection key does not fit 63 bits (" + std::to_string(b_obj + b_part + b_spp + b_loc) + ")");
-    c.key.sh_spp = b_loc;
-    c.key.sh_part = b_loc + b_spp;
-    c.key.sh_obj = b_loc + b_spp + b_part;
-    c.key.obj_max = (uint64_t{1} << b_obj) - 1;
+    if (!key_layout(tot, static_cast<int64_t>(sp.parts.size()), c.D(), sp.max_count, c.key))
+        fail(OSERVE_ERR_TOO_LARGE, "selection key does not fit 63 bits");
 }
 
-uint64_t shard_count(const oserve_gpu_ctx &c, uint64_t total) {
-    const uint64_t ch = c.chunk, w = static_cast<uint64_t>(c.world), r = static_cast<uint64_t>(c.rank);
+uint64_t shard_count_of(uint64_t total, uint64_t ch, uint64_t r, uint64_t w) {
     const uint64_t full = total / ch, rem = total % ch;
     uint64_t n = full > r ? ((full - r + w - 1) / w) * ch : 0;
     if (rem && full % w == r) n += rem;
     return n;
+}
+
+uint64_t shard_count(const oserve_gpu_ctx &c, uint64_t total) {
+    return shard_count_of(total, c.chunk, static_cast<uint64_t>(c.rank), static_cast<uint64_t>(c.world));
 }
 
 void unrank_host(const Space &sp, uint64_t rank, int64_t &p, uint64_t &local, std::vector<int> &picks) {
@@ -930,6 +939,28 @@ int oserve_gpu_destroy(oserve_gpu_ctx *ctx) {
 const char *oserve_gpu_last_error(const oserve_gpu_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 uint64_t oserve_gpu_launch_count(const oserve_gpu_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+uint64_t oserve_shard_count(uint64_t total, uint64_t chunk, int rank, int world) {
+    if (chunk == 0 || world < 1 || rank < 0 || rank >= world) return 0;
+    return shard_count_of(total, chunk, static_cast<uint64_t>(rank), static_cast<uint64_t>(world));
+}
+
+uint64_t oserve_shard_global_rank(uint64_t local, uint64_t chunk, int rank, int world) {
+    // same mapping as the kernels' shard_rank (oserve_kernels.cu)
+    const uint64_t c = local / chunk;
+    return (c * static_cast<uint64_t>(world) + static_cast<uint64_t>(rank)) * chunk + (local - c * chunk);
+}
+
+int oserve_key_layout(int64_t total_demand, int64_t partitions, int devices, uint64_t max_plans_per_partition,
+                      int *sh_obj, int *sh_part, int *sh_spp, uint64_t *obj_max) {
+    KeyLayout k{};
+    if (!key_layout(total_demand, partitions, devices, max_plans_per_partition, k)) return OSERVE_ERR_TOO_LARGE;
+    *sh_obj = k.sh_obj;
+    *sh_part = k.sh_part;
+    *sh_spp = k.sh_spp;
+    *obj_max = k.obj_max;
+    return OSERVE_OK;
+}
 
 int oserve_gpu_copy_bytes(const oserve_gpu_ctx *ctx, uint64_t *h2d_bytes, uint64_t *d2h_bytes) {
     if (!ctx) return OSERVE_ERR_INVALID_ARGUMENT;

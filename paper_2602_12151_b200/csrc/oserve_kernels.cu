@@ -380,12 +380,22 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
         // sequential fill; no 64-bit division.
         int64_t mrem[KPL];
         uint32_t held[KPL];
+        uint32_t areg[KPL];  // lane c: A[c] word per ownership slot, built replica by replica
 #pragma unroll
         for (int kk = 0; kk < KPL; ++kk) {
             mrem[kk] = 0;
             held[kk] = 0;
+            areg[kk] = 0;
         }
-        for (int k = 0; k < R; ++k) {
+        // shape-run boundaries: bit k set when replica k+1 has another shape
+        uint32_t bnd[KPL];
+#pragma unroll
+        for (int kk = 0; kk < KPL; ++kk) {
+            const int k = g.gl + G * kk;
+            const bool last = k < R && (k + 1 == R || shpS[k + 1] != shpS[k]);
+            bnd[kk] = g.ballot(last);
+        }
+        for (int k = 0; k < R;) {
             const int s = shpS[k];
             const int ol = sOlen[s];
             const bool act = g.gl < ol;
@@ -393,10 +403,11 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
             const int32_t lamp = g.bcast(lamr, j);
             const int64_t Ms = sM[s];
             int64_t u = 1;
-            int32_t a = 0;
+            int32_t a = 0, capj = 0;
             if (act) {
                 u = sUnit[s * J + j];
-                a = min(sCap[s * J + j], lamp);
+                capj = sCap[s * J + j];
+                a = min(capj, lamp);
             }
             const uint64_t cost = static_cast<uint64_t>(a) * static_cast<uint64_t>(u);
             const uint64_t csum = g.scan_sat64(cost, static_cast<uint64_t>(Ms) + 1, jw);
@@ -410,20 +421,59 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
             if (act) {
                 if (g.gl < pb) take = a;
                 else if (g.gl == pb) take = quot_small(Ms - static_cast<int64_t>(excl), u, sInv[s * J + j]);
-                if (take) xs[j * RMAX + k] = take;
             }
             const uint64_t used_l = (g.gl == pb) ? excl + static_cast<uint64_t>(take) * static_cast<uint64_t>(u) : csum;
             const uint64_t used = ol ? g.bcast(used_l, pb < ol ? pb : ol - 1) : 0ull;
             const uint32_t hb = g.or_all(take > 0 ? (1u << j) : 0u);
-            const int rp = g.gl < J ? sRank[s * kMaxJ + g.gl] : 0xff;
-            const int32_t tk = g.bcast(take, rp < G ? rp : 0);
-            if (rp != 0xff) lamr -= tk;
+            const int64_t mfin = Ms - static_cast<int64_t>(used);
+            // run-length step: the next c replicas of the same shape take the
+            // identical fill while lam_p - i*take_p >= a_p at every position
+            // p <= pb with take_p > 0 (then min(cap, lam) is unchanged up to
+            // the binding position, hence so are the costs and the fill).
+            int run_end = R - 1;
 #pragma unroll
-            for (int kk = 0; kk < KPL; ++kk)
-                if (g.gl + G * kk == k) {
-                    mrem[kk] = Ms - static_cast<int64_t>(used);
+            for (int kk = KPL - 1; kk >= 0; --kk) {
+                const int lo = k - G * kk;  // first bit of this slot at or after k
+                uint32_t m = bnd[kk];
+                if (lo >= G) m = 0;
+                else if (lo > 0) m &= ~((1u << lo) - 1u);
+                if (m) run_end = __ffs(m) - 1 + G * kk;
+            }
+            uint32_t cb = 0xffffffffu;
+            if (act && take > 0 && g.gl <= pb) cb = static_cast<uint32_t>(lamp - a) / static_cast<uint32_t>(take);
+            cb = __reduce_min_sync(g.mask, cb);
+            const int c = min(static_cast<int>(min(cb, 0x7fffffffu)), run_end - k);
+            if (act && take) {
+                for (int q = 0; q <= c; ++q) xs[j * RMAX + k + q] = take;
+            }
+            // direct-take bit of (class at this position, replicas k..k+c)
+            const bool abit = act && take < capj && mfin >= u;
+            const int rp = g.gl < J ? sRank[s * kMaxJ + g.gl] : 0xff;
+            const int src_p = rp < G ? rp : 0;
+            const int32_t tk = g.bcast(take, src_p);
+            const bool ab = g.bcast(abit ? 1 : 0, src_p) != 0;
+            if (rp != 0xff) {
+                lamr -= tk * (c + 1);
+                if (ab) {
+#pragma unroll
+                    for (int kk = 0; kk < KPL; ++kk) {
+                        const int lo = max(k, G * kk) - G * kk, hi = min(k + c, G * kk + G - 1) - G * kk;
+                        if (lo <= hi) {
+                            const uint32_t span = (hi - lo == 31) ? 0xffffffffu : (((1u << (hi - lo + 1)) - 1u) << lo);
+                            areg[kk] |= span;
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int kk = 0; kk < KPL; ++kk) {
+                const int kq = g.gl + G * kk;
+                if (kq >= k && kq <= k + c) {
+                    mrem[kk] = mfin;
                     held[kk] = hb;
                 }
+            }
+            k += c + 1;
         }
         g.sync();
 
@@ -439,30 +489,15 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
         // after it F is recomputed for those two and for replicas holding a
         // class whose A set crossed size 2 (the only way A[j2]\{k} can change
         // emptiness for a third replica).
+        if (g.gl < J) {
 #pragma unroll
-        for (int kk = 0; kk < KPL; ++kk) {
-            const int k = g.gl + G * kk;
-            const int s = shp[kk];
-            for (int j = 0; j < J; ++j) {
-                bool p = false;
-                if (k < R) {
-                    const int64_t u = sUnit[s * J + j];
-                    p = u > 0 && xs[j * RMAX + k] < sCap[s * J + j] && mrem[kk] >= u;
-                }
-                const uint32_t b = g.ballot(p);
-                if (g.gl == 0) Am[j * KPL + kk] = b;
-            }
+            for (int kk = 0; kk < KPL; ++kk) Am[g.gl * KPL + kk] = areg[kk];
         }
         uint32_t lam_mask = g.ballot(g.gl < J && lamr > 0);
         g.sync();
-        // feasible classes of owned replica kk (top-2 eligible held unit)
-        auto feasible_row = [&](int kk) -> uint32_t {
-            const int k = g.gl + G * kk;
-            if (k >= R) return 0u;
-            const int s = shp[kk];
-            int64_t e1 = -1, e2 = -1;
-            int e1j = -1;
-            uint32_t hb = held[kk];
+        // held classes of owned replica kk whose A set minus k is non-empty
+        auto eligible_held = [&](int kk) -> uint32_t {
+            uint32_t el = 0, hb = held[kk];
             while (hb) {
                 const int j2 = __ffs(hb) - 1;
                 hb &= hb - 1;
@@ -473,7 +508,21 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
                     if (k2 == kk) w &= ~(1u << g.gl);
                     any |= w;
                 }
-                if (any) {
+                if (any) el |= 1u << j2;
+            }
+            return el;
+        };
+        // feasible classes of owned replica kk given its eligible held set
+        auto feasible_row = [&](int kk, uint32_t el) -> uint32_t {
+            const int k = g.gl + G * kk;
+            if (k >= R) return 0u;
+            const int s = shp[kk];
+            int64_t e1 = -1, e2 = -1;
+            int e1j = -1;
+            while (el) {
+                const int j2 = __ffs(el) - 1;
+                el &= el - 1;
+                {
                     const int64_t u2 = sUnit[s * J + j2];
                     if (u2 > e1) {
                         e2 = e1;
@@ -494,9 +543,12 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
             }
             return f;
         };
-        uint32_t F[KPL];
+        uint32_t F[KPL], E[KPL];
 #pragma unroll
-        for (int kk = 0; kk < KPL; ++kk) F[kk] = feasible_row(kk);
+        for (int kk = 0; kk < KPL; ++kk) {
+            E[kk] = g.gl + G * kk < R ? eligible_held(kk) : 0u;
+            F[kk] = feasible_row(kk, E[kk]);
+        }
         for (;;) {
             uint32_t anyF = 0;
 #pragma unroll
@@ -597,8 +649,21 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
 #pragma unroll
             for (int kk = 0; kk < KPL; ++kk) {
                 const int k = g.gl + G * kk;
-                if (k == kf || k == k2 || (held[kk] & dirty)) F[kk] = feasible_row(kk);
-                else F[kk] &= lam_mask;
+                if (k >= R) continue;
+                if (k == kf || k == k2) {
+                    E[kk] = eligible_held(kk);
+                    F[kk] = feasible_row(kk, E[kk]);
+                } else if (held[kk] & dirty) {
+                    const uint32_t el = eligible_held(kk);
+                    if (el != E[kk]) {
+                        E[kk] = el;
+                        F[kk] = feasible_row(kk, el);
+                    } else {
+                        F[kk] &= lam_mask;
+                    }
+                } else {
+                    F[kk] &= lam_mask;
+                }
             }
         }
 
@@ -1120,18 +1185,18 @@ int launch_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayou
     if (int e = ensure_binom()) return e;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (src.count == 0) return 0;
-    // lanes double as class positions in the greedy scan: G >= J.  Default:
-    // the narrowest group that covers the classes (more plans per warp,
-    // every lane busy in the class-parallel phases); OSERVE_K1_G=32 forces
-    // warp-wide groups (A/B experiments).
+    // lanes double as class positions in the greedy scan: G >= J.  Plans with
+    // more than 16 replicas use warp-wide groups (measured: two 16-lane plans
+    // per warp diverge on exchange length and lose 12%); OSERVE_K1_G=16 opts
+    // into 16-lane groups owning up to 4 replicas each.
     const int need = rmax > prm.J ? rmax : prm.J;
-    static const int force32 = [] {
+    static const int opt16 = [] {
         const char *e = getenv("OSERVE_K1_G");
-        return e && atoi(e) == 32;
+        return e && atoi(e) == 16;
     }();
     if (need <= 8) return run_plan_eval<8, 1>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
     if (need <= 16) return run_plan_eval<16, 1>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
-    if (prm.J <= 16 && !force32) {
+    if (prm.J <= 16 && opt16) {
         if (rmax <= 32) return run_plan_eval<16, 2>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
         if (rmax <= 64) return run_plan_eval<16, 4>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
     }
