@@ -646,23 +646,63 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
             }
             dirty = g.or_all(dirty);
             g.sync();
+            // rows whose feasible set must be rebuilt: kf, k2, and rows whose
+            // eligible-held set changed (only possible through dirty classes)
+            bool redo[KPL];
 #pragma unroll
             for (int kk = 0; kk < KPL; ++kk) {
                 const int k = g.gl + G * kk;
+                redo[kk] = false;
                 if (k >= R) continue;
-                if (k == kf || k == k2) {
-                    E[kk] = eligible_held(kk);
-                    F[kk] = feasible_row(kk, E[kk]);
-                } else if (held[kk] & dirty) {
-                    const uint32_t el = eligible_held(kk);
-                    if (el != E[kk]) {
-                        E[kk] = el;
-                        F[kk] = feasible_row(kk, el);
-                    } else {
-                        F[kk] &= lam_mask;
+                if (k == kf || k == k2) redo[kk] = true;
+                else if ((held[kk] & dirty) && eligible_held(kk) != E[kk]) redo[kk] = true;
+                else F[kk] &= lam_mask;
+            }
+#pragma unroll
+            for (int kk = 0; kk < KPL; ++kk) {
+                uint32_t rows = g.ballot(redo[kk]);
+                while (rows) {  // class-parallel rebuild, one row at a time
+                    const int rgl = __ffs(rows) - 1;
+                    rows &= rows - 1;
+                    const int r = rgl + G * kk;
+                    const int sr = shpS[r];
+                    const int64_t mr = g.bcast(mrem[kk], rgl);
+                    const uint32_t hr = g.bcast(held[kk], rgl);
+                    const int j = g.gl;
+                    bool el = false;
+                    if (j < J && ((hr >> j) & 1u)) {
+                        uint32_t any = 0;
+#pragma unroll
+                        for (int k3 = 0; k3 < KPL; ++k3) {
+                            uint32_t w = Am[j * KPL + k3];
+                            if (k3 == kk) w &= ~(1u << rgl);
+                            any |= w;
+                        }
+                        el = any != 0;
                     }
-                } else {
-                    F[kk] &= lam_mask;
+                    const uint32_t Er = g.ballot(el);
+                    // top-2 eligible unit: order positions ascend with unit
+                    const uint32_t rk1 = el ? static_cast<uint32_t>(sRank[sr * kMaxJ + j]) + 1u : 0u;
+                    const uint32_t t1 = __reduce_max_sync(g.mask, rk1);
+                    const uint32_t t2 = __reduce_max_sync(g.mask, rk1 == t1 ? 0u : rk1);
+                    int64_t e1 = -1, e2 = -1;
+                    int e1j = -1;
+                    if (t1) {
+                        e1j = sOrder[sr * kMaxJ + t1 - 1];
+                        e1 = sUnit[sr * J + e1j];
+                    }
+                    if (t2) e2 = sUnit[sr * J + sOrder[sr * kMaxJ + t2 - 1]];
+                    bool f = false;
+                    if (j < J && ((lam_mask >> j) & 1u)) {
+                        const int64_t u = sUnit[sr * J + j];
+                        if (u > 0 && xs[j * RMAX + r] < sCap[sr * J + j])
+                            f = mr >= u || (e1j == j ? e2 : e1) >= u - mr;
+                    }
+                    const uint32_t Fr = g.ballot(f);
+                    if (g.gl == rgl) {
+                        E[kk] = Er;
+                        F[kk] = Fr;
+                    }
                 }
             }
         }
