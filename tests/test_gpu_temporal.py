@@ -1,0 +1,67 @@
+"""Config 4 (temporal, 24 windows) and the C++ drop-in, on the GPU.
+
+The per-window loop (paper_2602_12151_b200/orchestrate.py, following
+orchestrate.cpp:94-154 with the full-space round) is replayed on the CPU
+oracle window by window: round winner, keep rule, assignment x and the greedy
+switch plan (transfers + estimate) must be identical."""
+import os
+import subprocess
+
+import pytest
+
+from paper_2602_12151_b200 import core, orchestrate, workloads
+from paper_2602_12151_b200._native import GpuContext
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+NCPU = os.cpu_count() or 1
+
+
+def cpu_timeline(port, w, forecasts, min_gain):
+    from pyoracle import Problem
+    entries, current, prev_lam, prev_x = [], None, None, None
+    for s, lam in enumerate(forecasts):
+        if entries and lam == prev_lam:
+            continue
+        pr = Problem(w.cluster, w.model, w.types, lam, w.span_s, w.params)
+        found = port.round(pr, w.space_mode, w.space_sizes, threads=NCPU)
+        chosen = found.deployment
+        if current is not None:
+            keep = port.evaluate_deployment(pr, current)
+            if float(found.throughput) <= float(keep) * (1.0 + min_gain):
+                chosen = current
+        t = port.capacity_table(pr, chosen)
+        x = port.solve_assignment(t.n, t.e, lam).assignment.x
+        same = current is not None and orchestrate._same(chosen, current)
+        if not entries:
+            entries.append((s, chosen.shapes(), x, None))
+        elif not same:
+            plan, _ = port.switch_plan(w.cluster, w.model.param_bytes, current, chosen)
+            entries.append((s, chosen.shapes(), x, (plan.est_seconds,
+                                                     [(t.range.begin, t.range.end, t.src, t.dst) for t in plan.transfers])))
+        elif x != prev_x:
+            entries.append((s, chosen.shapes(), x, None))
+        current, prev_lam, prev_x = chosen, lam, x
+    return entries
+
+
+def test_cfg4_timeline_matches_cpu(cuda, port):
+    w = workloads.load("cfg4")
+    fc = w.raw["forecasts"]
+    g = GpuContext(w.cluster, w.model, w.params)
+    tl = orchestrate.build_adaptive_timeline(g, w.types, fc, w.span_s, w.raw["min_gain"], w.space_mode, w.space_sizes)
+    got = [(e.span_index, e.deployment.shapes(), e.assignment,
+            None if e.switch is None else (e.switch_seconds, [(t.range.begin, t.range.end, t.src, t.dst)
+                                                              for t in e.switch.transfers])) for e in tl.entries]
+    exp = cpu_timeline(port, w, fc, w.raw["min_gain"])
+    assert got == exp
+    assert tl.windows == 24 and tl.rounds >= 1
+
+
+def test_cpp_dropin(cuda):
+    exe = os.path.join(ROOT, "oracle", "_ref", "dropin_test")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/dropin_test not built (needs /root/reference at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "DROPIN OK" in out.stdout
