@@ -190,6 +190,20 @@ int oserve_gpu_decode_key(oserve_gpu_ctx *ctx, uint64_t key, oserve_round_result
 int oserve_gpu_round(oserve_gpu_ctx *ctx, const oserve_space_desc *space,
                      oserve_round_result *out);
 
+/* Top-K round: the K best plans (packed keys ascending = best first) of this
+ * shard of the prepared space, written to device memory d_keys[K] (unused
+ * slots UINT64_MAX).  Exact: per-group candidate lists are verified on the
+ * device and an exact threshold pass runs if a list could have dropped one of
+ * the K best.  Synchronous.  Also writes the single best key to d_best (may
+ * be NULL).  Multi-GPU: all-gather the per-rank lists and keep the K smallest. */
+int oserve_gpu_round_topk(oserve_gpu_ctx *ctx, int K, uint64_t *d_keys, uint64_t *d_best);
+/* Switching cost (layout + greedy_plan + estimate_time, switchplan.cpp:40-140)
+ * from `current` to the deployments of `count` packed keys of the prepared
+ * space (device memory), decoded on the device: one CTA per pair.  Outputs
+ * are host arrays (max_link_bytes may be NULL). */
+int oserve_gpu_switch_cost_keys(oserve_gpu_ctx *ctx, const oserve_deployment *current, int count,
+                                const uint64_t *d_keys, double *est_seconds, uint64_t *max_link_bytes);
+
 /* Drop-in for search::exhaustive (deploysearch.cpp:436-466): ordered space,
  * D <= 16 guard, ModelTooLarge when nothing is feasible. */
 int oserve_gpu_exhaustive(oserve_gpu_ctx *ctx, oserve_round_result *out);

@@ -27,6 +27,7 @@ EXPORTS = [
     "oserve_gpu_solve_batch", "oserve_gpu_switch_cost_batch", "oserve_gpu_switch_plan",
     "oserve_gpu_launch_count", "oserve_gpu_copy_bytes",
     "oserve_shard_count", "oserve_shard_global_rank", "oserve_key_layout",
+    "oserve_gpu_round_topk", "oserve_gpu_switch_cost_keys",
 ]
 
 _lib = None
@@ -70,6 +71,8 @@ def load_library() -> C.CDLL:
     L.oserve_gpu_launch_count.argtypes = [vp]
     L.oserve_gpu_launch_count.restype = C.c_uint64
     L.oserve_gpu_copy_bytes.argtypes = [vp, P(C.c_uint64), P(C.c_uint64)]
+    L.oserve_gpu_round_topk.argtypes = [vp, C.c_int, vp, vp]
+    L.oserve_gpu_switch_cost_keys.argtypes = [vp, P(A.DeploymentDesc), C.c_int, vp, P(C.c_double), P(C.c_uint64)]
     L.oserve_shard_count.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.c_int]
     L.oserve_shard_count.restype = C.c_uint64
     L.oserve_shard_global_rank.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.c_int]
@@ -203,6 +206,20 @@ class GpuContext:
         res = A.RoundResult()
         self._chk(self.lib.oserve_gpu_round(self.h, C.byref(sd), C.byref(res)))
         return A.result_to_state(res)
+
+    def round_topk(self, K: int, d_keys_ptr: int, d_best_ptr: int = 0):
+        """Top-K packed keys of this shard into device memory (uint64[K])."""
+        self._chk(self.lib.oserve_gpu_round_topk(self.h, int(K), C.c_void_p(d_keys_ptr),
+                                                 C.c_void_p(d_best_ptr) if d_best_ptr else None))
+
+    def switch_cost_keys(self, current: core.Deployment, d_keys_ptr: int, count: int):
+        """Switching cost current -> plan(key) for `count` device-resident keys."""
+        keep = A.Keep()
+        s = A.deployment_desc(current, keep)
+        est = (C.c_double * max(1, count))()
+        mb = (C.c_uint64 * max(1, count))()
+        self._chk(self.lib.oserve_gpu_switch_cost_keys(self.h, C.byref(s), int(count), C.c_void_p(d_keys_ptr), est, mb))
+        return list(est[:count]), list(mb[:count])
 
     def exhaustive(self) -> core.SearchState:
         res = A.RoundResult()

@@ -187,6 +187,9 @@ struct oserve_gpu_ctx {
     int rank = 0, world = 1;
     uint64_t chunk = OSERVE_SHARD_CHUNK;
     // scratch
+    DBuf d_topk, d_topk_meta, d_topk_tmp, d_collect, d_collect_n, d_bad;
+    void *cub_temp = nullptr;
+    size_t cub_temp_bytes = 0;
     DBuf d_key, d_obj, d_spp, d_x, d_used, d_aborted, d_aborted_n, d_ranks, d_listR, d_listOff, d_listShapes,
         d_listLam, d_sw[12];
 
@@ -867,6 +870,134 @@ void run_switch(oserve_gpu_ctx &c, const oserve_deployment *src, int count, cons
     if (in_out) *in_out = std::move(in);
 }
 
+
+// Top-K of this shard (see oserve_gpu_round_topk).
+void round_topk(oserve_gpu_ctx &c, int K, uint64_t *d_keys, uint64_t *d_best) {
+    if (K < 1 || K > 65536) fail(OSERVE_ERR_INVALID_ARGUMENT, "K must be in [1, 65536]");
+    ensure_tables(c);
+    Space &sp = c.space;
+    refresh_exact(c, sp);
+    if (sp.any_exact) fail(OSERVE_ERR_UNSUPPORTED, "top-K round on exact-path (branch-and-bound) plans");
+    make_key_layout(c, sp);
+    cudaStream_t s = c.stream;
+    PlanSource src{};
+    src.mode = 0;
+    src.count = shard_count(c, sp.total);
+    src.rank = c.rank;
+    src.world = c.world;
+    src.chunk = c.chunk;
+    SolveParams prm = solve_params(c);
+    count_h2d(sizeof(int64_t) * c.J);
+    const int groups = k1_groups(sp.rmax, c.J, c.sm_count, c.tables, src.count);
+    if (groups < 0) fail(OSERVE_ERR_CUDA, "K1 geometry");
+    const size_t nlist = static_cast<size_t>(std::max(groups, 1)) * kTopK;
+    uint64_t *best = d_best ? d_best : static_cast<uint64_t *>(c.d_key.get(sizeof(uint64_t)));
+    cuda_ok(cudaMemsetAsync(best, 0xff, sizeof(uint64_t), s), "memset");
+    PlanOutputs out{};
+    out.best_key = best;
+    out.topk = static_cast<uint64_t *>(c.d_topk.get(sizeof(uint64_t) * nlist));
+    out.topk_meta = static_cast<uint64_t *>(c.d_topk_meta.get(sizeof(uint64_t) * std::max(groups, 1)));
+    cuda_ok(cudaMemsetAsync(out.topk, 0xff, sizeof(uint64_t) * nlist, s), "memset");
+    cuda_ok(cudaMemsetAsync(out.topk_meta, 0xff, sizeof(uint64_t) * std::max(groups, 1), s), "memset");
+    cuda_ok(launch_plan_eval(c.tables, sp.view, c.key, src, out, prm, sp.rmax, c.sm_count, 0, s, &c.launches),
+            "plan kernel (top-K)");
+    uint64_t *sorted = static_cast<uint64_t *>(c.d_topk_tmp.get(sizeof(uint64_t) * nlist));
+    cuda_ok(sort_keys(out.topk, sorted, static_cast<int>(nlist), &c.cub_temp, &c.cub_temp_bytes, s), "sort");
+    ++c.launches;
+    const uint64_t *kth = sorted + std::min<size_t>(K, nlist) - 1;
+    unsigned *bad = static_cast<unsigned *>(c.d_bad.get(sizeof(unsigned)));
+    cuda_ok(cudaMemsetAsync(bad, 0, sizeof(unsigned), s), "memset");
+    cuda_ok(launch_topk_check(out.topk_meta, groups, kth, bad, s), "top-K check");
+    ++c.launches;
+    unsigned nbad = 0;
+    cuda_ok(d2h(&nbad, bad, sizeof(unsigned), s), "D2H");
+    cuda_ok(cudaStreamSynchronize(s), "sync");
+    const uint64_t *final_sorted = sorted;
+    size_t final_n = nlist;
+    if (nbad) {
+        // exact fallback: collect every key <= the candidate K-th (an upper
+        // bound of the true K-th), grow the buffer until nothing overflows
+        uint64_t thr = kNoKey;
+        cuda_ok(d2h(&thr, kth, sizeof(uint64_t), s), "D2H");
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+        unsigned cap = static_cast<unsigned>(std::max(4 * K, 4096));
+        for (;;) {
+            PlanOutputs co{};
+            co.collect = static_cast<uint64_t *>(c.d_collect.get(sizeof(uint64_t) * cap));
+            co.collect_n = static_cast<unsigned *>(c.d_collect_n.get(sizeof(unsigned)));
+            co.collect_cap = cap;
+            co.collect_thr = thr;
+            co.best_key = best;
+            cuda_ok(cudaMemsetAsync(co.collect_n, 0, sizeof(unsigned), s), "memset");
+            cuda_ok(launch_plan_eval(c.tables, sp.view, c.key, src, co, prm, sp.rmax, c.sm_count, 0, s, &c.launches),
+                    "plan kernel (threshold collect)");
+            unsigned n = 0;
+            cuda_ok(d2h(&n, co.collect_n, sizeof(unsigned), s), "D2H");
+            cuda_ok(cudaStreamSynchronize(s), "sync");
+            if (n <= cap) {
+                uint64_t *tmp = static_cast<uint64_t *>(c.d_topk_tmp.get(sizeof(uint64_t) * std::max<size_t>(n, nlist)));
+                cuda_ok(sort_keys(co.collect, tmp, static_cast<int>(n), &c.cub_temp, &c.cub_temp_bytes, s), "sort");
+                final_sorted = tmp;
+                final_n = n;
+                break;
+            }
+            cap = n + 1024;
+        }
+    }
+    cuda_ok(cudaMemsetAsync(d_keys, 0xff, sizeof(uint64_t) * K, s), "memset");
+    cuda_ok(cudaMemcpyAsync(d_keys, final_sorted, sizeof(uint64_t) * std::min<size_t>(K, final_n),
+                            cudaMemcpyDeviceToDevice, s),
+            "D2D");
+}
+
+void switch_cost_keys(oserve_gpu_ctx &c, const oserve_deployment &current, int count, const uint64_t *d_keys,
+                      double *est, uint64_t *maxb) {
+    if (!c.space.valid) fail(OSERVE_ERR_INVALID_ARGUMENT, "no prepared space");
+    ensure_tables(c);
+    if (c.D() > 256) fail(OSERVE_ERR_UNSUPPORTED, "switch kernel limited to 256 devices");
+    // slots = the cluster's sorted devices (the candidates' canonical blocks)
+    std::map<int, int> slots;
+    SwitchInput in;
+    for (int i = 0; i < c.D(); ++i) {
+        slots.emplace(c.dev_sorted[i], i);
+        in.dev_id.push_back(c.dev_sorted[i]);
+        in.machine.push_back(c.machine(c.dev_sorted[i]));
+    }
+    add_deployment(c, in, slots, current);
+    in.dep_rep_off.push_back(static_cast<int32_t>(in.rep_tp.size()));
+    in.rep_dev_off.push_back(static_cast<int32_t>(in.rep_devs.size()));
+    if (in.dep_rep_off[1] > 128) fail(OSERVE_ERR_UNSUPPORTED, "switch: > 128 source replicas");
+    if (c.model.param_bytes >= (uint64_t{1} << 46)) fail(OSERVE_ERR_UNSUPPORTED, "switch: param_bytes >= 2^46");
+    make_key_layout(c, c.space);
+    cudaStream_t s = c.stream;
+    SwitchDeps d{};
+    d.count = count;
+    d.num_devices = static_cast<int>(in.dev_id.size());
+    d.machine = c.d_sw[0].upload(in.machine, s);
+    d.dev_id = c.d_sw[1].upload(in.dev_id, s);
+    d.dep_rep_off = c.d_sw[2].upload(in.dep_rep_off, s);
+    d.rep_tp = c.d_sw[3].upload(in.rep_tp, s);
+    d.rep_pp = c.d_sw[4].upload(in.rep_pp, s);
+    d.rep_dev_off = c.d_sw[5].upload(in.rep_dev_off, s);
+    d.rep_devs = c.d_sw[6].upload(in.rep_devs, s);
+    d.P = c.model.param_bytes;
+    d.intra_bw = c.intra;
+    d.inter_bw = c.inter;
+    SwitchOut o{};
+    o.est = static_cast<double *>(c.d_sw[7].get(sizeof(double) * count));
+    o.max_bytes = static_cast<uint64_t *>(c.d_sw[8].get(sizeof(uint64_t) * count));
+    o.status = static_cast<int32_t *>(c.d_sw[9].get(sizeof(int32_t) * count));
+    cuda_ok(launch_switch_cost_keys(d, c.space.view, c.key, c.tables, d_keys, count, nullptr, o, s, &c.launches),
+            "switch kernel (keys)");
+    std::vector<int32_t> st;
+    cuda_ok(d2h(est, o.est, sizeof(double) * count, s), "D2H");
+    if (maxb) cuda_ok(d2h(maxb, o.max_bytes, sizeof(uint64_t) * count, s), "D2H");
+    download(st, o.status, count, s);
+    cuda_ok(cudaStreamSynchronize(s), "sync");
+    for (int i = 0; i < count; ++i)
+        if (st[i]) fail(OSERVE_ERR_UNSOURCED_FRAGMENT, "required bytes have no source holder");
+}
+
 }  // namespace
 
 // ====================================================================== ABI
@@ -932,6 +1063,7 @@ int oserve_gpu_destroy(oserve_gpu_ctx *ctx) {
         cudaStreamSynchronize(ctx->own);
         cudaStreamDestroy(ctx->own);
     }
+    if (ctx->cub_temp) cudaFree(ctx->cub_temp);
     delete ctx;
     return OSERVE_OK;
 }
@@ -1055,6 +1187,21 @@ int oserve_gpu_round(oserve_gpu_ctx *ctx, const oserve_space_desc *space, oserve
         cuda_ok(cudaStreamSynchronize(ctx->stream), "sync");
         decode_key(*ctx, key, out);
         if (key == kNoKey && ctx->world == 1) fail(OSERVE_ERR_MODEL_TOO_LARGE, "round: no feasible deployment");
+    });
+}
+
+int oserve_gpu_round_topk(oserve_gpu_ctx *ctx, int K, uint64_t *d_keys, uint64_t *d_best) {
+    return guarded(ctx, [&] {
+        if (!ctx->space.valid) fail(OSERVE_ERR_INVALID_ARGUMENT, "no prepared space");
+        round_topk(*ctx, K, d_keys, d_best);
+    });
+}
+
+int oserve_gpu_switch_cost_keys(oserve_gpu_ctx *ctx, const oserve_deployment *current, int count,
+                                const uint64_t *d_keys, double *est_seconds, uint64_t *max_link_bytes) {
+    return guarded(ctx, [&] {
+        if (count <= 0) return;
+        switch_cost_keys(*ctx, *current, count, d_keys, est_seconds, max_link_bytes);
     });
 }
 

@@ -20,6 +20,7 @@ constexpr int kMaxJ = 16;       // classes (OSERVE_MAX_CLASSES)
 constexpr int kMaxCand = 8;     // (tp, pp) candidates per replica block
 constexpr int kMaxExactCells = 64;
 constexpr uint64_t kNoKey = ~0ull;
+constexpr int kTopK = 64;  // per-group candidate list of the top-K round
 
 // Per-shape inputs of the cost kernel (K0).
 struct ShapeParam {
@@ -99,6 +100,15 @@ struct PlanOutputs {
     uint64_t *best_key;   // argmin target (atomicMin) or null
     uint64_t *aborted;    // [count] ranks whose B&B blew the budget (K4) or null
     unsigned int *aborted_n;
+    // top-K round: per-group best-kTopK key lists + the worst kept key of
+    // groups that dropped any key (kNoKey otherwise)
+    uint64_t *topk;       // [groups * kTopK] or null
+    uint64_t *topk_meta;  // [groups]
+    // threshold collect (exact fallback): every key <= collect_thr appended
+    uint64_t *collect;
+    unsigned int *collect_n;
+    unsigned int collect_cap;
+    uint64_t collect_thr;
 };
 
 struct SolveParams {
@@ -149,5 +159,15 @@ struct SwitchOut {
     int max_frags;
 };
 int launch_switch_cost(const SwitchDeps &d, const SwitchOut &o, void *stream, uint64_t *launches);
+// K2 with candidates decoded on the device from packed keys (canonical blocks
+// of a prepared space): est[i] = switching cost src -> plan(keys[i]).
+int launch_switch_cost_keys(const SwitchDeps &src, const SpaceTables &sp, const KeyLayout &key, const ShapeTables &t,
+                            const uint64_t *keys, int count, const int32_t *part_off, const SwitchOut &o,
+                            void *stream, uint64_t *launches);
+// Sort n u64 keys ascending on the device (CUB radix sort); temp is reused.
+int sort_keys(uint64_t *keys, uint64_t *tmp_keys, int n, void **temp, size_t *temp_bytes, void *stream);
+// Groups whose list dropped a key better than `kth` (0 => the lists are exact).
+int launch_topk_check(const uint64_t *meta, int groups, const uint64_t *kth, unsigned int *bad, void *stream);
+int k1_groups(int rmax, int J, int sm_count, const ShapeTables &t, uint64_t count);
 
 }  // namespace oserve_gpu

@@ -24,6 +24,10 @@
 
 #include "oserve_internal.h"
 
+#include <cub/device/device_radix_sort.cuh>
+
+#define OSERVE_MAX_REPLICAS_DEV 128
+
 #ifndef OSERVE_K1_MINB
 #define OSERVE_K1_MINB 4  // CTAs of 256 threads per SM the register budget must allow (64 regs; measured 5% faster than 3)
 #endif
@@ -309,6 +313,13 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
     int jw = 1;
     while (jw < J) jw <<= 1;  // scan width over class positions
     uint64_t best = kNoKey;
+    constexpr int TKE = kTopK / G;  // top-K list entries per lane
+    uint64_t tk[TKE];
+#pragma unroll
+    for (int e = 0; e < TKE; ++e) tk[e] = kNoKey;
+    uint64_t tk_max = kNoKey;
+    int tk_lane = 0, tk_slot = 0;
+    bool lossy = false;
     const uint64_t ngroups = static_cast<uint64_t>(gridDim.x) * GPB;
 
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * GPB + gib; i < src.count; i += ngroups) {
@@ -758,13 +769,12 @@ size_t plan_eval_smem(int S, int J, bool stage) {
     return shapes + group_scratch_bytes(J, RMAX, KPL) * GPB + GPB * 8;
 }
 
+// Launch geometry of K1 (also used to size the top-K lists).
 template <int G, int KPL>
-int run_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key, const PlanSource &src,
-                  const PlanOutputs &out, const SolveParams &prm, int sm_count, int skip_exact,
-                  cudaStream_t stream, uint64_t *launches) {
-    cudaGetLastError();  // clear any stale (non-sticky) error before launching
-    const bool stage = plan_eval_smem<G, KPL>(t.num_shapes, prm.J, true) <= 160 * 1024;
-    const size_t smem = plan_eval_smem<G, KPL>(t.num_shapes, prm.J, stage);
+int plan_eval_geometry(const ShapeTables &t, int J, int sm_count, uint64_t count, size_t *smem_out, bool *stage_out,
+                       uint64_t *grid_out) {
+    const bool stage = plan_eval_smem<G, KPL>(t.num_shapes, J, true) <= 160 * 1024;
+    const size_t smem = plan_eval_smem<G, KPL>(t.num_shapes, J, stage);
     auto kern = stage ? k_plan_eval<G, KPL, true> : k_plan_eval<G, KPL, false>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -775,9 +785,25 @@ int run_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &
     if (e != cudaSuccess) return static_cast<int>(e);
     if (per_sm < 1) return static_cast<int>(cudaErrorInvalidConfiguration);
     constexpr int GPB = 256 / G;
-    uint64_t need = (src.count + GPB - 1) / GPB;
+    uint64_t need = (count + GPB - 1) / GPB;
     uint64_t grid = static_cast<uint64_t>(per_sm) * sm_count;
     if (need < grid) grid = need;
+    *smem_out = smem;
+    *stage_out = stage;
+    *grid_out = grid;
+    return 0;
+}
+
+template <int G, int KPL>
+int run_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key, const PlanSource &src,
+                  const PlanOutputs &out, const SolveParams &prm, int sm_count, int skip_exact,
+                  cudaStream_t stream, uint64_t *launches) {
+    cudaGetLastError();  // clear any stale (non-sticky) error before launching
+    size_t smem = 0;
+    bool stage = false;
+    uint64_t grid = 0;
+    if (int e = plan_eval_geometry<G, KPL>(t, prm.J, sm_count, src.count, &smem, &stage, &grid)) return e;
+    auto kern = stage ? k_plan_eval<G, KPL, true> : k_plan_eval<G, KPL, false>;
     if (grid == 0) return 0;
     kern<<<static_cast<unsigned>(grid), 256, smem, stream>>>(t, sp, key, src, out, prm, skip_exact);
     if (launches) ++*launches;
@@ -979,39 +1005,13 @@ __device__ __forceinline__ double link_bw(const SwitchDeps &d, int s, int t) {
     return d.machine[s] >= 0 && d.machine[s] == d.machine[t] ? d.intra_bw : d.inter_bw;
 }
 
-__global__ void __launch_bounds__(256) k_switch_cost(SwitchDeps d, SwitchOut o) {
-    __shared__ uint64_t sB[2][kSwMaxDev], sE[2][kSwMaxDev];
-    __shared__ uint64_t cuts[kSwMaxCuts];
-    __shared__ int ncuts_s;
-    __shared__ double wmax[8];
-    __shared__ unsigned long long wbytes[8];
-    __shared__ int wstatus[8];
-    const int pair = blockIdx.x;
+// Cut points, per-target greedy holder choice and the link-time maximum for
+// one (source, destination) pair whose layouts are in sB[0]/sE[0] (source)
+// and sB[1]/sE[1] (destination).
+__device__ __forceinline__ void switch_core(const SwitchDeps &d, const SwitchOut &o, int pair, uint64_t (*sB)[kSwMaxDev],
+                                            uint64_t (*sE)[kSwMaxDev], uint64_t *cuts, int &ncuts_s, double *wmax,
+                                            unsigned long long *wbytes, int *wstatus) {
     const int ND = d.num_devices;
-    const int deps[2] = {0, pair + 1};
-    // ---- layouts (switchplan.cpp:40-63): one slice per device slot ----
-    for (int i = threadIdx.x; i < 2 * kSwMaxDev; i += blockDim.x) {
-        sB[i / kSwMaxDev][i % kSwMaxDev] = 0;
-        sE[i / kSwMaxDev][i % kSwMaxDev] = 0;
-    }
-    __syncthreads();
-    for (int w = 0; w < 2; ++w) {
-        const int r0 = d.dep_rep_off[deps[w]], r1 = d.dep_rep_off[deps[w] + 1];
-        for (int r = r0; r < r1; ++r) {
-            const uint64_t tp = d.rep_tp[r], pp = d.rep_pp[r];
-            const int dev0 = d.rep_dev_off[r];
-            const int nd = d.rep_dev_off[r + 1] - dev0;
-            for (int q = threadIdx.x; q < nd; q += blockDim.x) {
-                const uint64_t s = q / tp, i = q % tp;
-                if (s >= pp) continue;
-                const uint64_t sb = d.P * s / pp, se = d.P * (s + 1) / pp, len = se - sb;
-                const int slot = d.rep_devs[dev0 + q];
-                sB[w][slot] = sb + len * i / tp;
-                sE[w][slot] = sb + len * (i + 1) / tp;
-            }
-        }
-    }
-    __syncthreads();
     // ---- cut points (:70-85): sorted unique begin/end of non-empty ranges ----
     int P2 = 1;
     while (P2 < 4 * ND) P2 <<= 1;
@@ -1176,6 +1176,122 @@ __global__ void __launch_bounds__(256) k_switch_cost(SwitchDeps d, SwitchOut o) 
     }
 }
 
+__global__ void __launch_bounds__(256) k_switch_cost(SwitchDeps d, SwitchOut o) {
+    __shared__ uint64_t sB[2][kSwMaxDev], sE[2][kSwMaxDev];
+    __shared__ uint64_t cuts[kSwMaxCuts];
+    __shared__ int ncuts_s;
+    __shared__ double wmax[8];
+    __shared__ unsigned long long wbytes[8];
+    __shared__ int wstatus[8];
+    const int pair = blockIdx.x;
+    const int ND = d.num_devices;
+    const int deps[2] = {0, pair + 1};
+    // ---- layouts (switchplan.cpp:40-63): one slice per device slot ----
+    for (int i = threadIdx.x; i < 2 * kSwMaxDev; i += blockDim.x) {
+        sB[i / kSwMaxDev][i % kSwMaxDev] = 0;
+        sE[i / kSwMaxDev][i % kSwMaxDev] = 0;
+    }
+    __syncthreads();
+    for (int w = 0; w < 2; ++w) {
+        const int r0 = d.dep_rep_off[deps[w]], r1 = d.dep_rep_off[deps[w] + 1];
+        for (int r = r0; r < r1; ++r) {
+            const uint64_t tp = d.rep_tp[r], pp = d.rep_pp[r];
+            const int dev0 = d.rep_dev_off[r];
+            const int nd = d.rep_dev_off[r + 1] - dev0;
+            for (int q = threadIdx.x; q < nd; q += blockDim.x) {
+                const uint64_t s = q / tp, i = q % tp;
+                if (s >= pp) continue;
+                const uint64_t sb = d.P * s / pp, se = d.P * (s + 1) / pp, len = se - sb;
+                const int slot = d.rep_devs[dev0 + q];
+                sB[w][slot] = sb + len * i / tp;
+                sE[w][slot] = sb + len * (i + 1) / tp;
+            }
+        }
+    }
+    __syncthreads();
+    switch_core(d, o, pair, sB, sE, cuts, ncuts_s, wmax, wbytes, wstatus);
+}
+
+// K2 over candidates given as packed round keys: the destination deployment
+// is unranked on the device (canonical blocks: replica r owns device slots
+// [off_r, off_r + d_r) of the cluster's sorted devices).
+__global__ void __launch_bounds__(256) k_switch_cost_keys(SwitchDeps d, SpaceTables sp, KeyLayout key,
+                                                          ShapeTables t, const uint64_t *keys, SwitchOut o) {
+    __shared__ uint64_t sB[2][kSwMaxDev], sE[2][kSwMaxDev];
+    __shared__ uint64_t cuts[kSwMaxCuts];
+    __shared__ int ncuts_s;
+    __shared__ double wmax[8];
+    __shared__ unsigned long long wbytes[8];
+    __shared__ int wstatus[8];
+    __shared__ uint8_t pick[OSERVE_MAX_REPLICAS_DEV];
+    __shared__ int rtp[OSERVE_MAX_REPLICAS_DEV], rpp[OSERVE_MAX_REPLICAS_DEV], roff[OSERVE_MAX_REPLICAS_DEV + 1];
+    __shared__ int nrep;
+    const int pair = blockIdx.x;
+    const uint64_t kv = keys[pair];
+    for (int i = threadIdx.x; i < 2 * kSwMaxDev; i += blockDim.x) {
+        sB[i / kSwMaxDev][i % kSwMaxDev] = 0;
+        sE[i / kSwMaxDev][i % kSwMaxDev] = 0;
+    }
+    if (threadIdx.x == 0) {
+        const uint64_t local = kv & ((uint64_t{1} << key.sh_spp) - 1);
+        const int64_t part = static_cast<int64_t>((kv >> key.sh_part) & ((uint64_t{1} << (key.sh_obj - key.sh_part)) - 1));
+        const int R = sp.R[part];
+        const int ro = sp.rep_off[part], runo = sp.run_off[part], nr = sp.nruns[part];
+        for (int ri = 0; ri < nr; ++ri) {
+            const uint64_t w = sp.run_weight[runo + ri], c = sp.run_count[runo + ri];
+            const uint64_t rr = (local / w) % c;
+            unrank_run(rr, sp.run_len[runo + ri], sp.run_q[runo + ri], pick + sp.run_start[runo + ri]);
+        }
+        int off = 0;
+        for (int r = 0; r < R; ++r) {
+            const int shape = sp.cl_shape[sp.rep_list[ro + r] * kMaxCand + pick[r]];
+            rtp[r] = t.param[shape].tp;
+            rpp[r] = t.param[shape].pp;
+            roff[r] = off;
+            off += rtp[r] * rpp[r];
+        }
+        roff[R] = off;
+        nrep = R;
+    }
+    __syncthreads();
+    // ---- layouts (switchplan.cpp:40-63) ----
+    {
+        const int r0 = d.dep_rep_off[0], r1 = d.dep_rep_off[1];
+        for (int r = r0; r < r1; ++r) {
+            const uint64_t tp = d.rep_tp[r], pp = d.rep_pp[r];
+            const int dev0 = d.rep_dev_off[r];
+            const int nd = d.rep_dev_off[r + 1] - dev0;
+            for (int q = threadIdx.x; q < nd; q += blockDim.x) {
+                const uint64_t s2 = q / tp, i = q % tp;
+                if (s2 >= pp) continue;
+                const uint64_t sb = d.P * s2 / pp, se = d.P * (s2 + 1) / pp, len = se - sb;
+                const int slot = d.rep_devs[dev0 + q];
+                sB[0][slot] = sb + len * i / tp;
+                sE[0][slot] = sb + len * (i + 1) / tp;
+            }
+        }
+        for (int r = 0; r < nrep; ++r) {
+            const uint64_t tp = rtp[r], pp = rpp[r];
+            const int nd = roff[r + 1] - roff[r];
+            for (int q = threadIdx.x; q < nd; q += blockDim.x) {
+                const uint64_t s2 = q / tp, i = q % tp;
+                const uint64_t sb = d.P * s2 / pp, se = d.P * (s2 + 1) / pp, len = se - sb;
+                const int slot = roff[r] + q;
+                sB[1][slot] = sb + len * i / tp;
+                sE[1][slot] = sb + len * (i + 1) / tp;
+            }
+        }
+    }
+    __syncthreads();
+    switch_core(d, o, pair, sB, sE, cuts, ncuts_s, wmax, wbytes, wstatus);
+}
+
+__global__ void k_topk_check(const uint64_t *meta, int groups, const uint64_t *kth, unsigned int *bad) {
+    const uint64_t kk = *kth;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < groups; i += gridDim.x * blockDim.x)
+        if (meta[i] < kk) atomicAdd(bad, 1u);
+}
+
 }  // namespace
 
 // ------------------------------------------------------------- launchers ---
@@ -1268,6 +1384,58 @@ int launch_switch_cost(const SwitchDeps &d, const SwitchOut &o, void *stream, ui
     if (d.num_devices > kSwMaxDev) return static_cast<int>(cudaErrorInvalidValue);
     k_switch_cost<<<d.count, 256, 0, static_cast<cudaStream_t>(stream)>>>(d, o);
     if (launches) ++*launches;
+    return check(cudaGetLastError());
+}
+
+int k1_groups(int rmax, int J, int sm_count, const ShapeTables &t, uint64_t count) {
+    size_t smem = 0;
+    bool stage = false;
+    uint64_t grid = 0;
+    const int need = rmax > J ? rmax : J;
+    const char *env = getenv("OSERVE_K1_G");
+    const bool opt16 = env && atoi(env) == 16;
+    int e = 0, gpb = 0;
+    if (need <= 8) e = plan_eval_geometry<8, 1>(t, J, sm_count, count, &smem, &stage, &grid), gpb = 32;
+    else if (need <= 16) e = plan_eval_geometry<16, 1>(t, J, sm_count, count, &smem, &stage, &grid), gpb = 16;
+    else if (J <= 16 && opt16 && rmax <= 32) e = plan_eval_geometry<16, 2>(t, J, sm_count, count, &smem, &stage, &grid), gpb = 16;
+    else if (J <= 16 && opt16 && rmax <= 64) e = plan_eval_geometry<16, 4>(t, J, sm_count, count, &smem, &stage, &grid), gpb = 16;
+    else if (rmax <= 32) e = plan_eval_geometry<32, 1>(t, J, sm_count, count, &smem, &stage, &grid), gpb = 8;
+    else if (rmax <= 64) e = plan_eval_geometry<32, 2>(t, J, sm_count, count, &smem, &stage, &grid), gpb = 8;
+    else e = plan_eval_geometry<32, 4>(t, J, sm_count, count, &smem, &stage, &grid), gpb = 8;
+    if (e) return -1;
+    return static_cast<int>(grid) * gpb;
+}
+
+int launch_switch_cost_keys(const SwitchDeps &src, const SpaceTables &sp, const KeyLayout &key, const ShapeTables &t,
+                            const uint64_t *keys, int count, const int32_t *, const SwitchOut &o, void *stream,
+                            uint64_t *launches) {
+    cudaGetLastError();
+    if (count == 0) return 0;
+    if (src.num_devices > kSwMaxDev) return static_cast<int>(cudaErrorInvalidValue);
+    k_switch_cost_keys<<<count, 256, 0, static_cast<cudaStream_t>(stream)>>>(src, sp, key, t, keys, o);
+    if (launches) ++*launches;
+    return check(cudaGetLastError());
+}
+
+int sort_keys(uint64_t *keys, uint64_t *tmp_keys, int n, void **temp, size_t *temp_bytes, void *stream) {
+    size_t need = 0;
+    cudaError_t e = cub::DeviceRadixSort::SortKeys(nullptr, need, keys, tmp_keys, n, 0, 64,
+                                                   static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return static_cast<int>(e);
+    if (need > *temp_bytes) {
+        if (*temp) cudaFree(*temp);
+        e = cudaMalloc(temp, need);
+        if (e != cudaSuccess) return static_cast<int>(e);
+        *temp_bytes = need;
+    }
+    e = cub::DeviceRadixSort::SortKeys(*temp, need, keys, tmp_keys, n, 0, 64, static_cast<cudaStream_t>(stream));
+    return static_cast<int>(e);
+}
+
+int launch_topk_check(const uint64_t *meta, int groups, const uint64_t *kth, unsigned int *bad, void *stream) {
+    cudaGetLastError();
+    if (groups <= 0) return 0;
+    k_topk_check<<<(groups + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(meta, groups, kth, bad);
     return check(cudaGetLastError());
 }
 

@@ -201,3 +201,89 @@ def test_best_strategies_dropin(cuda, port):
         exp = port.best_strategies(pr, sizes)
         assert got.objective == exp.objective, sizes
         assert same_deployment(got.deployment, exp.deployment), sizes
+
+
+@pytest.mark.parametrize("name,K", [("cfg3_70b", 1024), ("cfg2", 512), ("cfg5", 256)])
+def test_topk_round_and_switch_batch(cuda, port, name, K):
+    """Exact top-K of the packed key over the whole space (checked against
+    every plan's objective from the per-plan path and the oracle's key
+    fields), then the switching cost from init_uniform to each of the K plans
+    decoded on the device (K2 key mode) vs explicit deployments and the CPU."""
+    import torch
+    w = workloads.load(name)
+    g = ctx_for(w)
+    pr = problem_for(w)
+    parts, plans = g.prepare_space(w.space_mode, w.space_sizes)
+    d_keys = torch.empty(K, dtype=torch.int64, device="cuda")
+    d_best = torch.empty(1, dtype=torch.int64, device="cuda")
+    g.round_topk(K, d_keys.data_ptr(), d_best.data_ptr())
+    keys = [int(k) & ((1 << 64) - 1) for k in d_keys.cpu().tolist()]
+    assert keys == sorted(keys) and len(set(keys)) == K
+    assert keys[0] == int(d_best.item()) == g.round(w.space_mode, w.space_sizes).key
+    obj, spp = g.evaluate_ranks(0, plans)
+    states = [g.decode_key(k) for k in keys]
+    kth_obj = states[-1].throughput
+    cand = np.nonzero(obj >= kth_obj)[0]
+    assert len(cand) < 200000
+    from paper_2602_12151_b200 import _native
+    lay = None
+    full = []
+    for r in cand:
+        dep, pi, lr = port.space_plan(pr, w.space_mode, int(r), w.space_sizes)
+        full.append((-int(obj[r]), pi, int(spp[r]), lr))
+    full.sort()
+    exp = [(-s.throughput, s.partition_index, s.sum_pp, s.local_rank) for s in states]
+    assert full[:K] == exp
+    # switching batch: K2 key mode == K2 explicit == greedy_plan on the CPU
+    gm = g.min_feasible_group()
+    R = w.cluster.device_count() // gm
+    current = core.canonical_deployment(w.cluster, [gm] * R, [gm] * R)
+    est_k, mb_k = g.switch_cost_keys(current, d_keys.data_ptr(), K)
+    est_x, mb_x = g.switch_cost_batch(current, [s.deployment for s in states])
+    assert est_k == est_x and mb_k == mb_x
+    for s, e in list(zip(states, est_k))[:: max(1, K // 16)]:
+        plan, _ = port.switch_plan(w.cluster, w.model.param_bytes, current, s.deployment)
+        assert e == plan.est_seconds
+
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg1_bnb", "cfg2", "cfg2_low", "cfg3_70b", "cfg3_7b", "cfg5", "cfg5_low"])
+def test_gpu_matches_reference_goldens(cuda, name):
+    """GPU per-plan objectives against the REFERENCE's own values (tests/golden,
+    generated from the unmodified reference by oracle/gen_golden.py)."""
+    import json
+    w = workloads.load(name)
+    g = ctx_for(w)
+    p = json.load(open(os.path.join(GOLD, f"plans_{name}.json")))
+    parts, plans = g.prepare_space(w.space_mode, w.space_sizes)
+    assert (parts, plans) == (p["partitions"], p["plans"])
+    if "all_objective_sha256" in p:
+        import hashlib
+        obj, _ = g.evaluate_ranks(0, plans)
+        assert hashlib.sha256(np.ascontiguousarray(obj, dtype="<i8").tobytes()).hexdigest() == p["all_objective_sha256"]
+        assert int(obj.sum()) == p["objective_sum"]
+    for r, o, s in zip(p["ranks"], p["objective"], p["sum_pp"]):
+        ob, sp_ = g.evaluate_ranks(int(r), 1)
+        assert (int(ob[0]), int(sp_[0])) == (o, s), r
+    rounds = json.load(open(os.path.join(GOLD, "rounds.json")))
+    if name in rounds:
+        gr = rounds[name]
+        st = g.exhaustive() if name.startswith("cfg1") else g.round(w.space_mode, w.space_sizes)
+        assert st.throughput == gr["objective"]
+        assert [[r.device_ids, r.tp, r.pp] for r in st.deployment.replicas] == gr["deployment"]
+
+
+def test_gpu_switch_matches_reference_goldens(cuda):
+    import json
+    for case in json.load(open(os.path.join(GOLD, "switch.json"))):
+        w = workloads.load(case["config"])
+        g = GpuContext(w.cluster, w.model, w.params)
+        src = core.Deployment([core.ReplicaConfig(i, t, p) for i, t, p in case["src"]])
+        dst = core.Deployment([core.ReplicaConfig(i, t, p) for i, t, p in case["dst"]])
+        plan = g.switch_plan(src, dst)
+        assert plan.est_seconds == case["est_seconds"]
+        assert [[t.range.begin, t.range.end, t.src, t.dst] for t in plan.transfers] == case["transfers"]
+        est, mb = g.switch_cost_batch(src, [dst])
+        assert est[0] == case["est_seconds"] and mb[0] == case["max_link_bytes"]
