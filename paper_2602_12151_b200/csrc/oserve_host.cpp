@@ -948,6 +948,7 @@ void round_topk(oserve_gpu_ctx &c, int K, uint64_t *d_keys, uint64_t *d_best) {
     cuda_ok(cudaMemcpyAsync(d_keys, final_sorted, sizeof(uint64_t) * std::min<size_t>(K, final_n),
                             cudaMemcpyDeviceToDevice, s),
             "D2D");
+    cuda_ok(cudaStreamSynchronize(s), "sync");  // synchronous API: d_keys is ready on return
 }
 
 void switch_cost_keys(oserve_gpu_ctx &c, const oserve_deployment &current, int count, const uint64_t *d_keys,
