@@ -240,7 +240,8 @@ struct Group {
 };
 
 __host__ __device__ constexpr size_t group_scratch_bytes(int J, int RMAX, int KPL) {
-    return ((size_t)J * RMAX * 4 + (size_t)kMaxJ * KPL * 4 + (size_t)RMAX * 2 + RMAX + 15) & ~size_t(15);
+    return ((size_t)kTopK * 8 + (size_t)J * RMAX * 4 + (size_t)kMaxJ * KPL * 4 + (size_t)RMAX * 2 + RMAX + 15) &
+           ~size_t(15);
 }
 
 template <int G, int KPL, bool SMEM>
@@ -302,7 +303,8 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
     const int gib = threadIdx.x / G;
     const size_t per_group = group_scratch_bytes(J, RMAX, KPL);
     unsigned char *gs = smem + off + per_group * gib;
-    int32_t *xs = reinterpret_cast<int32_t *>(gs);                      // [J][RMAX] assignment x
+    uint64_t *tks = reinterpret_cast<uint64_t *>(gs);                   // [kTopK] top-K candidate list
+    int32_t *xs = reinterpret_cast<int32_t *>(tks + kTopK);             // [J][RMAX] assignment x
     uint32_t *Am = reinterpret_cast<uint32_t *>(xs + J * RMAX);         // [kMaxJ][KPL] direct-take masks
     uint16_t *shpS = reinterpret_cast<uint16_t *>(Am + kMaxJ * KPL);    // [RMAX] shape per replica
     uint8_t *pick = reinterpret_cast<uint8_t *>(shpS + RMAX);           // [RMAX] candidate pick per replica
@@ -313,12 +315,10 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
     int jw = 1;
     while (jw < J) jw <<= 1;  // scan width over class positions
     uint64_t best = kNoKey;
-    constexpr int TKE = kTopK / G;  // top-K list entries per lane
-    uint64_t tk[TKE];
-#pragma unroll
-    for (int e = 0; e < TKE; ++e) tk[e] = kNoKey;
+    constexpr int TKE = kTopK / G;  // top-K list entries per lane (shared memory)
+    for (int e = 0; e < TKE; ++e) tks[g.gl * TKE + e] = kNoKey;
     uint64_t tk_max = kNoKey;
-    int tk_lane = 0, tk_slot = 0;
+    int tk_idx = 0;
     bool lossy = false;
     const uint64_t ngroups = static_cast<uint64_t>(gridDim.x) * GPB;
 
@@ -744,8 +744,47 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
                                 (static_cast<uint64_t>(part) << key.sh_part) |
                                 (static_cast<uint64_t>(spp) << key.sh_spp) | local;
             best = kv < best ? kv : best;
+            if (out.topk) {
+                // per-group top-kTopK list, kTopK/G entries per lane (registers)
+                if (kv < tk_max) {
+                    if (tk_max != kNoKey) lossy = true;  // evicts the current worst
+                    if (g.gl == 0) tks[tk_idx] = kv;
+                    g.sync();
+                    uint64_t lm = tks[g.gl * TKE];
+                    int ls = 0;
+#pragma unroll
+                    for (int e = 1; e < TKE; ++e) {
+                        const uint64_t v = tks[g.gl * TKE + e];
+                        if (v > lm) {
+                            lm = v;
+                            ls = e;
+                        }
+                    }
+                    uint64_t gm = lm;
+#pragma unroll
+                    for (int d = G / 2; d > 0; d >>= 1) {
+                        const uint64_t o = __shfl_xor_sync(g.mask, gm, d, G);
+                        gm = o > gm ? o : gm;
+                    }
+                    const int ml = __ffs(g.ballot(lm == gm)) - 1;
+                    tk_idx = ml * TKE + g.bcast(ls, ml);
+                    tk_max = gm;
+                } else {
+                    lossy = true;
+                }
+            }
+            if (out.collect && kv <= out.collect_thr && g.gl == 0) {
+                const unsigned slot = atomicAdd(out.collect_n, 1u);
+                if (slot < out.collect_cap) out.collect[slot] = kv;
+            }
         }
         g.sync();
+    }
+    if (out.topk) {
+        const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * GPB + gib;
+        g.sync();
+        for (int e = 0; e < TKE; ++e) out.topk[gid * kTopK + g.gl * TKE + e] = tks[g.gl * TKE + e];
+        if (g.gl == 0) out.topk_meta[gid] = lossy ? tk_max : kNoKey;
     }
 
     // ---- CTA argmin -> global atomicMin ----
