@@ -9,13 +9,16 @@ on config 5 (128-GPU cluster, 16 request classes, canonical plan space of
 
 One step = one full scheduling round over the whole plan space:
   value : device-resident inputs; K1 (enumerate/unrank -> cost gather -> assign
-          -> objective -> argmin) on every rank's shard + NCCL all-reduce(min) of
-          the packed key; CUDA events on the launching stream, max over ranks;
-          L2 flushed (256 MiB write) between timed iterations.
+          -> objective -> argmin) on every rank's shard, NCCL all-reduce(min) of
+          the packed key, K2 switching cost current -> winner (decoded on the
+          device) — no host round-trip; CUDA events on the launching stream, max
+          over ranks; L2 flushed (256 MiB write) between timed iterations.
   e2e   : the public C-ABI from host buffers every step — enumerate + upload the
-          space tables, upload the workload, cost kernel K0, K1, all-reduce,
-          key D2H, decode, then the switching-cost plan (K2) from the current
-          (init_uniform) deployment to the winner, transfers D2H.
+          space tables, upload the workload, K0 cost kernel, K1 with the exact
+          top-K (default 1024) of the packed key, all-gather + merge across
+          ranks, K2 switching batch current -> each of the K best, key D2H,
+          decode, and the full greedy switch plan current -> winner (transfers
+          D2H).  "current" is init_uniform (deploysearch.cpp:120-136).
 The reference arm (--impl reference) times the reference's own CPU path
 (oracle/_ref: /root/reference/proj compiled unmodified; evaluate_deployment per
 plan, OpenMP over all host threads) on a bounded sample of the same space.
@@ -200,6 +203,9 @@ def run_ours(args, rank, world, local):
     g_min = ctx.min_feasible_group()
     current = init_uniform(w, g_min)
     d_key = torch.empty(1, dtype=torch.int64, device=dev)
+    d_est = torch.empty(1, dtype=torch.float64, device=dev)
+    K = args.topk
+    d_topk = torch.empty(K, dtype=torch.int64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # > 126 MB L2
 
     def barrier():
@@ -208,9 +214,12 @@ def run_ours(args, rank, world, local):
         torch.cuda.synchronize(dev)
 
     def device_step():
+        # enumerate/unrank -> cost gather -> assign -> objective -> shard argmin (K1),
+        # global argmin (NCCL min), switching cost current -> winner (K2, key decoded on device)
         ctx.launch_round_async(d_key.data_ptr())
         if world > 1:
             dist.all_reduce(d_key, op=dist.ReduceOp.MIN)
+        ctx.switch_cost_keys_async(current, d_key.data_ptr(), 1, d_est.data_ptr())
 
     # ---- value: device-resident round, per-step events, L2 flushed between ----
     for _ in range(args.warmup):
@@ -230,7 +239,7 @@ def run_ours(args, rank, world, local):
     barrier()
     clk = clocks.stop()
     launches = ctx.launch_count() - launches0
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    step_ms = [s_.elapsed_time(e_) for s_, e_ in zip(starts, ends)]
     t_local = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
@@ -239,40 +248,44 @@ def run_ours(args, rank, world, local):
     value = plans / (ms_per_step / 1e3)
     key = int(d_key.item())
     state = ctx.decode_key(key)
+    est_winner = float(d_est.item())
 
     # ---- dominant kernel alone (K1 on this rank's shard), CUDA events ----
     k_ms = []
     for i in range(3):
         flush.fill_(i)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_.record(stream)
         ctx.launch_round_async(d_key.data_ptr())
-        b.record(stream)
-        b.synchronize()
-        k_ms.append(a.elapsed_time(b))
+        b_.record(stream)
+        b_.synchronize()
+        k_ms.append(a_.elapsed_time(b_))
     k_ms = statistics.median(k_ms)
     kt = torch.tensor([k_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(kt, op=dist.ReduceOp.MAX)
     k_ms = float(kt.item())
 
-    # ---- e2e: public C-ABI from host buffers, every step ----
+    # ---- e2e: the public C-ABI from host buffers, every step ----
     e2e_ms = []
     bytes0 = None
+    sw_est = []
     for i in range(args.warmup + args.steps):
         barrier()
         if i == args.warmup:
             bytes0 = ctx.copy_bytes()
         t0 = time.perf_counter()
-        _, _ = ctx.prepare_space(w.space_mode, w.space_sizes)      # enumerate + H2D tables
-        ctx.set_workload(w.types, w.lam, w.span_s)                 # H2D workload (K0 runs in the round)
-        ctx.launch_round_async(d_key.data_ptr())                  # K0 + K1 (+K4) on this shard
-        if world > 1:
-            dist.all_reduce(d_key, op=dist.ReduceOp.MIN)
-        k = int(d_key.item())                                      # D2H result key
+        ctx.prepare_space(w.space_mode, w.space_sizes)             # enumerate + H2D space tables
+        ctx.set_workload(w.types, w.lam, w.span_s)                 # H2D workload; K0 cost kernel in the round
+        ctx.round_topk(K, d_topk.data_ptr())                       # K0 + K1 + top-K (exact) on this shard
+        if world > 1:                                              # global top-K: all-gather + merge
+            allk = torch.empty(world * K, dtype=torch.int64, device=dev)
+            dist.all_gather_into_tensor(allk, d_topk)
+            d_topk.copy_(torch.sort(allk).values[:K])
+        sw_est, _ = ctx.switch_cost_keys(current, d_topk.data_ptr(), K)  # K2 batch: current -> K best
+        k = int(d_topk[0].item())                                  # D2H result key
         st = ctx.decode_key(k)
-        if rank == 0:
-            plan = ctx.switch_plan(current, st.deployment)         # K2 + transfers D2H
+        plan = ctx.switch_plan(current, st.deployment)             # K2 detail + transfers D2H
         torch.cuda.synchronize(dev)
         dt = (time.perf_counter() - t0) * 1e3
         dtt = torch.tensor([dt], dtype=torch.float64, device=dev)
@@ -285,6 +298,7 @@ def run_ours(args, rank, world, local):
     bytes1 = ctx.copy_bytes()
     h2d = (bytes1[0] - bytes0[0]) // args.steps
     d2h = (bytes1[1] - bytes0[1]) // args.steps + 8  # + the key read through torch (.item())
+    assert k == key, "e2e and device-resident rounds disagree"
 
     if rank != 0:
         return
@@ -314,10 +328,12 @@ def run_ours(args, rank, world, local):
                    "parallelism": f"plan space sharded x{world} (interleaved 4096-plan chunks) + NCCL min",
                    "l2": "flushed between timed iterations (256 MiB write outside the events)"},
         "winner": {"objective": state.throughput, "key": key, "partition": state.partition_index,
-                   "local_rank": state.local_rank, "shapes": state.deployment.shapes()},
+                   "local_rank": state.local_rank, "deployment": label(state.deployment),
+                   "switch_from": label(current), "switch_est_seconds": est_winner},
         "e2e": {"value": plans / (e2e_step / 1e3), "unit": "plans/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "round_latency_ms": e2e_step,
-                "switch_est_seconds": plan.est_seconds, "switch_transfers": len(plan.transfers)},
+                "d2h_bytes_per_step": d2h, "round_latency_ms": e2e_step, "topk": K,
+                "switch_batch_pairs": K, "switch_est_min_max_s": [min(sw_est), max(sw_est)],
+                "winner_switch_est_seconds": plan.est_seconds, "winner_switch_transfers": len(plan.transfers)},
         "roofline": {"bound": "issue", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tlane-op/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "k_plan_eval (K1)", "kernel_ms": k_ms,
@@ -328,6 +344,15 @@ def run_ours(args, rank, world, local):
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)
+
+
+def label(dep: core.Deployment) -> str:
+    """deployment_label (orchestrate.cpp:34-47): "2x(d4,tp1,pp4)+..."."""
+    groups = {}
+    for r in dep.replicas:
+        k = (r.device_count(), r.tp, r.pp)
+        groups[k] = groups.get(k, 0) + 1
+    return "+".join(f"{c}x(d{d},tp{t},pp{p})" for (d, t, p), c in sorted(groups.items()))
 
 
 def profile_traffic(name):
@@ -348,6 +373,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--topk", type=int, default=1024, help="candidates costed by the switching batch (e2e)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup raised to 3 (timing rules)")

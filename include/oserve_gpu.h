@@ -204,6 +204,12 @@ int oserve_gpu_round_topk(oserve_gpu_ctx *ctx, int K, uint64_t *d_keys, uint64_t
 int oserve_gpu_switch_cost_keys(oserve_gpu_ctx *ctx, const oserve_deployment *current, int count,
                                 const uint64_t *d_keys, double *est_seconds, uint64_t *max_link_bytes);
 
+/* Asynchronous variant on the context's stream: est_seconds written to
+ * device memory d_est[count] (no host synchronisation), e.g. right after the
+ * all-reduce of the round key. */
+int oserve_gpu_switch_cost_keys_async(oserve_gpu_ctx *ctx, const oserve_deployment *current, int count,
+                                      const uint64_t *d_keys, double *d_est);
+
 /* Drop-in for search::exhaustive (deploysearch.cpp:436-466): ordered space,
  * D <= 16 guard, ModelTooLarge when nothing is feasible. */
 int oserve_gpu_exhaustive(oserve_gpu_ctx *ctx, oserve_round_result *out);

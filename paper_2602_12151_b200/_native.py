@@ -27,7 +27,7 @@ EXPORTS = [
     "oserve_gpu_solve_batch", "oserve_gpu_switch_cost_batch", "oserve_gpu_switch_plan",
     "oserve_gpu_launch_count", "oserve_gpu_copy_bytes",
     "oserve_shard_count", "oserve_shard_global_rank", "oserve_key_layout",
-    "oserve_gpu_round_topk", "oserve_gpu_switch_cost_keys",
+    "oserve_gpu_round_topk", "oserve_gpu_switch_cost_keys", "oserve_gpu_switch_cost_keys_async",
 ]
 
 _lib = None
@@ -73,6 +73,7 @@ def load_library() -> C.CDLL:
     L.oserve_gpu_copy_bytes.argtypes = [vp, P(C.c_uint64), P(C.c_uint64)]
     L.oserve_gpu_round_topk.argtypes = [vp, C.c_int, vp, vp]
     L.oserve_gpu_switch_cost_keys.argtypes = [vp, P(A.DeploymentDesc), C.c_int, vp, P(C.c_double), P(C.c_uint64)]
+    L.oserve_gpu_switch_cost_keys_async.argtypes = [vp, P(A.DeploymentDesc), C.c_int, vp, vp]
     L.oserve_shard_count.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.c_int]
     L.oserve_shard_count.restype = C.c_uint64
     L.oserve_shard_global_rank.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.c_int]
@@ -220,6 +221,13 @@ class GpuContext:
         mb = (C.c_uint64 * max(1, count))()
         self._chk(self.lib.oserve_gpu_switch_cost_keys(self.h, C.byref(s), int(count), C.c_void_p(d_keys_ptr), est, mb))
         return list(est[:count]), list(mb[:count])
+
+    def switch_cost_keys_async(self, current: core.Deployment, d_keys_ptr: int, count: int, d_est_ptr: int):
+        """Asynchronous K2 on the context stream; est written to device memory."""
+        keep = A.Keep()
+        s = A.deployment_desc(current, keep)
+        self._chk(self.lib.oserve_gpu_switch_cost_keys_async(self.h, C.byref(s), int(count), C.c_void_p(d_keys_ptr),
+                                                             C.c_void_p(d_est_ptr)))
 
     def exhaustive(self) -> core.SearchState:
         res = A.RoundResult()

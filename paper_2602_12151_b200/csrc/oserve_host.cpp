@@ -952,7 +952,7 @@ void round_topk(oserve_gpu_ctx &c, int K, uint64_t *d_keys, uint64_t *d_best) {
 }
 
 void switch_cost_keys(oserve_gpu_ctx &c, const oserve_deployment &current, int count, const uint64_t *d_keys,
-                      double *est, uint64_t *maxb) {
+                      double *est, uint64_t *maxb, double *d_est_async = nullptr) {
     if (!c.space.valid) fail(OSERVE_ERR_INVALID_ARGUMENT, "no prepared space");
     ensure_tables(c);
     if (c.D() > 256) fail(OSERVE_ERR_UNSUPPORTED, "switch kernel limited to 256 devices");
@@ -985,11 +985,12 @@ void switch_cost_keys(oserve_gpu_ctx &c, const oserve_deployment &current, int c
     d.intra_bw = c.intra;
     d.inter_bw = c.inter;
     SwitchOut o{};
-    o.est = static_cast<double *>(c.d_sw[7].get(sizeof(double) * count));
+    o.est = d_est_async ? d_est_async : static_cast<double *>(c.d_sw[7].get(sizeof(double) * count));
     o.max_bytes = static_cast<uint64_t *>(c.d_sw[8].get(sizeof(uint64_t) * count));
     o.status = static_cast<int32_t *>(c.d_sw[9].get(sizeof(int32_t) * count));
     cuda_ok(launch_switch_cost_keys(d, c.space.view, c.key, c.tables, d_keys, count, nullptr, o, s, &c.launches),
             "switch kernel (keys)");
+    if (d_est_async) return;
     std::vector<int32_t> st;
     cuda_ok(d2h(est, o.est, sizeof(double) * count, s), "D2H");
     if (maxb) cuda_ok(d2h(maxb, o.max_bytes, sizeof(uint64_t) * count, s), "D2H");
@@ -1203,6 +1204,15 @@ int oserve_gpu_switch_cost_keys(oserve_gpu_ctx *ctx, const oserve_deployment *cu
     return guarded(ctx, [&] {
         if (count <= 0) return;
         switch_cost_keys(*ctx, *current, count, d_keys, est_seconds, max_link_bytes);
+    });
+}
+
+int oserve_gpu_switch_cost_keys_async(oserve_gpu_ctx *ctx, const oserve_deployment *current, int count,
+                                      const uint64_t *d_keys, double *d_est) {
+    return guarded(ctx, [&] {
+        if (count <= 0) return;
+        if (!d_est) fail(OSERVE_ERR_INVALID_ARGUMENT, "null d_est");
+        switch_cost_keys(*ctx, *current, count, d_keys, nullptr, nullptr, d_est);
     });
 }
 
