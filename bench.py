@@ -52,6 +52,22 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+_RESULT_FD = None
+
+
+def emit(line: dict):
+    """The one JSON line on the original stdout (libraries' banners, e.g.
+    NCCL's version line, are redirected to stderr at the fd level)."""
+    os.write(_RESULT_FD if _RESULT_FD is not None else 1, (json.dumps(line) + "\n").encode())
+
+
+def quiet_stdout():
+    global _RESULT_FD
+    sys.stdout.flush()
+    _RESULT_FD = os.dup(1)
+    os.dup2(2, 1)
+
+
 def init_dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -185,7 +201,7 @@ def run_reference(args, rank, world):
                              "sample": f"{per_step} uniform random plans of {plans} per step "
                                        f"(evaluate_deployment each, OpenMP dynamic,4 over {threads} threads)"},
             "e2e": {"value": value, "unit": "plans/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def run_ours(args, rank, world, local):
@@ -343,7 +359,7 @@ def run_ours(args, rank, world, local):
         "gpu_launches": launches,
         "clocks": clk,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def label(dep: core.Deployment) -> str:
@@ -378,6 +394,7 @@ def main():
     if args.warmup < 3:
         log("warmup raised to 3 (timing rules)")
         args.warmup = 3
+    quiet_stdout()
     rank, world, local = init_dist()
     try:
         if args.impl == "reference":
