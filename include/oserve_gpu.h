@@ -218,6 +218,43 @@ int oserve_gpu_exhaustive(oserve_gpu_ctx *ctx, oserve_round_result *out);
 int oserve_gpu_best_strategies(oserve_gpu_ctx *ctx, int num_replicas, const int *sizes,
                                oserve_round_result *out);
 
+/* ---- flow-guided heuristic search (deploysearch.cpp:341-417) ----------- */
+
+/* search::SearchOptions (deploysearch.hpp:76-84). */
+typedef struct {
+    uint64_t seed;                        /* default 0   */
+    int max_iters;                        /* default 500 */
+    int stale_limit;                      /* default 20  */
+    int mutation_retries;                 /* default 8   */
+    const oserve_deployment *warm_start;  /* NULL: init_uniform */
+} oserve_search_options;
+
+/* search::SearchLogRow (deploysearch.hpp:68-74). */
+typedef struct {
+    int iteration;
+    int accepted;
+    int64_t throughput;
+    int devices;
+    char op[120];
+} oserve_search_log_row;
+
+/* search::SearchState (deploysearch.hpp:86-92). */
+typedef struct {
+    int64_t throughput;
+    uint64_t rng_seed;
+    int stale_iters;
+    int iterations;
+    int log_count;         /* rows written to the caller's log buffer */
+    oserve_plan deployment;
+} oserve_search_result;
+
+/* Drop-in for search::search: the reference's mutate / enumerate / revert
+ * loop on the host (same mt19937_64 stream, mutate_sizes, classify,
+ * absorb_leftovers), every best_strategies and the per-iteration
+ * capacity-table + assignment on the GPU.  Uses the context's workload. */
+int oserve_gpu_search(oserve_gpu_ctx *ctx, const oserve_search_options *opts, oserve_search_result *out,
+                      oserve_search_log_row *log, int log_capacity);
+
 /* Per-plan objectives for ranks [first, first+count) of the prepared space
  * (host output arrays; sum_pp may be NULL). */
 int oserve_gpu_evaluate_ranks(oserve_gpu_ctx *ctx, uint64_t first, uint64_t count,

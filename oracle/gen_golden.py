@@ -143,6 +143,25 @@ def main():
                             "local_rank": s.local_rank, "sum_pp": s.sum_pp, "deployment": dep_json(s.deployment)}
     json.dump(rounds, open(os.path.join(OUT, "rounds.json"), "w"), indent=1)
 
+    # ---- search::search (flow-guided heuristic) with its log ----
+    srch = []
+    for name, seeds in (("cfg1", range(5)), ("cfg1_bnb", range(2)), ("cfg2", range(3)), ("cfg2_low", range(2))):
+        w = workloads.load(name)
+        pr = problem(w)
+        for seed in seeds:
+            st, log = ref.search(pr, seed=seed)
+            srch.append({"config": name, "seed": seed, "throughput": st.throughput, "iterations": st.iterations,
+                         "stale_iters": st.stale_iters, "deployment": dep_json(st.deployment),
+                         "log": [list(r) for r in log]})
+    # warm-started (build_adaptive_timeline style, orchestrate.cpp:116-123)
+    w = workloads.load("cfg2")
+    warm = core.canonical_deployment(w.cluster, [4] * 8, [4] * 8)
+    st, log = ref.search(problem(w), seed=0, max_iters=150, warm_start=warm)
+    srch.append({"config": "cfg2", "seed": 0, "max_iters": 150, "warm_start": dep_json(warm),
+                 "throughput": st.throughput, "iterations": st.iterations, "stale_iters": st.stale_iters,
+                 "deployment": dep_json(st.deployment), "log": [list(r) for r in log]})
+    json.dump(srch, open(os.path.join(OUT, "search.json"), "w"))
+
     # ---- switching: greedy_plan + estimate_time on seeded pairs ----
     sw = []
     for name in ("cfg1", "cfg2", "cfg5"):

@@ -69,6 +69,10 @@ int oracle_switch_plan(const oserve_cluster_desc *c, uint64_t param_bytes,
                        oserve_transfer *transfers, int *num_transfers, double *est_seconds,
                        uint64_t *max_link_bytes);
 
+/* search::search (deploysearch.cpp:341-417) with its log (reference only). */
+int oracle_search(const oracle_problem *p, const oserve_search_options *opts, oserve_search_result *out,
+                  oserve_search_log_row *log, int log_capacity);
+
 /* Reference-only helpers used to generate the synthetic workloads. */
 int oracle_fit_types(int64_t n, const uint32_t *input_len, const uint32_t *output_len, int k,
                      uint64_t seed, double *centroid_in, double *centroid_out);

@@ -879,6 +879,12 @@ int oracle_switch_plan(const oserve_cluster_desc *cd, uint64_t P, const oserve_d
     });
 }
 
+int oracle_search(const oracle_problem *, const oserve_search_options *, oserve_search_result *,
+                  oserve_search_log_row *, int) {
+    g_err = "search: reference-only (use the _ref oracle)";
+    return OSERVE_ERR_UNSUPPORTED;
+}
+
 int oracle_fit_types(int64_t, const uint32_t *, const uint32_t *, int, uint64_t, double *, double *) {
     g_err = "fit_types: reference-only (use the _ref oracle)";
     return OSERVE_ERR_UNSUPPORTED;

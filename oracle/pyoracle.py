@@ -182,6 +182,15 @@ class Oracle:
         transfers = [core.Transfer(core.ByteRange(t.begin, t.end), t.src, t.dst) for t in tr[:cap]]
         return core.SwitchPlan(transfers, est.value), mx.value
 
+    def search(self, pr: Problem, seed: int = 0, max_iters: int = 500, stale_limit: int = 20,
+               mutation_retries: int = 8, warm_start: Optional[core.Deployment] = None, log_capacity: int = 1024):
+        keep = A.Keep()
+        o = A.search_options(seed, max_iters, stale_limit, mutation_retries, warm_start, keep)
+        res = A.SearchResult()
+        log = (A.SearchLogRow * log_capacity)()
+        self._chk(self.lib.oracle_search(C.byref(pr.desc), C.byref(o), C.byref(res), log, log_capacity))
+        return A.search_outcome(res, log, res.log_count)
+
     # -- workload (reference only) -------------------------------------------
     def fit_types(self, input_len, output_len, k: int, seed: int = 0):
         inp = np.ascontiguousarray(np.asarray(input_len, np.uint32))

@@ -19,6 +19,7 @@
 // which restates the reference's anonymous-namespace partitions_desc.
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -502,6 +503,44 @@ int oracle_switch_plan(const oserve_cluster_desc *c, uint64_t param_bytes, const
             for (const auto &[link, bytes] : plan.link_load) m = std::max(m, bytes);
             *max_link_bytes = m;
         }
+    });
+}
+
+int oracle_search(const oracle_problem *p, const oserve_search_options *o, oserve_search_result *out,
+                  oserve_search_log_row *log, int log_capacity) {
+    return guarded([&] {
+        Problem pr(*p);
+        search::SearchOptions so;
+        so.seed = o->seed;
+        so.max_iters = o->max_iters;
+        so.stale_limit = o->stale_limit;
+        so.mutation_retries = o->mutation_retries;
+        so.parallel = true;
+        Deployment warm;
+        if (o->warm_start) {
+            warm = to_dep(*o->warm_start);
+            so.warm_start = &warm;
+        }
+        int n = 0;
+        so.log = [&](const search::SearchLogRow &r) {
+            if (log && n < log_capacity) {
+                oserve_search_log_row &row = log[n];
+                row.iteration = r.iteration;
+                row.accepted = r.accepted ? 1 : 0;
+                row.throughput = r.throughput;
+                row.devices = r.devices;
+                std::snprintf(row.op, sizeof(row.op), "%s", r.op.c_str());
+            }
+            ++n;
+        };
+        search::SearchState st = search::search(pr.cluster, pr.model, pr.types, pr.span, pr.span_s, pr.params, so);
+        std::memset(out, 0, sizeof(*out));
+        out->throughput = st.throughput;
+        out->rng_seed = st.rng_seed;
+        out->stale_iters = st.stale_iters;
+        out->iterations = st.iterations;
+        out->log_count = n;
+        from_dep(st.deployment, &out->deployment);
     });
 }
 

@@ -84,6 +84,38 @@ class TransferDesc(C.Structure):
     _fields_ = [("begin", C.c_uint64), ("end", C.c_uint64), ("src", C.c_int), ("dst", C.c_int)]
 
 
+class SearchOptionsDesc(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("max_iters", C.c_int), ("stale_limit", C.c_int),
+                ("mutation_retries", C.c_int), ("warm_start", C.POINTER(DeploymentDesc))]
+
+
+class SearchLogRow(C.Structure):
+    _fields_ = [("iteration", C.c_int), ("accepted", C.c_int), ("throughput", C.c_int64), ("devices", C.c_int),
+                ("op", C.c_char * 120)]
+
+
+class SearchResult(C.Structure):
+    _fields_ = [("throughput", C.c_int64), ("rng_seed", C.c_uint64), ("stale_iters", C.c_int),
+                ("iterations", C.c_int), ("log_count", C.c_int), ("deployment", Plan)]
+
+
+def search_options(seed=0, max_iters=500, stale_limit=20, mutation_retries=8, warm_start=None, keep=None):
+    keep = keep or Keep()
+    ws = None
+    if warm_start is not None and warm_start.replicas:
+        ws = C.pointer(keep(deployment_desc(warm_start, keep)))
+    return SearchOptionsDesc(seed, max_iters, stale_limit, mutation_retries, ws)
+
+
+def search_outcome(res: SearchResult, log, n: int):
+    rows = [(log[i].iteration, log[i].op.decode(), bool(log[i].accepted), log[i].throughput, log[i].devices)
+            for i in range(min(n, len(log)))]
+    st = core.SearchState(plan_to_deployment(res.deployment), res.throughput, res.iterations)
+    st.stale_iters = res.stale_iters
+    st.rng_seed = res.rng_seed
+    return st, rows
+
+
 class ProblemDesc(C.Structure):
     """oracle_problem (oracle/oracle_api.h) — test infrastructure only."""
     _fields_ = [("cluster", ClusterDesc), ("model", ModelDesc), ("profile", Profile),

@@ -28,6 +28,7 @@ EXPORTS = [
     "oserve_gpu_launch_count", "oserve_gpu_copy_bytes",
     "oserve_shard_count", "oserve_shard_global_rank", "oserve_key_layout",
     "oserve_gpu_round_topk", "oserve_gpu_switch_cost_keys", "oserve_gpu_switch_cost_keys_async",
+    "oserve_gpu_search",
 ]
 
 _lib = None
@@ -74,6 +75,7 @@ def load_library() -> C.CDLL:
     L.oserve_gpu_round_topk.argtypes = [vp, C.c_int, vp, vp]
     L.oserve_gpu_switch_cost_keys.argtypes = [vp, P(A.DeploymentDesc), C.c_int, vp, P(C.c_double), P(C.c_uint64)]
     L.oserve_gpu_switch_cost_keys_async.argtypes = [vp, P(A.DeploymentDesc), C.c_int, vp, vp]
+    L.oserve_gpu_search.argtypes = [vp, P(A.SearchOptionsDesc), P(A.SearchResult), P(A.SearchLogRow), C.c_int]
     L.oserve_shard_count.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.c_int]
     L.oserve_shard_count.restype = C.c_uint64
     L.oserve_shard_global_rank.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.c_int]
@@ -228,6 +230,16 @@ class GpuContext:
         s = A.deployment_desc(current, keep)
         self._chk(self.lib.oserve_gpu_switch_cost_keys_async(self.h, C.byref(s), int(count), C.c_void_p(d_keys_ptr),
                                                              C.c_void_p(d_est_ptr)))
+
+    def search(self, seed: int = 0, max_iters: int = 500, stale_limit: int = 20, mutation_retries: int = 8,
+               warm_start: Optional[core.Deployment] = None, log_capacity: int = 1024):
+        """search::search (deploysearch.cpp:341-417) -> (SearchState, log rows)."""
+        keep = A.Keep()
+        o = A.search_options(seed, max_iters, stale_limit, mutation_retries, warm_start, keep)
+        res = A.SearchResult()
+        log = (A.SearchLogRow * log_capacity)()
+        self._chk(self.lib.oserve_gpu_search(self.h, C.byref(o), C.byref(res), log, log_capacity))
+        return A.search_outcome(res, log, res.log_count)
 
     def exhaustive(self) -> core.SearchState:
         res = A.RoundResult()

@@ -26,6 +26,8 @@
 #include <map>
 #include <memory>
 #include <numeric>
+#include <random>
+#include <sstream>
 #include <set>
 #include <stdexcept>
 #include <string>
@@ -1250,6 +1252,234 @@ int oserve_gpu_best_strategies(oserve_gpu_ctx *ctx, int num_replicas, const int 
         decode_key(*ctx, key, out);
         if (out->objective < 0) out->objective = 0;
     });
+}
+
+// ---------------------------------------------------------------------------
+// search::search (deploysearch.cpp:341-417): the reference's host loop, with
+// best_strategies and the per-iteration capacity table + assignment on the
+// GPU.  classify (:57-75), mutate_sizes (:240-319), absorb_leftovers
+// (:324-337) and init_uniform (:120-136) are restated; the mt19937_64 stream
+// and every draw (rng() % n) happen in the reference's order.
+namespace {
+
+struct Mutation {
+    std::vector<int> sizes;
+    std::string op;
+};
+
+Mutation mutate_sizes(const std::vector<int> &sizes, const std::vector<int> &pps, const std::vector<int> &over,
+                      const std::vector<int> &under, int g_min, std::mt19937_64 &rng) {
+    std::vector<int> sz = sizes;
+    std::vector<char> alive(sz.size(), 1);
+    std::ostringstream ops;
+    auto below = [&](uint64_t n) { return rng() % n; };
+    auto alive_in = [&](const std::vector<int> &set, int except) {
+        std::vector<int> o;
+        for (int r : set)
+            if (r != except && alive[r]) o.push_back(r);
+        return o;
+    };
+    std::vector<std::pair<int, int>> splits;
+    for (int r : over) {
+        if (!alive[r]) continue;
+        const bool try_merge = below(2) == 0;
+        std::vector<int> others = alive_in(over, r);
+        std::vector<int> donors;
+        for (int u : alive_in(under, -1))
+            if (sz[u] > g_min) donors.push_back(u);
+        if (try_merge && !others.empty()) {
+            const int r2 = others[below(others.size())];
+            sz[r] += sz[r2];
+            alive[r2] = 0;
+            ops << "merge(" << r << "," << r2 << ");";
+        } else if (!donors.empty()) {
+            const int u = donors[below(donors.size())];
+            int delta = std::max(1, sz[u] / std::max(1, pps[u]));
+            delta = std::min(delta, sz[u] - g_min);
+            if (delta <= 0) continue;
+            sz[r] += delta;
+            sz[u] -= delta;
+            ops << "swap(" << r << "<-" << u << ",d=" << delta << ");";
+        } else if (!others.empty()) {
+            const int r2 = others[below(others.size())];
+            sz[r] += sz[r2];
+            alive[r2] = 0;
+            ops << "merge(" << r << "," << r2 << ");";
+        }
+    }
+    for (int r : under) {
+        if (!alive[r]) continue;
+        const bool try_split = below(2) == 0;
+        const bool can_split = sz[r] >= 2 * g_min;
+        std::vector<int> receivers = alive_in(over, -1);
+        int delta = std::max(1, sz[r] / std::max(1, pps[r]));
+        delta = std::min(delta, sz[r] - g_min);
+        const bool can_swap = !receivers.empty() && delta > 0;
+        if (try_split && can_split) {
+            splits.emplace_back(r, sz[r] / 2);
+            ops << "split(" << r << ");";
+        } else if (can_swap) {
+            const int o = receivers[below(receivers.size())];
+            sz[o] += delta;
+            sz[r] -= delta;
+            ops << "swap(" << o << "<-" << r << ",d=" << delta << ");";
+        } else if (can_split) {
+            splits.emplace_back(r, sz[r] / 2);
+            ops << "split(" << r << ");";
+        }
+    }
+    Mutation m;
+    for (size_t r = 0; r < sz.size(); ++r) {
+        if (!alive[r]) continue;
+        auto it = std::find_if(splits.begin(), splits.end(), [&](const auto &p) { return p.first == static_cast<int>(r); });
+        if (it != splits.end()) {
+            m.sizes.push_back(it->second);
+            m.sizes.push_back(sz[r] - it->second);
+        } else {
+            m.sizes.push_back(sz[r]);
+        }
+    }
+    m.op = ops.str();
+    return m;
+}
+
+std::vector<int> absorb_leftovers(std::vector<int> sizes, int D, int g_min) {
+    int left = D - std::accumulate(sizes.begin(), sizes.end(), 0);
+    while (left >= g_min) {
+        sizes.push_back(g_min);
+        left -= g_min;
+    }
+    while (left > 0 && !sizes.empty()) {
+        *std::min_element(sizes.begin(), sizes.end()) += 1;
+        --left;
+    }
+    return sizes;
+}
+
+int64_t device_total(const oserve_plan &p) {
+    int64_t n = 0;
+    for (int r = 0; r < p.num_replicas; ++r) n += p.replica_num_devices[r];
+    return n;
+}
+
+void check_status(int st, oserve_gpu_ctx *ctx) {
+    if (st != OSERVE_OK) fail(st, ctx->err);
+}
+
+}  // namespace
+
+int oserve_gpu_search(oserve_gpu_ctx *ctx, const oserve_search_options *opts, oserve_search_result *out,
+                      oserve_search_log_row *log, int log_capacity) {
+    if (!ctx || !opts || !out) return OSERVE_ERR_INVALID_ARGUMENT;
+    std::string err;
+    int code = OSERVE_OK;
+    try {
+        const int g_min = [&] {
+            int g = 0;
+            check_status(oserve_gpu_min_feasible_group(ctx, &g), ctx);
+            return g;
+        }();
+        const int D = ctx->D();
+        std::vector<int> sizes;
+        if (opts->warm_start && opts->warm_start->num_replicas > 0) {
+            for (int r = 0; r < opts->warm_start->num_replicas; ++r)
+                sizes.push_back(opts->warm_start->replica_num_devices[r]);
+        } else {
+            // init_uniform: D / g_min replicas of g_min devices, each block must
+            // have a feasible strategy
+            const int R = D / g_min;
+            for (int r = 0; r < R; ++r) {
+                std::vector<int> ids;
+                candidates(*ctx, r * g_min, g_min, ids);
+                if (ids.empty())
+                    fail(OSERVE_ERR_MODEL_TOO_LARGE, "no feasible strategy for a " + std::to_string(g_min) +
+                                                         "-device replica");
+                sizes.push_back(g_min);
+            }
+        }
+        sizes = absorb_leftovers(std::move(sizes), D, g_min);
+        auto current = std::make_unique<oserve_round_result>();
+        check_status(oserve_gpu_best_strategies(ctx, static_cast<int>(sizes.size()), sizes.data(), current.get()), ctx);
+        if (current->plan.num_replicas == 0)
+            fail(OSERVE_ERR_MODEL_TOO_LARGE, "search: no feasible strategy for the initial deployment");
+        std::mt19937_64 rng(opts->seed);
+        int stale = 0, iter = 0, nlog = 0;
+        auto emit = [&](const std::string &op, bool accepted) {
+            if (log && nlog < log_capacity) {
+                oserve_search_log_row &row = log[nlog];
+                row.iteration = iter;
+                row.accepted = accepted ? 1 : 0;
+                row.throughput = current->objective;
+                row.devices = static_cast<int>(device_total(current->plan));
+                std::snprintf(row.op, sizeof(row.op), "%s", op.c_str());
+            }
+            ++nlog;
+        };
+        auto candidate = std::make_unique<oserve_round_result>();
+        while (iter < opts->max_iters && stale < opts->stale_limit) {
+            ++iter;
+            // capacity table + assignment of the current deployment (GPU), classify
+            const oserve_plan &cp = current->plan;
+            const int R = cp.num_replicas, J = ctx->J;
+            oserve_deployment dd{R, cp.replica_num_devices, cp.device_ids, cp.tp, cp.pp};
+            std::vector<int64_t> M(R), unit(static_cast<size_t>(R) * J), used(R);
+            check_status(oserve_gpu_plan_detail(ctx, &dd, nullptr, nullptr, nullptr, nullptr, M.data(), unit.data(),
+                                                used.data(), nullptr),
+                         ctx);
+            std::vector<int> over, under, cur_sizes, cur_pps;
+            for (int k = 0; k < R; ++k) {
+                int64_t min_unit = std::numeric_limits<int64_t>::max();
+                for (int j = 0; j < J; ++j)
+                    if (unit[k * J + j] > 0) min_unit = std::min(min_unit, unit[k * J + j]);
+                const bool saturated =
+                    min_unit != std::numeric_limits<int64_t>::max() && M[k] - used[k] < min_unit;
+                (saturated ? over : under).push_back(k);
+                cur_sizes.push_back(cp.replica_num_devices[k]);
+                cur_pps.push_back(cp.pp[k]);
+            }
+            Mutation mut;
+            bool found = false;
+            for (int attempt = 0; attempt < opts->mutation_retries && !found; ++attempt) {
+                mut = mutate_sizes(cur_sizes, cur_pps, over, under, g_min, rng);
+                std::vector<int> a = mut.sizes, b = cur_sizes;
+                std::sort(a.begin(), a.end());
+                std::sort(b.begin(), b.end());
+                found = !mut.op.empty() && a != b;
+            }
+            if (!found) {
+                ++stale;
+                emit("stale(no-mutation)", false);
+                continue;
+            }
+            check_status(oserve_gpu_best_strategies(ctx, static_cast<int>(mut.sizes.size()), mut.sizes.data(),
+                                                    candidate.get()),
+                         ctx);
+            const bool accepted = candidate->plan.num_replicas > 0 && candidate->objective > current->objective;
+            if (accepted) {
+                std::swap(current, candidate);
+                stale = 0;
+            } else {
+                ++stale;
+            }
+            emit(mut.op, accepted);
+        }
+        std::memset(out, 0, sizeof(*out));
+        out->throughput = current->objective;
+        out->rng_seed = opts->seed;
+        out->stale_iters = stale;
+        out->iterations = iter;
+        out->log_count = nlog;
+        out->deployment = current->plan;
+        ctx->err.clear();
+    } catch (const Fail &e) {
+        code = e.code;
+        err = e.what();
+    } catch (const std::exception &e) {
+        code = OSERVE_ERR_INVALID_ARGUMENT;
+        err = e.what();
+    }
+    if (code != OSERVE_OK) ctx->err = err;
+    return code;
 }
 
 int oserve_gpu_evaluate_ranks(oserve_gpu_ctx *ctx, uint64_t first, uint64_t count, int64_t *objective,

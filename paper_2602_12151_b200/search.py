@@ -71,6 +71,18 @@ def exhaustive(cluster: core.ClusterSpec, model: core.ModelSpec, types: Sequence
     return g.exhaustive()
 
 
+def search(cluster: core.ClusterSpec, model: core.ModelSpec, types: Sequence[core.WorkloadType],
+           span: core.TraceSpan, span_seconds: float, params: Optional[core.ProfileParams] = None,
+           seed: int = 0, max_iters: int = 500, stale_limit: int = 20, mutation_retries: int = 8,
+           warm_start: Optional[core.Deployment] = None, device: int = 0):
+    """search::search (deploysearch.cpp:341-417): flow-guided mutate / enumerate
+    / revert loop; returns (SearchState, log rows (iteration, op, accepted,
+    throughput, devices))."""
+    g = GpuContext(cluster, model, params or core.ProfileParams(), device)
+    g.set_workload(list(types), span.counts, span_seconds)
+    return g.search(seed, max_iters, stale_limit, mutation_retries, warm_start)
+
+
 def scheduling_round(ctx: EvalContext, mode: int = A.SPACE_ORDERED, sizes: Sequence[int] = ()) -> core.SearchState:
     """Argmin over a whole plan space (no D <= 16 guard)."""
     return ctx.gpu().round(mode, list(sizes))
