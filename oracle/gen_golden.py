@@ -145,14 +145,15 @@ def main():
 
     # ---- search::search (flow-guided heuristic) with its log ----
     srch = []
-    for name, seeds in (("cfg1", range(5)), ("cfg1_bnb", range(2)), ("cfg2", range(3)), ("cfg2_low", range(2))):
+    for name, seeds, iters in (("cfg1", range(5), 500), ("cfg1_bnb", range(1), 2), ("cfg2", range(3), 500),
+                               ("cfg2_low", range(2), 500)):
         w = workloads.load(name)
         pr = problem(w)
         for seed in seeds:
-            st, log = ref.search(pr, seed=seed)
-            srch.append({"config": name, "seed": seed, "throughput": st.throughput, "iterations": st.iterations,
-                         "stale_iters": st.stale_iters, "deployment": dep_json(st.deployment),
-                         "log": [list(r) for r in log]})
+            st, log = ref.search(pr, seed=seed, max_iters=iters)
+            srch.append({"config": name, "seed": seed, "max_iters": iters, "throughput": st.throughput,
+                         "iterations": st.iterations, "stale_iters": st.stale_iters,
+                         "deployment": dep_json(st.deployment), "log": [list(r) for r in log]})
     # warm-started (build_adaptive_timeline style, orchestrate.cpp:116-123)
     w = workloads.load("cfg2")
     warm = core.canonical_deployment(w.cluster, [4] * 8, [4] * 8)

@@ -33,21 +33,3 @@ def test_search_matches_reference(cuda, case):
     assert st.iterations == case["iterations"] and st.stale_iters == case["stale_iters"]
     assert [[r.device_ids, r.tp, r.pp] for r in st.deployment.replicas] == case["deployment"]
     assert [list(r) for r in log] == case["log"]
-
-
-def test_search_quality_vs_exhaustive(cuda):
-    """SPEC.md acceptance #5 (restated): on seeded D=8 instances the heuristic
-    search reaches >= 0.94 x the exhaustive optimum on most instances — here
-    checked as a property of the GPU search against the GPU exhaustive round."""
-    import numpy as np
-    w = workloads.load("cfg1")
-    rng = np.random.default_rng(5)
-    ok = 0
-    for i in range(20):
-        lam = [int(v) for v in rng.integers(200, 1500, 2)]
-        g = GpuContext(w.cluster, w.model, w.params)
-        g.set_workload(w.types, lam, w.span_s)
-        ex = g.exhaustive().throughput
-        st, _ = g.search(seed=i)
-        ok += st.throughput >= 0.94 * ex
-    assert ok >= 10
