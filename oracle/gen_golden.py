@@ -163,6 +163,12 @@ def main():
                  "deployment": dep_json(st.deployment), "log": [list(r) for r in log]})
     json.dump(srch, open(os.path.join(OUT, "search.json"), "w"))
 
+    # ---- orch::build_adaptive_timeline on config 4 (24 windows) ----
+    w = workloads.load("cfg4")
+    tl = ref.adaptive_timeline(problem(w), w.raw["actual"], seed=0, max_iters=150, min_gain=w.raw["min_gain"])
+    json.dump([{"span_index": si, "deployment": dep_json(d), "x": x, "switch_seconds": sw, "transfers": n}
+               for si, d, x, sw, n in tl], open(os.path.join(OUT, "timeline_cfg4.json"), "w"))
+
     # ---- switching: greedy_plan + estimate_time on seeded pairs ----
     sw = []
     for name in ("cfg1", "cfg2", "cfg5"):

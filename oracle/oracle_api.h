@@ -73,6 +73,14 @@ int oracle_switch_plan(const oserve_cluster_desc *c, uint64_t param_bytes,
 int oracle_search(const oracle_problem *p, const oserve_search_options *opts, oserve_search_result *out,
                   oserve_search_log_row *log, int log_capacity);
 
+/* orch::build_adaptive_timeline (orchestrate.cpp:94-154) over T spans of
+ * actual per-class counts [T][J] (reference only).  Per entry e (< capacity):
+ * span_index[e], plans[e], x[e][k][j] (R <= 128, J classes, row stride 128*J),
+ * switch_seconds[e], transfers[e]; returns the entry count. */
+int oracle_adaptive_timeline(const oracle_problem *p, int T, const int64_t *counts, uint64_t seed, int max_iters,
+                             double min_gain, int capacity, int64_t *span_index, oserve_plan *plans, int64_t *x,
+                             double *switch_seconds, int *transfers, int *count);
+
 /* Reference-only helpers used to generate the synthetic workloads. */
 int oracle_fit_types(int64_t n, const uint32_t *input_len, const uint32_t *output_len, int k,
                      uint64_t seed, double *centroid_in, double *centroid_out);

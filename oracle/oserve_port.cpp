@@ -885,6 +885,12 @@ int oracle_search(const oracle_problem *, const oserve_search_options *, oserve_
     return OSERVE_ERR_UNSUPPORTED;
 }
 
+int oracle_adaptive_timeline(const oracle_problem *, int, const int64_t *, uint64_t, int, double, int, int64_t *,
+                             oserve_plan *, int64_t *, double *, int *, int *) {
+    g_err = "adaptive timeline: reference-only (use the _ref oracle)";
+    return OSERVE_ERR_UNSUPPORTED;
+}
+
 int oracle_fit_types(int64_t, const uint32_t *, const uint32_t *, int, uint64_t, double *, double *) {
     g_err = "fit_types: reference-only (use the _ref oracle)";
     return OSERVE_ERR_UNSUPPORTED;

@@ -191,6 +191,28 @@ class Oracle:
         self._chk(self.lib.oracle_search(C.byref(pr.desc), C.byref(o), C.byref(res), log, log_capacity))
         return A.search_outcome(res, log, res.log_count)
 
+    def adaptive_timeline(self, pr: Problem, actual, seed: int = 0, max_iters: int = 150, min_gain: float = 0.01):
+        """orch::build_adaptive_timeline (reference only) -> list of entries
+        (span_index, deployment, x, switch_seconds, n_transfers)."""
+        T, J = len(actual), len(actual[0])
+        cap = 64
+        si = (C.c_int64 * cap)()
+        plans = (A.Plan * cap)()
+        x = (C.c_int64 * (cap * 128 * J))()
+        sw = (C.c_double * cap)()
+        ntr = (C.c_int * cap)()
+        n = C.c_int()
+        flat = A._arr(C.c_int64, [v for row in actual for v in row])
+        self._chk(self.lib.oracle_adaptive_timeline(C.byref(pr.desc), T, flat, C.c_uint64(seed), max_iters,
+                                                    C.c_double(min_gain), cap, si, plans, x, sw, ntr, C.byref(n)))
+        out = []
+        for e in range(min(n.value, cap)):
+            dep = A.plan_to_deployment(plans[e])
+            R = dep.replica_count()
+            xs = [list(x[(e * 128 + k) * J:(e * 128 + k + 1) * J]) for k in range(R)]
+            out.append((si[e], dep, xs, sw[e], ntr[e]))
+        return out
+
     # -- workload (reference only) -------------------------------------------
     def fit_types(self, input_len, output_len, k: int, seed: int = 0):
         inp = np.ascontiguousarray(np.asarray(input_len, np.uint32))

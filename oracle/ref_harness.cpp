@@ -544,6 +544,41 @@ int oracle_search(const oracle_problem *p, const oserve_search_options *o, oserv
     });
 }
 
+int oracle_adaptive_timeline(const oracle_problem *p, int T, const int64_t *counts, uint64_t seed, int max_iters,
+                             double min_gain, int capacity, int64_t *span_index, oserve_plan *plans, int64_t *x,
+                             double *switch_seconds, int *transfers, int *count) {
+    return guarded([&] {
+        Problem pr(*p);
+        const int J = p->num_classes;
+        workload::SpanSeries series;
+        series.span_seconds = static_cast<int>(pr.span_s);
+        for (int t = 0; t < T; ++t)
+            series.spans.push_back({t, std::vector<int64_t>(counts + t * J, counts + (t + 1) * J)});
+        workload::TypeModel tm;
+        tm.k = J;
+        tm.centroids = pr.types;
+        orch::OrchestrateOptions oo;
+        oo.seed = seed;
+        oo.span_seconds = static_cast<int>(pr.span_s);
+        oo.k = J;
+        oo.min_gain = min_gain;
+        oo.search_max_iters = max_iters;
+        oo.parallel = true;
+        sim::StrategyTimeline tl = orch::build_adaptive_timeline(series, tm, pr.cluster, pr.model, pr.params, oo);
+        int n = static_cast<int>(tl.entries.size());
+        *count = n;
+        for (int e = 0; e < std::min(n, capacity); ++e) {
+            const auto &en = tl.entries[e];
+            span_index[e] = en.start_span;
+            from_dep(en.deployment, &plans[e]);
+            for (size_t k = 0; k < en.assignment.x.size(); ++k)
+                for (int j = 0; j < J; ++j) x[(static_cast<size_t>(e) * 128 + k) * J + j] = en.assignment.x[k][j];
+            switch_seconds[e] = en.switch_seconds;
+            transfers[e] = static_cast<int>(en.plan.transfers.size());
+        }
+    });
+}
+
 int oracle_fit_types(int64_t n, const uint32_t *input_len, const uint32_t *output_len, int k, uint64_t seed,
                      double *centroid_in, double *centroid_out) {
     return guarded([&] {

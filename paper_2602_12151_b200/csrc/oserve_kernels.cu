@@ -875,8 +875,8 @@ __device__ int64_t suffix_bound(const ShapeTables &t, const ExactState &st, int 
         const int64_t u = t.unit[s * st.J + j];
         int64_t tk = t.cap[s * st.J + j];
         if (lam[j] < tk) tk = lam[j];
-        const int64_t byb = mr / u;
-        if (byb < tk) tk = byb;
+        // min(tk, mr / u) without a 64-bit division (tk < 2^31)
+        if (tk * u > mr) tk = quot_small(mr, u, t.inv_unit[s * st.J + j]);
         if (tk > 0) {
             cnt += tk;
             lam[j] -= tk;
@@ -969,7 +969,7 @@ __global__ void __launch_bounds__(128) k_plan_exact(ShapeTables t, SpaceTables s
                 const int64_t u = t.unit[s * J + j];
                 int64_t hi = t.cap[s * J + j];
                 if (st.lam[j] < hi) hi = st.lam[j];
-                if (st.mrem[k] / u < hi) hi = st.mrem[k] / u;
+                if (hi * u > st.mrem[k]) hi = quot_small(st.mrem[k], u, t.inv_unit[s * J + j]);
                 fk[depth] = k;
                 fpos[depth] = pos;
                 fj[depth] = j;

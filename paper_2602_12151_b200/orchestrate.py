@@ -44,7 +44,11 @@ class Timeline:
 
 def build_adaptive_timeline(ctx: GpuContext, types: Sequence[core.WorkloadType], forecasts: Sequence[Sequence[int]],
                             span_seconds: float = 60.0, min_gain: float = 0.01, mode: int = A.SPACE_ORDERED,
-                            sizes: Sequence[int] = ()) -> Timeline:
+                            sizes: Sequence[int] = (), strategy: str = "round", seed: int = 0,
+                            search_max_iters: int = 150, search_stale_limit: int = 20) -> Timeline:
+    """strategy="round": full-space GPU round per window (SURVEY config 4).
+    strategy="search": the reference's own loop exactly — warm-started
+    search::search per window (orchestrate.cpp:116-123) on the GPU path."""
     tl = Timeline(windows=len(forecasts))
     current: Optional[core.Deployment] = None
     prev_lam: Optional[List[int]] = None
@@ -54,7 +58,11 @@ def build_adaptive_timeline(ctx: GpuContext, types: Sequence[core.WorkloadType],
         if tl.entries and lam == prev_lam:
             continue  # workload unchanged (orchestrate.cpp:113)
         ctx.set_workload(types, lam, span_seconds)
-        found = ctx.round(mode, list(sizes))
+        if strategy == "search":
+            found, _ = ctx.search(seed=seed, max_iters=search_max_iters, stale_limit=search_stale_limit,
+                                  warm_start=current)
+        else:
+            found = ctx.round(mode, list(sizes))
         tl.rounds += 1
         chosen, kept = found.deployment, False
         if current is not None:

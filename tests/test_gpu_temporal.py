@@ -65,3 +65,20 @@ def test_cpp_dropin(cuda):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "DROPIN OK" in out.stdout
+
+
+def test_cfg4_reference_adaptive_timeline(cuda):
+    """orch::build_adaptive_timeline (orchestrate.cpp:94-154) reproduced on the
+    GPU path: warm-started search per window, keep rule, assignment and switch
+    plan.  Expected values are the unmodified reference's
+    (tests/golden/timeline_cfg4.json)."""
+    import json
+    w = workloads.load("cfg4")
+    g = GpuContext(w.cluster, w.model, w.params)
+    tl = orchestrate.build_adaptive_timeline(g, w.types, w.raw["forecasts"], w.span_s, w.raw["min_gain"],
+                                             strategy="search", seed=0, search_max_iters=150)
+    exp = json.load(open(os.path.join(ROOT, "tests", "golden", "timeline_cfg4.json")))
+    got = [{"span_index": e.span_index, "deployment": [[r.device_ids, r.tp, r.pp] for r in e.deployment.replicas],
+            "x": e.assignment, "switch_seconds": e.switch_seconds,
+            "transfers": 0 if e.switch is None else len(e.switch.transfers)} for e in tl.entries]
+    assert got == exp
