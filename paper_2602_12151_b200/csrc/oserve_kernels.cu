@@ -450,10 +450,13 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
                 else if (lo > 0) m &= ~((1u << lo) - 1u);
                 if (m) run_end = __ffs(m) - 1 + G * kk;
             }
-            uint32_t cb = 0xffffffffu;
-            if (act && take > 0 && g.gl <= pb) cb = static_cast<uint32_t>(lamp - a) / static_cast<uint32_t>(take);
-            cb = __reduce_min_sync(g.mask, cb);
-            const int c = min(static_cast<int>(min(cb, 0x7fffffffu)), run_end - k);
+            int c = 0;
+            if (run_end > k) {  // same shape follows: how many can take the identical fill
+                uint32_t cb = 0xffffffffu;
+                if (act && take > 0 && g.gl <= pb) cb = static_cast<uint32_t>(lamp - a) / static_cast<uint32_t>(take);
+                cb = __reduce_min_sync(g.mask, cb);
+                c = min(static_cast<int>(min(cb, 0x7fffffffu)), run_end - k);
+            }
             if (act && take) {
                 for (int q = 0; q <= c; ++q) xs[j * RMAX + k + q] = take;
             }
@@ -668,6 +671,20 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
                 if (k == kf || k == k2) redo[kk] = true;
                 else if ((held[kk] & dirty) && eligible_held(kk) != E[kk]) redo[kk] = true;
                 else F[kk] &= lam_mask;
+            }
+            // many rows: every lane rebuilds its own rows (in parallel);
+            // few rows: class-parallel rebuild, one row at a time
+            int nredo = 0;
+#pragma unroll
+            for (int kk = 0; kk < KPL; ++kk) nredo += __popc(g.ballot(redo[kk]));
+            if (nredo > 4) {
+#pragma unroll
+                for (int kk = 0; kk < KPL; ++kk)
+                    if (redo[kk]) {
+                        E[kk] = eligible_held(kk);
+                        F[kk] = feasible_row(kk, E[kk]);
+                        redo[kk] = false;
+                    }
             }
 #pragma unroll
             for (int kk = 0; kk < KPL; ++kk) {
