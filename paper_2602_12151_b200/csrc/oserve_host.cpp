@@ -150,6 +150,16 @@ struct Space {
     SpaceTables view{};
     std::vector<uint8_t> exact;  // per partition, for the current workload
     bool any_exact = false;
+    // R-buckets: plans with R <= 32 run one replica per lane, the rest two or
+    // four (K1 instantiations); each bucket is a list of rank ranges.
+    struct Bucket {
+        int rmax = 0;
+        uint64_t total = 0;
+        std::vector<uint64_t> start, prefix;
+        DBuf d_start, d_prefix;
+    };
+    Bucket buckets[2];
+    bool use_buckets = false;
 };
 
 }  // namespace
@@ -467,6 +477,34 @@ void build_space(oserve_gpu_ctx &c, Space &sp, int mode, const std::vector<int> 
             cl_shape[l * kMaxCand + q] = static_cast<uint16_t>(sp.list_shapes[l][q]);
     }
     cudaStream_t s = c.stream;
+    // R-buckets
+    for (auto &b : sp.buckets) {
+        b.rmax = 0;
+        b.total = 0;
+        b.start.clear();
+        b.prefix.clear();
+    }
+    for (size_t i = 0; i < P; ++i) {
+        const auto &part = sp.parts[i];
+        if (part.count == 0) continue;
+        const int R = static_cast<int>(part.sizes.size());
+        auto &b = sp.buckets[R <= 32 ? 0 : 1];
+        b.rmax = std::max(b.rmax, R);
+        if (!b.start.empty() && b.start.back() + (b.total - b.prefix.back()) == sp.prefix[i]) {
+            // contiguous with the previous range of this bucket: extend it
+        } else {
+            b.start.push_back(sp.prefix[i]);
+            b.prefix.push_back(b.total);
+        }
+        b.total += part.count;
+    }
+    sp.use_buckets = sp.buckets[0].total > 0 && sp.buckets[1].total > 0;
+    if (sp.use_buckets) {
+        for (auto &b : sp.buckets) {
+            b.d_start.upload(b.start, s);
+            b.d_prefix.upload(b.prefix, s);
+        }
+    }
     SpaceTables v{};
     v.num_parts = static_cast<int64_t>(P);
     v.prefix = sp.d_prefix.upload(sp.prefix, s);
@@ -604,6 +642,34 @@ void decode_key(oserve_gpu_ctx &c, uint64_t key, oserve_round_result *out) {
     fill_plan(c, sp, p2, picks, &out->plan);
 }
 
+// The K1 launches covering this shard of the prepared space: one per R-bucket
+// (mode 3) when the space mixes R <= 32 and R > 32, else one (mode 0).
+template <class F>
+void for_each_k1_launch(oserve_gpu_ctx &c, Space &sp, F &&fn) {
+    if (sp.use_buckets) {
+        for (auto &b : sp.buckets) {
+            PlanSource src{};
+            src.mode = 3;
+            src.count = shard_count_of(b.total, c.chunk, static_cast<uint64_t>(c.rank), static_cast<uint64_t>(c.world));
+            src.rank = c.rank;
+            src.world = c.world;
+            src.chunk = c.chunk;
+            src.range_start = static_cast<const uint64_t *>(b.d_start.p);
+            src.range_prefix = static_cast<const uint64_t *>(b.d_prefix.p);
+            src.num_ranges = static_cast<int>(b.start.size());
+            fn(src, b.rmax);
+        }
+        return;
+    }
+    PlanSource src{};
+    src.mode = 0;
+    src.count = shard_count(c, sp.total);
+    src.rank = c.rank;
+    src.world = c.world;
+    src.chunk = c.chunk;
+    fn(src, sp.rmax);
+}
+
 // Launch K1 (+K4, + heuristic fallback for aborted B&B) over this shard of
 // the prepared space; best key -> d_key.
 void launch_round(oserve_gpu_ctx &c, uint64_t *d_key) {
@@ -623,9 +689,11 @@ void launch_round(oserve_gpu_ctx &c, uint64_t *d_key) {
     out.best_key = d_key;
     SolveParams prm = solve_params(c);
     count_h2d(sizeof(int64_t) * c.J);  // the demand vector travels as a kernel parameter
-    cuda_ok(launch_plan_eval(c.tables, sp.view, c.key, src, out, prm, sp.rmax, c.sm_count, sp.any_exact ? 1 : 0, s,
-                             &c.launches),
-            "plan kernel");
+    for_each_k1_launch(c, sp, [&](const PlanSource &ls, int rmax) {
+        cuda_ok(launch_plan_eval(c.tables, sp.view, c.key, ls, out, prm, rmax, c.sm_count, sp.any_exact ? 1 : 0, s,
+                                 &c.launches),
+                "plan kernel");
+    });
     if (sp.any_exact) {
         uint64_t *ab = static_cast<uint64_t *>(c.d_aborted.get(sizeof(uint64_t) * std::max<uint64_t>(src.count, 1)));
         unsigned *abn = static_cast<unsigned *>(c.d_aborted_n.get(sizeof(unsigned)));
@@ -890,8 +958,16 @@ void round_topk(oserve_gpu_ctx &c, int K, uint64_t *d_keys, uint64_t *d_best) {
     src.chunk = c.chunk;
     SolveParams prm = solve_params(c);
     count_h2d(sizeof(int64_t) * c.J);
-    const int groups = k1_groups(sp.rmax, c.J, c.sm_count, c.tables, src.count);
-    if (groups < 0) fail(OSERVE_ERR_CUDA, "K1 geometry");
+    std::vector<std::pair<PlanSource, int>> launches;
+    for_each_k1_launch(c, sp, [&](const PlanSource &ls, int rmax) { launches.emplace_back(ls, rmax); });
+    std::vector<int> lgroups;
+    int groups = 0;
+    for (auto &[ls, rmax] : launches) {
+        const int g = k1_groups(rmax, c.J, c.sm_count, c.tables, ls.count);
+        if (g < 0) fail(OSERVE_ERR_CUDA, "K1 geometry");
+        lgroups.push_back(g);
+        groups += g;
+    }
     const size_t nlist = static_cast<size_t>(std::max(groups, 1)) * kTopK;
     uint64_t *best = d_best ? d_best : static_cast<uint64_t *>(c.d_key.get(sizeof(uint64_t)));
     cuda_ok(cudaMemsetAsync(best, 0xff, sizeof(uint64_t), s), "memset");
@@ -901,8 +977,18 @@ void round_topk(oserve_gpu_ctx &c, int K, uint64_t *d_keys, uint64_t *d_best) {
     out.topk_meta = static_cast<uint64_t *>(c.d_topk_meta.get(sizeof(uint64_t) * std::max(groups, 1)));
     cuda_ok(cudaMemsetAsync(out.topk, 0xff, sizeof(uint64_t) * nlist, s), "memset");
     cuda_ok(cudaMemsetAsync(out.topk_meta, 0xff, sizeof(uint64_t) * std::max(groups, 1), s), "memset");
-    cuda_ok(launch_plan_eval(c.tables, sp.view, c.key, src, out, prm, sp.rmax, c.sm_count, 0, s, &c.launches),
-            "plan kernel (top-K)");
+    {
+        size_t goff = 0;
+        for (size_t q = 0; q < launches.size(); ++q) {
+            PlanOutputs lo = out;
+            lo.topk = out.topk + goff * kTopK;
+            lo.topk_meta = out.topk_meta + goff;
+            cuda_ok(launch_plan_eval(c.tables, sp.view, c.key, launches[q].first, lo, prm, launches[q].second,
+                                     c.sm_count, 0, s, &c.launches),
+                    "plan kernel (top-K)");
+            goff += static_cast<size_t>(lgroups[q]);
+        }
+    }
     uint64_t *sorted = static_cast<uint64_t *>(c.d_topk_tmp.get(sizeof(uint64_t) * nlist));
     cuda_ok(sort_keys(out.topk, sorted, static_cast<int>(nlist), &c.cub_temp, &c.cub_temp_bytes, s), "sort");
     ++c.launches;
@@ -931,8 +1017,9 @@ void round_topk(oserve_gpu_ctx &c, int K, uint64_t *d_keys, uint64_t *d_best) {
             co.collect_thr = thr;
             co.best_key = best;
             cuda_ok(cudaMemsetAsync(co.collect_n, 0, sizeof(unsigned), s), "memset");
-            cuda_ok(launch_plan_eval(c.tables, sp.view, c.key, src, co, prm, sp.rmax, c.sm_count, 0, s, &c.launches),
-                    "plan kernel (threshold collect)");
+            for (auto &[ls, rmax] : launches)
+                cuda_ok(launch_plan_eval(c.tables, sp.view, c.key, ls, co, prm, rmax, c.sm_count, 0, s, &c.launches),
+                        "plan kernel (threshold collect)");
             unsigned n = 0;
             cuda_ok(d2h(&n, co.collect_n, sizeof(unsigned), s), "D2H");
             cuda_ok(cudaStreamSynchronize(s), "sync");

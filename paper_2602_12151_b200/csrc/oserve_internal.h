@@ -88,6 +88,11 @@ struct PlanSource {
     const int32_t *list_off;
     const int32_t *list_shapes;
     const int64_t *list_lambda;  // optional per-plan lambda [count*J] (solve_batch)
+    // mode 3: bucket of rank ranges; bucket index b -> global rank
+    //   range r = last with range_prefix[r] <= b, rank = range_start[r] + (b - range_prefix[r])
+    const uint64_t *range_start;
+    const uint64_t *range_prefix;
+    int num_ranges;
 };
 
 // Optional per-plan outputs.

@@ -159,6 +159,20 @@ __device__ __forceinline__ uint64_t shard_rank(const PlanSource &src, uint64_t l
     return (c * static_cast<uint64_t>(src.world) + static_cast<uint64_t>(src.rank)) * src.chunk + (li - c * src.chunk);
 }
 
+// Global plan rank of launch-local index li (modes 0, 1, 3).
+__device__ __forceinline__ uint64_t source_rank(const PlanSource &src, uint64_t li) {
+    if (src.mode == 1) return src.ranks[li];
+    const uint64_t b = shard_rank(src, li);
+    if (src.mode == 0) return b;
+    int lo = 0, hi = src.num_ranges - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(src.range_prefix + mid) <= b) lo = mid;
+        else hi = mid - 1;
+    }
+    return __ldg(src.range_start + lo) + (b - __ldg(src.range_prefix + lo));
+}
+
 // Unrank a non-decreasing pick sequence of length len over [0, q) (lex order).
 __device__ __forceinline__ void unrank_run(uint64_t r, int len, int q, uint8_t *out) {
     int prev = 0;
@@ -345,7 +359,7 @@ __global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t
                 if (tot <= prm.exact_demand_limit && R * J <= prm.exact_cell_limit) continue;
             }
         } else {
-            const uint64_t gr = src.mode == 0 ? shard_rank(src, src.first + i) : src.ranks[src.first + i];
+            const uint64_t gr = source_rank(src, src.first + i);
             part = find_partition(sp, gr);
             if (skip_exact && sp.exact[part]) continue;
             local = gr - __ldg(sp.prefix + part);
