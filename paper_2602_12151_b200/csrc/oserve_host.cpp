@@ -950,12 +950,6 @@ void round_topk(oserve_gpu_ctx &c, int K, uint64_t *d_keys, uint64_t *d_best) {
     if (sp.any_exact) fail(OSERVE_ERR_UNSUPPORTED, "top-K round on exact-path (branch-and-bound) plans");
     make_key_layout(c, sp);
     cudaStream_t s = c.stream;
-    PlanSource src{};
-    src.mode = 0;
-    src.count = shard_count(c, sp.total);
-    src.rank = c.rank;
-    src.world = c.world;
-    src.chunk = c.chunk;
     SolveParams prm = solve_params(c);
     count_h2d(sizeof(int64_t) * c.J);
     std::vector<std::pair<PlanSource, int>> launches;
