@@ -670,6 +670,99 @@ void for_each_k1_launch(oserve_gpu_ctx &c, Space &sp, F &&fn) {
     fn(src, sp.rmax);
 }
 
+// Exact (B&B) path for the plans of `src` that take it: the split kernel
+// (kExactSlots threads per plan) + combine, then the sequential kernel for any
+// plan whose node count could not be certified.  Plans whose B&B blows the
+// budget are appended to eo.aborted (the caller reruns them through K1).
+constexpr uint64_t kSplitMaxPlans = 16384;
+
+void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key, const PlanSource &src0,
+               const PlanOutputs &eo, const SolveParams &prm, const Space *sp) {
+    cudaStream_t s = c.stream;
+    PlanSource src = src0;
+    DBuf d_exact_ranks;
+    if (sp && src.mode == 0) {
+        // restrict to this shard's exact-path plans
+        std::vector<uint64_t> ranks;
+        bool small = true;
+        for (size_t p = 0; p < sp->parts.size() && small; ++p) {
+            if (!sp->exact[p]) continue;
+            for (uint64_t g = sp->prefix[p]; g < sp->prefix[p] + sp->parts[p].count; ++g) {
+                if ((g / c.chunk) % static_cast<uint64_t>(c.world) != static_cast<uint64_t>(c.rank)) continue;
+                ranks.push_back(g);
+                if (ranks.size() > kSplitMaxPlans) {
+                    small = false;
+                    break;
+                }
+            }
+        }
+        if (!small) {  // too many exact plans for the split buffers: sequential kernel
+            cuda_ok(launch_plan_exact(c.tables, view, key, src, eo, prm, c.sm_count, s, &c.launches), "exact kernel");
+            return;
+        }
+        src.mode = 1;
+        src.first = 0;
+        src.count = ranks.size();
+        src.ranks = d_exact_ranks.upload(ranks, s);
+        if (ranks.empty()) return;
+    }
+    if (src.count > kSplitMaxPlans) {
+        cuda_ok(launch_plan_exact(c.tables, view, key, src, eo, prm, c.sm_count, s, &c.launches), "exact kernel");
+        return;
+    }
+    const uint64_t nt = src.count * kExactSlots;
+    DBuf b_state, b_best, b_bv, b_nodes, b_pre, b_x, b_redo, b_redo_n;
+    ExactSplit es{};
+    es.state = static_cast<uint8_t *>(b_state.get(nt));
+    es.best = static_cast<int64_t *>(b_best.get(sizeof(int64_t) * nt));
+    es.best_v = static_cast<int64_t *>(b_bv.get(sizeof(int64_t) * nt));
+    es.nodes = static_cast<uint64_t *>(b_nodes.get(sizeof(uint64_t) * nt));
+    es.prefix = static_cast<uint64_t *>(b_pre.get(sizeof(uint64_t) * nt));
+    es.x = static_cast<int32_t *>(b_x.get(sizeof(int32_t) * nt * kMaxExactCells));
+    es.redo = static_cast<uint64_t *>(b_redo.get(sizeof(uint64_t) * src.count));
+    es.redo_n = static_cast<unsigned *>(b_redo_n.get(sizeof(unsigned)));
+    cuda_ok(cudaMemsetAsync(es.redo_n, 0, sizeof(unsigned), s), "memset");
+    cuda_ok(launch_plan_exact(c.tables, view, key, src, eo, prm, c.sm_count, s, &c.launches, &es),
+            "exact kernel (split)");
+    unsigned nredo = 0;
+    cuda_ok(d2h(&nredo, es.redo_n, sizeof(unsigned), s), "D2H");
+    cuda_ok(cudaStreamSynchronize(s), "sync");
+    if (!nredo) return;
+    std::vector<uint64_t> redo;
+    download(redo, es.redo, nredo, s);
+    cuda_ok(cudaStreamSynchronize(s), "sync");
+    if (src.mode == 2 || (src.mode == 0 && (eo.objective || eo.x))) {
+        // per-plan outputs (lists, or an identity-mapped rank range)
+        for (uint64_t li : redo) {  // rare: one sequential launch per uncertified plan
+            PlanSource one = src;
+            one.first = li;
+            one.count = 1;
+            PlanOutputs o1 = eo;
+            if (eo.objective) o1.objective = eo.objective + (li - src.first);
+            if (eo.sum_pp) o1.sum_pp = eo.sum_pp + (li - src.first);
+            if (eo.x) {
+                o1.x = eo.x + (li - src.first) * eo.rmax * prm.J;
+                o1.used = eo.used + (li - src.first) * eo.rmax;
+            }
+            cuda_ok(launch_plan_exact(c.tables, view, key, one, o1, prm, c.sm_count, s, &c.launches),
+                    "exact kernel (sequential)");
+        }
+        cuda_ok(cudaStreamSynchronize(s), "sync");  // scratch buffers are freed on return
+    } else {
+        // space plans: outputs are keyed (argmin), no per-plan arrays
+        PlanSource rs{};
+        rs.mode = 1;
+        rs.count = nredo;
+        rs.ranks = es.redo;
+        PlanOutputs o1 = eo;
+        o1.objective = nullptr;
+        o1.sum_pp = nullptr;
+        cuda_ok(launch_plan_exact(c.tables, view, key, rs, o1, prm, c.sm_count, s, &c.launches),
+                "exact kernel (sequential)");
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+    }
+}
+
 // Launch K1 (+K4, + heuristic fallback for aborted B&B) over this shard of
 // the prepared space; best key -> d_key.
 void launch_round(oserve_gpu_ctx &c, uint64_t *d_key) {
@@ -701,7 +794,7 @@ void launch_round(oserve_gpu_ctx &c, uint64_t *d_key) {
         PlanOutputs eo = out;
         eo.aborted = ab;
         eo.aborted_n = abn;
-        cuda_ok(launch_plan_exact(c.tables, sp.view, c.key, src, eo, prm, c.sm_count, s, &c.launches), "exact kernel");
+        run_exact(c, sp.view, c.key, src, eo, prm, &sp);
         unsigned n_ab = 0;
         cuda_ok(d2h(&n_ab, abn, sizeof(unsigned), s), "D2H");
         cuda_ok(cudaStreamSynchronize(s), "sync");
@@ -812,7 +905,7 @@ void eval_lists(oserve_gpu_ctx &c, const std::vector<int32_t> &listR, const std:
         PlanOutputs eo = out;
         eo.aborted = ab;
         eo.aborted_n = abn;
-        cuda_ok(launch_plan_exact(c.tables, none, nk, src, eo, prm, c.sm_count, s, &c.launches), "exact kernel");
+        run_exact(c, none, nk, src, eo, prm, nullptr);
         unsigned n_ab = 0;
         cuda_ok(d2h(&n_ab, abn, sizeof(unsigned), s), "D2H");
         cuda_ok(cudaStreamSynchronize(s), "sync");
@@ -1594,8 +1687,7 @@ int oserve_gpu_evaluate_ranks(oserve_gpu_ctx *ctx, uint64_t first, uint64_t coun
             PlanOutputs eo = out;
             eo.aborted = ab;
             eo.aborted_n = abn;
-            cuda_ok(launch_plan_exact(ctx->tables, sp.view, nk, src, eo, prm, ctx->sm_count, s, &ctx->launches),
-                    "exact kernel");
+            run_exact(*ctx, sp.view, nk, src, eo, prm, nullptr);
             unsigned n_ab = 0;
             cuda_ok(d2h(&n_ab, abn, sizeof(unsigned), s), "D2H");
             cuda_ok(cudaStreamSynchronize(s), "sync");

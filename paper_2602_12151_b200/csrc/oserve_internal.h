@@ -116,6 +116,19 @@ struct PlanOutputs {
     uint64_t collect_thr;
 };
 
+// Split exact path: kExactSlots threads per plan (see k_plan_exact).
+constexpr int kExactSlots = 32;
+struct ExactSplit {
+    uint8_t *state;      // [plans*slots] 0 not exact, 1 done, 2 aborted
+    int64_t *best;       // [plans*slots]
+    int64_t *best_v;     // first-level branch of the slot's best
+    uint64_t *nodes;     // nodes below the first branching cell
+    uint64_t *prefix;    // nodes up to the first branching cell
+    int32_t *x;          // [plans*slots*kMaxExactCells]
+    uint64_t *redo;      // plans to rerun sequentially (rank or list index)
+    unsigned int *redo_n;
+};
+
 struct SolveParams {
     int J;
     int64_t lambda[kMaxJ];
@@ -136,7 +149,7 @@ int launch_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayou
 // Exact branch-and-bound path (thread per plan).
 int launch_plan_exact(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key, const PlanSource &src,
                       const PlanOutputs &out, const SolveParams &sp_params, int sm_count, void *stream,
-                      uint64_t *launches);
+                      uint64_t *launches, const ExactSplit *split = nullptr);
 
 // Switching cost (K2).
 struct SwitchDeps {

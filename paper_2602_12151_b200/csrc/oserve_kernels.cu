@@ -917,55 +917,109 @@ __device__ int64_t suffix_bound(const ShapeTables &t, const ExactState &st, int 
     return cnt;
 }
 
-__global__ void __launch_bounds__(128) k_plan_exact(ShapeTables t, SpaceTables sp, KeyLayout key, PlanSource src,
-                                                    PlanOutputs out, SolveParams prm) {
+// Resolve plan i of a source into an ExactState; false if it does not take
+// the exact path.
+__device__ __forceinline__ bool exact_setup(const ShapeTables &t, const SpaceTables &sp, const PlanSource &src,
+                                            const SolveParams &prm, uint64_t i, ExactState &st, int64_t &part,
+                                            uint64_t &local, uint64_t &gr, const int64_t *&lam_src) {
     const int J = prm.J;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < src.count;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        ExactState st;
-        st.J = J;
-        int64_t part = 0;
-        uint64_t local = 0, gr = 0;
-        const int64_t *lam_src = prm.lambda;
-        if (src.mode == 2) {
-            const uint64_t li = src.first + i;
-            st.R = src.list_R[li];
-            if (st.R * J > kMaxExactCells) continue;
-            const int32_t *ls = src.list_shapes + src.list_off[li];
-            for (int k = 0; k < st.R; ++k) st.shp[k] = ls[k];
-            if (src.list_lambda) lam_src = src.list_lambda + li * J;
-            int64_t tot = 0;
-            for (int j = 0; j < J; ++j) tot += lam_src[j];
-            if (!(tot <= prm.exact_demand_limit && st.R * J <= prm.exact_cell_limit)) continue;
-            gr = li;
-        } else {
-            gr = src.mode == 0 ? shard_rank(src, src.first + i) : src.ranks[src.first + i];
-            part = find_partition(sp, gr);
-            if (!sp.exact[part]) continue;
-            local = gr - sp.prefix[part];
-            st.R = sp.R[part];
-            const int ro = sp.rep_off[part], runo = sp.run_off[part], nr = sp.nruns[part];
-            uint8_t pick[kMaxExactCells];
-            for (int ri = 0; ri < nr; ++ri) {
-                const uint64_t w = sp.run_weight[runo + ri], c = sp.run_count[runo + ri];
-                const uint64_t rr = (local / w) % c;
-                unrank_run(rr, sp.run_len[runo + ri], sp.run_q[runo + ri], pick + sp.run_start[runo + ri]);
+    st.J = J;
+    part = 0;
+    local = 0;
+    lam_src = prm.lambda;
+    if (src.mode == 2) {
+        const uint64_t li = src.first + i;
+        st.R = src.list_R[li];
+        if (st.R * J > kMaxExactCells) return false;
+        const int32_t *ls = src.list_shapes + src.list_off[li];
+        for (int k = 0; k < st.R; ++k) st.shp[k] = ls[k];
+        if (src.list_lambda) lam_src = src.list_lambda + li * J;
+        int64_t tot = 0;
+        for (int j = 0; j < J; ++j) tot += lam_src[j];
+        if (!(tot <= prm.exact_demand_limit && st.R * J <= prm.exact_cell_limit)) return false;
+        gr = li;
+    } else {
+        gr = source_rank(src, src.first + i);
+        part = find_partition(sp, gr);
+        if (!sp.exact[part]) return false;
+        local = gr - sp.prefix[part];
+        st.R = sp.R[part];
+        const int ro = sp.rep_off[part], runo = sp.run_off[part], nr = sp.nruns[part];
+        uint8_t pick[kMaxExactCells];
+        for (int ri = 0; ri < nr; ++ri) {
+            const uint64_t w = sp.run_weight[runo + ri], c = sp.run_count[runo + ri];
+            const uint64_t rr = (local / w) % c;
+            unrank_run(rr, sp.run_len[runo + ri], sp.run_q[runo + ri], pick + sp.run_start[runo + ri]);
+        }
+        for (int k = 0; k < st.R; ++k) st.shp[k] = sp.cl_shape[sp.rep_list[ro + k] * kMaxCand + pick[k]];
+    }
+    for (int j = 0; j < J; ++j) st.lam[j] = lam_src[j];
+    for (int k = 0; k < st.R; ++k) st.mrem[k] = t.M[st.shp[k]];
+    for (int c = 0; c < st.R * J; ++c) {
+        st.x[c] = 0;
+        st.bx[c] = 0;
+    }
+    return true;
+}
+
+// Write the final outputs of an exact-path plan.
+__device__ __forceinline__ void exact_emit(const ShapeTables &t, const KeyLayout &key, const PlanOutputs &out,
+                                           uint64_t i, const ExactState &st, const int32_t *bx, int64_t bestc,
+                                           int64_t part, uint64_t local) {
+    const int R = st.R, J = st.J;
+    int spp = 0;
+    for (int kk = 0; kk < R; ++kk) spp += t.pp[st.shp[kk]];
+    if (out.objective) out.objective[i] = bestc;
+    if (out.sum_pp) out.sum_pp[i] = spp;
+    if (out.x) {
+        for (int kk = 0; kk < R; ++kk) {
+            int64_t used = 0;
+            for (int j = 0; j < J; ++j) {
+                out.x[(i * out.rmax + kk) * J + j] = bx[kk * J + j];
+                used += static_cast<int64_t>(bx[kk * J + j]) * t.unit[st.shp[kk] * J + j];
             }
-            for (int k = 0; k < st.R; ++k) st.shp[k] = sp.cl_shape[sp.rep_list[ro + k] * kMaxCand + pick[k]];
+            if (out.used) out.used[i * out.rmax + kk] = used;
+        }
+    }
+    if (out.best_key) {
+        const uint64_t kv = ((key.obj_max - static_cast<uint64_t>(bestc)) << key.sh_obj) |
+                            (static_cast<uint64_t>(part) << key.sh_part) |
+                            (static_cast<uint64_t>(spp) << key.sh_spp) | local;
+        atomicMin(reinterpret_cast<unsigned long long *>(out.best_key), kv);
+    }
+}
+
+// Exact branch-and-bound (flowassign.cpp:296-369).  SPLIT = false: thread per
+// plan, the reference's DFS verbatim.  SPLIT = true: kExactSlots threads per
+// plan; at the first branching cell slot q explores the branches v = hi-q,
+// hi-q-S, ... (descending) with its own running best.  Each slot's best is <=
+// the sequential best at the same point, so it prunes a subset and counts a
+// superset of the sequential nodes; k_exact_combine takes the max (first
+// branch in DFS order on ties) and certifies "no abort" when the summed node
+// counts stay within the budget — else the plan reruns sequentially.
+template <bool SPLIT>
+__global__ void __launch_bounds__(128) k_plan_exact(ShapeTables t, SpaceTables sp, KeyLayout key, PlanSource src,
+                                                    PlanOutputs out, SolveParams prm, ExactSplit es) {
+    const int J = prm.J;
+    const uint64_t ntask = SPLIT ? src.count * kExactSlots : src.count;
+    for (uint64_t tix = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; tix < ntask;
+         tix += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t i = SPLIT ? tix / kExactSlots : tix;
+        const int slot = SPLIT ? static_cast<int>(tix % kExactSlots) : 0;
+        ExactState st;
+        int64_t part;
+        uint64_t local, gr;
+        const int64_t *lam_src;
+        if (!exact_setup(t, sp, src, prm, i, st, part, local, gr, lam_src)) {
+            if (SPLIT) es.state[tix] = 0;  // not an exact-path plan
+            continue;
         }
         const int R = st.R;
-        for (int j = 0; j < J; ++j) st.lam[j] = lam_src[j];
-        for (int k = 0; k < R; ++k) st.mrem[k] = t.M[st.shp[k]];
-        for (int c = 0; c < R * J; ++c) {
-            st.x[c] = 0;
-            st.bx[c] = 0;
-        }
-        // explicit DFS stack: one frame per (k, pos) being iterated over v
         int fk[kMaxExactCells + 1], fpos[kMaxExactCells + 1], fj[kMaxExactCells + 1];
         int64_t fv[kMaxExactCells + 1];
         int depth = 0;
-        int64_t count = 0, bestc = -1, nodes = 0;
-        bool aborted = false;
+        int64_t count = 0, bestc = -1, nodes = 0, prefix_nodes = 0, best_v = -1;
+        bool aborted = false, branched = false;
         int k = 0, pos = 0;
         bool calling = true;  // true: enter visit(k, pos); false: return to frame on top
         while (true) {
@@ -977,6 +1031,7 @@ __global__ void __launch_bounds__(128) k_plan_exact(ShapeTables t, SpaceTables s
                 if (k == R) {
                     if (count > bestc) {
                         bestc = count;
+                        best_v = depth > 0 ? fv[0] : 0;
                         for (int c = 0; c < R * J; ++c) st.bx[c] = st.x[c];
                     }
                     calling = false;
@@ -1001,6 +1056,12 @@ __global__ void __launch_bounds__(128) k_plan_exact(ShapeTables t, SpaceTables s
                 int64_t hi = t.cap[s * J + j];
                 if (st.lam[j] < hi) hi = st.lam[j];
                 if (hi * u > st.mrem[k]) hi = quot_small(st.mrem[k], u, t.inv_unit[s * J + j]);
+                if (SPLIT && depth == 0) {  // first branching cell: this slot's branches
+                    branched = true;
+                    prefix_nodes = nodes;
+                    hi -= slot;
+                    if (hi < 0) break;  // no branch for this slot
+                }
                 fk[depth] = k;
                 fpos[depth] = pos;
                 fj[depth] = j;
@@ -1023,11 +1084,12 @@ __global__ void __launch_bounds__(128) k_plan_exact(ShapeTables t, SpaceTables s
             st.mrem[kk] += v * u;
             st.lam[j] += v;
             st.x[kk * J + j] = 0;
-            if (v == 0) {
+            const int64_t step = (SPLIT && d == 0) ? kExactSlots : 1;
+            if (v - step < 0) {
                 --depth;  // loop exhausted: return from this visit
                 continue;
             }
-            --v;
+            v -= step;
             fv[d] = v;
             st.x[kk * J + j] = static_cast<int32_t>(v);
             st.lam[j] -= v;
@@ -1037,33 +1099,64 @@ __global__ void __launch_bounds__(128) k_plan_exact(ShapeTables t, SpaceTables s
             pos = fpos[d] + 1;
             calling = true;
         }
+        if (SPLIT) {
+            // per-slot result for k_exact_combine
+            es.state[tix] = aborted ? 2 : 1;
+            es.best[tix] = bestc;
+            es.best_v[tix] = best_v;
+            es.nodes[tix] = branched ? static_cast<uint64_t>(nodes - prefix_nodes) : static_cast<uint64_t>(nodes);
+            es.prefix[tix] = branched ? static_cast<uint64_t>(prefix_nodes) : 0;
+            for (int c = 0; c < R * J; ++c) es.x[tix * kMaxExactCells + c] = st.bx[c];
+            continue;
+        }
         if (aborted) {
             if (out.aborted) {
-                const unsigned slot = atomicAdd(out.aborted_n, 1u);
-                out.aborted[slot] = gr;
+                const unsigned slot2 = atomicAdd(out.aborted_n, 1u);
+                out.aborted[slot2] = gr;
             }
             continue;
         }
-        int spp = 0;
-        for (int kk = 0; kk < R; ++kk) spp += t.pp[st.shp[kk]];
-        if (out.objective) out.objective[i] = bestc;
-        if (out.sum_pp) out.sum_pp[i] = spp;
-        if (out.x) {
-            for (int kk = 0; kk < R; ++kk) {
-                int64_t used = 0;
-                for (int j = 0; j < J; ++j) {
-                    out.x[(i * out.rmax + kk) * J + j] = st.bx[kk * J + j];
-                    used += static_cast<int64_t>(st.bx[kk * J + j]) * t.unit[st.shp[kk] * J + j];
-                }
-                if (out.used) out.used[i * out.rmax + kk] = used;
+        exact_emit(t, key, out, i, st, st.bx, bestc, part, local);
+    }
+}
+
+// Combine the kExactSlots slot results of each split plan (see k_plan_exact).
+__global__ void k_exact_combine(ShapeTables t, SpaceTables sp, KeyLayout key, PlanSource src, PlanOutputs out,
+                                SolveParams prm, ExactSplit es) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < src.count;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t t0 = i * kExactSlots;
+        if (es.state[t0] == 0) continue;  // not an exact-path plan
+        uint64_t total = 0;
+        bool any_abort = false;
+        int64_t best = -1, bv = -1;
+        int bslot = -1;
+        for (int q = 0; q < kExactSlots; ++q) {
+            const uint64_t tq = t0 + q;
+            if (es.state[tq] == 2) any_abort = true;
+            total += es.nodes[tq];
+            const int64_t b = es.best[tq], v = es.best_v[tq];
+            if (b > best || (b == best && b >= 0 && v > bv)) {
+                best = b;
+                bv = v;
+                bslot = q;
             }
         }
-        if (out.best_key) {
-            const uint64_t kv = ((key.obj_max - static_cast<uint64_t>(bestc)) << key.sh_obj) |
-                                (static_cast<uint64_t>(part) << key.sh_part) |
-                                (static_cast<uint64_t>(spp) << key.sh_spp) | local;
-            atomicMin(reinterpret_cast<unsigned long long *>(out.best_key), kv);
+        uint64_t pre = 0;
+        for (int q = 0; q < kExactSlots; ++q) pre = es.prefix[t0 + q] > pre ? es.prefix[t0 + q] : pre;
+        total += pre;
+        ExactState st;
+        int64_t part;
+        uint64_t local, gr;
+        const int64_t *lam_src;
+        exact_setup(t, sp, src, prm, i, st, part, local, gr, lam_src);
+        if (any_abort || total > static_cast<uint64_t>(prm.node_budget) || bslot < 0) {
+            // could not certify the sequential node count: rerun sequentially
+            const unsigned slot2 = atomicAdd(es.redo_n, 1u);
+            es.redo[slot2] = src.mode == 2 ? src.first + i : gr;
+            continue;
         }
+        exact_emit(t, key, out, i, st, es.x + (t0 + bslot) * kMaxExactCells, best, part, local);
     }
 }
 
@@ -1434,16 +1527,26 @@ int launch_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayou
 
 int launch_plan_exact(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key, const PlanSource &src,
                       const PlanOutputs &out, const SolveParams &prm, int sm_count, void *stream,
-                      uint64_t *launches) {
+                      uint64_t *launches, const ExactSplit *split) {
     cudaGetLastError();
     if (int e = ensure_binom()) return e;
     if (src.count == 0) return 0;
     const int block = 128;
-    uint64_t grid = (src.count + block - 1) / block;
     const uint64_t cap = static_cast<uint64_t>(sm_count) * 16;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (split) {
+        uint64_t grid = (src.count * kExactSlots + block - 1) / block;
+        if (grid > cap) grid = cap;
+        k_plan_exact<true><<<static_cast<unsigned>(grid), block, 0, s>>>(t, sp, key, src, out, prm, *split);
+        uint64_t g2 = (src.count + block - 1) / block;
+        if (g2 > cap) g2 = cap;
+        k_exact_combine<<<static_cast<unsigned>(g2), block, 0, s>>>(t, sp, key, src, out, prm, *split);
+        if (launches) *launches += 2;
+        return check(cudaGetLastError());
+    }
+    uint64_t grid = (src.count + block - 1) / block;
     if (grid > cap) grid = cap;
-    k_plan_exact<<<static_cast<unsigned>(grid), block, 0, static_cast<cudaStream_t>(stream)>>>(t, sp, key, src, out,
-                                                                                               prm);
+    k_plan_exact<false><<<static_cast<unsigned>(grid), block, 0, s>>>(t, sp, key, src, out, prm, ExactSplit{});
     if (launches) ++*launches;
     return check(cudaGetLastError());
 }
