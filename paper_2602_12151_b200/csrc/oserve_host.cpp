@@ -711,8 +711,12 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
         return;
     }
     const uint64_t nt = src.count * kExactSlots;
-    DBuf b_state, b_best, b_bv, b_nodes, b_pre, b_x, b_redo, b_redo_n;
+    DBuf b_state, b_best, b_bv, b_nodes, b_pre, b_x, b_redo, b_redo_n, b_p1s, b_p1b, b_p1n, b_p1x;
     ExactSplit es{};
+    es.p1_state = static_cast<uint8_t *>(b_p1s.get(src.count));
+    es.p1_best = static_cast<int64_t *>(b_p1b.get(sizeof(int64_t) * src.count));
+    es.p1_nodes = static_cast<uint64_t *>(b_p1n.get(sizeof(uint64_t) * src.count));
+    es.p1_x = static_cast<int32_t *>(b_p1x.get(sizeof(int32_t) * src.count * kMaxExactCells));
     es.state = static_cast<uint8_t *>(b_state.get(nt));
     es.best = static_cast<int64_t *>(b_best.get(sizeof(int64_t) * nt));
     es.best_v = static_cast<int64_t *>(b_bv.get(sizeof(int64_t) * nt));

@@ -119,11 +119,18 @@ struct PlanOutputs {
 // Split exact path: kExactSlots threads per plan (see k_plan_exact).
 constexpr int kExactSlots = 32;
 struct ExactSplit {
-    uint8_t *state;      // [plans*slots] 0 not exact, 1 done, 2 aborted
-    int64_t *best;       // [plans*slots]
+    int phase;           // 1: first branch only; 2: remaining branches over slots
+    // phase 1, per plan: 0 not exact, 1 branched, 2 aborted, 3 no branching cell
+    uint8_t *p1_state;
+    int64_t *p1_best;
+    uint64_t *p1_nodes;  // prefix + first-branch nodes
+    int32_t *p1_x;       // [plans*kMaxExactCells]
+    // phase 2, per (plan, slot)
+    uint8_t *state;      // 0 idle, 1 done, 2 aborted
+    int64_t *best;
     int64_t *best_v;     // first-level branch of the slot's best
     uint64_t *nodes;     // nodes below the first branching cell
-    uint64_t *prefix;    // nodes up to the first branching cell
+    uint64_t *prefix;    // unused (kept for layout stability)
     int32_t *x;          // [plans*slots*kMaxExactCells]
     uint64_t *redo;      // plans to rerun sequentially (rank or list index)
     unsigned int *redo_n;

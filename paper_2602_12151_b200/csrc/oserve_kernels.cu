@@ -1001,24 +1001,31 @@ template <bool SPLIT>
 __global__ void __launch_bounds__(128) k_plan_exact(ShapeTables t, SpaceTables sp, KeyLayout key, PlanSource src,
                                                     PlanOutputs out, SolveParams prm, ExactSplit es) {
     const int J = prm.J;
-    const uint64_t ntask = SPLIT ? src.count * kExactSlots : src.count;
+    const int phase = SPLIT ? es.phase : 0;
+    const uint64_t ntask = phase == 2 ? src.count * kExactSlots : src.count;
     for (uint64_t tix = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; tix < ntask;
          tix += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint64_t i = SPLIT ? tix / kExactSlots : tix;
-        const int slot = SPLIT ? static_cast<int>(tix % kExactSlots) : 0;
+        const uint64_t i = phase == 2 ? tix / kExactSlots : tix;
+        const int slot = phase == 2 ? static_cast<int>(tix % kExactSlots) : 0;
+        if (phase == 2 && es.p1_state[i] != 1) {  // not exact, or phase 1 already decided it
+            es.state[tix] = 0;
+            continue;
+        }
         ExactState st;
         int64_t part;
         uint64_t local, gr;
         const int64_t *lam_src;
         if (!exact_setup(t, sp, src, prm, i, st, part, local, gr, lam_src)) {
-            if (SPLIT) es.state[tix] = 0;  // not an exact-path plan
+            if (phase == 1) es.p1_state[i] = 0;  // not an exact-path plan
             continue;
         }
         const int R = st.R;
         int fk[kMaxExactCells + 1], fpos[kMaxExactCells + 1], fj[kMaxExactCells + 1];
         int64_t fv[kMaxExactCells + 1];
         int depth = 0;
-        int64_t count = 0, bestc = -1, nodes = 0, prefix_nodes = 0, best_v = -1;
+        // phase 2 slots start from the first branch's best: a lower bound of the
+        // sequential best for every later branch
+        int64_t count = 0, bestc = phase == 2 ? es.p1_best[i] : -1, nodes = 0, prefix_nodes = 0, best_v = -1;
         bool aborted = false, branched = false;
         int k = 0, pos = 0;
         bool calling = true;  // true: enter visit(k, pos); false: return to frame on top
@@ -1056,11 +1063,13 @@ __global__ void __launch_bounds__(128) k_plan_exact(ShapeTables t, SpaceTables s
                 int64_t hi = t.cap[s * J + j];
                 if (st.lam[j] < hi) hi = st.lam[j];
                 if (hi * u > st.mrem[k]) hi = quot_small(st.mrem[k], u, t.inv_unit[s * J + j]);
-                if (SPLIT && depth == 0) {  // first branching cell: this slot's branches
+                if (SPLIT && depth == 0) {  // first branching cell
                     branched = true;
                     prefix_nodes = nodes;
-                    hi -= slot;
-                    if (hi < 0) break;  // no branch for this slot
+                    if (phase == 2) {  // this slot's branches: hi-1-slot, hi-1-slot-S, ...
+                        hi -= 1 + slot;
+                        if (hi < 0) break;
+                    }
                 }
                 fk[depth] = k;
                 fpos[depth] = pos;
@@ -1084,7 +1093,7 @@ __global__ void __launch_bounds__(128) k_plan_exact(ShapeTables t, SpaceTables s
             st.mrem[kk] += v * u;
             st.lam[j] += v;
             st.x[kk * J + j] = 0;
-            const int64_t step = (SPLIT && d == 0) ? kExactSlots : 1;
+            const int64_t step = (SPLIT && d == 0) ? (phase == 1 ? (int64_t{1} << 62) : kExactSlots) : 1;
             if (v - step < 0) {
                 --depth;  // loop exhausted: return from this visit
                 continue;
@@ -1099,13 +1108,21 @@ __global__ void __launch_bounds__(128) k_plan_exact(ShapeTables t, SpaceTables s
             pos = fpos[d] + 1;
             calling = true;
         }
+        if (SPLIT && phase == 1) {
+            // first branch only: identical to the sequential DFS up to there, so
+            // an abort here is the reference's abort; no branching => done
+            es.p1_state[i] = aborted ? 2 : (branched ? 1 : 3);
+            es.p1_best[i] = bestc;
+            es.p1_nodes[i] = static_cast<uint64_t>(nodes);
+            for (int c = 0; c < R * J; ++c) es.p1_x[i * kMaxExactCells + c] = st.bx[c];
+            continue;
+        }
         if (SPLIT) {
-            // per-slot result for k_exact_combine
+            // per-slot result for k_exact_combine (nodes below the first cell)
             es.state[tix] = aborted ? 2 : 1;
             es.best[tix] = bestc;
             es.best_v[tix] = best_v;
-            es.nodes[tix] = branched ? static_cast<uint64_t>(nodes - prefix_nodes) : static_cast<uint64_t>(nodes);
-            es.prefix[tix] = branched ? static_cast<uint64_t>(prefix_nodes) : 0;
+            es.nodes[tix] = static_cast<uint64_t>(nodes - prefix_nodes);
             for (int c = 0; c < R * J; ++c) es.x[tix * kMaxExactCells + c] = st.bx[c];
             continue;
         }
@@ -1120,43 +1137,55 @@ __global__ void __launch_bounds__(128) k_plan_exact(ShapeTables t, SpaceTables s
     }
 }
 
-// Combine the kExactSlots slot results of each split plan (see k_plan_exact).
+// Combine phase 1 (first branch) and the kExactSlots phase-2 slots of each
+// split plan (see k_plan_exact).
 __global__ void k_exact_combine(ShapeTables t, SpaceTables sp, KeyLayout key, PlanSource src, PlanOutputs out,
                                 SolveParams prm, ExactSplit es) {
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < src.count;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint64_t t0 = i * kExactSlots;
-        if (es.state[t0] == 0) continue;  // not an exact-path plan
-        uint64_t total = 0;
-        bool any_abort = false;
-        int64_t best = -1, bv = -1;
-        int bslot = -1;
-        for (int q = 0; q < kExactSlots; ++q) {
-            const uint64_t tq = t0 + q;
-            if (es.state[tq] == 2) any_abort = true;
-            total += es.nodes[tq];
-            const int64_t b = es.best[tq], v = es.best_v[tq];
-            if (b > best || (b == best && b >= 0 && v > bv)) {
-                best = b;
-                bv = v;
-                bslot = q;
-            }
-        }
-        uint64_t pre = 0;
-        for (int q = 0; q < kExactSlots; ++q) pre = es.prefix[t0 + q] > pre ? es.prefix[t0 + q] : pre;
-        total += pre;
+        const uint8_t p1 = es.p1_state[i];
+        if (p1 == 0) continue;  // not an exact-path plan
         ExactState st;
         int64_t part;
         uint64_t local, gr;
         const int64_t *lam_src;
         exact_setup(t, sp, src, prm, i, st, part, local, gr, lam_src);
-        if (any_abort || total > static_cast<uint64_t>(prm.node_budget) || bslot < 0) {
+        if (p1 == 2) {  // the reference aborts too (same nodes up to here)
+            if (out.aborted) {
+                const unsigned slot2 = atomicAdd(out.aborted_n, 1u);
+                out.aborted[slot2] = gr;
+            }
+            continue;
+        }
+        if (p1 == 3) {  // no branching cell: the first-branch DFS was the whole DFS
+            exact_emit(t, key, out, i, st, es.p1_x + i * kMaxExactCells, es.p1_best[i], part, local);
+            continue;
+        }
+        uint64_t total = es.p1_nodes[i];
+        bool any_abort = false;
+        int64_t best = es.p1_best[i], bv = 1ll << 62;  // phase 1 wins ties (earliest branch)
+        int bslot = -1;
+        const uint64_t t0 = i * kExactSlots;
+        for (int q = 0; q < kExactSlots; ++q) {
+            const uint64_t tq = t0 + q;
+            if (es.state[tq] == 0) continue;
+            if (es.state[tq] == 2) any_abort = true;
+            total += es.nodes[tq];
+            const int64_t b = es.best[tq], v = es.best_v[tq];
+            if (b > best || (b == best && bslot >= 0 && v > bv)) {
+                best = b;
+                bv = v;
+                bslot = q;
+            }
+        }
+        if (any_abort || total > static_cast<uint64_t>(prm.node_budget)) {
             // could not certify the sequential node count: rerun sequentially
             const unsigned slot2 = atomicAdd(es.redo_n, 1u);
             es.redo[slot2] = src.mode == 2 ? src.first + i : gr;
             continue;
         }
-        exact_emit(t, key, out, i, st, es.x + (t0 + bslot) * kMaxExactCells, best, part, local);
+        const int32_t *bx = bslot < 0 ? es.p1_x + i * kMaxExactCells : es.x + (t0 + bslot) * kMaxExactCells;
+        exact_emit(t, key, out, i, st, bx, best, part, local);
     }
 }
 
@@ -1535,9 +1564,17 @@ int launch_plan_exact(const ShapeTables &t, const SpaceTables &sp, const KeyLayo
     const uint64_t cap = static_cast<uint64_t>(sm_count) * 16;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (split) {
+        ExactSplit e1 = *split;
+        e1.phase = 1;
+        uint64_t g1 = (src.count + block - 1) / block;
+        if (g1 > cap) g1 = cap;
+        k_plan_exact<true><<<static_cast<unsigned>(g1), block, 0, s>>>(t, sp, key, src, out, prm, e1);
+        ExactSplit e2 = *split;
+        e2.phase = 2;
         uint64_t grid = (src.count * kExactSlots + block - 1) / block;
         if (grid > cap) grid = cap;
-        k_plan_exact<true><<<static_cast<unsigned>(grid), block, 0, s>>>(t, sp, key, src, out, prm, *split);
+        k_plan_exact<true><<<static_cast<unsigned>(grid), block, 0, s>>>(t, sp, key, src, out, prm, e2);
+        if (launches) ++*launches;
         uint64_t g2 = (src.count + block - 1) / block;
         if (g2 > cap) g2 = cap;
         k_exact_combine<<<static_cast<unsigned>(g2), block, 0, s>>>(t, sp, key, src, out, prm, *split);
