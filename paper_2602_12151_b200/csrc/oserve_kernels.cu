@@ -893,11 +893,11 @@ struct ExactState {
     int64_t mrem[kMaxExactCells];
 };
 
-__device__ int64_t suffix_bound(const ShapeTables &t, const ExactState &st, int k, int pos, const int64_t *lam_in,
+__device__ int64_t suffix_bound(const ShapeTables &t, const ExactState &st, int k, int pos, const int64_t *lam,
                                 int64_t mr) {
-    // greedy_suffix (flowassign.cpp:298-311) on a private copy of lam
-    int64_t lam[kMaxJ];
-    for (int j = 0; j < st.J; ++j) lam[j] = lam_in[j];
+    // greedy_suffix (flowassign.cpp:298-311).  The reference takes lam by
+    // value; each class occurs once in a replica's order, so reading it in
+    // place gives the same takes without the copy.
     const int s = st.shp[k];
     const int ol = t.olen[s];
     int64_t cnt = 0;
@@ -906,11 +906,9 @@ __device__ int64_t suffix_bound(const ShapeTables &t, const ExactState &st, int 
         const int64_t u = t.unit[s * st.J + j];
         int64_t tk = t.cap[s * st.J + j];
         if (lam[j] < tk) tk = lam[j];
-        // min(tk, mr / u) without a 64-bit division (tk < 2^31)
         if (tk * u > mr) tk = quot_small(mr, u, t.inv_unit[s * st.J + j]);
         if (tk > 0) {
             cnt += tk;
-            lam[j] -= tk;
             mr -= tk * u;
         }
     }
@@ -1558,6 +1556,11 @@ int launch_plan_exact(const ShapeTables &t, const SpaceTables &sp, const KeyLayo
                       const PlanOutputs &out, const SolveParams &prm, int sm_count, void *stream,
                       uint64_t *launches, const ExactSplit *split) {
     cudaGetLastError();
+    static const bool no_split = [] {
+        const char *e = getenv("OSERVE_K4_SPLIT");
+        return e && atoi(e) == 0;
+    }();
+    if (no_split) split = nullptr;
     if (int e = ensure_binom()) return e;
     if (src.count == 0) return 0;
     const int block = 128;
