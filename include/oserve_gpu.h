@@ -308,6 +308,43 @@ int oserve_key_layout(int64_t total_demand, int64_t partitions, int devices, uin
 /* Default interleave chunk of oserve_gpu_set_shard. */
 #define OSERVE_SHARD_CHUNK 4096
 
+/* ---- KV-cache migration plan (switchplan.cpp:142-207) ------------------ */
+
+/* switchplan::InflightRequest (switchplan.hpp:63-68). */
+typedef struct {
+    int64_t request_id;
+    int64_t generated_tokens;
+    uint64_t kv_bytes;
+    int source_replica;
+} oserve_inflight;
+
+/* switchplan::KvTransfer (switchplan.hpp:70-77). */
+typedef struct {
+    int64_t request_id;
+    uint64_t kv_bytes;
+    int src;
+    int dst;
+} oserve_kv_transfer;
+
+/* Drop-in for switchplan::kv_plan: short requests (generated <= threshold)
+ * drain on the source; the rest migrate round-robin over the destination
+ * replicas to the least inbound-loaded device, from the (intra-first,
+ * least-loaded, lowest-id) source device; link loads start from `carry`
+ * (the parameter switch plan's transfers; may be NULL).  Runs as one warp on
+ * the device (requests in order, lane-parallel selections).  Outputs are
+ * host arrays sized n_inflight. */
+int oserve_gpu_kv_plan(oserve_gpu_ctx *ctx, int n_inflight, const oserve_inflight *inflight,
+                       int64_t threshold_tokens, const oserve_deployment *src, const oserve_deployment *dst,
+                       double headroom, int n_carry, const oserve_transfer *carry, int64_t *drained,
+                       int *n_drained, oserve_kv_transfer *migrated, int *n_migrated, uint64_t *buffer_bytes);
+
+/* orch::forecast_series (orchestrate.cpp:75-92) with HoltForecaster
+ * (workload.cpp:204-222): counts [T][J] of actual arrivals -> per-span
+ * demand [T][J]; span 0 uses its own counts, later spans the Holt forecast
+ * over the trailing `window` spans, llround, clamped at 0.  Host-side. */
+int oserve_forecast_series(int J, int T, const int64_t *counts, int window, double alpha, double beta,
+                           int64_t *lambda_out);
+
 /* Kernel launches issued by this context since creation (evidence counter). */
 uint64_t oserve_gpu_launch_count(const oserve_gpu_ctx *ctx);
 /* Host->device / device->host bytes copied by this context since creation

@@ -265,6 +265,37 @@ inline oserve::switchplan::SwitchPlan greedy_plan(const oserve::Deployment &from
     return plan;
 }
 
+// kv_plan (switchplan.cpp:142-207) on the device; `carry` may be null.
+inline oserve::switchplan::KvPlan kv_plan(const std::vector<oserve::switchplan::InflightRequest> &inflight,
+                                          std::int64_t threshold_tokens, const oserve::Deployment &src,
+                                          const oserve::Deployment &dst, const oserve::ClusterSpec &cluster,
+                                          double headroom, const oserve::switchplan::SwitchPlan *carry = nullptr) {
+    oserve::ModelSpec model;
+    model.param_bytes = 1;  // the migration plan does not depend on the model
+    model.num_layers = 1;
+    model.min_mem_bytes = 1;
+    Context c(cluster, model, oserve::cost::ProfileParams{});
+    DeploymentBuf a(src), b(dst);
+    std::vector<oserve_inflight> req;
+    for (const auto &r : inflight) req.push_back({r.request_id, r.generated_tokens, r.kv_bytes, r.source_replica});
+    std::vector<oserve_transfer> tr;
+    if (carry != nullptr)
+        for (const auto &t : carry->transfers) tr.push_back({t.range.begin, t.range.end, t.src, t.dst});
+    std::vector<int64_t> drained(inflight.size() + 1);
+    std::vector<oserve_kv_transfer> mig(inflight.size() + 1);
+    int nd = 0, nm = 0;
+    uint64_t buf = 0;
+    check(oserve_gpu_kv_plan(c.get(), static_cast<int>(req.size()), req.data(), threshold_tokens, &a.desc, &b.desc,
+                             headroom, static_cast<int>(tr.size()), tr.data(), drained.data(), &nd, mig.data(), &nm,
+                             &buf),
+          c.get());
+    oserve::switchplan::KvPlan out;
+    out.drained.assign(drained.begin(), drained.begin() + nd);
+    for (int i = 0; i < nm; ++i) out.migrated.push_back({mig[i].request_id, mig[i].kv_bytes, mig[i].src, mig[i].dst});
+    out.buffer_bytes = buf;
+    return out;
+}
+
 }  // namespace switchplan
 
 }  // namespace oserve_gpu

@@ -114,6 +114,15 @@ int main() {
             auto p2 = oserve_gpu::switchplan::greedy_plan(a, b, m, c24);
             EXPECT(p1.transfers == p2.transfers && p1.link_load == p2.link_load && p1.est_seconds == p2.est_seconds,
                    "switchplan::greedy_plan");
+            // kv_plan with the parameter plan as carry (switchplan.cpp:142-207)
+            std::vector<switchplan::InflightRequest> inflight;
+            for (int q = 0; q < 200; ++q)
+                inflight.push_back({q, (q * 37) % 101, static_cast<std::uint64_t>(((q * 7919) % 97 + 1) << 20),
+                                    q % a.replica_count()});
+            auto k1 = switchplan::kv_plan(inflight, 30, a, b, c24, 0.1, &p1);
+            auto k2 = oserve_gpu::switchplan::kv_plan(inflight, 30, a, b, c24, 0.1, &p1);
+            EXPECT(k1.drained == k2.drained && k1.migrated == k2.migrated && k1.buffer_bytes == k2.buffer_bytes,
+                   "switchplan::kv_plan");
         }
     std::printf(failures ? "DROPIN FAILED (%d)\n" : "DROPIN OK\n", failures);
     return failures ? 1 : 0;

@@ -11,6 +11,10 @@ the GPU path on machines without the reference:
   plans_<cfg>.json per-plan objectives: every plan of cfg1 / cfg1_bnb, a
                    seeded sample elsewhere, plus an all-plan checksum for cfg2
   switch.json      greedy_plan/estimate_time on seeded deployment pairs
+  kv_plan.json     switchplan::kv_plan on seeded in-flight sets (with and
+                   without the parameter plan's link loads as carry)
+  timeline_cfg4_ref.json  io::save_timeline of orch::build_adaptive_timeline
+                   on config 4, the reference's own file
 """
 import hashlib
 import json
@@ -184,8 +188,52 @@ def main():
                        "max_link_bytes": mx, "transfers": [[t.range.begin, t.range.end, t.src, t.dst]
                                                            for t in plan.transfers]})
     json.dump(sw, open(os.path.join(OUT, "switch.json"), "w"))
+    gen_f3(ref)
     print("golden fixtures written to", OUT)
 
 
+def kv_cases(ref, seed=4242):
+    """Seeded kv_plan cases on the switch.json deployment pairs."""
+    rng = np.random.default_rng(seed)
+    sw = json.load(open(os.path.join(OUT, "switch.json")))
+    cases = []
+    for k, pair in enumerate(sw):
+        w = workloads.load(pair["config"])
+        src = core.Deployment([core.ReplicaConfig(ids, tp, pp) for ids, tp, pp in pair["src"]])
+        dst = core.Deployment([core.ReplicaConfig(ids, tp, pp) for ids, tp, pp in pair["dst"]])
+        for variant in range(3):
+            n = int(rng.integers(0, 400)) if variant else int(rng.integers(1, 12))
+            thr = int(rng.integers(0, 2000))
+            reqs = [core.InflightRequest(int(1000 * k + q), int(rng.integers(0, 4000)),
+                                         int(rng.integers(1, 1 << 33)), int(rng.integers(0, src.replica_count())))
+                    for q in range(n)]
+            if variant == 2 and n:  # equal kv sizes stress the lowest-id tie-breaks
+                for r in reqs:
+                    r.kv_bytes = 1 << 20
+            headroom = float(rng.choice([0.0, 0.1, 0.25, 0.5, float(rng.random() * 0.5)]))
+            carry = None
+            if variant != 1:
+                carry = core.SwitchPlan([core.Transfer(core.ByteRange(b, e), s_, d_)
+                                         for b, e, s_, d_ in pair["transfers"]])
+            kv = ref.kv_plan(w.cluster, reqs, thr, src, dst, headroom, carry)
+            cases.append({"config": pair["config"], "src": pair["src"], "dst": pair["dst"], "threshold": thr,
+                          "headroom": headroom, "carry": variant != 1,
+                          "inflight": [[r.request_id, r.generated_tokens, r.kv_bytes, r.source_replica]
+                                       for r in reqs],
+                          "drained": kv.drained, "buffer_bytes": kv.buffer_bytes,
+                          "migrated": [[m.request_id, m.kv_bytes, m.src, m.dst] for m in kv.migrated]})
+    return cases
+
+
+def gen_f3(ref):
+    json.dump(kv_cases(ref), open(os.path.join(OUT, "kv_plan.json"), "w"))
+    w = workloads.load("cfg4")
+    ref.adaptive_timeline_json(problem(w), w.raw["actual"], os.path.join(OUT, "timeline_cfg4_ref.json"), seed=0,
+                               max_iters=150, min_gain=w.raw["min_gain"])
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["f3"]:
+        gen_f3(Oracle("ref"))
+    else:
+        main()

@@ -86,6 +86,21 @@ int oracle_fit_types(int64_t n, const uint32_t *input_len, const uint32_t *outpu
                      uint64_t seed, double *centroid_in, double *centroid_out);
 int oracle_holt_forecast(int J, int T, const int64_t *counts, int window, int64_t *lambda_out);
 
+/* switchplan::kv_plan (reference only); carry = a switch plan's transfers. */
+int oracle_kv_plan(const oserve_cluster_desc *c, int n_inflight, const oserve_inflight *inflight,
+                   int64_t threshold_tokens, const oserve_deployment *src, const oserve_deployment *dst,
+                   double headroom, int n_carry, const oserve_transfer *carry, int64_t *drained, int *n_drained,
+                   oserve_kv_transfer *migrated, int *n_migrated, uint64_t *buffer_bytes);
+
+/* io::save_timeline of orch::build_adaptive_timeline (reference only). */
+int oracle_adaptive_timeline_json(const oracle_problem *p, int T, const int64_t *counts, uint64_t seed,
+                                  int max_iters, double min_gain, const char *path);
+
+/* io::load_timeline(in) then io::save_timeline(out); io::load_deployment /
+ * save_deployment likewise (reference only) — schema checks. */
+int oracle_timeline_resave(const char *in_path, const char *out_path, int *entries);
+int oracle_deployment_resave(const char *in_path, const char *out_path, int *replicas);
+
 #ifdef __cplusplus
 }
 #endif

@@ -922,4 +922,26 @@ int oracle_holt_forecast(int J, int T, const int64_t *counts, int window, int64_
     });
 }
 
+// kv_plan and the JSON schema checks are reference-only (the restatement
+// has no counterpart; the GPU product is checked against _ref directly).
+int oracle_kv_plan(const oserve_cluster_desc *, int, const oserve_inflight *, int64_t, const oserve_deployment *,
+                   const oserve_deployment *, double, int, const oserve_transfer *, int64_t *, int *,
+                   oserve_kv_transfer *, int *, uint64_t *) {
+    g_err = "kv_plan: reference-only (use the _ref oracle)";
+    return OSERVE_ERR_UNSUPPORTED;
+}
+int oracle_adaptive_timeline_json(const oracle_problem *, int, const int64_t *, uint64_t, int, double,
+                                  const char *) {
+    g_err = "adaptive_timeline_json: reference-only";
+    return OSERVE_ERR_UNSUPPORTED;
+}
+int oracle_timeline_resave(const char *, const char *, int *) {
+    g_err = "timeline_resave: reference-only";
+    return OSERVE_ERR_UNSUPPORTED;
+}
+int oracle_deployment_resave(const char *, const char *, int *) {
+    g_err = "deployment_resave: reference-only";
+    return OSERVE_ERR_UNSUPPORTED;
+}
+
 }  // extern "C"

@@ -59,6 +59,13 @@ class Oracle:
         L.oracle_fit_types.argtypes = [C.c_int64, P(C.c_uint32), P(C.c_uint32), C.c_int, C.c_uint64,
                                        P(C.c_double), P(C.c_double)]
         L.oracle_holt_forecast.argtypes = [C.c_int, C.c_int, P(C.c_int64), C.c_int, P(C.c_int64)]
+        L.oracle_kv_plan.argtypes = [P(A.ClusterDesc), C.c_int, P(A.InflightDesc), C.c_int64, P(A.DeploymentDesc),
+                                     P(A.DeploymentDesc), C.c_double, C.c_int, P(A.TransferDesc), P(C.c_int64),
+                                     P(C.c_int), P(A.KvTransferDesc), P(C.c_int), P(C.c_uint64)]
+        L.oracle_adaptive_timeline_json.argtypes = [P(A.ProblemDesc), C.c_int, P(C.c_int64), C.c_uint64, C.c_int,
+                                                    C.c_double, C.c_char_p]
+        L.oracle_timeline_resave.argtypes = [C.c_char_p, C.c_char_p, P(C.c_int)]
+        L.oracle_deployment_resave.argtypes = [C.c_char_p, C.c_char_p, P(C.c_int)]
         L.oracle_solve_assignment.argtypes = [C.c_int, C.c_int, P(C.c_int64), P(C.c_int64), P(C.c_int64),
                                               P(A.SolveOptionsDesc), P(C.c_int64), P(C.c_int64), P(C.c_int64),
                                               P(C.c_int64), P(C.c_int64), P(C.c_uint64)]
@@ -222,6 +229,41 @@ class Oracle:
                                             out.ctypes.data_as(C.POINTER(C.c_uint32)), k, C.c_uint64(seed),
                                             ci, co))
         return [core.WorkloadType(c, ci[c], co[c]) for c in range(k)]
+
+    def kv_plan(self, cl: core.ClusterSpec, inflight, threshold_tokens: int, src: core.Deployment,
+                dst: core.Deployment, headroom: float = 0.1, carry=None) -> core.KvPlan:
+        keep = A.Keep()
+        c = A.cluster_desc(cl, keep)
+        s, d = A.deployment_desc(src, keep), A.deployment_desc(dst, keep)
+        reqs = A.inflight_arr(inflight, keep)
+        tr, ntr = A.transfer_arr(carry, keep)
+        n = len(inflight)
+        drained = (C.c_int64 * max(1, n))()
+        mig = (A.KvTransferDesc * max(1, n))()
+        nd, nm, buf = C.c_int(), C.c_int(), C.c_uint64()
+        self._chk(self.lib.oracle_kv_plan(C.byref(c), n, reqs, threshold_tokens, C.byref(s), C.byref(d),
+                                          float(headroom), ntr, tr, drained, C.byref(nd), mig, C.byref(nm),
+                                          C.byref(buf)))
+        return core.KvPlan(list(drained[:nd.value]),
+                           [core.KvTransfer(m.request_id, m.kv_bytes, m.src, m.dst) for m in mig[:nm.value]],
+                           buf.value)
+
+    def adaptive_timeline_json(self, pr: Problem, counts, path: str, seed: int = 0, max_iters: int = 150,
+                               min_gain: float = 0.01):
+        T = len(counts)
+        flat = A._arr(C.c_int64, [v for row in counts for v in row])
+        self._chk(self.lib.oracle_adaptive_timeline_json(C.byref(pr.desc), T, flat, C.c_uint64(seed), max_iters,
+                                                         min_gain, path.encode()))
+
+    def timeline_resave(self, src: str, dst: str) -> int:
+        n = C.c_int()
+        self._chk(self.lib.oracle_timeline_resave(src.encode(), dst.encode(), C.byref(n)))
+        return n.value
+
+    def deployment_resave(self, src: str, dst: str) -> int:
+        n = C.c_int()
+        self._chk(self.lib.oracle_deployment_resave(src.encode(), dst.encode(), C.byref(n)))
+        return n.value
 
     def holt_forecast(self, counts: List[List[int]], window: int = 50) -> List[List[int]]:
         T, J = len(counts), len(counts[0])

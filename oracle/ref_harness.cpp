@@ -34,6 +34,7 @@
 #include "oserve/deploysearch.hpp"
 #include "oserve/errors.hpp"
 #include "oserve/flowassign.hpp"
+#include "oserve/json_io.hpp"
 #include "oserve/orchestrate.hpp"
 #include "oserve/switchplan.hpp"
 #include "oserve/workload.hpp"
@@ -605,6 +606,77 @@ int oracle_holt_forecast(int J, int T, const int64_t *counts, int window, int64_
         auto f = orch::forecast_series(series, predictor, window);
         for (int t = 0; t < T; ++t)
             for (int j = 0; j < J; ++j) lambda_out[t * J + j] = f[t][j];
+    });
+}
+
+int oracle_kv_plan(const oserve_cluster_desc *c, int n_inflight, const oserve_inflight *inflight,
+                   int64_t threshold_tokens, const oserve_deployment *src, const oserve_deployment *dst,
+                   double headroom, int n_carry, const oserve_transfer *carry, int64_t *drained, int *n_drained,
+                   oserve_kv_transfer *migrated, int *n_migrated, uint64_t *buffer_bytes) {
+    return guarded([&] {
+        ClusterSpec cl = to_cluster(*c);
+        std::vector<switchplan::InflightRequest> reqs;
+        for (int q = 0; q < n_inflight; ++q)
+            reqs.push_back({inflight[q].request_id, inflight[q].generated_tokens, inflight[q].kv_bytes,
+                            inflight[q].source_replica});
+        switchplan::SwitchPlan cp;
+        for (int i = 0; i < n_carry; ++i) {
+            switchplan::Transfer t;
+            t.range.begin = carry[i].begin;
+            t.range.end = carry[i].end;
+            t.src = carry[i].src;
+            t.dst = carry[i].dst;
+            cp.transfers.push_back(t);
+            cp.link_load[{t.src, t.dst}] += t.range.len();
+        }
+        auto kv = switchplan::kv_plan(reqs, threshold_tokens, to_dep(*src), to_dep(*dst), cl, headroom,
+                                      n_carry > 0 ? &cp : nullptr);
+        *n_drained = static_cast<int>(kv.drained.size());
+        for (size_t i = 0; i < kv.drained.size(); ++i) drained[i] = kv.drained[i];
+        *n_migrated = static_cast<int>(kv.migrated.size());
+        for (size_t i = 0; i < kv.migrated.size(); ++i)
+            migrated[i] = {kv.migrated[i].request_id, kv.migrated[i].kv_bytes, kv.migrated[i].src,
+                           kv.migrated[i].dst};
+        *buffer_bytes = kv.buffer_bytes;
+    });
+}
+
+int oracle_adaptive_timeline_json(const oracle_problem *p, int T, const int64_t *counts, uint64_t seed,
+                                  int max_iters, double min_gain, const char *path) {
+    return guarded([&] {
+        Problem pr(*p);
+        const int J = p->num_classes;
+        workload::SpanSeries series;
+        series.span_seconds = static_cast<int>(pr.span_s);
+        for (int t = 0; t < T; ++t)
+            series.spans.push_back({t, std::vector<int64_t>(counts + t * J, counts + (t + 1) * J)});
+        workload::TypeModel tm;
+        tm.k = J;
+        tm.centroids = pr.types;
+        orch::OrchestrateOptions oo;
+        oo.seed = seed;
+        oo.span_seconds = static_cast<int>(pr.span_s);
+        oo.k = J;
+        oo.min_gain = min_gain;
+        oo.search_max_iters = max_iters;
+        oo.parallel = true;
+        io::save_timeline(path, orch::build_adaptive_timeline(series, tm, pr.cluster, pr.model, pr.params, oo));
+    });
+}
+
+int oracle_timeline_resave(const char *in_path, const char *out_path, int *entries) {
+    return guarded([&] {
+        auto tl = io::load_timeline(in_path);
+        *entries = static_cast<int>(tl.entries.size());
+        io::save_timeline(out_path, tl);
+    });
+}
+
+int oracle_deployment_resave(const char *in_path, const char *out_path, int *replicas) {
+    return guarded([&] {
+        auto d = io::load_deployment(in_path);
+        *replicas = d.replica_count();
+        io::save_deployment(out_path, d);
     });
 }
 

@@ -84,6 +84,30 @@ class TransferDesc(C.Structure):
     _fields_ = [("begin", C.c_uint64), ("end", C.c_uint64), ("src", C.c_int), ("dst", C.c_int)]
 
 
+class InflightDesc(C.Structure):
+    _fields_ = [("request_id", C.c_int64), ("generated_tokens", C.c_int64), ("kv_bytes", C.c_uint64),
+                ("source_replica", C.c_int)]
+
+
+class KvTransferDesc(C.Structure):
+    _fields_ = [("request_id", C.c_int64), ("kv_bytes", C.c_uint64), ("src", C.c_int), ("dst", C.c_int)]
+
+
+def inflight_arr(reqs, keep: "Keep"):
+    arr = (InflightDesc * max(1, len(reqs)))()
+    for i, r in enumerate(reqs):
+        arr[i] = InflightDesc(r.request_id, r.generated_tokens, r.kv_bytes, r.source_replica)
+    return keep(arr)
+
+
+def transfer_arr(plan, keep: "Keep"):
+    tr = [] if plan is None else plan.transfers
+    arr = (TransferDesc * max(1, len(tr)))()
+    for i, t in enumerate(tr):
+        arr[i] = TransferDesc(t.range.begin, t.range.end, t.src, t.dst)
+    return keep(arr), len(tr)
+
+
 class SearchOptionsDesc(C.Structure):
     _fields_ = [("seed", C.c_uint64), ("max_iters", C.c_int), ("stale_limit", C.c_int),
                 ("mutation_retries", C.c_int), ("warm_start", C.POINTER(DeploymentDesc))]

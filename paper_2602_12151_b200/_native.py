@@ -28,7 +28,7 @@ EXPORTS = [
     "oserve_gpu_launch_count", "oserve_gpu_copy_bytes",
     "oserve_shard_count", "oserve_shard_global_rank", "oserve_key_layout",
     "oserve_gpu_round_topk", "oserve_gpu_switch_cost_keys", "oserve_gpu_switch_cost_keys_async",
-    "oserve_gpu_search",
+    "oserve_gpu_search", "oserve_gpu_kv_plan", "oserve_forecast_series",
 ]
 
 _lib = None
@@ -76,6 +76,11 @@ def load_library() -> C.CDLL:
     L.oserve_gpu_switch_cost_keys.argtypes = [vp, P(A.DeploymentDesc), C.c_int, vp, P(C.c_double), P(C.c_uint64)]
     L.oserve_gpu_switch_cost_keys_async.argtypes = [vp, P(A.DeploymentDesc), C.c_int, vp, vp]
     L.oserve_gpu_search.argtypes = [vp, P(A.SearchOptionsDesc), P(A.SearchResult), P(A.SearchLogRow), C.c_int]
+    L.oserve_gpu_kv_plan.argtypes = [vp, C.c_int, P(A.InflightDesc), C.c_int64, P(A.DeploymentDesc),
+                                     P(A.DeploymentDesc), C.c_double, C.c_int, P(A.TransferDesc), P(C.c_int64),
+                                     P(C.c_int), P(A.KvTransferDesc), P(C.c_int), P(C.c_uint64)]
+    L.oserve_forecast_series.argtypes = [C.c_int, C.c_int, P(C.c_int64), C.c_int, C.c_double, C.c_double,
+                                         P(C.c_int64)]
     L.oserve_shard_count.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.c_int]
     L.oserve_shard_count.restype = C.c_uint64
     L.oserve_shard_global_rank.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.c_int]
@@ -87,6 +92,19 @@ def load_library() -> C.CDLL:
 
 
 SHARD_CHUNK = 4096
+
+
+def forecast_series(counts: Sequence[Sequence[int]], window: int = 50, alpha: float = 0.45,
+                    beta: float = 0.25) -> List[List[int]]:
+    """orch::forecast_series (orchestrate.cpp:75-92) with HoltForecaster
+    (workload.cpp:204-222): per-span demand from the actual counts [T][J]."""
+    T = len(counts)
+    J = len(counts[0]) if T else 1
+    flat = A._arr(C.c_int64, [int(v) for row in counts for v in row])
+    out = (C.c_int64 * max(1, T * J))()
+    A.raise_for(load_library().oserve_forecast_series(J, T, flat, window, alpha, beta, out),
+                "forecast_series: invalid arguments")
+    return A.i64_rows(out, T, J)
 
 
 def shard_count(total: int, rank: int, world: int, chunk: int = SHARD_CHUNK) -> int:
@@ -309,6 +327,24 @@ class GpuContext:
         mb = (C.c_uint64 * max(1, len(dsts)))()
         self._chk(self.lib.oserve_gpu_switch_cost_batch(self.h, C.byref(s), len(dsts), arr, est, mb))
         return list(est[:len(dsts)]), list(mb[:len(dsts)])
+
+    def kv_plan(self, inflight: Sequence[core.InflightRequest], threshold_tokens: int, src: core.Deployment,
+                dst: core.Deployment, headroom: float = 0.1, carry: Optional[core.SwitchPlan] = None) -> core.KvPlan:
+        """switchplan::kv_plan (switchplan.cpp:142-207) on the device (K5)."""
+        keep = A.Keep()
+        s, d = A.deployment_desc(src, keep), A.deployment_desc(dst, keep)
+        reqs = A.inflight_arr(inflight, keep)
+        tr, ntr = A.transfer_arr(carry, keep)
+        n = len(inflight)
+        drained = (C.c_int64 * max(1, n))()
+        mig = (A.KvTransferDesc * max(1, n))()
+        nd, nm, buf = C.c_int(), C.c_int(), C.c_uint64()
+        self._chk(self.lib.oserve_gpu_kv_plan(self.h, n, reqs, threshold_tokens, C.byref(s), C.byref(d),
+                                              float(headroom), ntr, tr, drained, C.byref(nd), mig, C.byref(nm),
+                                              C.byref(buf)))
+        return core.KvPlan(list(drained[:nd.value]),
+                           [core.KvTransfer(m.request_id, m.kv_bytes, m.src, m.dst) for m in mig[:nm.value]],
+                           buf.value)
 
     def switch_plan(self, src: core.Deployment, dst: core.Deployment) -> core.SwitchPlan:
         keep = A.Keep()

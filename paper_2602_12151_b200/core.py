@@ -221,6 +221,32 @@ class SwitchPlan:
     est_seconds: float = 0.0
 
 
+@dataclass
+class InflightRequest:
+    """switchplan::InflightRequest (switchplan.hpp:63-68)."""
+    request_id: int
+    generated_tokens: int
+    kv_bytes: int
+    source_replica: int
+
+
+@dataclass
+class KvTransfer:
+    """switchplan::KvTransfer (switchplan.hpp:70-77)."""
+    request_id: int
+    kv_bytes: int
+    src: int
+    dst: int
+
+
+@dataclass
+class KvPlan:
+    """switchplan::KvPlan (switchplan.hpp:79-84)."""
+    drained: List[int] = field(default_factory=list)
+    migrated: List[KvTransfer] = field(default_factory=list)
+    buffer_bytes: int = 0
+
+
 # ---- fixtures (proj/tests/fixtures.hpp:20-73), used by tests and configs ----
 def cluster(machines: int, devices_per_machine: int, mem_per_device: int = 80 * KGB,
             intra_bw: float = 400e9, inter_bw: float = 200e9) -> ClusterSpec:

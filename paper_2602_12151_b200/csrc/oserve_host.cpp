@@ -1396,6 +1396,142 @@ int oserve_gpu_switch_cost_keys_async(oserve_gpu_ctx *ctx, const oserve_deployme
     });
 }
 
+int oserve_gpu_kv_plan(oserve_gpu_ctx *ctx, int n_inflight, const oserve_inflight *inflight, int64_t threshold_tokens,
+                       const oserve_deployment *src, const oserve_deployment *dst, double headroom, int n_carry,
+                       const oserve_transfer *carry, int64_t *drained, int *n_drained, oserve_kv_transfer *migrated,
+                       int *n_migrated, uint64_t *buffer_bytes) {
+    return guarded(ctx, [&] {
+        if (headroom < 0.0 || headroom > 0.5) fail(OSERVE_ERR_INVALID_ARGUMENT, "kv_plan: headroom must be in [0, 0.5]");
+        for (int q = 0; q < n_inflight; ++q) {
+            const auto &r = inflight[q];
+            if (r.generated_tokens <= threshold_tokens) continue;
+            if (r.source_replica < 0 || r.source_replica >= src->num_replicas)
+                fail(OSERVE_ERR_INVALID_ARGUMENT, "kv_plan: request " + std::to_string(r.request_id) +
+                                                      " names unknown source replica");
+        }
+        // device slots: cluster devices plus any id of the deployments / carry, ascending
+        std::set<int> ids(ctx->dev_sorted.begin(), ctx->dev_sorted.end());
+        auto add = [&](const oserve_deployment &d) {
+            int n = 0;
+            for (int r = 0; r < d.num_replicas; ++r) n += d.replica_num_devices[r];
+            for (int i = 0; i < n; ++i) ids.insert(d.device_ids[i]);
+        };
+        add(*src);
+        add(*dst);
+        for (const oserve_deployment *d : {src, dst})  // an empty replica picks device -1 (switchplan.cpp:170-176)
+            for (int r = 0; r < d->num_replicas; ++r)
+                if (d->replica_num_devices[r] == 0) ids.insert(-1);
+        for (int i = 0; i < n_carry; ++i) {
+            ids.insert(carry[i].src);
+            ids.insert(carry[i].dst);
+        }
+        if (ids.size() > 4096) fail(OSERVE_ERR_UNSUPPORTED, "kv_plan limited to 4096 devices");
+        std::map<int, int> slot;
+        std::vector<int32_t> machine, dev_id;
+        for (int id : ids) {
+            slot.emplace(id, static_cast<int>(dev_id.size()));
+            dev_id.push_back(id);
+            machine.push_back(ctx->machine(id));
+        }
+        const int NS = static_cast<int>(dev_id.size());
+        auto flat = [&](const oserve_deployment &d, std::vector<int32_t> &off, std::vector<int32_t> &devs) {
+            int pos = 0;
+            off.push_back(0);
+            for (int r = 0; r < d.num_replicas; ++r) {
+                for (int i = 0; i < d.replica_num_devices[r]; ++i) devs.push_back(slot[d.device_ids[pos++]]);
+                off.push_back(static_cast<int32_t>(devs.size()));
+            }
+        };
+        std::vector<int32_t> soff, sdev, doff, ddev;
+        flat(*src, soff, sdev);
+        flat(*dst, doff, ddev);
+        std::vector<uint64_t> load(static_cast<size_t>(NS) * NS, 0);
+        for (int i = 0; i < n_carry; ++i)  // SwitchPlan::link_load from its transfers
+            load[static_cast<size_t>(slot[carry[i].src]) * NS + slot[carry[i].dst]] += carry[i].end - carry[i].begin;
+        for (uint64_t v : load)
+            if (v >= (uint64_t{1} << 46)) fail(OSERVE_ERR_UNSUPPORTED, "kv_plan: link load >= 2^46 bytes");
+        std::vector<int64_t> gen(n_inflight);
+        std::vector<uint64_t> kv(n_inflight);
+        std::vector<int32_t> sr(n_inflight);
+        uint64_t kv_total = 0;
+        for (int q = 0; q < n_inflight; ++q) {
+            gen[q] = inflight[q].generated_tokens;
+            kv[q] = inflight[q].kv_bytes;
+            sr[q] = inflight[q].source_replica;
+            kv_total += kv[q];
+        }
+        if (kv_total >= (uint64_t{1} << 46)) fail(OSERVE_ERR_UNSUPPORTED, "kv_plan: kv bytes >= 2^46");
+        cudaStream_t s = ctx->stream;
+        DBuf b[14];
+        KvPlanIn in{};
+        in.n = n_inflight;
+        in.gen = b[0].upload(gen, s);
+        in.kv = b[1].upload(kv, s);
+        in.srcrep = b[2].upload(sr, s);
+        in.threshold = threshold_tokens;
+        in.num_slots = NS;
+        in.none_slot = slot.count(-1) ? slot[-1] : -1;
+        in.machine = b[3].upload(machine, s);
+        in.dev_id = b[4].upload(dev_id, s);
+        in.src_reps = src->num_replicas;
+        in.dst_reps = dst->num_replicas;
+        in.src_off = b[5].upload(soff, s);
+        in.src_devs = b[6].upload(sdev, s);
+        in.dst_off = b[7].upload(doff, s);
+        in.dst_devs = b[8].upload(ddev, s);
+        in.load = b[9].upload(load, s);
+        in.inbound = static_cast<uint64_t *>(b[10].get(sizeof(uint64_t) * NS));
+        cuda_ok(cudaMemsetAsync(in.inbound, 0, sizeof(uint64_t) * NS, s), "memset");
+        in.kind = static_cast<int32_t *>(b[11].get(sizeof(int32_t) * std::max(n_inflight, 1)));
+        in.mig_src = static_cast<int32_t *>(b[12].get(sizeof(int32_t) * std::max(n_inflight, 1)));
+        in.mig_dst = static_cast<int32_t *>(b[13].get(sizeof(int32_t) * std::max(n_inflight, 1)));
+        cuda_ok(launch_kv_plan(in, s, &ctx->launches), "kv_plan kernel");
+        std::vector<int32_t> kind, ms, md;
+        download(kind, in.kind, n_inflight, s);
+        download(ms, in.mig_src, n_inflight, s);
+        download(md, in.mig_dst, n_inflight, s);
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+        int nd = 0, nm = 0;
+        uint64_t migrated_bytes = 0;
+        for (int q = 0; q < n_inflight; ++q) {
+            if (kind[q] == 0) {
+                drained[nd++] = inflight[q].request_id;
+            } else {
+                migrated[nm++] = {inflight[q].request_id, inflight[q].kv_bytes, ms[q], md[q]};
+                migrated_bytes += inflight[q].kv_bytes;
+            }
+        }
+        *n_drained = nd;
+        *n_migrated = nm;
+        *buffer_bytes = static_cast<uint64_t>(std::ceil(static_cast<double>(migrated_bytes) * (1.0 + headroom)));
+    });
+}
+
+int oserve_forecast_series(int J, int T, const int64_t *counts, int window, double alpha, double beta,
+                           int64_t *lambda_out) {
+    if (J < 1 || T < 0 || window < 1) return OSERVE_ERR_INVALID_ARGUMENT;
+    for (int t = 0; t < T; ++t) {
+        for (int j = 0; j < J; ++j) {
+            if (t == 0) {  // cold start: the first span's own counts
+                lambda_out[j] = counts[j];
+                continue;
+            }
+            // HoltForecaster::predict over the trailing window (workload.cpp:204-222, :231-244)
+            const int start = std::max(0, t - window);
+            double level = static_cast<double>(counts[static_cast<size_t>(start) * J + j]), trend = 0.0;
+            for (int u = start + 1; u < t; ++u) {
+                const double prev = level;
+                level = alpha * static_cast<double>(counts[static_cast<size_t>(u) * J + j]) +
+                        (1.0 - alpha) * (level + trend);
+                trend = beta * (level - prev) + (1.0 - beta) * trend;
+            }
+            const double v = std::max(0.0, std::max(0.0, level + trend));
+            lambda_out[static_cast<size_t>(t) * J + j] = std::max<int64_t>(0, std::llround(v));
+        }
+    }
+    return OSERVE_OK;
+}
+
 int oserve_gpu_exhaustive(oserve_gpu_ctx *ctx, oserve_round_result *out) {
     oserve_space_desc d{OSERVE_SPACE_ORDERED, 0, nullptr, 16};
     int rc = oserve_gpu_round(ctx, &d, out);

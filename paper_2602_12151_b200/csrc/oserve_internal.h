@@ -189,6 +189,30 @@ int launch_switch_cost(const SwitchDeps &d, const SwitchOut &o, void *stream, ui
 int launch_switch_cost_keys(const SwitchDeps &src, const SpaceTables &sp, const KeyLayout &key, const ShapeTables &t,
                             const uint64_t *keys, int count, const int32_t *part_off, const SwitchOut &o,
                             void *stream, uint64_t *launches);
+// kv_plan (K5): one warp, requests in order.
+struct KvPlanIn {
+    int n;                       // inflight requests
+    const int64_t *gen;          // generated tokens
+    const uint64_t *kv;          // kv bytes
+    const int32_t *srcrep;       // source replica
+    int64_t threshold;
+    int num_slots;
+    int none_slot;               // slot of device id -1 (an empty replica's pick), or -1
+    const int32_t *machine;      // [slots]
+    const int32_t *dev_id;       // [slots]
+    int src_reps, dst_reps;
+    const int32_t *src_off;      // [src_reps+1] into src_devs
+    const int32_t *src_devs;     // device slots
+    const int32_t *dst_off;
+    const int32_t *dst_devs;
+    uint64_t *load;              // [slots*slots] link loads (pre-filled with carry)
+    uint64_t *inbound;           // [slots] zero
+    // outputs
+    int32_t *kind;               // [n] 0 drained, 1 migrated
+    int32_t *mig_src, *mig_dst;  // [n] device ids
+};
+int launch_kv_plan(const KvPlanIn &in, void *stream, uint64_t *launches);
+
 // Sort n u64 keys ascending on the device (CUB radix sort); temp is reused.
 int sort_keys(uint64_t *keys, uint64_t *tmp_keys, int n, void **temp, size_t *temp_bytes, void *stream);
 // Groups whose list dropped a key better than `kth` (0 => the lists are exact).

@@ -1476,6 +1476,59 @@ __global__ void __launch_bounds__(256) k_switch_cost_keys(SwitchDeps d, SpaceTab
     switch_core(d, o, pair, sB, sE, cuts, ncuts_s, wmax, wbytes, wstatus);
 }
 
+// ------------------------------------------------------------------- K5 ---
+// kv_plan (switchplan.cpp:142-207): requests in order (the link/inbound loads
+// carry over), lanes evaluate the candidate devices of each choice.
+__global__ void __launch_bounds__(32) k_kv_plan(KvPlanIn in) {
+    const int lane = threadIdx.x;
+    int rr = 0;
+    for (int q = 0; q < in.n; ++q) {
+        if (in.gen[q] <= in.threshold || in.dst_reps == 0) {
+            if (lane == 0) in.kind[q] = 0;  // drained
+            continue;
+        }
+        const int trep = rr % in.dst_reps;
+        ++rr;
+        // target: least inbound-loaded device of the target replica, lowest id on ties
+        unsigned long long tk = ~0ull;
+        for (int p = in.dst_off[trep] + lane; p < in.dst_off[trep + 1]; p += 32) {
+            const int slot = in.dst_devs[p];
+            // inbound < 2^47 (bytes), slot < 2^16: pack (inbound, id order = slot order)
+            const unsigned long long k = (static_cast<unsigned long long>(in.inbound[slot]) << 16) | slot;
+            tk = k < tk ? k : tk;
+        }
+        for (int d = 16; d > 0; d >>= 1) {
+            const unsigned long long o = __shfl_xor_sync(0xffffffffu, tk, d);
+            tk = o < tk ? o : tk;
+        }
+        const int target = tk == ~0ull ? in.none_slot : static_cast<int>(tk & 0xffff);
+        // source: intra-machine first, then least load toward target, then lowest id
+        const int srep = in.srcrep[q];
+        unsigned long long sk = ~0ull;
+        for (int p = in.src_off[srep] + lane; p < in.src_off[srep + 1]; p += 32) {
+            const int slot = in.src_devs[p];
+            const bool intra = in.machine[slot] >= 0 && in.machine[slot] == in.machine[target];
+            const unsigned long long k = (static_cast<unsigned long long>(!intra) << 63) |
+                                         (static_cast<unsigned long long>(in.load[slot * in.num_slots + target]) << 16) |
+                                         slot;
+            sk = k < sk ? k : sk;
+        }
+        for (int d = 16; d > 0; d >>= 1) {
+            const unsigned long long o = __shfl_xor_sync(0xffffffffu, sk, d);
+            sk = o < sk ? o : sk;
+        }
+        const int best = sk == ~0ull ? in.none_slot : static_cast<int>(sk & 0xffff);
+        if (lane == 0) {
+            in.load[best * in.num_slots + target] += in.kv[q];
+            in.inbound[target] += in.kv[q];
+            in.kind[q] = 1;
+            in.mig_src[q] = in.dev_id[best];
+            in.mig_dst[q] = in.dev_id[target];
+        }
+        __syncwarp();
+    }
+}
+
 __global__ void k_topk_check(const uint64_t *meta, int groups, const uint64_t *kth, unsigned int *bad) {
     const uint64_t kk = *kth;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < groups; i += gridDim.x * blockDim.x)
@@ -1646,6 +1699,14 @@ int sort_keys(uint64_t *keys, uint64_t *tmp_keys, int n, void **temp, size_t *te
     }
     e = cub::DeviceRadixSort::SortKeys(*temp, need, keys, tmp_keys, n, 0, 64, static_cast<cudaStream_t>(stream));
     return static_cast<int>(e);
+}
+
+int launch_kv_plan(const KvPlanIn &in, void *stream, uint64_t *launches) {
+    cudaGetLastError();
+    if (in.n == 0) return 0;
+    k_kv_plan<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(in);
+    if (launches) ++*launches;
+    return check(cudaGetLastError());
 }
 
 int launch_topk_check(const uint64_t *meta, int groups, const uint64_t *kth, unsigned int *bad, void *stream) {

@@ -86,6 +86,15 @@ def build_adaptive_timeline(ctx: GpuContext, types: Sequence[core.WorkloadType],
     return tl
 
 
+def adaptive_timeline(ctx: GpuContext, types: Sequence[core.WorkloadType], actual: Sequence[Sequence[int]],
+                      window: int = 50, **kw) -> Timeline:
+    """orch::build_adaptive_timeline entry point over observed per-span
+    counts: Holt forecasts (forecast_series, orchestrate.cpp:75-92, host
+    C++ in liboserve_gpu) feed the per-window loop above."""
+    from ._native import forecast_series
+    return build_adaptive_timeline(ctx, types, forecast_series(actual, window), **kw)
+
+
 def _same(a: core.Deployment, b: core.Deployment) -> bool:
     return [(sorted(r.device_ids), r.tp, r.pp) for r in a.replicas] == \
         [(sorted(r.device_ids), r.tp, r.pp) for r in b.replicas]

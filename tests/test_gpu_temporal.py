@@ -82,3 +82,16 @@ def test_cfg4_reference_adaptive_timeline(cuda):
             "x": e.assignment, "switch_seconds": e.switch_seconds,
             "transfers": 0 if e.switch is None else len(e.switch.transfers)} for e in tl.entries]
     assert got == exp
+
+
+def test_cfg4_timeline_file_is_the_references(cuda):
+    """From the observed counts (Holt forecasts in liboserve_gpu) through the
+    GPU search loop to the timeline file: byte-identical to the file the
+    reference's build_adaptive_timeline + io::save_timeline wrote."""
+    from paper_2602_12151_b200 import json_io
+    w = workloads.load("cfg4")
+    g = GpuContext(w.cluster, w.model, w.params)
+    tl = orchestrate.adaptive_timeline(g, w.types, w.raw["actual"], 50, span_seconds=w.span_s,
+                                       min_gain=w.raw["min_gain"], strategy="search", seed=0, search_max_iters=150)
+    text = open(os.path.join(ROOT, "tests", "golden", "timeline_cfg4_ref.json")).read()
+    assert json_io.dumps(json_io.timeline_json(tl, w.span_s)) == text
