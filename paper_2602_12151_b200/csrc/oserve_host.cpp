@@ -1448,19 +1448,14 @@ int oserve_gpu_kv_plan(oserve_gpu_ctx *ctx, int n_inflight, const oserve_infligh
         std::vector<uint64_t> load(static_cast<size_t>(NS) * NS, 0);
         for (int i = 0; i < n_carry; ++i)  // SwitchPlan::link_load from its transfers
             load[static_cast<size_t>(slot[carry[i].src]) * NS + slot[carry[i].dst]] += carry[i].end - carry[i].begin;
-        for (uint64_t v : load)
-            if (v >= (uint64_t{1} << 46)) fail(OSERVE_ERR_UNSUPPORTED, "kv_plan: link load >= 2^46 bytes");
         std::vector<int64_t> gen(n_inflight);
         std::vector<uint64_t> kv(n_inflight);
         std::vector<int32_t> sr(n_inflight);
-        uint64_t kv_total = 0;
         for (int q = 0; q < n_inflight; ++q) {
             gen[q] = inflight[q].generated_tokens;
             kv[q] = inflight[q].kv_bytes;
             sr[q] = inflight[q].source_replica;
-            kv_total += kv[q];
         }
-        if (kv_total >= (uint64_t{1} << 46)) fail(OSERVE_ERR_UNSUPPORTED, "kv_plan: kv bytes >= 2^46");
         cudaStream_t s = ctx->stream;
         DBuf b[14];
         KvPlanIn in{};

@@ -1478,9 +1478,34 @@ __global__ void __launch_bounds__(256) k_switch_cost_keys(SwitchDeps d, SpaceTab
 
 // ------------------------------------------------------------------- K5 ---
 // kv_plan (switchplan.cpp:142-207): requests in order (the link/inbound loads
-// carry over), lanes evaluate the candidate devices of each choice.
+// carry over), lanes evaluate the candidate devices of each choice and a
+// shuffle reduction takes the lexicographic minimum.
+struct KvPick {
+    unsigned long long v;  // load (with the !intra flag ahead of it for sources)
+    int cls;               // 0 intra / 1 not (sources); 0 for targets
+    int slot;              // slot order == device id order
+};
+
+__device__ __forceinline__ bool kv_less(const KvPick &a, const KvPick &b) {
+    if (a.cls != b.cls) return a.cls < b.cls;
+    if (a.v != b.v) return a.v < b.v;
+    return a.slot < b.slot;
+}
+
+__device__ __forceinline__ KvPick kv_warp_min(KvPick p) {
+    for (int d = 16; d > 0; d >>= 1) {
+        KvPick o;
+        o.v = __shfl_xor_sync(0xffffffffu, p.v, d);
+        o.cls = __shfl_xor_sync(0xffffffffu, p.cls, d);
+        o.slot = __shfl_xor_sync(0xffffffffu, p.slot, d);
+        if (kv_less(o, p)) p = o;
+    }
+    return p;
+}
+
 __global__ void __launch_bounds__(32) k_kv_plan(KvPlanIn in) {
     const int lane = threadIdx.x;
+    constexpr int kNone = 0x7fffffff;
     int rr = 0;
     for (int q = 0; q < in.n; ++q) {
         if (in.gen[q] <= in.threshold || in.dst_reps == 0) {
@@ -1490,36 +1515,26 @@ __global__ void __launch_bounds__(32) k_kv_plan(KvPlanIn in) {
         const int trep = rr % in.dst_reps;
         ++rr;
         // target: least inbound-loaded device of the target replica, lowest id on ties
-        unsigned long long tk = ~0ull;
+        KvPick t{~0ull, 2, kNone};
         for (int p = in.dst_off[trep] + lane; p < in.dst_off[trep + 1]; p += 32) {
-            const int slot = in.dst_devs[p];
-            // inbound < 2^47 (bytes), slot < 2^16: pack (inbound, id order = slot order)
-            const unsigned long long k = (static_cast<unsigned long long>(in.inbound[slot]) << 16) | slot;
-            tk = k < tk ? k : tk;
+            const KvPick c{in.inbound[in.dst_devs[p]], 0, in.dst_devs[p]};
+            if (kv_less(c, t)) t = c;
         }
-        for (int d = 16; d > 0; d >>= 1) {
-            const unsigned long long o = __shfl_xor_sync(0xffffffffu, tk, d);
-            tk = o < tk ? o : tk;
-        }
-        const int target = tk == ~0ull ? in.none_slot : static_cast<int>(tk & 0xffff);
+        t = kv_warp_min(t);
+        const int target = t.slot == kNone ? in.none_slot : t.slot;
         // source: intra-machine first, then least load toward target, then lowest id
         const int srep = in.srcrep[q];
-        unsigned long long sk = ~0ull;
+        KvPick b{~0ull, 2, kNone};
         for (int p = in.src_off[srep] + lane; p < in.src_off[srep + 1]; p += 32) {
             const int slot = in.src_devs[p];
             const bool intra = in.machine[slot] >= 0 && in.machine[slot] == in.machine[target];
-            const unsigned long long k = (static_cast<unsigned long long>(!intra) << 63) |
-                                         (static_cast<unsigned long long>(in.load[slot * in.num_slots + target]) << 16) |
-                                         slot;
-            sk = k < sk ? k : sk;
+            const KvPick c{in.load[static_cast<size_t>(slot) * in.num_slots + target], intra ? 0 : 1, slot};
+            if (kv_less(c, b)) b = c;
         }
-        for (int d = 16; d > 0; d >>= 1) {
-            const unsigned long long o = __shfl_xor_sync(0xffffffffu, sk, d);
-            sk = o < sk ? o : sk;
-        }
-        const int best = sk == ~0ull ? in.none_slot : static_cast<int>(sk & 0xffff);
+        b = kv_warp_min(b);
+        const int best = b.slot == kNone ? in.none_slot : b.slot;
         if (lane == 0) {
-            in.load[best * in.num_slots + target] += in.kv[q];
+            in.load[static_cast<size_t>(best) * in.num_slots + target] += in.kv[q];
             in.inbound[target] += in.kv[q];
             in.kind[q] = 1;
             in.mig_src[q] = in.dev_id[best];
