@@ -345,6 +345,49 @@ int oserve_gpu_kv_plan(oserve_gpu_ctx *ctx, int n_inflight, const oserve_infligh
 int oserve_forecast_series(int J, int T, const int64_t *counts, int window, double alpha, double beta,
                            int64_t *lambda_out);
 
+/* ---- flow-network formulation (flowassign.cpp:67-245, 505-519, 559-645) -- */
+
+/* flow::Graph::Edge (flowassign.hpp:32-36). */
+typedef struct {
+    int from;
+    int to;
+    int64_t cap;
+} oserve_flow_edge;
+
+/* Drop-in for flow::max_flow (FIFO push-relabel, flowassign.cpp:67-147) over
+ * `count` independent graphs, one device thread each: graph g has
+ * num_nodes[g] nodes and edges[edge_offset[g] .. edge_offset[g+1]).  Writes
+ * per-edge flows (parallel to `edges`) and the value per graph — the
+ * reference's exact flows, not just an equal value.  Bad source/sink or a
+ * negative capacity: OSERVE_ERR_INVALID_ARGUMENT. */
+int oserve_gpu_max_flow_batch(oserve_gpu_ctx *ctx, int count, const int *num_nodes, const int64_t *edge_offset,
+                              const oserve_flow_edge *edges, const int *source, const int *sink, int64_t *flow,
+                              int64_t *value);
+
+/* flow::build_network + max_flow + extract_assignment (flowassign.cpp:152-199,
+ * 505-519) for `count` instances of one shape [R][J] (raw n/e rows as in
+ * oserve_gpu_solve_batch).  Outputs x [count][R][J], objective and flow
+ * value [count], optionally the per-edge flows [count][J+2RJ+2R] in
+ * FlowNetwork edge order (edge_flow may be NULL).  Instances that qualify
+ * for the exact path (Σλ <= exact_demand_limit, R*J <= exact_cell_limit)
+ * take the branch-and-bound result unless its node budget is exceeded, as
+ * solve_instance does. */
+int oserve_gpu_flow_assign_batch(oserve_gpu_ctx *ctx, int count, int R, int J, const int64_t *n, const int64_t *e,
+                                 const int64_t *lambda, int64_t *x, int64_t *objective, int64_t *flow_value,
+                                 int64_t *edge_flow);
+
+/* flow::extract_assignment (flowassign.cpp:505-519) of GIVEN per-edge flows
+ * [count][J+2RJ+2R] (FlowNetwork edge order) on instances as above. */
+int oserve_gpu_extract_assignment_batch(oserve_gpu_ctx *ctx, int count, int R, int J, const int64_t *n,
+                                        const int64_t *e, const int64_t *lambda, const int64_t *edge_flow,
+                                        int64_t *x, int64_t *objective);
+
+/* flow::solve_fractional (dense Bland's-rule simplex, flowassign.cpp:559-645)
+ * for `count` instances of one shape; f [count][R][J], objective [count].
+ * Bit-identical FP64 pivots.  An unbounded tableau: OSERVE_ERR_LOGIC. */
+int oserve_gpu_solve_fractional_batch(oserve_gpu_ctx *ctx, int count, int R, int J, const int64_t *n,
+                                      const int64_t *e, const int64_t *lambda, double *f, double *objective);
+
 /* Kernel launches issued by this context since creation (evidence counter). */
 uint64_t oserve_gpu_launch_count(const oserve_gpu_ctx *ctx);
 /* Host->device / device->host bytes copied by this context since creation

@@ -13,6 +13,9 @@ the GPU path on machines without the reference:
   switch.json      greedy_plan/estimate_time on seeded deployment pairs
   kv_plan.json     switchplan::kv_plan on seeded in-flight sets (with and
                    without the parameter plan's link loads as carry)
+  flow.json        flow::max_flow on random graphs, build_network +
+                   max_flow + extract_assignment and solve_fractional on
+                   random instances, to_dot texts
   timeline_cfg4_ref.json  io::save_timeline of orch::build_adaptive_timeline
                    on config 4, the reference's own file
 """
@@ -189,6 +192,7 @@ def main():
                                                            for t in plan.transfers]})
     json.dump(sw, open(os.path.join(OUT, "switch.json"), "w"))
     gen_f3(ref)
+    gen_f4(ref)
     print("golden fixtures written to", OUT)
 
 
@@ -225,6 +229,39 @@ def kv_cases(ref, seed=4242):
     return cases
 
 
+def gen_f4(ref):
+    rng = np.random.default_rng(2602)
+    graphs = []
+    for trial in range(400):
+        nn = int(rng.integers(2, 13 if trial < 200 else 60))
+        edges = []
+        for _ in range(int(rng.integers(1, 3 * nn + 1))):
+            u, v = int(rng.integers(0, nn)), int(rng.integers(0, nn))
+            if u == v and trial < 200:
+                continue
+            edges.append((u, v, int(rng.integers(0, 50 if trial % 3 else 1 << 40))))
+        src, snk = (0, nn - 1) if trial % 5 else (nn - 1, 0)
+        value, flow = ref.max_flow(nn, edges, src, snk)
+        graphs.append({"num_nodes": nn, "edges": edges, "source": src, "sink": snk, "value": value, "flow": flow})
+    inst = []
+    for seed, cnt, mr, mj, ml in ((7, 120, 3, 3, 60), (11, 160, 6, 5, 500), (13, 80, 12, 8, 3000),
+                                  (17, 40, 20, 16, 20000)):
+        for n, e, lam in random_instances(seed, cnt, mr, mj, ml):
+            x, obj, val, fl = ref.flow_assign(n, e, lam)
+            inst.append({"n": n, "e": e, "lambda": lam, "x": x, "objective": obj, "value": val, "flow": fl})
+    lps = []
+    for seed, cnt, mr, mj, ml in ((19, 60, 3, 3, 60), (23, 30, 6, 5, 500), (29, 6, 12, 8, 3000)):
+        for n, e, lam in random_instances(seed, cnt, mr, mj, ml):
+            f, obj = ref.solve_fractional(n, e, lam)
+            lps.append({"n": n, "e": e, "lambda": lam, "f": f, "objective": obj})
+    dots = []
+    for n, e, lam in (([[80]], [[80]], [10]), ([[80, 50], [40, 20]], [[80, 50], [40, 20]], [10, 10]),
+                      ([[10, 10, 10], [10, 10, 10]], [[10, 10, 10], [10, 10, 10]], [5, 5, 5])):
+        for wf in (False, True):
+            dots.append({"n": n, "e": e, "lambda": lam, "with_flow": wf, "dot": ref.to_dot(n, e, lam, wf)})
+    json.dump({"graphs": graphs, "instances": inst, "lp": lps, "dot": dots}, open(os.path.join(OUT, "flow.json"), "w"))
+
+
 def gen_f3(ref):
     json.dump(kv_cases(ref), open(os.path.join(OUT, "kv_plan.json"), "w"))
     w = workloads.load("cfg4")
@@ -235,5 +272,7 @@ def gen_f3(ref):
 if __name__ == "__main__":
     if sys.argv[1:] == ["f3"]:
         gen_f3(Oracle("ref"))
+    elif sys.argv[1:] == ["f4"]:
+        gen_f4(Oracle("ref"))
     else:
         main()

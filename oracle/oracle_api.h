@@ -98,6 +98,19 @@ int oracle_adaptive_timeline_json(const oracle_problem *p, int T, const int64_t 
 
 /* io::load_timeline(in) then io::save_timeline(out); io::load_deployment /
  * save_deployment likewise (reference only) — schema checks. */
+/* flow::max_flow / build_network+max_flow+extract_assignment /
+ * solve_fractional / to_dot (reference only; flowassign.cpp:67-245,
+ * 505-519, 559-645). */
+int oracle_max_flow(int num_nodes, int num_edges, const oserve_flow_edge *edges, int source, int sink,
+                    int64_t *flow, int64_t *value);
+int oracle_flow_assign(int R, int J, const int64_t *n, const int64_t *e, const int64_t *lambda,
+                       const oserve_solve_options *opts, int64_t *x, int64_t *objective, int64_t *flow_value,
+                       int64_t *edge_flow);
+int oracle_solve_fractional(int R, int J, const int64_t *n, const int64_t *e, const int64_t *lambda, double *f,
+                            double *objective);
+int oracle_to_dot(int R, int J, const int64_t *n, const int64_t *e, const int64_t *lambda, int with_flow,
+                  char *buf, int cap, int *len);
+
 int oracle_timeline_resave(const char *in_path, const char *out_path, int *entries);
 int oracle_deployment_resave(const char *in_path, const char *out_path, int *replicas);
 

@@ -944,4 +944,22 @@ int oracle_deployment_resave(const char *, const char *, int *) {
     return OSERVE_ERR_UNSUPPORTED;
 }
 
+int oracle_max_flow(int, int, const oserve_flow_edge *, int, int, int64_t *, int64_t *) {
+    g_err = "max_flow: reference-only";
+    return OSERVE_ERR_UNSUPPORTED;
+}
+int oracle_flow_assign(int, int, const int64_t *, const int64_t *, const int64_t *, const oserve_solve_options *,
+                       int64_t *, int64_t *, int64_t *, int64_t *) {
+    g_err = "flow_assign: reference-only";
+    return OSERVE_ERR_UNSUPPORTED;
+}
+int oracle_solve_fractional(int, int, const int64_t *, const int64_t *, const int64_t *, double *, double *) {
+    g_err = "solve_fractional: reference-only";
+    return OSERVE_ERR_UNSUPPORTED;
+}
+int oracle_to_dot(int, int, const int64_t *, const int64_t *, const int64_t *, int, char *, int, int *) {
+    g_err = "to_dot: reference-only";
+    return OSERVE_ERR_UNSUPPORTED;
+}
+
 }  // extern "C"

@@ -64,6 +64,15 @@ class Oracle:
                                      P(C.c_int), P(A.KvTransferDesc), P(C.c_int), P(C.c_uint64)]
         L.oracle_adaptive_timeline_json.argtypes = [P(A.ProblemDesc), C.c_int, P(C.c_int64), C.c_uint64, C.c_int,
                                                     C.c_double, C.c_char_p]
+        L.oracle_max_flow.argtypes = [C.c_int, C.c_int, P(A.FlowEdgeDesc), C.c_int, C.c_int, P(C.c_int64),
+                                      P(C.c_int64)]
+        L.oracle_flow_assign.argtypes = [C.c_int, C.c_int, P(C.c_int64), P(C.c_int64), P(C.c_int64),
+                                         P(A.SolveOptionsDesc), P(C.c_int64), P(C.c_int64), P(C.c_int64),
+                                         P(C.c_int64)]
+        L.oracle_solve_fractional.argtypes = [C.c_int, C.c_int, P(C.c_int64), P(C.c_int64), P(C.c_int64),
+                                              P(C.c_double), P(C.c_double)]
+        L.oracle_to_dot.argtypes = [C.c_int, C.c_int, P(C.c_int64), P(C.c_int64), P(C.c_int64), C.c_int, C.c_char_p,
+                                    C.c_int, P(C.c_int)]
         L.oracle_timeline_resave.argtypes = [C.c_char_p, C.c_char_p, P(C.c_int)]
         L.oracle_deployment_resave.argtypes = [C.c_char_p, C.c_char_p, P(C.c_int)]
         L.oracle_solve_assignment.argtypes = [C.c_int, C.c_int, P(C.c_int64), P(C.c_int64), P(C.c_int64),
@@ -254,6 +263,45 @@ class Oracle:
         flat = A._arr(C.c_int64, [v for row in counts for v in row])
         self._chk(self.lib.oracle_adaptive_timeline_json(C.byref(pr.desc), T, flat, C.c_uint64(seed), max_iters,
                                                          min_gain, path.encode()))
+
+    def max_flow(self, num_nodes: int, edges, source: int, sink: int):
+        ed = (A.FlowEdgeDesc * max(1, len(edges)))(*[A.FlowEdgeDesc(a, b, c) for a, b, c in edges])
+        fl = (C.c_int64 * max(1, len(edges)))()
+        v = C.c_int64()
+        self._chk(self.lib.oracle_max_flow(num_nodes, len(edges), ed, source, sink, fl, C.byref(v)))
+        return v.value, list(fl[:len(edges)])
+
+    def flow_assign(self, n, e, lam, opts=None):
+        """build_network + max_flow + extract_assignment -> (x, objective, value, edge flows)."""
+        R, J = len(n), len(lam)
+        m = J + 2 * R * J + 2 * R
+        fn = A._arr(C.c_int64, [v for r in n for v in r])
+        fe = A._arr(C.c_int64, [v for r in e for v in r])
+        x, fl = (C.c_int64 * (R * J))(), (C.c_int64 * m)()
+        obj, val = C.c_int64(), C.c_int64()
+        o = C.byref(A.SolveOptionsDesc(opts.exact_demand_limit, opts.exact_cell_limit, opts.node_budget)) \
+            if opts else None
+        self._chk(self.lib.oracle_flow_assign(R, J, fn, fe, A._arr(C.c_int64, lam), o, x, C.byref(obj),
+                                              C.byref(val), fl))
+        return A.i64_rows(x, R, J), obj.value, val.value, list(fl)
+
+    def solve_fractional(self, n, e, lam):
+        R, J = len(n), len(lam)
+        f, obj = (C.c_double * (R * J))(), C.c_double()
+        self._chk(self.lib.oracle_solve_fractional(R, J, A._arr(C.c_int64, [v for r in n for v in r]),
+                                                   A._arr(C.c_int64, [v for r in e for v in r]),
+                                                   A._arr(C.c_int64, lam), f, C.byref(obj)))
+        return [list(f[k * J:(k + 1) * J]) for k in range(R)], obj.value
+
+    def to_dot(self, n, e, lam, with_flow: bool) -> str:
+        R, J = len(n), len(lam)
+        args = (R, J, A._arr(C.c_int64, [v for r in n for v in r]), A._arr(C.c_int64, [v for r in e for v in r]),
+                A._arr(C.c_int64, lam), int(with_flow))
+        ln = C.c_int()
+        self._chk(self.lib.oracle_to_dot(*args, None, 0, C.byref(ln)))
+        buf = C.create_string_buffer(ln.value + 1)
+        self._chk(self.lib.oracle_to_dot(*args, buf, ln.value + 1, C.byref(ln)))
+        return buf.value.decode()
 
     def timeline_resave(self, src: str, dst: str) -> int:
         n = C.c_int()

@@ -680,4 +680,86 @@ int oracle_deployment_resave(const char *in_path, const char *out_path, int *rep
     });
 }
 
+static cost::CapacityTable raw_table(int R, int J, const int64_t *n, const int64_t *e) {
+    cost::CapacityTable t;
+    t.n.assign(R, std::vector<int64_t>(J));
+    t.e.assign(R, std::vector<int64_t>(J));
+    t.latency.assign(R, std::vector<double>(J, 0.1));
+    for (int k = 0; k < R; ++k)
+        for (int j = 0; j < J; ++j) {
+            t.n[k][j] = n[k * J + j];
+            t.e[k][j] = e[k * J + j];
+        }
+    return t;
+}
+
+int oracle_max_flow(int num_nodes, int num_edges, const oserve_flow_edge *edges, int source, int sink,
+                    int64_t *flow, int64_t *value) {
+    return guarded([&] {
+        flow::Graph g;
+        g.num_nodes = num_nodes;
+        for (int i = 0; i < num_edges; ++i) g.edges.push_back({edges[i].from, edges[i].to, edges[i].cap});
+        auto r = flow::max_flow(g, source, sink);
+        for (int i = 0; i < num_edges; ++i) flow[i] = r.flow[i];
+        *value = r.value;
+    });
+}
+
+int oracle_flow_assign(int R, int J, const int64_t *n, const int64_t *e, const int64_t *lambda,
+                       const oserve_solve_options *opts, int64_t *x, int64_t *objective, int64_t *flow_value,
+                       int64_t *edge_flow) {
+    return guarded([&] {
+        auto t = raw_table(R, J, n, e);
+        TraceSpan span{0, std::vector<int64_t>(lambda, lambda + J)};
+        auto net = flow::build_network(span, t);
+        auto fr = flow::max_flow(net.graph, net.source(), net.sink());
+        flow::SolveOptions so;
+        if (opts) {
+            so.exact_demand_limit = opts->exact_demand_limit;
+            so.exact_cell_limit = opts->exact_cell_limit;
+            so.node_budget = opts->node_budget;
+        }
+        auto a = flow::extract_assignment(net, fr, so);
+        for (int k = 0; k < R; ++k)
+            for (int j = 0; j < J; ++j) x[k * J + j] = a.x[k][j];
+        *objective = a.objective;
+        if (flow_value) *flow_value = fr.value;
+        if (edge_flow)
+            for (size_t i = 0; i < fr.flow.size(); ++i) edge_flow[i] = fr.flow[i];
+    });
+}
+
+int oracle_solve_fractional(int R, int J, const int64_t *n, const int64_t *e, const int64_t *lambda, double *f,
+                            double *objective) {
+    return guarded([&] {
+        auto t = raw_table(R, J, n, e);
+        auto lp = flow::solve_fractional(t, std::vector<int64_t>(lambda, lambda + J));
+        for (int k = 0; k < R; ++k)
+            for (int j = 0; j < J; ++j) f[k * J + j] = lp.f[k][j];
+        *objective = lp.objective;
+    });
+}
+
+int oracle_to_dot(int R, int J, const int64_t *n, const int64_t *e, const int64_t *lambda, int with_flow,
+                  char *buf, int cap, int *len) {
+    return guarded([&] {
+        auto t = raw_table(R, J, n, e);
+        TraceSpan span{0, std::vector<int64_t>(lambda, lambda + J)};
+        auto net = flow::build_network(span, t);
+        std::string d;
+        if (with_flow) {
+            auto fr = flow::max_flow(net.graph, net.source(), net.sink());
+            d = flow::to_dot(net, &fr);
+        } else {
+            d = flow::to_dot(net);
+        }
+        *len = static_cast<int>(d.size());
+        if (buf && cap > 0) {
+            const int c = std::min(cap - 1, *len);
+            std::memcpy(buf, d.data(), c);
+            buf[c] = 0;
+        }
+    });
+}
+
 }  // extern "C"

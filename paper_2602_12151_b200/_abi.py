@@ -84,6 +84,10 @@ class TransferDesc(C.Structure):
     _fields_ = [("begin", C.c_uint64), ("end", C.c_uint64), ("src", C.c_int), ("dst", C.c_int)]
 
 
+class FlowEdgeDesc(C.Structure):
+    _fields_ = [("from_", C.c_int), ("to", C.c_int), ("cap", C.c_int64)]
+
+
 class InflightDesc(C.Structure):
     _fields_ = [("request_id", C.c_int64), ("generated_tokens", C.c_int64), ("kv_bytes", C.c_uint64),
                 ("source_replica", C.c_int)]

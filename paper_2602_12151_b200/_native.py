@@ -29,6 +29,8 @@ EXPORTS = [
     "oserve_shard_count", "oserve_shard_global_rank", "oserve_key_layout",
     "oserve_gpu_round_topk", "oserve_gpu_switch_cost_keys", "oserve_gpu_switch_cost_keys_async",
     "oserve_gpu_search", "oserve_gpu_kv_plan", "oserve_forecast_series",
+    "oserve_gpu_max_flow_batch", "oserve_gpu_flow_assign_batch", "oserve_gpu_extract_assignment_batch",
+    "oserve_gpu_solve_fractional_batch",
 ]
 
 _lib = None
@@ -79,6 +81,12 @@ def load_library() -> C.CDLL:
     L.oserve_gpu_kv_plan.argtypes = [vp, C.c_int, P(A.InflightDesc), C.c_int64, P(A.DeploymentDesc),
                                      P(A.DeploymentDesc), C.c_double, C.c_int, P(A.TransferDesc), P(C.c_int64),
                                      P(C.c_int), P(A.KvTransferDesc), P(C.c_int), P(C.c_uint64)]
+    L.oserve_gpu_max_flow_batch.argtypes = [vp, C.c_int, P(C.c_int), P(C.c_int64), P(A.FlowEdgeDesc), P(C.c_int),
+                                            P(C.c_int), P(C.c_int64), P(C.c_int64)]
+    L.oserve_gpu_flow_assign_batch.argtypes = [vp, C.c_int, C.c_int, C.c_int] + [P(C.c_int64)] * 7
+    L.oserve_gpu_extract_assignment_batch.argtypes = [vp, C.c_int, C.c_int, C.c_int] + [P(C.c_int64)] * 6
+    L.oserve_gpu_solve_fractional_batch.argtypes = [vp, C.c_int, C.c_int, C.c_int] + [P(C.c_int64)] * 3 + \
+        [P(C.c_double)] * 2
     L.oserve_forecast_series.argtypes = [C.c_int, C.c_int, P(C.c_int64), C.c_int, C.c_double, C.c_double,
                                          P(C.c_int64)]
     L.oserve_shard_count.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.c_int]
@@ -327,6 +335,66 @@ class GpuContext:
         mb = (C.c_uint64 * max(1, len(dsts)))()
         self._chk(self.lib.oserve_gpu_switch_cost_batch(self.h, C.byref(s), len(dsts), arr, est, mb))
         return list(est[:len(dsts)]), list(mb[:len(dsts)])
+
+    # -- flow-network formulation (K6, K7) ---------------------------------------
+    def max_flow_batch(self, graphs: Sequence[Tuple[int, Sequence[Tuple[int, int, int]]]], sources: Sequence[int],
+                       sinks: Sequence[int]):
+        """flow::max_flow per graph (num_nodes, [(from, to, cap)]) -> [(value, flows)]."""
+        G = len(graphs)
+        offs, edges = [0], []
+        for _, es in graphs:
+            edges.extend(es)
+            offs.append(len(edges))
+        ed = (A.FlowEdgeDesc * max(1, len(edges)))(*[A.FlowEdgeDesc(int(a), int(b), int(c)) for a, b, c in edges])
+        nn = A._arr(C.c_int, [g[0] for g in graphs])
+        off = A._arr(C.c_int64, offs)
+        fl = (C.c_int64 * max(1, len(edges)))()
+        val = (C.c_int64 * max(1, G))()
+        self._chk(self.lib.oserve_gpu_max_flow_batch(self.h, G, nn, off, ed, A._arr(C.c_int, sources),
+                                                     A._arr(C.c_int, sinks), fl, val))
+        return [(val[g], list(fl[offs[g]:offs[g + 1]])) for g in range(G)]
+
+    def flow_assign_batch(self, n: np.ndarray, e: np.ndarray, lam: np.ndarray, edge_flows: bool = False):
+        """build_network + max_flow + extract_assignment per instance [count][R][J]."""
+        n = np.ascontiguousarray(n, dtype=np.int64)
+        e = np.ascontiguousarray(e, dtype=np.int64)
+        lam = np.ascontiguousarray(lam, dtype=np.int64)
+        cnt, R, J = n.shape
+        m = J + 2 * R * J + 2 * R
+        x = np.zeros((cnt, R, J), np.int64)
+        obj, val = np.zeros(cnt, np.int64), np.zeros(cnt, np.int64)
+        fl = np.zeros((cnt, m), np.int64) if edge_flows else None
+        p = C.c_int64
+        self._chk(self.lib.oserve_gpu_flow_assign_batch(
+            self.h, cnt, R, J, _np_ptr(n, p), _np_ptr(e, p), _np_ptr(lam, p), _np_ptr(x, p), _np_ptr(obj, p),
+            _np_ptr(val, p), _np_ptr(fl, p) if fl is not None else None))
+        return x, obj, val, fl
+
+    def extract_assignment_batch(self, n: np.ndarray, e: np.ndarray, lam: np.ndarray, edge_flow: np.ndarray):
+        n = np.ascontiguousarray(n, dtype=np.int64)
+        e = np.ascontiguousarray(e, dtype=np.int64)
+        lam = np.ascontiguousarray(lam, dtype=np.int64)
+        fl = np.ascontiguousarray(edge_flow, dtype=np.int64)
+        cnt, R, J = n.shape
+        x = np.zeros((cnt, R, J), np.int64)
+        obj = np.zeros(cnt, np.int64)
+        p = C.c_int64
+        self._chk(self.lib.oserve_gpu_extract_assignment_batch(
+            self.h, cnt, R, J, _np_ptr(n, p), _np_ptr(e, p), _np_ptr(lam, p), _np_ptr(fl, p), _np_ptr(x, p),
+            _np_ptr(obj, p)))
+        return x, obj
+
+    def solve_fractional_batch(self, n: np.ndarray, e: np.ndarray, lam: np.ndarray):
+        n = np.ascontiguousarray(n, dtype=np.int64)
+        e = np.ascontiguousarray(e, dtype=np.int64)
+        lam = np.ascontiguousarray(lam, dtype=np.int64)
+        cnt, R, J = n.shape
+        f = np.zeros((cnt, R, J), np.float64)
+        obj = np.zeros(cnt, np.float64)
+        p, d = C.c_int64, C.c_double
+        self._chk(self.lib.oserve_gpu_solve_fractional_batch(self.h, cnt, R, J, _np_ptr(n, p), _np_ptr(e, p),
+                                                             _np_ptr(lam, p), _np_ptr(f, d), _np_ptr(obj, d)))
+        return f, obj
 
     def kv_plan(self, inflight: Sequence[core.InflightRequest], threshold_tokens: int, src: core.Deployment,
                 dst: core.Deployment, headroom: float = 0.1, carry: Optional[core.SwitchPlan] = None) -> core.KvPlan:

@@ -89,6 +89,12 @@ struct DBuf {
         return p;
     }
     template <class T>
+    T *upload(const T *src, size_t n, cudaStream_t s) {
+        T *d = static_cast<T *>(get(n * sizeof(T)));
+        if (n) cuda_ok(h2d(d, src, n * sizeof(T), s), "H2D");
+        return d;
+    }
+    template <class T>
     T *upload(const std::vector<T> &v, cudaStream_t s) {
         T *d = static_cast<T *>(get(v.size() * sizeof(T)));
         if (!v.empty()) cuda_ok(h2d(d, v.data(), v.size() * sizeof(T), s), "H2D");
@@ -870,7 +876,7 @@ std::vector<int> deployment_shapes(oserve_gpu_ctx &c, const oserve_deployment &d
 void eval_lists(oserve_gpu_ctx &c, const std::vector<int32_t> &listR, const std::vector<int32_t> &listOff,
                 const std::vector<int32_t> &shapes, const std::vector<int64_t> *lam_per_plan, int rmax,
                 std::vector<int64_t> &obj, std::vector<int64_t> *x, std::vector<int64_t> *used,
-                const SolveParams &prm) {
+                const SolveParams &prm, std::vector<uint64_t> *aborted_out = nullptr) {
     cudaStream_t s = c.stream;
     const uint64_t n = listR.size();
     PlanSource src{};
@@ -918,6 +924,10 @@ void eval_lists(oserve_gpu_ctx &c, const std::vector<int32_t> &listR, const std:
             download(idx, ab, n_ab, s);
             cuda_ok(cudaStreamSynchronize(s), "sync");
             std::sort(idx.begin(), idx.end());
+            if (aborted_out) {
+                *aborted_out = idx;
+                idx.clear();
+            }
             for (uint64_t li : idx) {  // heuristic fallback, one plan per launch (rare)
                 PlanSource one = src;
                 one.first = li;
@@ -1917,68 +1927,98 @@ int oserve_gpu_plan_detail(oserve_gpu_ctx *ctx, const oserve_deployment *dep, in
     });
 }
 
+// Raw [count][R][J] rows staged as the shape tables of one call (K0b only).
+struct RawRows {
+    DBuf dn, de, dM, du, dc, dord, dol, dpp, dsc, dlat, dinv, drank;
+    ShapeTables t{};
+};
+
+void validate_raw(int count, int R, int J, const int64_t *n, const int64_t *lambda) {
+    if (J < 1 || J > OSERVE_MAX_CLASSES) fail(OSERVE_ERR_UNSUPPORTED, "classes must be in [1, 16]");
+    if (R < 1 || R > OSERVE_MAX_REPLICAS) fail(OSERVE_ERR_UNSUPPORTED, "replicas must be in [1, 128]");
+    const int64_t rows = static_cast<int64_t>(count) * R;
+    for (int64_t i = 0; i < rows * J; ++i) {
+        if (n[i] < 0) fail(OSERVE_ERR_INVALID_ARGUMENT, "normalize: negative capacity");
+    }
+    for (int64_t i = 0; i < static_cast<int64_t>(count); ++i) {
+        int64_t tot = 0;
+        for (int j = 0; j < J; ++j) {
+            if (lambda[i * J + j] < 0 || lambda[i * J + j] > 0x7fffffffll)
+                fail(OSERVE_ERR_UNSUPPORTED, "demand per class must be in [0, 2^31)");
+            tot += lambda[i * J + j];
+        }
+        if (tot > 0x7fffffffll) fail(OSERVE_ERR_UNSUPPORTED, "total demand must be < 2^31");
+    }
+}
+
+void stage_raw_rows(oserve_gpu_ctx &c, int64_t rows, int J, const int64_t *n, const int64_t *e, RawRows &rr) {
+    cudaStream_t s = c.stream;
+    ShapeTables &t = rr.t;
+    t.num_shapes = static_cast<int>(rows);
+    t.J = J;
+    t.n = static_cast<int64_t *>(rr.dn.get(sizeof(int64_t) * rows * J));
+    t.e = static_cast<int64_t *>(rr.de.get(sizeof(int64_t) * rows * J));
+    cuda_ok(h2d(t.n, n, sizeof(int64_t) * rows * J, s), "H2D");
+    cuda_ok(h2d(t.e, e, sizeof(int64_t) * rows * J, s), "H2D");
+    t.latency = static_cast<double *>(rr.dlat.get(8));
+    t.M = static_cast<int64_t *>(rr.dM.get(sizeof(int64_t) * rows));
+    t.unit = static_cast<int64_t *>(rr.du.get(sizeof(int64_t) * rows * J));
+    t.inv_unit = static_cast<double *>(rr.dinv.get(sizeof(double) * rows * J));
+    t.cap = static_cast<int32_t *>(rr.dc.get(sizeof(int32_t) * rows * J));
+    t.order = static_cast<uint8_t *>(rr.dord.get(rows * kMaxJ));
+    t.rank = static_cast<uint8_t *>(rr.drank.get(rows * kMaxJ));
+    t.olen = static_cast<uint8_t *>(rr.dol.get(rows));
+    t.scaled = static_cast<uint8_t *>(rr.dsc.get(rows));
+    t.pp = static_cast<uint8_t *>(rr.dpp.get(rows));
+    cuda_ok(cudaMemsetAsync(t.pp, 1, rows, s), "memset");
+    cuda_ok(launch_normalize_rows(t, s), "normalize kernel");
+    c.launches += 1;
+}
+
+// solve_assignment over the staged rows of instances `which` (each R rows);
+// aborted_out (when given) receives the local indices whose B&B blew the
+// node budget instead of running the heuristic fallback for them.
+void solve_staged(oserve_gpu_ctx &c, RawRows &rr, const std::vector<int> &which, int R, int J,
+                  const int64_t *lambda, std::vector<int64_t> &obj, std::vector<int64_t> &xs,
+                  std::vector<int64_t> &us, std::vector<uint64_t> *aborted_out) {
+    const int cnt = static_cast<int>(which.size());
+    std::vector<int32_t> listR(cnt, R), listOff(cnt), shapes(static_cast<size_t>(cnt) * R);
+    std::vector<int64_t> lam(static_cast<size_t>(cnt) * J);
+    for (int q = 0; q < cnt; ++q) {
+        listOff[q] = q * R;
+        for (int k = 0; k < R; ++k) shapes[static_cast<size_t>(q) * R + k] = which[q] * R + k;
+        for (int j = 0; j < J; ++j) lam[static_cast<size_t>(q) * J + j] = lambda[static_cast<int64_t>(which[q]) * J + j];
+    }
+    SolveParams prm = solve_params(c);
+    prm.J = J;
+    ShapeTables saved = c.tables;
+    c.tables = rr.t;
+    try {
+        eval_lists(c, listR, listOff, shapes, &lam, R, obj, &xs, &us, prm, aborted_out);
+    } catch (...) {
+        c.tables = saved;
+        throw;
+    }
+    c.tables = saved;
+}
+
 int oserve_gpu_solve_batch(oserve_gpu_ctx *ctx, int count, int R, int J, const int64_t *n, const int64_t *e,
                            const int64_t *lambda, int64_t *x, int64_t *objective, int64_t *M, int64_t *unit,
                            int64_t *used) {
     return guarded(ctx, [&] {
         if (count <= 0) return;
-        if (J < 1 || J > OSERVE_MAX_CLASSES) fail(OSERVE_ERR_UNSUPPORTED, "classes must be in [1, 16]");
-        if (R < 1 || R > OSERVE_MAX_REPLICAS) fail(OSERVE_ERR_UNSUPPORTED, "replicas must be in [1, 128]");
+        validate_raw(count, R, J, n, lambda);
         const int64_t rows = static_cast<int64_t>(count) * R;
-        for (int64_t i = 0; i < rows * J; ++i) {
-            if (n[i] < 0) fail(OSERVE_ERR_INVALID_ARGUMENT, "normalize: negative capacity");
-        }
-        for (int64_t i = 0; i < static_cast<int64_t>(count); ++i) {
-            int64_t tot = 0;
-            for (int j = 0; j < J; ++j) {
-                if (lambda[i * J + j] < 0 || lambda[i * J + j] > 0x7fffffffll)
-                    fail(OSERVE_ERR_UNSUPPORTED, "demand per class must be in [0, 2^31)");
-                tot += lambda[i * J + j];
-            }
-            if (tot > 0x7fffffffll) fail(OSERVE_ERR_UNSUPPORTED, "total demand must be < 2^31");
-        }
-        // Raw rows become the shape tables of this call (K0b only).
         cudaStream_t s = ctx->stream;
-        DBuf dn, de, dM, du, dc, dord, dol, dpp, dsc, dlat, dinv, drank;
-        ShapeTables t{};
-        t.num_shapes = static_cast<int>(rows);
-        t.J = J;
-        t.n = static_cast<int64_t *>(dn.get(sizeof(int64_t) * rows * J));
-        t.e = static_cast<int64_t *>(de.get(sizeof(int64_t) * rows * J));
-        cuda_ok(h2d(t.n, n, sizeof(int64_t) * rows * J, s), "H2D");
-        cuda_ok(h2d(t.e, e, sizeof(int64_t) * rows * J, s), "H2D");
-        t.latency = static_cast<double *>(dlat.get(8));
-        t.M = static_cast<int64_t *>(dM.get(sizeof(int64_t) * rows));
-        t.unit = static_cast<int64_t *>(du.get(sizeof(int64_t) * rows * J));
-        t.inv_unit = static_cast<double *>(dinv.get(sizeof(double) * rows * J));
-        t.cap = static_cast<int32_t *>(dc.get(sizeof(int32_t) * rows * J));
-        t.order = static_cast<uint8_t *>(dord.get(rows * kMaxJ));
-        t.rank = static_cast<uint8_t *>(drank.get(rows * kMaxJ));
-        t.olen = static_cast<uint8_t *>(dol.get(rows));
-        t.scaled = static_cast<uint8_t *>(dsc.get(rows));
-        t.pp = static_cast<uint8_t *>(dpp.get(rows));
-        cuda_ok(cudaMemsetAsync(t.pp, 1, rows, s), "memset");
-        cuda_ok(launch_normalize_rows(t, s), "normalize kernel");
-        ctx->launches += 1;
-        std::vector<int32_t> listR(count, R), listOff(count), shapes(rows);
-        for (int i = 0; i < count; ++i) listOff[i] = i * R;
-        std::iota(shapes.begin(), shapes.end(), 0);
-        std::vector<int64_t> lam(lambda, lambda + static_cast<int64_t>(count) * J);
-        SolveParams prm = solve_params(*ctx);
-        prm.J = J;
-        ShapeTables saved = ctx->tables;
-        ctx->tables = t;
+        RawRows rr;
+        stage_raw_rows(*ctx, rows, J, n, e, rr);
+        std::vector<int> all(count);
+        std::iota(all.begin(), all.end(), 0);
         std::vector<int64_t> obj, xs, us;
-        try {
-            eval_lists(*ctx, listR, listOff, shapes, &lam, R, obj, &xs, &us, prm);
-        } catch (...) {
-            ctx->tables = saved;
-            throw;
-        }
-        ctx->tables = saved;
+        solve_staged(*ctx, rr, all, R, J, lambda, obj, xs, us, nullptr);
         std::vector<int64_t> hM, hu;
-        download(hM, t.M, rows, s);
-        download(hu, t.unit, rows * J, s);
+        download(hM, rr.t.M, rows, s);
+        download(hu, rr.t.unit, rows * J, s);
         cuda_ok(cudaStreamSynchronize(s), "sync");
         for (int i = 0; i < count; ++i) {
             if (objective) objective[i] = obj[i];
@@ -1991,6 +2031,195 @@ int oserve_gpu_solve_batch(oserve_gpu_ctx *ctx, int count, int R, int J, const i
                 if (M) M[row] = hM[row];
                 if (used) used[row] = us[row];
             }
+        }
+    });
+}
+
+namespace {
+int flow_assign_impl(oserve_gpu_ctx *ctx, int count, int R, int J, const int64_t *n, const int64_t *e,
+                     const int64_t *lambda, const int64_t *flow_in, int64_t *x, int64_t *objective,
+                     int64_t *flow_value, int64_t *edge_flow) {
+    return guarded(ctx, [&] {
+        if (count <= 0) return;
+        validate_raw(count, R, J, n, lambda);
+        const int64_t rows = static_cast<int64_t>(count) * R;
+        cudaStream_t s = ctx->stream;
+        RawRows rr;
+        stage_raw_rows(*ctx, rows, J, n, e, rr);
+        // K6b: network, push-relabel, rounded chain flows, warm greedy + exchange
+        size_t n32 = 0, n64 = 0, n8 = 0;
+        flow_assign_workspace(R, J, count, &n32, &n64, &n8);
+        const int m = J + 2 * R * J + 2 * R;
+        DBuf w32, w64, w8, dlam, dx, dobj, dval, dflow, dst;
+        FlowAssignBatch fb{};
+        fb.count = count;
+        fb.R = R;
+        fb.J = J;
+        fb.lambda = dlam.upload(lambda, static_cast<size_t>(count) * J, s);
+        fb.ws_i32 = static_cast<int32_t *>(w32.get(sizeof(int32_t) * n32));
+        fb.ws_i64 = static_cast<int64_t *>(w64.get(sizeof(int64_t) * n64));
+        fb.ws_u8 = static_cast<uint8_t *>(w8.get(n8));
+        fb.x = static_cast<int64_t *>(dx.get(sizeof(int64_t) * rows * J));
+        fb.objective = static_cast<int64_t *>(dobj.get(sizeof(int64_t) * count));
+        fb.value = static_cast<int64_t *>(dval.get(sizeof(int64_t) * count));
+        fb.edge_flow = edge_flow ? static_cast<int64_t *>(dflow.get(sizeof(int64_t) * count * m)) : nullptr;
+        fb.status = static_cast<int32_t *>(dst.get(sizeof(int32_t) * count));
+        DBuf dfin;
+        if (flow_in) fb.flow_in = dfin.upload(flow_in, static_cast<size_t>(count) * m, s);
+        cuda_ok(launch_flow_assign(rr.t, fb, s, &ctx->launches), "flow assign kernel");
+        std::vector<int64_t> hx, hobj, hval, hflow;
+        std::vector<int32_t> hst;
+        download(hx, fb.x, rows * J, s);
+        download(hobj, fb.objective, count, s);
+        download(hval, fb.value, count, s);
+        download(hst, fb.status, count, s);
+        if (edge_flow) download(hflow, fb.edge_flow, static_cast<size_t>(count) * m, s);
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+        for (int i = 0; i < count; ++i)
+            if (hst[i] != 0) fail(OSERVE_ERR_INVALID_ARGUMENT, "max_flow: negative capacity");
+        // solve_instance: the exact path ignores the warm start unless its budget blows
+        std::vector<int> exact;
+        for (int i = 0; i < count; ++i) {
+            int64_t tot = 0;
+            for (int j = 0; j < J; ++j) tot += lambda[static_cast<int64_t>(i) * J + j];
+            if (tot <= ctx->opts.exact_demand_limit && static_cast<int64_t>(R) * J <= ctx->opts.exact_cell_limit)
+                exact.push_back(i);
+        }
+        if (!exact.empty()) {
+            std::vector<int64_t> obj, xs, us;
+            std::vector<uint64_t> aborted;
+            solve_staged(*ctx, rr, exact, R, J, lambda, obj, xs, us, &aborted);
+            std::set<uint64_t> ab(aborted.begin(), aborted.end());
+            for (size_t q = 0; q < exact.size(); ++q) {
+                if (ab.count(q)) continue;
+                const int i = exact[q];
+                hobj[i] = obj[q];
+                std::copy(xs.begin() + static_cast<int64_t>(q) * R * J, xs.begin() + static_cast<int64_t>(q + 1) * R * J,
+                          hx.begin() + static_cast<int64_t>(i) * R * J);
+            }
+        }
+        std::copy(hx.begin(), hx.end(), x);
+        std::copy(hobj.begin(), hobj.end(), objective);
+        if (flow_value) std::copy(hval.begin(), hval.end(), flow_value);
+        if (edge_flow) std::copy(hflow.begin(), hflow.end(), edge_flow);
+    });
+}
+}  // namespace
+
+int oserve_gpu_flow_assign_batch(oserve_gpu_ctx *ctx, int count, int R, int J, const int64_t *n, const int64_t *e,
+                                 const int64_t *lambda, int64_t *x, int64_t *objective, int64_t *flow_value,
+                                 int64_t *edge_flow) {
+    return flow_assign_impl(ctx, count, R, J, n, e, lambda, nullptr, x, objective, flow_value, edge_flow);
+}
+
+int oserve_gpu_extract_assignment_batch(oserve_gpu_ctx *ctx, int count, int R, int J, const int64_t *n,
+                                        const int64_t *e, const int64_t *lambda, const int64_t *edge_flow,
+                                        int64_t *x, int64_t *objective) {
+    if (!edge_flow) return OSERVE_ERR_INVALID_ARGUMENT;
+    return flow_assign_impl(ctx, count, R, J, n, e, lambda, edge_flow, x, objective, nullptr, nullptr);
+}
+
+int oserve_gpu_max_flow_batch(oserve_gpu_ctx *ctx, int count, const int *num_nodes, const int64_t *edge_offset,
+                              const oserve_flow_edge *edges, const int *source, const int *sink, int64_t *flow,
+                              int64_t *value) {
+    return guarded(ctx, [&] {
+        if (count <= 0) return;
+        std::vector<int64_t> node_off(count + 1, 0), eoff(edge_offset, edge_offset + count + 1);
+        for (int g = 0; g < count; ++g) {
+            const int nn = num_nodes[g];
+            if (source[g] < 0 || source[g] >= nn || sink[g] < 0 || sink[g] >= nn || source[g] == sink[g])
+                fail(OSERVE_ERR_INVALID_ARGUMENT, "max_flow: bad source/sink");
+            if (eoff[g + 1] < eoff[g]) fail(OSERVE_ERR_INVALID_ARGUMENT, "max_flow: edge offsets must not decrease");
+            if (eoff[g + 1] - eoff[g] > (int64_t{1} << 29)) fail(OSERVE_ERR_UNSUPPORTED, "max_flow: too many edges");
+            for (int64_t i = eoff[g]; i < eoff[g + 1]; ++i) {
+                if (edges[i].from < 0 || edges[i].from >= nn || edges[i].to < 0 || edges[i].to >= nn)
+                    fail(OSERVE_ERR_INVALID_ARGUMENT, "max_flow: edge endpoint out of range");
+                if (edges[i].cap < 0) fail(OSERVE_ERR_INVALID_ARGUMENT, "max_flow: negative capacity");
+            }
+            node_off[g + 1] = node_off[g] + nn;
+        }
+        const int64_t E = eoff[count] - eoff[0], N = node_off[count];
+        if (eoff[0] != 0) {
+            for (auto &v : eoff) v -= edge_offset[0];
+        }
+        std::vector<int32_t> from(E), to(E), nn(num_nodes, num_nodes + count), src(source, source + count),
+            snk(sink, sink + count);
+        std::vector<int64_t> cap(E);
+        for (int64_t i = 0; i < E; ++i) {
+            from[i] = edges[edge_offset[0] + i].from;
+            to[i] = edges[edge_offset[0] + i].to;
+            cap[i] = edges[edge_offset[0] + i].cap;
+        }
+        cudaStream_t s = ctx->stream;
+        DBuf b[20];
+        MaxFlowBatch mb{};
+        mb.count = count;
+        mb.num_nodes = b[0].upload(nn, s);
+        mb.edge_off = b[1].upload(eoff, s);
+        mb.node_off = b[2].upload(node_off, s);
+        mb.from = b[3].upload(from, s);
+        mb.to = b[4].upload(to, s);
+        mb.cap = b[5].upload(cap, s);
+        mb.source = b[6].upload(src, s);
+        mb.sink = b[7].upload(snk, s);
+        mb.res = static_cast<int64_t *>(b[8].get(sizeof(int64_t) * 2 * E));
+        mb.excess = static_cast<int64_t *>(b[9].get(sizeof(int64_t) * N));
+        mb.arc_to = static_cast<int32_t *>(b[10].get(sizeof(int32_t) * 2 * E));
+        mb.adj = static_cast<int32_t *>(b[11].get(sizeof(int32_t) * 2 * E));
+        mb.adj_off = static_cast<int32_t *>(b[12].get(sizeof(int32_t) * (N + count)));
+        mb.height = static_cast<int32_t *>(b[13].get(sizeof(int32_t) * N));
+        mb.cur = static_cast<int32_t *>(b[14].get(sizeof(int32_t) * N));
+        mb.fifo = static_cast<int32_t *>(b[15].get(sizeof(int32_t) * N));
+        mb.active = static_cast<uint8_t *>(b[16].get(N));
+        mb.flow = static_cast<int64_t *>(b[17].get(sizeof(int64_t) * E));
+        mb.value = static_cast<int64_t *>(b[18].get(sizeof(int64_t) * count));
+        mb.status = static_cast<int32_t *>(b[19].get(sizeof(int32_t) * count));
+        cuda_ok(launch_max_flow(mb, s, &ctx->launches), "max flow kernel");
+        std::vector<int64_t> hf, hv;
+        download(hf, mb.flow, E, s);
+        download(hv, mb.value, count, s);
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+        std::copy(hf.begin(), hf.end(), flow);
+        std::copy(hv.begin(), hv.end(), value);
+    });
+}
+
+int oserve_gpu_solve_fractional_batch(oserve_gpu_ctx *ctx, int count, int R, int J, const int64_t *n,
+                                      const int64_t *e, const int64_t *lambda, double *f, double *objective) {
+    return guarded(ctx, [&] {
+        if (count <= 0) return;
+        if (R < 1 || J < 1) fail(OSERVE_ERR_INVALID_ARGUMENT, "solve_fractional: empty instance");
+        const size_t per = simplex_tableau_doubles(R, J) * sizeof(double);
+        const size_t budget = size_t{1} << 31;
+        if (per > budget) fail(OSERVE_ERR_UNSUPPORTED, "solve_fractional: tableau exceeds 2 GiB");
+        const int chunk = static_cast<int>(std::min<size_t>(count, std::max<size_t>(1, budget / per)));
+        const int nv = R * J;
+        cudaStream_t s = ctx->stream;
+        DBuf dn, de, dl, dt, df, dobj, dst;
+        for (int c0 = 0; c0 < count; c0 += chunk) {
+            const int cn = std::min(chunk, count - c0);
+            LpBatch lb{};
+            lb.count = cn;
+            lb.R = R;
+            lb.J = J;
+            lb.n = dn.upload(n + static_cast<int64_t>(c0) * nv, static_cast<size_t>(cn) * nv, s);
+            lb.e = de.upload(e + static_cast<int64_t>(c0) * nv, static_cast<size_t>(cn) * nv, s);
+            lb.lambda = dl.upload(lambda + static_cast<int64_t>(c0) * J, static_cast<size_t>(cn) * J, s);
+            lb.tab = static_cast<double *>(dt.get(per * cn));
+            lb.f = static_cast<double *>(df.get(sizeof(double) * cn * nv));
+            lb.objective = static_cast<double *>(dobj.get(sizeof(double) * cn));
+            lb.status = static_cast<int32_t *>(dst.get(sizeof(int32_t) * cn));
+            cuda_ok(launch_simplex(lb, s, &ctx->launches), "simplex kernel");
+            std::vector<double> hf, ho;
+            std::vector<int32_t> hs;
+            download(hf, lb.f, static_cast<size_t>(cn) * nv, s);
+            download(ho, lb.objective, cn, s);
+            download(hs, lb.status, cn, s);
+            cuda_ok(cudaStreamSynchronize(s), "sync");
+            for (int i = 0; i < cn; ++i)
+                if (hs[i] != 0) fail(OSERVE_ERR_LOGIC, "solve_fractional: unbounded LP (malformed instance)");
+            std::copy(hf.begin(), hf.end(), f + static_cast<int64_t>(c0) * nv);
+            std::copy(ho.begin(), ho.end(), objective + c0);
         }
     });
 }

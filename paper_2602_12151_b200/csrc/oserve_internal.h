@@ -213,6 +213,52 @@ struct KvPlanIn {
 };
 int launch_kv_plan(const KvPlanIn &in, void *stream, uint64_t *launches);
 
+// K6a: max_flow over a ragged batch of graphs (packed per graph).
+struct MaxFlowBatch {
+    int count;
+    const int32_t *num_nodes;  // [count]
+    const int64_t *edge_off;   // [count+1]
+    const int64_t *node_off;   // [count+1] (adj_off uses node_off[g] + g)
+    const int32_t *from, *to;
+    const int64_t *cap;
+    const int32_t *source, *sink;
+    int64_t *res, *excess;
+    int32_t *arc_to, *adj, *adj_off, *height, *cur, *fifo;
+    uint8_t *active;
+    int64_t *flow, *value;
+    int32_t *status;
+};
+int launch_max_flow(const MaxFlowBatch &b, void *stream, uint64_t *launches);
+
+// K6b: build_network + max_flow + extract_assignment over equal-shape
+// instances whose rows are already normalised in a ShapeTables (rows i*R+k).
+struct FlowAssignBatch {
+    int count, R, J;
+    const int64_t *lambda;  // [count][J]
+    int32_t *ws_i32;
+    int64_t *ws_i64;
+    uint8_t *ws_u8;
+    int64_t *x;             // [count][R][J]
+    int64_t *objective, *value;
+    int64_t *edge_flow;     // [count][edges] or null
+    const int64_t *flow_in; // [count][edges]: given flows (extract_assignment only), or null
+    int32_t *status;
+};
+struct ShapeTables;
+int launch_flow_assign(const ShapeTables &t, const FlowAssignBatch &b, void *stream, uint64_t *launches);
+void flow_assign_workspace(int R, int J, int64_t count, size_t *i32, size_t *i64, size_t *u8);
+
+// K7: solve_fractional's dense simplex, CTA per instance.
+struct LpBatch {
+    int count, R, J;
+    const int64_t *n, *e, *lambda;
+    double *tab;  // [count][(nrows+1)*ncols]
+    double *f, *objective;
+    int32_t *status;
+};
+int launch_simplex(const LpBatch &b, void *stream, uint64_t *launches);
+size_t simplex_tableau_doubles(int R, int J);
+
 // Sort n u64 keys ascending on the device (CUB radix sort); temp is reused.
 int sort_keys(uint64_t *keys, uint64_t *tmp_keys, int n, void **temp, size_t *temp_bytes, void *stream);
 // Groups whose list dropped a key better than `kth` (0 => the lists are exact).
