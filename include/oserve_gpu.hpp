@@ -241,6 +241,70 @@ inline oserve::flow::LowerLevel solve_assignment(const oserve::cost::CapacityTab
     return out;
 }
 
+namespace detail {
+inline std::unique_ptr<Context> scratch_context() {
+    oserve::ClusterSpec cl;
+    cl.machines.push_back({"m0", {0}, 1});
+    cl.intra_bw = cl.inter_bw = 1.0;
+    return std::make_unique<Context>(cl, oserve::ModelSpec{}, oserve::cost::ProfileParams{});
+}
+}  // namespace detail
+
+// oserve::flow::max_flow (flowassign.cpp:67-147) on the device (K6a).
+inline oserve::flow::FlowResult max_flow(const oserve::flow::Graph &g, int source, int sink) {
+    auto c = detail::scratch_context();
+    std::vector<oserve_flow_edge> ed;
+    for (const auto &e : g.edges) ed.push_back({e.from, e.to, e.cap});
+    const int64_t off[2] = {0, static_cast<int64_t>(ed.size())};
+    oserve::flow::FlowResult out;
+    out.flow.resize(ed.size());
+    check(oserve_gpu_max_flow_batch(c->get(), 1, &g.num_nodes, off, ed.data(), &source, &sink, out.flow.data(),
+                                    &out.value),
+          c->get());
+    return out;
+}
+
+// oserve::flow::extract_assignment (flowassign.cpp:505-519) on the device (K6b).
+inline oserve::flow::AssignmentMatrix extract_assignment(const oserve::flow::FlowNetwork &net,
+                                                         const oserve::flow::FlowResult &flow,
+                                                         const oserve::flow::SolveOptions &opts = {}) {
+    auto c = detail::scratch_context();
+    oserve_solve_options so{opts.exact_demand_limit, opts.exact_cell_limit, opts.node_budget};
+    check(oserve_gpu_set_solve_options(c->get(), &so), c->get());
+    std::vector<int64_t> n, e, x(static_cast<size_t>(net.R) * net.J);
+    for (int k = 0; k < net.R; ++k) {
+        n.insert(n.end(), net.n[k].begin(), net.n[k].end());
+        e.insert(e.end(), net.e[k].begin(), net.e[k].end());
+    }
+    int64_t obj = 0;
+    check(oserve_gpu_extract_assignment_batch(c->get(), 1, net.R, net.J, n.data(), e.data(), net.lambda.data(),
+                                              flow.flow.data(), x.data(), &obj),
+          c->get());
+    oserve::flow::AssignmentMatrix out;
+    out.objective = obj;
+    for (int k = 0; k < net.R; ++k) out.x.emplace_back(x.begin() + k * net.J, x.begin() + (k + 1) * net.J);
+    return out;
+}
+
+// oserve::flow::solve_fractional (flowassign.cpp:559-645) on the device (K7).
+inline oserve::flow::FractionalSolution solve_fractional(const oserve::cost::CapacityTable &table,
+                                                         const std::vector<int64_t> &lambda) {
+    auto c = detail::scratch_context();
+    const int R = table.replicas(), J = table.types();
+    std::vector<int64_t> n, e;
+    for (int k = 0; k < R; ++k) {
+        n.insert(n.end(), table.n[k].begin(), table.n[k].end());
+        e.insert(e.end(), table.e[k].begin(), table.e[k].end());
+    }
+    std::vector<double> f(static_cast<size_t>(R) * J);
+    oserve::flow::FractionalSolution out;
+    check(oserve_gpu_solve_fractional_batch(c->get(), 1, R, J, n.data(), e.data(), lambda.data(), f.data(),
+                                            &out.objective),
+          c->get());
+    for (int k = 0; k < R; ++k) out.f.emplace_back(f.begin() + k * J, f.begin() + (k + 1) * J);
+    return out;
+}
+
 }  // namespace flow
 
 namespace switchplan {

@@ -92,6 +92,16 @@ int main() {
         auto a = flow::solve_assignment(t, lam);
         auto b = oserve_gpu::flow::solve_assignment(t, lam);
         EXPECT(a.assignment == b.assignment && a.used == b.used, "flow::solve_assignment (random, exact path)");
+        // flow-network formulation: max_flow, extract_assignment, solve_fractional
+        auto net = flow::build_network(TraceSpan{0, lam}, t);
+        auto f1 = flow::max_flow(net.graph, net.source(), net.sink());
+        auto f2 = oserve_gpu::flow::max_flow(net.graph, net.source(), net.sink());
+        EXPECT(f1.value == f2.value && f1.flow == f2.flow, "flow::max_flow");
+        EXPECT(flow::extract_assignment(net, f1) == oserve_gpu::flow::extract_assignment(net, f1),
+               "flow::extract_assignment");
+        auto l1 = flow::solve_fractional(t, lam);
+        auto l2 = oserve_gpu::flow::solve_fractional(t, lam);
+        EXPECT(l1.f == l2.f && l1.objective == l2.objective, "flow::solve_fractional");
     }
     // switching on a 2x4 cluster (SPEC.md acceptance #9 fixture)
     ClusterSpec c24 = cluster(2, 4);
