@@ -193,6 +193,7 @@ def main():
     json.dump(sw, open(os.path.join(OUT, "switch.json"), "w"))
     gen_f3(ref)
     gen_f4(ref)
+    gen_exact_budget(ref, Oracle("port"))
     print("golden fixtures written to", OUT)
 
 
@@ -262,6 +263,25 @@ def gen_f4(ref):
     json.dump({"graphs": graphs, "instances": inst, "lp": lps, "dot": dots}, open(os.path.join(OUT, "flow.json"), "w"))
 
 
+def gen_exact_budget(ref, port):
+    """B&B abort boundary: budgets N-1 / N around the reference's node count N
+    (counted by the restatement, checked here against the reference)."""
+    cases = []
+    for n, e, lam in random_instances(31, 400, 6, 3, 130):
+        R, J = len(n), len(lam)
+        if R * J > 20 or sum(lam) > 400:
+            continue
+        N = port.solve_assignment(n, e, lam).work
+        if N < 50:
+            continue
+        row = {"n": n, "e": e, "lambda": lam, "nodes": N, "budgets": []}
+        for b in (N - 1, N, N // 2):
+            ll = ref.solve_assignment(n, e, lam, core.SolveOptions(400, 20, b))
+            row["budgets"].append({"budget": b, "x": ll.assignment.x, "objective": ll.assignment.objective})
+        cases.append(row)
+    json.dump(cases, open(os.path.join(OUT, "exact_budget.json"), "w"))
+
+
 def gen_f3(ref):
     json.dump(kv_cases(ref), open(os.path.join(OUT, "kv_plan.json"), "w"))
     w = workloads.load("cfg4")
@@ -274,5 +294,7 @@ if __name__ == "__main__":
         gen_f3(Oracle("ref"))
     elif sys.argv[1:] == ["f4"]:
         gen_f4(Oracle("ref"))
+    elif sys.argv[1:] == ["exact"]:
+        gen_exact_budget(Oracle("ref"), Oracle("port"))
     else:
         main()

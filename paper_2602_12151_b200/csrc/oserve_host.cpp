@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -676,12 +678,11 @@ void for_each_k1_launch(oserve_gpu_ctx &c, Space &sp, F &&fn) {
     fn(src, sp.rmax);
 }
 
-// Exact (B&B) path for the plans of `src` that take it: the split kernel
-// (kExactSlots threads per plan) + combine, then the sequential kernel for any
-// plan whose node count could not be certified.  Plans whose B&B blows the
-// budget are appended to eo.aborted (the caller reruns them through K1).
-constexpr uint64_t kSplitMaxPlans = 16384;
-
+// Exact (B&B) path for the plans of `src` that take it: the frontier-parallel
+// passes (k_exact_plan / k_exact_task), then the sequential kernel for plans
+// whose tree could not be cut within the task caps or whose phase A hit the
+// budget.  Plans whose B&B blows the budget are appended to eo.aborted (the
+// caller reruns them through K1).
 void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key, const PlanSource &src0,
                const PlanOutputs &eo, const SolveParams &prm, const Space *sp) {
     cudaStream_t s = c.stream;
@@ -690,21 +691,12 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
     if (sp && src.mode == 0) {
         // restrict to this shard's exact-path plans
         std::vector<uint64_t> ranks;
-        bool small = true;
-        for (size_t p = 0; p < sp->parts.size() && small; ++p) {
+        for (size_t p = 0; p < sp->parts.size(); ++p) {
             if (!sp->exact[p]) continue;
             for (uint64_t g = sp->prefix[p]; g < sp->prefix[p] + sp->parts[p].count; ++g) {
                 if ((g / c.chunk) % static_cast<uint64_t>(c.world) != static_cast<uint64_t>(c.rank)) continue;
                 ranks.push_back(g);
-                if (ranks.size() > kSplitMaxPlans) {
-                    small = false;
-                    break;
-                }
             }
-        }
-        if (!small) {  // too many exact plans for the split buffers: sequential kernel
-            cuda_ok(launch_plan_exact(c.tables, view, key, src, eo, prm, c.sm_count, s, &c.launches), "exact kernel");
-            return;
         }
         src.mode = 1;
         src.first = 0;
@@ -712,65 +704,197 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
         src.ranks = d_exact_ranks.upload(ranks, s);
         if (ranks.empty()) return;
     }
-    if (src.count > kSplitMaxPlans) {
-        cuda_ok(launch_plan_exact(c.tables, view, key, src, eo, prm, c.sm_count, s, &c.launches), "exact kernel");
-        return;
+    if (src.count == 0) return;
+    const uint64_t P = src.count;
+    DBuf b_depth, b_nt, b_off, b_top, b_opt, b_ist, b_state, b_bx, b_run;
+    ExactTasks et{};
+    et.depth = static_cast<int32_t *>(b_depth.get(sizeof(int32_t) * P));
+    et.ntask = static_cast<uint64_t *>(b_nt.get(sizeof(uint64_t) * P));
+    et.toff = static_cast<uint64_t *>(b_off.get(sizeof(uint64_t) * P));
+    et.top_nodes = static_cast<int64_t *>(b_top.get(sizeof(int64_t) * P));
+    et.opt = static_cast<int64_t *>(b_opt.get(sizeof(int64_t) * P));
+    et.istar = static_cast<int64_t *>(b_ist.get(sizeof(int64_t) * P));
+    et.state = static_cast<uint8_t *>(b_state.get(P));
+    et.bx = static_cast<int32_t *>(b_bx.get(sizeof(int32_t) * P * kMaxExactCells));
+    et.running = static_cast<unsigned long long *>(b_run.get(sizeof(unsigned long long) * P));
+    // ~2^21 tasks in flight at most; at least a few thousand per plan when few plans
+    const uint64_t budget_tasks = uint64_t{1} << 21;
+    static const uint64_t target_env = [] {
+        const char *e = getenv("OSERVE_EXACT_TARGET");
+        return e ? static_cast<uint64_t>(atoll(e)) : 0ull;
+    }();
+    et.target = target_env ? target_env : std::max<uint64_t>(64, std::min<uint64_t>(4096, budget_tasks / P));
+    et.max_tasks = et.target * 8;
+    cuda_ok(launch_exact_plan_pass(0, c.tables, view, key, src, eo, prm, et, c.sm_count, s, &c.launches),
+            "exact plan pass 0");
+    std::vector<uint64_t> nt;
+    std::vector<uint8_t> state;
+    download(nt, et.ntask, P, s);
+    download(state, et.state, P, s);
+    cuda_ok(cudaStreamSynchronize(s), "sync");
+    std::vector<uint64_t> off(P);
+    uint64_t total = 0;
+    for (uint64_t i = 0; i < P; ++i) {
+        if (state[i] == 1 && total + nt[i] > 4 * budget_tasks) state[i] = 2;  // task buffers full
+        off[i] = total;
+        if (state[i] == 1) total += nt[i];
     }
-    const uint64_t nt = src.count * kExactSlots;
-    DBuf b_state, b_best, b_bv, b_nodes, b_pre, b_x, b_redo, b_redo_n, b_p1s, b_p1b, b_p1n, b_p1x;
-    ExactSplit es{};
-    es.p1_state = static_cast<uint8_t *>(b_p1s.get(src.count));
-    es.p1_best = static_cast<int64_t *>(b_p1b.get(sizeof(int64_t) * src.count));
-    es.p1_nodes = static_cast<uint64_t *>(b_p1n.get(sizeof(uint64_t) * src.count));
-    es.p1_x = static_cast<int32_t *>(b_p1x.get(sizeof(int32_t) * src.count * kMaxExactCells));
-    es.state = static_cast<uint8_t *>(b_state.get(nt));
-    es.best = static_cast<int64_t *>(b_best.get(sizeof(int64_t) * nt));
-    es.best_v = static_cast<int64_t *>(b_bv.get(sizeof(int64_t) * nt));
-    es.nodes = static_cast<uint64_t *>(b_nodes.get(sizeof(uint64_t) * nt));
-    es.prefix = static_cast<uint64_t *>(b_pre.get(sizeof(uint64_t) * nt));
-    es.x = static_cast<int32_t *>(b_x.get(sizeof(int32_t) * nt * kMaxExactCells));
-    es.redo = static_cast<uint64_t *>(b_redo.get(sizeof(uint64_t) * src.count));
-    es.redo_n = static_cast<unsigned *>(b_redo_n.get(sizeof(unsigned)));
-    cuda_ok(cudaMemsetAsync(es.redo_n, 0, sizeof(unsigned), s), "memset");
-    cuda_ok(launch_plan_exact(c.tables, view, key, src, eo, prm, c.sm_count, s, &c.launches, &es),
-            "exact kernel (split)");
-    unsigned nredo = 0;
-    cuda_ok(d2h(&nredo, es.redo_n, sizeof(unsigned), s), "D2H");
-    cuda_ok(cudaStreamSynchronize(s), "sync");
-    if (!nredo) return;
+    cuda_ok(h2d(et.toff, off.data(), sizeof(uint64_t) * P, s), "H2D");
+    cuda_ok(h2d(et.state, state.data(), P, s), "H2D");
+    // per-task arrays, double-buffered for the splitting rounds
+    struct TaskBufs {
+        DBuf plan, td, path, g, lb, m, inc, vis, nodes, cap, done, nch;
+        void bind(ExactTasks &e, uint64_t n) {
+            e.plan = static_cast<uint32_t *>(plan.get(sizeof(uint32_t) * n));
+            e.tdepth = static_cast<uint8_t *>(td.get(n));
+            e.path = static_cast<int32_t *>(path.get(sizeof(int32_t) * n * kTaskDepthMax));
+            e.g = static_cast<int64_t *>(g.get(sizeof(int64_t) * n));
+            e.lb = static_cast<int64_t *>(lb.get(sizeof(int64_t) * n));
+            e.m = static_cast<int64_t *>(m.get(sizeof(int64_t) * n));
+            e.inc = static_cast<int64_t *>(inc.get(sizeof(int64_t) * n));
+            e.vis = static_cast<uint8_t *>(vis.get(n));
+            e.nodes = static_cast<int64_t *>(nodes.get(sizeof(int64_t) * n));
+            e.capped = static_cast<uint8_t *>(cap.get(n));
+            e.done = static_cast<uint8_t *>(done.get(n));
+            e.nchild = static_cast<uint32_t *>(nch.get(sizeof(uint32_t) * n));
+        }
+    };
+    TaskBufs bufs[2];
+    int cur = 0;
+    if (total) {
+        bufs[cur].bind(et, total);
+        static const bool dbg = getenv("OSERVE_DEBUG_EXACT") != nullptr;
+        auto lap = [&](const char *what) {
+            if (!dbg) return;
+            static auto t0 = std::chrono::steady_clock::now();
+            cuda_ok(cudaStreamSynchronize(s), "sync");
+            const auto t1 = std::chrono::steady_clock::now();
+            std::fprintf(stderr, "[exact] %-14s %8.1f ms  (plans %llu, tasks %llu)\n", what,
+                         std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                         static_cast<unsigned long long>(P), static_cast<unsigned long long>(total));
+            t0 = t1;
+        };
+        lap("pass0");
+        cuda_ok(launch_exact_plan_pass(1, c.tables, view, key, src, eo, prm, et, c.sm_count, s, &c.launches),
+                "exact plan pass 1");
+        lap("emit");
+        // Phase A in rounds: tasks over the round's node cap are split into
+        // their children (preorder kept) and rerun; the last round runs with
+        // the full budget.
+        constexpr int kRounds = 6;
+        constexpr int64_t kRoundCap = 1 << 15;
+        for (int round = 0;; ++round) {
+            const bool last = round == kRounds || total > (uint64_t{1} << 24);
+            et.phase_cap = last ? prm.node_budget : kRoundCap;
+            cuda_ok(launch_exact_task_pass(2, c.tables, view, src, prm, et, total, c.sm_count, s, &c.launches),
+                    "exact task pass 2");
+            cuda_ok(launch_exact_plan_pass(4, c.tables, view, key, src, eo, prm, et, c.sm_count, s, &c.launches),
+                    "exact plan pass 4");
+            cuda_ok(launch_exact_task_pass(0, c.tables, view, src, prm, et, total, c.sm_count, s, &c.launches),
+                    "exact task pass 0");
+            lap("phaseA round");
+            if (last) break;
+            cuda_ok(launch_exact_task_pass(3, c.tables, view, src, prm, et, total, c.sm_count, s, &c.launches),
+                    "exact task pass 3");
+            std::vector<uint32_t> nch;
+            download(nch, et.nchild, total, s);
+            cuda_ok(cudaStreamSynchronize(s), "sync");
+            std::vector<uint64_t> newoff(total + 1, 0);
+            for (uint64_t q = 0; q < total; ++q) newoff[q + 1] = newoff[q] + nch[q];
+            if (newoff[total] == total) break;  // nothing capped: phase A complete
+            const uint64_t ntot = newoff[total];
+            ExactTasks ne = et;
+            bufs[cur ^ 1].bind(ne, ntot);
+            DBuf d_off;
+            uint64_t *d_newoff = d_off.upload(newoff, s);
+            cuda_ok(launch_exact_split(c.tables, view, src, prm, et, ne, d_newoff, total, c.sm_count, s, &c.launches),
+                    "exact split");
+            for (uint64_t i = 0; i < P; ++i) {  // per-plan ranges in the new list
+                if (state[i] != 1) continue;
+                const uint64_t a0 = newoff[off[i]], a1 = newoff[off[i] + nt[i]];
+                off[i] = a0;
+                nt[i] = a1 - a0;
+            }
+            cuda_ok(h2d(et.toff, off.data(), sizeof(uint64_t) * P, s), "H2D");
+            cuda_ok(h2d(et.ntask, nt.data(), sizeof(uint64_t) * P, s), "H2D");
+            cuda_ok(cudaStreamSynchronize(s), "sync");
+            et = ne;
+            cur ^= 1;
+            total = ntot;
+        }
+        cuda_ok(launch_exact_plan_pass(2, c.tables, view, key, src, eo, prm, et, c.sm_count, s, &c.launches),
+                "exact plan pass 2");
+        lap("top replay");
+        cuda_ok(launch_exact_task_pass(1, c.tables, view, src, prm, et, total, c.sm_count, s, &c.launches),
+                "exact task pass 1");
+        lap("phaseB");
+        cuda_ok(launch_exact_plan_pass(3, c.tables, view, key, src, eo, prm, et, c.sm_count, s, &c.launches),
+                "exact plan pass 3");
+        lap("finish");
+        if (dbg) {
+            std::vector<int64_t> nodes;
+            std::vector<uint8_t> vis;
+            download(nodes, et.nodes, total, s);
+            download(vis, et.vis, total, s);
+            cuda_ok(cudaStreamSynchronize(s), "sync");
+            int64_t mx = 0, sum = 0, nv = 0;
+            for (uint64_t q = 0; q < total; ++q)
+                if (vis[q]) {
+                    mx = std::max(mx, nodes[q]);
+                    sum += nodes[q];
+                    ++nv;
+                }
+            std::fprintf(stderr, "[exact] tasks %llu visited %lld, phase-A nodes sum %lld max %lld\n",
+                         static_cast<unsigned long long>(total), static_cast<long long>(nv),
+                         static_cast<long long>(sum), static_cast<long long>(mx));
+        }
+    }
+    download(state, et.state, P, s);
+    cuda_ok(cudaStreamSynchronize(s), "sync");  // scratch buffers are freed on return
     std::vector<uint64_t> redo;
-    download(redo, es.redo, nredo, s);
-    cuda_ok(cudaStreamSynchronize(s), "sync");
+    for (uint64_t i = 0; i < P; ++i)
+        if (state[i] == 2) redo.push_back(i);
+    if (redo.empty()) return;
     if (src.mode == 2 || (src.mode == 0 && (eo.objective || eo.x))) {
-        // per-plan outputs (lists, or an identity-mapped rank range)
-        for (uint64_t li : redo) {  // rare: one sequential launch per uncertified plan
+        for (uint64_t li : redo) {  // per-plan outputs: one sequential launch per plan (rare)
             PlanSource one = src;
-            one.first = li;
+            one.first = src.first + li;
             one.count = 1;
             PlanOutputs o1 = eo;
-            if (eo.objective) o1.objective = eo.objective + (li - src.first);
-            if (eo.sum_pp) o1.sum_pp = eo.sum_pp + (li - src.first);
+            if (eo.objective) o1.objective = eo.objective + li;
+            if (eo.sum_pp) o1.sum_pp = eo.sum_pp + li;
             if (eo.x) {
-                o1.x = eo.x + (li - src.first) * eo.rmax * prm.J;
-                o1.used = eo.used + (li - src.first) * eo.rmax;
+                o1.x = eo.x + li * eo.rmax * prm.J;
+                o1.used = eo.used + li * eo.rmax;
             }
             cuda_ok(launch_plan_exact(c.tables, view, key, one, o1, prm, c.sm_count, s, &c.launches),
                     "exact kernel (sequential)");
         }
-        cuda_ok(cudaStreamSynchronize(s), "sync");  // scratch buffers are freed on return
     } else {
-        // space plans: outputs are keyed (argmin), no per-plan arrays
+        // rank sources: outputs are keyed (argmin); rerun the listed ranks
+        std::vector<uint64_t> ranks;
+        for (uint64_t li : redo) {
+            if (src.mode == 1) {
+                uint64_t r = 0;
+                cuda_ok(d2h(&r, src.ranks + src.first + li, sizeof(uint64_t), s), "D2H");
+                cuda_ok(cudaStreamSynchronize(s), "sync");
+                ranks.push_back(r);
+            } else {
+                ranks.push_back(src.first + li);
+            }
+        }
+        DBuf d_r;
         PlanSource rs{};
         rs.mode = 1;
-        rs.count = nredo;
-        rs.ranks = es.redo;
+        rs.count = ranks.size();
+        rs.ranks = d_r.upload(ranks, s);
         PlanOutputs o1 = eo;
         o1.objective = nullptr;
         o1.sum_pp = nullptr;
         cuda_ok(launch_plan_exact(c.tables, view, key, rs, o1, prm, c.sm_count, s, &c.launches),
                 "exact kernel (sequential)");
-        cuda_ok(cudaStreamSynchronize(s), "sync");
     }
+    cuda_ok(cudaStreamSynchronize(s), "sync");
 }
 
 // Launch K1 (+K4, + heuristic fallback for aborted B&B) over this shard of

@@ -116,24 +116,37 @@ struct PlanOutputs {
     uint64_t collect_thr;
 };
 
-// Split exact path: kExactSlots threads per plan (see k_plan_exact).
-constexpr int kExactSlots = 32;
-struct ExactSplit {
-    int phase;           // 1: first branch only; 2: remaining branches over slots
-    // phase 1, per plan: 0 not exact, 1 branched, 2 aborted, 3 no branching cell
-    uint8_t *p1_state;
-    int64_t *p1_best;
-    uint64_t *p1_nodes;  // prefix + first-branch nodes
-    int32_t *p1_x;       // [plans*kMaxExactCells]
-    // phase 2, per (plan, slot)
-    uint8_t *state;      // 0 idle, 1 done, 2 aborted
-    int64_t *best;
-    int64_t *best_v;     // first-level branch of the slot's best
-    uint64_t *nodes;     // nodes below the first branching cell
-    uint64_t *prefix;    // unused (kept for layout stability)
-    int32_t *x;          // [plans*slots*kMaxExactCells]
-    uint64_t *redo;      // plans to rerun sequentially (rank or list index)
-    unsigned int *redo_n;
+// Frontier-parallel exact path (see k_exact_plan in oserve_kernels.cu).  The
+// B&B tree of each plan is cut after its first `depth` branching decisions;
+// every frontier node is a task.
+constexpr int kTaskDepthMax = 24;  // initial cut <= 6; phase-A splitting goes deeper
+struct ExactTasks {
+    // per plan (src index)
+    int32_t *depth;       // chosen cut depth; -1: not an exact-path plan
+    uint64_t *ntask;      // tasks of the plan (pass 0)
+    uint64_t *toff;       // first task of the plan (host exclusive scan)
+    int64_t *top_nodes;   // visited nodes above the cut (pass 2)
+    int64_t *opt;         // optimum (pass 2)
+    int64_t *istar;       // task holding the first optimal leaf (pass 2)
+    uint8_t *state;       // 0 not exact, 1 frontier, 2 sequential fallback, 3 frontier + phase-B counts
+    unsigned long long *running;  // phase-B running node total (top + finished task nodes)
+    int32_t *bx;          // [plans][kMaxExactCells] first optimal leaf
+    int64_t phase_cap;    // phase-A node cap of this round (tasks above it are split)
+    // per task (preorder within each plan; plans contiguous)
+    uint32_t *plan;
+    uint8_t *tdepth;      // decisions on the path; bit 7: root is a leaf reached above the cut
+    int32_t *path;        // [tasks][kTaskDepthMax]
+    int64_t *g;           // greedy-dive leaf count of the task
+    int64_t *lb;          // lower bound of the incumbent entering the task (prefix max of g)
+    int64_t *m;           // max(best leaf in the subtree, lb)  (phase A)
+    int64_t *inc;         // exact incumbent entering the task (pass 2)
+    uint8_t *vis;         // task root visited by the sequential DFS (pass 2)
+    int64_t *nodes;       // phase A node count (an upper bound of the sequential count below the task)
+    uint8_t *capped;      // phase A exceeded its cap
+    uint8_t *done;        // phase A finished (m, nodes valid)
+    uint32_t *nchild;     // tasks this one becomes in the next round
+    uint64_t target;      // desired tasks per plan
+    uint64_t max_tasks;   // cap per plan
 };
 
 struct SolveParams {
@@ -156,7 +169,22 @@ int launch_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayou
 // Exact branch-and-bound path (thread per plan).
 int launch_plan_exact(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key, const PlanSource &src,
                       const PlanOutputs &out, const SolveParams &sp_params, int sm_count, void *stream,
-                      uint64_t *launches, const ExactSplit *split = nullptr);
+                      uint64_t *launches);
+// Frontier-parallel exact path: per-plan passes (0 count/choose depth, 1 emit
+// tasks, 4 lower bounds from the dives, 2 replay the top of the tree,
+// 3 finish/emit) and per-task passes (2 greedy dives, 0 phase A subtree
+// maxima, 1 phase B node counts + first optimal leaf).
+int launch_exact_plan_pass(int pass, const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key,
+                           const PlanSource &src, const PlanOutputs &out, const SolveParams &prm,
+                           const ExactTasks &et, int sm_count, void *stream, uint64_t *launches);
+int launch_exact_task_pass(int pass, const ShapeTables &t, const SpaceTables &sp, const PlanSource &src,
+                           const SolveParams &prm, const ExactTasks &et, uint64_t total_tasks, int sm_count,
+                           void *stream, uint64_t *launches);
+// Split capped tasks into their children: `nt` receives the new list at the
+// exclusive-scan offsets `newoff` of et.nchild.
+int launch_exact_split(const ShapeTables &t, const SpaceTables &sp, const PlanSource &src, const SolveParams &prm,
+                       const ExactTasks &et, const ExactTasks &nt, const uint64_t *newoff, uint64_t total_tasks,
+                       int sm_count, void *stream, uint64_t *launches);
 
 // Switching cost (K2).
 struct SwitchDeps {

@@ -987,143 +987,214 @@ __device__ __forceinline__ void exact_emit(const ShapeTables &t, const KeyLayout
     }
 }
 
-// Exact branch-and-bound (flowassign.cpp:296-369).  SPLIT = false: thread per
-// plan, the reference's DFS verbatim.  SPLIT = true: kExactSlots threads per
-// plan; at the first branching cell slot q explores the branches v = hi-q,
-// hi-q-S, ... (descending) with its own running best.  Each slot's best is <=
-// the sequential best at the same point, so it prunes a subset and counts a
-// superset of the sequential nodes; k_exact_combine takes the max (first
-// branch in DFS order on ties) and certifies "no abort" when the summed node
-// counts stay within the budget — else the plan reruns sequentially.
-template <bool SPLIT>
-__global__ void __launch_bounds__(128) k_plan_exact(ShapeTables t, SpaceTables sp, KeyLayout key, PlanSource src,
-                                                    PlanOutputs out, SolveParams prm, ExactSplit es) {
-    const int J = prm.J;
-    const int phase = SPLIT ? es.phase : 0;
-    const uint64_t ntask = phase == 2 ? src.count * kExactSlots : src.count;
-    for (uint64_t tix = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; tix < ntask;
-         tix += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint64_t i = phase == 2 ? tix / kExactSlots : tix;
-        const int slot = phase == 2 ? static_cast<int>(tix % kExactSlots) : 0;
-        if (phase == 2 && es.p1_state[i] != 1) {  // not exact, or phase 1 already decided it
-            es.state[tix] = 0;
+// Subtree DFS of the reference's ExactSolver::dfs (flowassign.cpp:330-369)
+// from the node (k, pos) with `count` assigned above it and incumbent `best`:
+// the same node counting, bound, descending branch order and strictly-better
+// leaf rule.  Stops (capped) after `cap` nodes.  TRACK copies improving
+// leaves into bx.
+template <bool TRACK>
+__device__ void exact_dfs(const ShapeTables &t, ExactState &st, int k, int pos, int64_t count, int64_t &best,
+                          int64_t cap, int64_t &nodes, bool &capped, int32_t *bx) {
+    const int R = st.R, J = st.J;
+    int fk[kMaxExactCells + 1], fpos[kMaxExactCells + 1], fj[kMaxExactCells + 1];
+    int64_t fv[kMaxExactCells + 1];
+    int depth = 0;
+    bool calling = true;
+    capped = false;
+    while (true) {
+        if (calling) {
+            if (++nodes > cap) {
+                capped = true;
+                return;
+            }
+            if (k == R) {
+                if (count > best) {
+                    best = count;
+                    if (TRACK)
+                        for (int c = 0; c < R * J; ++c) bx[c] = st.x[c];
+                }
+                calling = false;
+                continue;
+            }
+            const int s = st.shp[k];
+            if (pos == t.olen[s]) {
+                ++k;
+                pos = 0;
+                continue;  // tail call dfs(k+1, 0)
+            }
+            int64_t lam_total = 0;
+            for (int j = 0; j < J; ++j) lam_total += st.lam[j];
+            int64_t bound = suffix_bound(t, st, k, pos, st.lam, st.mrem[k]);
+            for (int k2 = k + 1; k2 < R; ++k2) bound += suffix_bound(t, st, k2, 0, st.lam, t.M[st.shp[k2]]);
+            if (count + (lam_total < bound ? lam_total : bound) <= best) {
+                calling = false;
+                continue;
+            }
+            const int j = t.order[s * kMaxJ + pos];
+            const int64_t u = t.unit[s * J + j];
+            int64_t hi = t.cap[s * J + j];
+            if (st.lam[j] < hi) hi = st.lam[j];
+            if (hi * u > st.mrem[k]) hi = quot_small(st.mrem[k], u, t.inv_unit[s * J + j]);
+            fk[depth] = k;
+            fpos[depth] = pos;
+            fj[depth] = j;
+            fv[depth] = hi;
+            ++depth;
+            st.x[k * J + j] = static_cast<int32_t>(hi);
+            st.lam[j] -= hi;
+            st.mrem[k] -= hi * u;
+            count += hi;
+            pos = pos + 1;
+            continue;  // call dfs(k, pos+1)
+        }
+        // return into the frame on top of the stack
+        if (depth == 0) return;
+        const int d = depth - 1;
+        const int kk = fk[d], j = fj[d];
+        const int64_t u = t.unit[st.shp[kk] * J + j];
+        int64_t v = fv[d];
+        count -= v;
+        st.mrem[kk] += v * u;
+        st.lam[j] += v;
+        st.x[kk * J + j] = 0;
+        if (v == 0) {
+            --depth;  // loop exhausted: return from this visit
             continue;
         }
+        v -= 1;
+        fv[d] = v;
+        st.x[kk * J + j] = static_cast<int32_t>(v);
+        st.lam[j] -= v;
+        st.mrem[kk] -= v * u;
+        count += v;
+        k = kk;
+        pos = fpos[d] + 1;
+        calling = true;
+    }
+}
+
+// Warp-cooperative exact_dfs: all 32 lanes carry the identical DFS state and
+// control flow; the bound's per-replica greedy_suffix terms (the dominant
+// per-node cost, R*J dependent loads on one thread) are evaluated one replica
+// per lane and summed by a warp reduction.  `ctr` (optional) is a node total
+// shared with other warps: every 256 nodes the warp adds its progress and
+// stops (capped) once the total passes `ctr_limit`.
+template <bool TRACK>
+__device__ void exact_dfs_warp(const ShapeTables &t, ExactState &st, int k, int pos, int64_t count, int64_t &best,
+                               int64_t cap, int64_t &nodes, bool &capped, int32_t *bx, unsigned long long *ctr,
+                               int64_t ctr_limit) {
+    const int lane = threadIdx.x & 31;
+    const int R = st.R, J = st.J;
+    int fk[kMaxExactCells + 1], fpos[kMaxExactCells + 1], fj[kMaxExactCells + 1];
+    int64_t fv[kMaxExactCells + 1];
+    int depth = 0;
+    bool calling = true;
+    int64_t flushed = 0;
+    capped = false;
+    auto flush = [&]() -> bool {  // true: the shared total passed the limit
+        unsigned long long tot = 0;
+        if (lane == 0) tot = atomicAdd(ctr, static_cast<unsigned long long>(nodes - flushed)) + (nodes - flushed);
+        flushed = nodes;
+        tot = __shfl_sync(0xffffffffu, tot, 0);
+        return tot > static_cast<unsigned long long>(ctr_limit);
+    };
+    while (true) {
+        if (calling) {
+            if (++nodes > cap) {
+                capped = true;
+                break;
+            }
+            if (ctr && (nodes & 255) == 0 && flush()) {
+                capped = true;
+                break;
+            }
+            if (k == R) {
+                if (count > best) {
+                    best = count;
+                    if (TRACK)  // every lane: bx may be lane-local (identical copies)
+                        for (int c = 0; c < R * J; ++c) bx[c] = st.x[c];
+                }
+                calling = false;
+                continue;
+            }
+            const int s = st.shp[k];
+            if (pos == t.olen[s]) {
+                ++k;
+                pos = 0;
+                continue;  // tail call dfs(k+1, 0)
+            }
+            int64_t lam_total = 0;
+            for (int j = 0; j < J; ++j) lam_total += st.lam[j];
+            int64_t bound = 0;
+            for (int kk = lane; kk < R; kk += 32) {
+                if (kk == k) bound += suffix_bound(t, st, k, pos, st.lam, st.mrem[k]);
+                else if (kk > k) bound += suffix_bound(t, st, kk, 0, st.lam, t.M[st.shp[kk]]);
+            }
+            for (int d = 16; d > 0; d >>= 1) bound += __shfl_xor_sync(0xffffffffu, bound, d);
+            if (count + (lam_total < bound ? lam_total : bound) <= best) {
+                calling = false;
+                continue;
+            }
+            const int j = t.order[s * kMaxJ + pos];
+            const int64_t u = t.unit[s * J + j];
+            int64_t hi = t.cap[s * J + j];
+            if (st.lam[j] < hi) hi = st.lam[j];
+            if (hi * u > st.mrem[k]) hi = quot_small(st.mrem[k], u, t.inv_unit[s * J + j]);
+            fk[depth] = k;
+            fpos[depth] = pos;
+            fj[depth] = j;
+            fv[depth] = hi;
+            ++depth;
+            st.x[k * J + j] = static_cast<int32_t>(hi);
+            st.lam[j] -= hi;
+            st.mrem[k] -= hi * u;
+            count += hi;
+            pos = pos + 1;
+            continue;
+        }
+        if (depth == 0) break;
+        const int d = depth - 1;
+        const int kk = fk[d], j = fj[d];
+        const int64_t u = t.unit[st.shp[kk] * J + j];
+        int64_t v = fv[d];
+        count -= v;
+        st.mrem[kk] += v * u;
+        st.lam[j] += v;
+        st.x[kk * J + j] = 0;
+        if (v == 0) {
+            --depth;
+            continue;
+        }
+        v -= 1;
+        fv[d] = v;
+        st.x[kk * J + j] = static_cast<int32_t>(v);
+        st.lam[j] -= v;
+        st.mrem[kk] -= v * u;
+        count += v;
+        k = kk;
+        pos = fpos[d] + 1;
+        calling = true;
+    }
+    if (ctr && nodes != flushed) flush();
+}
+
+// Warp per plan: the reference's DFS verbatim (sequential fallback).
+__global__ void __launch_bounds__(128) k_plan_exact(ShapeTables t, SpaceTables sp, KeyLayout key, PlanSource src,
+                                                    PlanOutputs out, SolveParams prm) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t w0 = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t i = w0; i < src.count; i += nw) {
         ExactState st;
         int64_t part;
         uint64_t local, gr;
         const int64_t *lam_src;
-        if (!exact_setup(t, sp, src, prm, i, st, part, local, gr, lam_src)) {
-            if (phase == 1) es.p1_state[i] = 0;  // not an exact-path plan
-            continue;
-        }
-        const int R = st.R;
-        int fk[kMaxExactCells + 1], fpos[kMaxExactCells + 1], fj[kMaxExactCells + 1];
-        int64_t fv[kMaxExactCells + 1];
-        int depth = 0;
-        // phase 2 slots start from the first branch's best: a lower bound of the
-        // sequential best for every later branch
-        int64_t count = 0, bestc = phase == 2 ? es.p1_best[i] : -1, nodes = 0, prefix_nodes = 0, best_v = -1;
-        bool aborted = false, branched = false;
-        int k = 0, pos = 0;
-        bool calling = true;  // true: enter visit(k, pos); false: return to frame on top
-        while (true) {
-            if (calling) {
-                if (++nodes > prm.node_budget) {
-                    aborted = true;
-                    break;
-                }
-                if (k == R) {
-                    if (count > bestc) {
-                        bestc = count;
-                        best_v = depth > 0 ? fv[0] : 0;
-                        for (int c = 0; c < R * J; ++c) st.bx[c] = st.x[c];
-                    }
-                    calling = false;
-                    continue;
-                }
-                const int s = st.shp[k];
-                if (pos == t.olen[s]) {
-                    ++k;
-                    pos = 0;
-                    continue;  // tail call visit(k+1, 0)
-                }
-                int64_t lam_total = 0;
-                for (int j = 0; j < J; ++j) lam_total += st.lam[j];
-                int64_t bound = suffix_bound(t, st, k, pos, st.lam, st.mrem[k]);
-                for (int k2 = k + 1; k2 < R; ++k2) bound += suffix_bound(t, st, k2, 0, st.lam, t.M[st.shp[k2]]);
-                if (count + (lam_total < bound ? lam_total : bound) <= bestc) {
-                    calling = false;
-                    continue;
-                }
-                const int j = t.order[s * kMaxJ + pos];
-                const int64_t u = t.unit[s * J + j];
-                int64_t hi = t.cap[s * J + j];
-                if (st.lam[j] < hi) hi = st.lam[j];
-                if (hi * u > st.mrem[k]) hi = quot_small(st.mrem[k], u, t.inv_unit[s * J + j]);
-                if (SPLIT && depth == 0) {  // first branching cell
-                    branched = true;
-                    prefix_nodes = nodes;
-                    if (phase == 2) {  // this slot's branches: hi-1-slot, hi-1-slot-S, ...
-                        hi -= 1 + slot;
-                        if (hi < 0) break;
-                    }
-                }
-                fk[depth] = k;
-                fpos[depth] = pos;
-                fj[depth] = j;
-                fv[depth] = hi;
-                ++depth;
-                st.x[k * J + j] = static_cast<int32_t>(hi);
-                st.lam[j] -= hi;
-                st.mrem[k] -= hi * u;
-                count += hi;
-                pos = pos + 1;
-                continue;  // call visit(k, pos+1)
-            }
-            // return into the frame on top of the stack
-            if (depth == 0) break;
-            const int d = depth - 1;
-            const int kk = fk[d], j = fj[d];
-            const int64_t u = t.unit[st.shp[kk] * J + j];
-            int64_t v = fv[d];
-            count -= v;
-            st.mrem[kk] += v * u;
-            st.lam[j] += v;
-            st.x[kk * J + j] = 0;
-            const int64_t step = (SPLIT && d == 0) ? (phase == 1 ? (int64_t{1} << 62) : kExactSlots) : 1;
-            if (v - step < 0) {
-                --depth;  // loop exhausted: return from this visit
-                continue;
-            }
-            v -= step;
-            fv[d] = v;
-            st.x[kk * J + j] = static_cast<int32_t>(v);
-            st.lam[j] -= v;
-            st.mrem[kk] -= v * u;
-            count += v;
-            k = kk;
-            pos = fpos[d] + 1;
-            calling = true;
-        }
-        if (SPLIT && phase == 1) {
-            // first branch only: identical to the sequential DFS up to there, so
-            // an abort here is the reference's abort; no branching => done
-            es.p1_state[i] = aborted ? 2 : (branched ? 1 : 3);
-            es.p1_best[i] = bestc;
-            es.p1_nodes[i] = static_cast<uint64_t>(nodes);
-            for (int c = 0; c < R * J; ++c) es.p1_x[i * kMaxExactCells + c] = st.bx[c];
-            continue;
-        }
-        if (SPLIT) {
-            // per-slot result for k_exact_combine (nodes below the first cell)
-            es.state[tix] = aborted ? 2 : 1;
-            es.best[tix] = bestc;
-            es.best_v[tix] = best_v;
-            es.nodes[tix] = static_cast<uint64_t>(nodes - prefix_nodes);
-            for (int c = 0; c < R * J; ++c) es.x[tix * kMaxExactCells + c] = st.bx[c];
-            continue;
-        }
+        if (!exact_setup(t, sp, src, prm, i, st, part, local, gr, lam_src)) continue;
+        int64_t best = -1, nodes = 0;
+        bool aborted;
+        exact_dfs_warp<true>(t, st, 0, 0, 0, best, prm.node_budget, nodes, aborted, st.bx, nullptr, 0);
+        __syncwarp();
+        if (lane != 0) continue;
         if (aborted) {
             if (out.aborted) {
                 const unsigned slot2 = atomicAdd(out.aborted_n, 1u);
@@ -1131,59 +1202,343 @@ __global__ void __launch_bounds__(128) k_plan_exact(ShapeTables t, SpaceTables s
             }
             continue;
         }
-        exact_emit(t, key, out, i, st, st.bx, bestc, part, local);
+        exact_emit(t, key, out, i, st, st.bx, best, part, local);
     }
 }
 
-// Combine phase 1 (first branch) and the kExactSlots phase-2 slots of each
-// split plan (see k_plan_exact).
-__global__ void k_exact_combine(ShapeTables t, SpaceTables sp, KeyLayout key, PlanSource src, PlanOutputs out,
-                                SolveParams prm, ExactSplit es) {
+// ---- frontier-parallel exact path -------------------------------------------
+// The sequential DFS's result is decided by two facts (flowassign.cpp:330-369):
+//  * the incumbent when a node is checked equals the best leaf among ALL
+//    leaves before it in preorder (a pruned leaf is <= the incumbent that
+//    pruned it), so a node is visited iff every ancestor passes its bound
+//    check against that prefix maximum;
+//  * the answer is the first optimal leaf in preorder (pruning is <=, the
+//    leaf update strictly >), and the run aborts iff the visited-node count
+//    exceeds the budget.
+// So the tree is cut after `depth` branching decisions; each frontier node is
+// a task.  Phase A (task pass 0) gets each task's best leaf m (seeded with a
+// lower bound lb of its entering incumbent: the prefix max of cheap greedy
+// dives of earlier tasks, so m = max(best leaf, lb) — exactly what the
+// prefix maximum needs).  Pass 2 walks the top of the tree once, in preorder,
+// with the exact prefix-maximum incumbent: visited flags, the entering
+// incumbent of each task and the top-node count.  Phase B (task pass 1)
+// replays every visited task from its exact incumbent — now identical to the
+// sequential DFS inside it — and counts its nodes.  The first optimal leaf is
+// in the task where the prefix maximum last rose.
+
+// Task root state from its decision path; `leaf` follows the pass-through
+// chain to the leaf (a task created by reaching k == R above the cut).
+__device__ __forceinline__ void exact_restore(const ShapeTables &t, ExactState &st, const int32_t *path, int nd,
+                                              bool leaf, int &k, int &pos, int64_t &count) {
+    const int R = st.R, J = st.J;
+    k = 0;
+    pos = 0;
+    count = 0;
+    int a = 0;
+    while (k < R) {
+        const int s = st.shp[k];
+        if (a == nd && !leaf) break;
+        if (pos == t.olen[s]) {
+            ++k;
+            pos = 0;
+            continue;
+        }
+        if (a == nd) break;
+        const int j = t.order[s * kMaxJ + pos];
+        const int64_t u = t.unit[s * J + j];
+        const int64_t v = path[a++];
+        st.x[k * J + j] = static_cast<int32_t>(v);
+        st.lam[j] -= v;
+        st.mrem[k] -= v * u;
+        count += v;
+        ++pos;
+    }
+}
+
+// Count of the greedy dive (every branch at its largest value) from (k, pos):
+// a leaf of the subtree, so a lower bound of its best leaf.
+__device__ __forceinline__ int64_t exact_dive(const ShapeTables &t, const ExactState &st, int k, int pos,
+                                              int64_t count) {
+    const int R = st.R, J = st.J;
+    int64_t lam[kMaxJ];
+    for (int j = 0; j < J; ++j) lam[j] = st.lam[j];
+    for (; k < R; ++k, pos = 0) {
+        const int s = st.shp[k];
+        int64_t mr = st.mrem[k];  // replicas after k are untouched (mrem = M)
+        for (int i = pos; i < t.olen[s]; ++i) {
+            const int j = t.order[s * kMaxJ + i];
+            const int64_t u = t.unit[s * J + j];
+            int64_t hi = t.cap[s * J + j];
+            if (lam[j] < hi) hi = lam[j];
+            if (hi * u > mr) hi = quot_small(mr, u, t.inv_unit[s * J + j]);
+            lam[j] -= hi;
+            mr -= hi * u;
+            count += hi;
+        }
+    }
+    return count;
+}
+
+// Preorder walk of the tree above the cut.  MODE 0: count tasks (stop past
+// cap); 1: emit tasks; 2: exact replay (visited flags, entering incumbents,
+// top-node count).
+template <int MODE>
+__device__ uint64_t exact_top(const ShapeTables &t, ExactState &st, int cut, uint64_t cap, const ExactTasks &et,
+                              uint64_t base, uint32_t plan, int64_t &top_nodes, int64_t &opt, int64_t &istar) {
+    const int R = st.R, J = st.J;
+    int fk[kTaskDepthMax], fpos[kTaskDepthMax], fj[kTaskDepthMax];
+    int64_t fv[kTaskDepthMax];
+    bool falive[kTaskDepthMax];
+    int depth = 0, k = 0, pos = 0;
+    int64_t count = 0, inc = -1;
+    bool calling = true, vis = true;
+    uint64_t ti = 0;
+    top_nodes = 0;
+    istar = -1;
+    while (true) {
+        if (calling) {
+            const bool boundary = MODE == 2 ? (k == R || (ti < cap && depth == (et.tdepth[base + ti] & 0x7f)))
+                                            : (depth == cut || k == R);
+            if (boundary) {  // task boundary
+                if (MODE == 0) {
+                    if (++ti > cap) return ti;
+                } else if (MODE == 1) {
+                    const uint64_t q = base + ti;
+                    et.plan[q] = plan;
+                    et.tdepth[q] = static_cast<uint8_t>(depth | (k == R && depth < cut ? 0x80 : 0));
+                    for (int a = 0; a < depth; ++a) et.path[q * kTaskDepthMax + a] = static_cast<int32_t>(fv[a]);
+                    et.done[q] = 0;
+                    ++ti;
+                } else {
+                    const uint64_t q = base + ti;
+                    et.vis[q] = vis ? 1 : 0;
+                    et.inc[q] = inc;
+                    if (et.m[q] > inc) {
+                        inc = et.m[q];
+                        istar = static_cast<int64_t>(q);
+                    }
+                    ++ti;
+                }
+                calling = false;
+                continue;
+            }
+            if (MODE == 2 && vis) ++top_nodes;
+            const int s = st.shp[k];
+            if (pos == t.olen[s]) {
+                ++k;
+                pos = 0;
+                continue;
+            }
+            bool alive = true;
+            if (MODE == 2) {
+                alive = false;
+                if (vis) {
+                    int64_t lam_total = 0;
+                    for (int j = 0; j < J; ++j) lam_total += st.lam[j];
+                    int64_t bound = suffix_bound(t, st, k, pos, st.lam, st.mrem[k]);
+                    for (int k2 = k + 1; k2 < R; ++k2) bound += suffix_bound(t, st, k2, 0, st.lam, t.M[st.shp[k2]]);
+                    alive = count + (lam_total < bound ? lam_total : bound) > inc;
+                }
+            }
+            const int j = t.order[s * kMaxJ + pos];
+            const int64_t u = t.unit[s * J + j];
+            int64_t hi = t.cap[s * J + j];
+            if (st.lam[j] < hi) hi = st.lam[j];
+            if (hi * u > st.mrem[k]) hi = quot_small(st.mrem[k], u, t.inv_unit[s * J + j]);
+            fk[depth] = k;
+            fpos[depth] = pos;
+            fj[depth] = j;
+            fv[depth] = hi;
+            falive[depth] = alive;
+            ++depth;
+            st.x[k * J + j] = static_cast<int32_t>(hi);
+            st.lam[j] -= hi;
+            st.mrem[k] -= hi * u;
+            count += hi;
+            pos = pos + 1;
+            vis = alive;
+            continue;
+        }
+        if (depth == 0) break;
+        const int d = depth - 1;
+        const int kk = fk[d], j = fj[d];
+        const int64_t u = t.unit[st.shp[kk] * J + j];
+        int64_t v = fv[d];
+        count -= v;
+        st.mrem[kk] += v * u;
+        st.lam[j] += v;
+        st.x[kk * J + j] = 0;
+        if (v == 0) {
+            --depth;
+            continue;
+        }
+        v -= 1;
+        fv[d] = v;
+        st.x[kk * J + j] = static_cast<int32_t>(v);
+        st.lam[j] -= v;
+        st.mrem[kk] -= v * u;
+        count += v;
+        k = kk;
+        pos = fpos[d] + 1;
+        vis = falive[d];
+        calling = true;
+    }
+    opt = inc;
+    return ti;
+}
+
+// Per-plan passes: 0 choose the cut depth and count tasks, 1 emit tasks,
+// 2 exact replay of the top, 3 finish (abort decision or outputs).
+__global__ void __launch_bounds__(128) k_exact_plan(int pass, ShapeTables t, SpaceTables sp, KeyLayout key,
+                                                    PlanSource src, PlanOutputs out, SolveParams prm, ExactTasks et) {
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < src.count;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint8_t p1 = es.p1_state[i];
-        if (p1 == 0) continue;  // not an exact-path plan
         ExactState st;
-        int64_t part;
+        int64_t part, tn, opt, istar;
         uint64_t local, gr;
         const int64_t *lam_src;
-        exact_setup(t, sp, src, prm, i, st, part, local, gr, lam_src);
-        if (p1 == 2) {  // the reference aborts too (same nodes up to here)
+        const bool ex = exact_setup(t, sp, src, prm, i, st, part, local, gr, lam_src);
+        if (pass == 0) {
+            if (!ex) {
+                et.depth[i] = -1;
+                et.ntask[i] = 0;
+                et.state[i] = 0;
+                continue;
+            }
+            int chosen = 1;
+            uint64_t n = exact_top<0>(t, st, 1, et.max_tasks, et, 0, 0, tn, opt, istar);
+            for (int d = 2; d <= 6 && n < et.target; ++d) {  // initial cut; phase A splits deeper
+                const uint64_t n2 = exact_top<0>(t, st, d, et.max_tasks, et, 0, 0, tn, opt, istar);
+                if (n2 > et.max_tasks) break;
+                n = n2;
+                chosen = d;
+            }
+            const bool ok = n <= et.max_tasks;
+            et.depth[i] = chosen;
+            et.ntask[i] = ok ? n : 0;
+            et.state[i] = ok ? 1 : 2;
+            continue;
+        }
+        if (!ex || et.state[i] == 0) continue;
+        if (pass == 1) {
+            if (et.state[i] == 1)
+                exact_top<1>(t, st, et.depth[i], et.max_tasks, et, et.toff[i], static_cast<uint32_t>(i), tn, opt, istar);
+            continue;
+        }
+        if (pass == 4) {  // lb = exclusive prefix max of the tasks' dives; finished tasks: m = max(m, lb)
+            if (et.state[i] != 1) continue;
+            int64_t run = -1;
+            for (uint64_t q = et.toff[i]; q < et.toff[i] + et.ntask[i]; ++q) {
+                et.lb[q] = run;
+                if (et.done[q] && et.m[q] < run) et.m[q] = run;
+                run = et.g[q] > run ? et.g[q] : run;
+            }
+            continue;
+        }
+        if (pass == 2) {
+            if (et.state[i] != 1) continue;
+            bool capped = false;
+            for (uint64_t q = et.toff[i]; q < et.toff[i] + et.ntask[i]; ++q) capped = capped || et.capped[q];
+            if (capped) {  // phase A hit the budget somewhere: sequential DFS
+                et.state[i] = 2;
+                continue;
+            }
+            exact_top<2>(t, st, et.depth[i], et.ntask[i], et, et.toff[i], static_cast<uint32_t>(i), tn, opt, istar);
+            et.top_nodes[i] = tn;
+            et.opt[i] = opt;
+            et.istar[i] = istar;
+            et.running[i] = static_cast<unsigned long long>(tn);
+            // phase A visits a superset of the sequential nodes below each task
+            // (its incumbent is never stronger), so top + sum(A) bounds the count
+            int64_t ub = tn;
+            for (uint64_t q = et.toff[i]; q < et.toff[i] + et.ntask[i]; ++q)
+                if (et.vis[q]) ub += et.nodes[q];
+            if (ub > prm.node_budget) et.state[i] = 3;
+            continue;
+        }
+        // pass 3: finish
+        const uint8_t ps = et.state[i];
+        if (ps != 1 && ps != 3) continue;
+        if (ps == 3 && et.running[i] > static_cast<unsigned long long>(prm.node_budget)) {
             if (out.aborted) {
                 const unsigned slot2 = atomicAdd(out.aborted_n, 1u);
                 out.aborted[slot2] = gr;
             }
             continue;
         }
-        if (p1 == 3) {  // no branching cell: the first-branch DFS was the whole DFS
-            exact_emit(t, key, out, i, st, es.p1_x + i * kMaxExactCells, es.p1_best[i], part, local);
-            continue;
+        exact_emit(t, key, out, i, st, et.bx + i * kMaxExactCells, et.opt[i], part, local);
+    }
+}
+
+// Per-task passes, warp per task: 0 phase A (best leaf seeded with lb, node
+// count), 1 phase B (exact replay from the entering incumbent: the first
+// optimal leaf of the istar task; node counts into the plan's running total
+// when phase A's upper bound did not certify the plan).
+__global__ void __launch_bounds__(128) k_exact_task(int pass, ShapeTables t, SpaceTables sp, PlanSource src,
+                                                    SolveParams prm, ExactTasks et, uint64_t total) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t w0 = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t q = w0; q < total; q += nw) {
+        const uint64_t i = et.plan[q];
+        const uint8_t ps = et.state[i];
+        if ((pass == 0 || pass == 2 || pass == 3) && ps != 1) continue;
+        if ((pass == 0 || pass == 2) && et.done[q]) continue;
+        if (pass == 1) {
+            if (ps == 1 && static_cast<int64_t>(q) != et.istar[i]) continue;  // certified: only the winner's leaf
+            if (ps != 1 && (ps != 3 || !et.vis[q])) continue;
         }
-        uint64_t total = es.p1_nodes[i];
-        bool any_abort = false;
-        int64_t best = es.p1_best[i], bv = 1ll << 62;  // phase 1 wins ties (earliest branch)
-        int bslot = -1;
-        const uint64_t t0 = i * kExactSlots;
-        for (int q = 0; q < kExactSlots; ++q) {
-            const uint64_t tq = t0 + q;
-            if (es.state[tq] == 0) continue;
-            if (es.state[tq] == 2) any_abort = true;
-            total += es.nodes[tq];
-            const int64_t b = es.best[tq], v = es.best_v[tq];
-            if (b > best || (b == best && bslot >= 0 && v > bv)) {
-                best = b;
-                bv = v;
-                bslot = q;
+        ExactState st;
+        int64_t part;
+        uint64_t local, gr;
+        const int64_t *lam_src;
+        exact_setup(t, sp, src, prm, i, st, part, local, gr, lam_src);
+        const uint8_t td = et.tdepth[q];
+        int k, pos;
+        int64_t count;
+        exact_restore(t, st, et.path + q * kTaskDepthMax, td & 0x7f, (td & 0x80) != 0, k, pos, count);
+        int64_t nodes = 0;
+        bool capped;
+        if (pass == 2) {  // greedy dive of the task: a leaf, so a lower bound of its best
+            if (lane == 0) et.g[q] = exact_dive(t, st, k, pos, count);
+        } else if (pass == 3) {  // children count for the next round
+            uint32_t nc = 1;
+            if (et.capped[q] && et.phase_cap < prm.node_budget && (td & 0x7f) < kTaskDepthMax - 1) {
+                while (k < st.R && pos == t.olen[st.shp[k]]) {
+                    ++k;
+                    pos = 0;
+                }
+                if (k < st.R) {
+                    const int s = st.shp[k];
+                    const int j = t.order[s * kMaxJ + pos];
+                    const int64_t u = t.unit[s * st.J + j];
+                    int64_t hi = t.cap[s * st.J + j];
+                    if (st.lam[j] < hi) hi = st.lam[j];
+                    if (hi * u > st.mrem[k]) hi = quot_small(st.mrem[k], u, t.inv_unit[s * st.J + j]);
+                    nc = static_cast<uint32_t>(hi + 1);
+                }
             }
+            if (lane == 0) et.nchild[q] = nc;
+        } else if (pass == 0) {
+            int64_t best = et.lb[q];
+            exact_dfs_warp<false>(t, st, k, pos, count, best, et.phase_cap, nodes, capped, nullptr, nullptr, 0);
+            if (lane == 0) {
+                et.m[q] = best;
+                et.nodes[q] = nodes;
+                et.capped[q] = capped ? 1 : 0;
+                et.done[q] = capped ? 0 : 1;
+            }
+        } else {
+            int64_t best = et.inc[q];
+            unsigned long long *ctr = ps == 3 ? et.running + i : nullptr;
+            if (static_cast<int64_t>(q) == et.istar[i])
+                exact_dfs_warp<true>(t, st, k, pos, count, best, prm.node_budget + 1, nodes, capped,
+                                     et.bx + i * kMaxExactCells, ctr, prm.node_budget);
+            else
+                exact_dfs_warp<false>(t, st, k, pos, count, best, prm.node_budget + 1, nodes, capped, nullptr, ctr,
+                                      prm.node_budget);
         }
-        if (any_abort || total > static_cast<uint64_t>(prm.node_budget)) {
-            // could not certify the sequential node count: rerun sequentially
-            const unsigned slot2 = atomicAdd(es.redo_n, 1u);
-            es.redo[slot2] = src.mode == 2 ? src.first + i : gr;
-            continue;
-        }
-        const int32_t *bx = bslot < 0 ? es.p1_x + i * kMaxExactCells : es.x + (t0 + bslot) * kMaxExactCells;
-        exact_emit(t, key, out, i, st, bx, best, part, local);
+        __syncwarp();
     }
 }
 
@@ -1620,44 +1975,99 @@ int launch_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayou
     return static_cast<int>(cudaErrorInvalidValue);
 }
 
-int launch_plan_exact(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key, const PlanSource &src,
-                      const PlanOutputs &out, const SolveParams &prm, int sm_count, void *stream,
-                      uint64_t *launches, const ExactSplit *split) {
+// Thread per task: copy it to the new list, or write its children (the
+// branches v = hi .. 0 of its first decision node, in preorder).
+__global__ void __launch_bounds__(128) k_exact_split(ExactTasks et, ExactTasks nt, const uint64_t *newoff,
+                                                     uint64_t total) {
+    for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
+         q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t o = newoff[q];
+        const uint32_t nc = et.nchild[q];
+        const uint8_t td = et.tdepth[q];
+        const int dep = td & 0x7f;
+        for (uint32_t c = 0; c < nc; ++c) {
+            const uint64_t r = o + c;
+            nt.plan[r] = et.plan[q];
+            for (int a = 0; a < dep; ++a) nt.path[r * kTaskDepthMax + a] = et.path[q * kTaskDepthMax + a];
+            if (nc == 1) {  // unchanged task
+                nt.tdepth[r] = td;
+                nt.g[r] = et.g[q];
+                nt.m[r] = et.m[q];
+                nt.nodes[r] = et.nodes[q];
+                nt.capped[r] = et.capped[q];
+                nt.done[r] = et.done[q];
+            } else {
+                nt.tdepth[r] = static_cast<uint8_t>(dep + 1);
+                nt.path[r * kTaskDepthMax + dep] = static_cast<int32_t>(nc - 1 - c);  // v = hi - c
+                nt.capped[r] = 0;
+                nt.done[r] = 0;
+            }
+        }
+    }
+}
+
+int launch_exact_split(const ShapeTables &t, const SpaceTables &sp, const PlanSource &src, const SolveParams &prm,
+                       const ExactTasks &et, const ExactTasks &nt, const uint64_t *newoff, uint64_t total_tasks,
+                       int sm_count, void *stream, uint64_t *launches) {
+    (void)t;
+    (void)sp;
+    (void)src;
+    (void)prm;
     cudaGetLastError();
-    // The split variant is exact but measured slower on config 1-B&B (29 s vs
-    // 16.8 s: too many plans fail the node-count certification and rerun);
-    // opt-in with OSERVE_K4_SPLIT=1.
-    static const bool use_split = [] {
-        const char *e = getenv("OSERVE_K4_SPLIT");
-        return e && atoi(e) == 1;
-    }();
-    if (!use_split) split = nullptr;
-    if (int e = ensure_binom()) return e;
-    if (src.count == 0) return 0;
+    if (total_tasks == 0) return 0;
     const int block = 128;
     const uint64_t cap = static_cast<uint64_t>(sm_count) * 16;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (split) {
-        ExactSplit e1 = *split;
-        e1.phase = 1;
-        uint64_t g1 = (src.count + block - 1) / block;
-        if (g1 > cap) g1 = cap;
-        k_plan_exact<true><<<static_cast<unsigned>(g1), block, 0, s>>>(t, sp, key, src, out, prm, e1);
-        ExactSplit e2 = *split;
-        e2.phase = 2;
-        uint64_t grid = (src.count * kExactSlots + block - 1) / block;
-        if (grid > cap) grid = cap;
-        k_plan_exact<true><<<static_cast<unsigned>(grid), block, 0, s>>>(t, sp, key, src, out, prm, e2);
-        if (launches) ++*launches;
-        uint64_t g2 = (src.count + block - 1) / block;
-        if (g2 > cap) g2 = cap;
-        k_exact_combine<<<static_cast<unsigned>(g2), block, 0, s>>>(t, sp, key, src, out, prm, *split);
-        if (launches) *launches += 2;
-        return check(cudaGetLastError());
-    }
+    uint64_t grid = (total_tasks + block - 1) / block;
+    if (grid > cap) grid = cap;
+    k_exact_split<<<static_cast<unsigned>(grid), block, 0, static_cast<cudaStream_t>(stream)>>>(et, nt, newoff,
+                                                                                                total_tasks);
+    if (launches) ++*launches;
+    return check(cudaGetLastError());
+}
+
+int launch_plan_exact(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key, const PlanSource &src,
+                      const PlanOutputs &out, const SolveParams &prm, int sm_count, void *stream,
+                      uint64_t *launches) {
+    cudaGetLastError();
+    if (int e = ensure_binom()) return e;
+    if (src.count == 0) return 0;
+    const int block = 128;  // 4 warps, warp per plan
+    const uint64_t cap = static_cast<uint64_t>(sm_count) * 16;
+    uint64_t grid = (src.count * 32 + block - 1) / block;
+    if (grid > cap) grid = cap;
+    k_plan_exact<<<static_cast<unsigned>(grid), block, 0, static_cast<cudaStream_t>(stream)>>>(t, sp, key, src, out,
+                                                                                               prm);
+    if (launches) ++*launches;
+    return check(cudaGetLastError());
+}
+
+int launch_exact_plan_pass(int pass, const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key,
+                           const PlanSource &src, const PlanOutputs &out, const SolveParams &prm,
+                           const ExactTasks &et, int sm_count, void *stream, uint64_t *launches) {
+    cudaGetLastError();
+    if (int e = ensure_binom()) return e;
+    if (src.count == 0) return 0;
+    const int block = 64;
+    const uint64_t cap = static_cast<uint64_t>(sm_count) * 32;
     uint64_t grid = (src.count + block - 1) / block;
     if (grid > cap) grid = cap;
-    k_plan_exact<false><<<static_cast<unsigned>(grid), block, 0, s>>>(t, sp, key, src, out, prm, ExactSplit{});
+    k_exact_plan<<<static_cast<unsigned>(grid), block, 0, static_cast<cudaStream_t>(stream)>>>(pass, t, sp, key, src,
+                                                                                               out, prm, et);
+    if (launches) ++*launches;
+    return check(cudaGetLastError());
+}
+
+int launch_exact_task_pass(int pass, const ShapeTables &t, const SpaceTables &sp, const PlanSource &src,
+                           const SolveParams &prm, const ExactTasks &et, uint64_t total_tasks, int sm_count,
+                           void *stream, uint64_t *launches) {
+    cudaGetLastError();
+    if (total_tasks == 0) return 0;
+    const int block = 128;  // 4 warps, warp per task
+    const uint64_t cap = static_cast<uint64_t>(sm_count) * 16;
+    uint64_t grid = (total_tasks * 32 + block - 1) / block;
+    if (grid > cap) grid = cap;
+    k_exact_task<<<static_cast<unsigned>(grid), block, 0, static_cast<cudaStream_t>(stream)>>>(pass, t, sp, src, prm,
+                                                                                               et, total_tasks);
     if (launches) ++*launches;
     return check(cudaGetLastError());
 }
