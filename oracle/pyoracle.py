@@ -240,7 +240,7 @@ class Oracle:
         return [core.WorkloadType(c, ci[c], co[c]) for c in range(k)]
 
     def kv_plan(self, cl: core.ClusterSpec, inflight, threshold_tokens: int, src: core.Deployment,
-                dst: core.Deployment, headroom: float = 0.1, carry=None) -> core.KvPlan:
+                dst: core.Deployment, headroom: float = 0.1, carry=None, as_arrays: bool = False):
         keep = A.Keep()
         c = A.cluster_desc(cl, keep)
         s, d = A.deployment_desc(src, keep), A.deployment_desc(dst, keep)
@@ -253,6 +253,8 @@ class Oracle:
         self._chk(self.lib.oracle_kv_plan(C.byref(c), n, reqs, threshold_tokens, C.byref(s), C.byref(d),
                                           float(headroom), ntr, tr, drained, C.byref(nd), mig, C.byref(nm),
                                           C.byref(buf)))
+        if as_arrays:
+            return A.kv_arrays(drained, nd.value, mig, nm.value, buf.value)
         return core.KvPlan(list(drained[:nd.value]),
                            [core.KvTransfer(m.request_id, m.kv_bytes, m.src, m.dst) for m in mig[:nm.value]],
                            buf.value)
@@ -264,12 +266,14 @@ class Oracle:
         self._chk(self.lib.oracle_adaptive_timeline_json(C.byref(pr.desc), T, flat, C.c_uint64(seed), max_iters,
                                                          min_gain, path.encode()))
 
-    def max_flow(self, num_nodes: int, edges, source: int, sink: int):
-        ed = (A.FlowEdgeDesc * max(1, len(edges)))(*[A.FlowEdgeDesc(a, b, c) for a, b, c in edges])
-        fl = (C.c_int64 * max(1, len(edges)))()
+    def max_flow(self, num_nodes: int, edges, source: int, sink: int, as_array: bool = False):
+        keep = A.Keep()
+        ed = A.flow_edges(edges, keep)
+        fl = np.zeros(max(1, len(edges)), np.int64)
         v = C.c_int64()
-        self._chk(self.lib.oracle_max_flow(num_nodes, len(edges), ed, source, sink, fl, C.byref(v)))
-        return v.value, list(fl[:len(edges)])
+        self._chk(self.lib.oracle_max_flow(num_nodes, len(edges), ed, source, sink,
+                                           fl.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(v)))
+        return v.value, (fl[:len(edges)] if as_array else fl[:len(edges)].tolist())
 
     def flow_assign(self, n, e, lam, opts=None):
         """build_network + max_flow + extract_assignment -> (x, objective, value, edge flows)."""

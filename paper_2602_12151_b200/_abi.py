@@ -88,6 +88,27 @@ class FlowEdgeDesc(C.Structure):
     _fields_ = [("from_", C.c_int), ("to", C.c_int), ("cap", C.c_int64)]
 
 
+def flow_edge_dtype():
+    """numpy layout of oserve_flow_edge."""
+    import numpy as np
+    return np.dtype([("from", "<i4"), ("to", "<i4"), ("cap", "<i8")], align=True)
+
+
+def flow_edges(edges, keep: "Keep"):
+    """(from, to, cap) tuples or a flow_edge_dtype array -> oserve_flow_edge*."""
+    import numpy as np
+    if not isinstance(edges, np.ndarray):
+        a = np.zeros(len(edges), flow_edge_dtype())
+        if len(edges):
+            t = np.asarray(edges, dtype=np.int64).reshape(-1, 3)
+            a["from"], a["to"], a["cap"] = t[:, 0], t[:, 1], t[:, 2]
+        edges = a
+    a = keep(np.ascontiguousarray(edges, dtype=flow_edge_dtype()))
+    if not len(a):
+        return keep((FlowEdgeDesc * 1)())
+    return C.cast(a.ctypes.data, C.POINTER(FlowEdgeDesc))
+
+
 class InflightDesc(C.Structure):
     _fields_ = [("request_id", C.c_int64), ("generated_tokens", C.c_int64), ("kv_bytes", C.c_uint64),
                 ("source_replica", C.c_int)]
@@ -97,11 +118,36 @@ class KvTransferDesc(C.Structure):
     _fields_ = [("request_id", C.c_int64), ("kv_bytes", C.c_uint64), ("src", C.c_int), ("dst", C.c_int)]
 
 
+def inflight_dtype():
+    """numpy layout of oserve_inflight (a structured array may be passed
+    wherever a list of InflightRequest is accepted)."""
+    import numpy as np
+    return np.dtype([("request_id", "<i8"), ("generated_tokens", "<i8"), ("kv_bytes", "<u8"),
+                     ("source_replica", "<i4")], align=True)
+
+
 def inflight_arr(reqs, keep: "Keep"):
+    import numpy as np
+    if isinstance(reqs, np.ndarray):
+        a = keep(np.ascontiguousarray(reqs, dtype=inflight_dtype()))
+        assert a.dtype.itemsize == C.sizeof(InflightDesc)
+        return C.cast(a.ctypes.data, C.POINTER(InflightDesc)) if len(a) else (InflightDesc * 1)()
     arr = (InflightDesc * max(1, len(reqs)))()
     for i, r in enumerate(reqs):
         arr[i] = InflightDesc(r.request_id, r.generated_tokens, r.kv_bytes, r.source_replica)
     return keep(arr)
+
+
+def kv_arrays(drained, nd: int, mig, nm: int, buffer_bytes: int):
+    """kv_plan outputs as numpy: drained ids [nd], migrated rows [nm, 4] =
+    (request_id, kv_bytes, src, dst), buffer bytes."""
+    import numpy as np
+    d = np.ctypeslib.as_array(drained, shape=(max(1, nd),))[:nd].copy()
+    rec = np.dtype([("request_id", "<i8"), ("kv_bytes", "<u8"), ("src", "<i4"), ("dst", "<i4")])
+    raw = np.frombuffer(mig, dtype=rec, count=nm) if nm else np.zeros(0, rec)
+    m = np.stack([raw["request_id"], raw["kv_bytes"].astype(np.int64), raw["src"], raw["dst"]], axis=1) \
+        if nm else np.zeros((0, 4), np.int64)
+    return d, m, buffer_bytes
 
 
 def transfer_arr(plan, keep: "Keep"):

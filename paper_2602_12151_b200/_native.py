@@ -340,19 +340,29 @@ class GpuContext:
     def max_flow_batch(self, graphs: Sequence[Tuple[int, Sequence[Tuple[int, int, int]]]], sources: Sequence[int],
                        sinks: Sequence[int]):
         """flow::max_flow per graph (num_nodes, [(from, to, cap)]) -> [(value, flows)]."""
-        G = len(graphs)
-        offs, edges = [0], []
-        for _, es in graphs:
-            edges.extend(es)
-            offs.append(len(edges))
-        ed = (A.FlowEdgeDesc * max(1, len(edges)))(*[A.FlowEdgeDesc(int(a), int(b), int(c)) for a, b, c in edges])
-        nn = A._arr(C.c_int, [g[0] for g in graphs])
-        off = A._arr(C.c_int64, offs)
-        fl = (C.c_int64 * max(1, len(edges)))()
-        val = (C.c_int64 * max(1, G))()
-        self._chk(self.lib.oserve_gpu_max_flow_batch(self.h, G, nn, off, ed, A._arr(C.c_int, sources),
-                                                     A._arr(C.c_int, sinks), fl, val))
-        return [(val[g], list(fl[offs[g]:offs[g + 1]])) for g in range(G)]
+        offs = np.zeros(len(graphs) + 1, np.int64)
+        offs[1:] = np.cumsum([len(es) for _, es in graphs])
+        edges = [e for _, es in graphs for e in es]
+        val, fl = self.max_flow_arrays(np.asarray([g[0] for g in graphs], np.int32), offs, edges, sources, sinks)
+        return [(int(val[i]), fl[offs[i]:offs[i + 1]].tolist()) for i in range(len(graphs))]
+
+    def max_flow_arrays(self, num_nodes: np.ndarray, edge_offset: np.ndarray, edges, sources, sinks):
+        """Array form: num_nodes [G] i32, edge_offset [G+1] i64, edges (flow_edge_dtype or tuples)
+        -> (values [G], flows [E])."""
+        keep = A.Keep()
+        G = len(num_nodes)
+        nn = keep(np.ascontiguousarray(num_nodes, dtype=np.int32))
+        off = keep(np.ascontiguousarray(edge_offset, dtype=np.int64))
+        ed = A.flow_edges(edges, keep)
+        E = int(off[-1] - off[0]) if G else 0
+        fl = np.zeros(max(1, E), np.int64)
+        val = np.zeros(max(1, G), np.int64)
+        src = keep(np.ascontiguousarray(sources, dtype=np.int32))
+        snk = keep(np.ascontiguousarray(sinks, dtype=np.int32))
+        self._chk(self.lib.oserve_gpu_max_flow_batch(self.h, G, _np_ptr(nn, C.c_int), _np_ptr(off, C.c_int64), ed,
+                                                     _np_ptr(src, C.c_int), _np_ptr(snk, C.c_int),
+                                                     _np_ptr(fl, C.c_int64), _np_ptr(val, C.c_int64)))
+        return val[:G], fl[:E]
 
     def flow_assign_batch(self, n: np.ndarray, e: np.ndarray, lam: np.ndarray, edge_flows: bool = False):
         """build_network + max_flow + extract_assignment per instance [count][R][J]."""
@@ -397,8 +407,10 @@ class GpuContext:
         return f, obj
 
     def kv_plan(self, inflight: Sequence[core.InflightRequest], threshold_tokens: int, src: core.Deployment,
-                dst: core.Deployment, headroom: float = 0.1, carry: Optional[core.SwitchPlan] = None) -> core.KvPlan:
-        """switchplan::kv_plan (switchplan.cpp:142-207) on the device (K5)."""
+                dst: core.Deployment, headroom: float = 0.1, carry: Optional[core.SwitchPlan] = None,
+                as_arrays: bool = False):
+        """switchplan::kv_plan (switchplan.cpp:142-207) on the device (K5).
+        as_arrays: (drained ids, migrated [n,4] int64 rows, buffer_bytes)."""
         keep = A.Keep()
         s, d = A.deployment_desc(src, keep), A.deployment_desc(dst, keep)
         reqs = A.inflight_arr(inflight, keep)
@@ -410,6 +422,8 @@ class GpuContext:
         self._chk(self.lib.oserve_gpu_kv_plan(self.h, n, reqs, threshold_tokens, C.byref(s), C.byref(d),
                                               float(headroom), ntr, tr, drained, C.byref(nd), mig, C.byref(nm),
                                               C.byref(buf)))
+        if as_arrays:
+            return A.kv_arrays(drained, nd.value, mig, nm.value, buf.value)
         return core.KvPlan(list(drained[:nd.value]),
                            [core.KvTransfer(m.request_id, m.kv_bytes, m.src, m.dst) for m in mig[:nm.value]],
                            buf.value)

@@ -172,6 +172,31 @@ struct Space {
 
 }  // namespace
 
+// Per-task arrays of the frontier-parallel exact path (double-buffered for
+// the splitting rounds; kept in the context so repeated rounds reuse them).
+struct TaskBufs {
+    DBuf plan, td, path, g, lb, m, inc, vis, nodes, cap, done, nch;
+    void bind(ExactTasks &e, uint64_t n) {
+        e.plan = static_cast<uint32_t *>(plan.get(sizeof(uint32_t) * n));
+        e.tdepth = static_cast<uint8_t *>(td.get(n));
+        e.path = static_cast<int32_t *>(path.get(sizeof(int32_t) * n * kTaskDepthMax));
+        e.g = static_cast<int64_t *>(g.get(sizeof(int64_t) * n));
+        e.lb = static_cast<int64_t *>(lb.get(sizeof(int64_t) * n));
+        e.m = static_cast<int64_t *>(m.get(sizeof(int64_t) * n));
+        e.inc = static_cast<int64_t *>(inc.get(sizeof(int64_t) * n));
+        e.vis = static_cast<uint8_t *>(vis.get(n));
+        e.nodes = static_cast<int64_t *>(nodes.get(sizeof(int64_t) * n));
+        e.capped = static_cast<uint8_t *>(cap.get(n));
+        e.done = static_cast<uint8_t *>(done.get(n));
+        e.nchild = static_cast<uint32_t *>(nch.get(sizeof(uint32_t) * n));
+    }
+};
+
+struct ExactScratch {
+    DBuf depth, nt, off, top, opt, ist, state, bx, run, ranks, newoff;
+    TaskBufs bufs[2];
+};
+
 struct oserve_gpu_ctx {
     int device = 0;
     int sm_count = 148;
@@ -212,6 +237,7 @@ struct oserve_gpu_ctx {
     size_t cub_temp_bytes = 0;
     DBuf d_key, d_obj, d_spp, d_x, d_used, d_aborted, d_aborted_n, d_ranks, d_listR, d_listOff, d_listShapes,
         d_listLam, d_sw[12];
+    ExactScratch exact;
 
     int D() const { return static_cast<int>(dev_sorted.size()); }
     int machine(int d) const {
@@ -687,7 +713,7 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
                const PlanOutputs &eo, const SolveParams &prm, const Space *sp) {
     cudaStream_t s = c.stream;
     PlanSource src = src0;
-    DBuf d_exact_ranks;
+    DBuf &d_exact_ranks = c.exact.ranks;
     if (sp && src.mode == 0) {
         // restrict to this shard's exact-path plans
         std::vector<uint64_t> ranks;
@@ -706,17 +732,17 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
     }
     if (src.count == 0) return;
     const uint64_t P = src.count;
-    DBuf b_depth, b_nt, b_off, b_top, b_opt, b_ist, b_state, b_bx, b_run;
+    ExactScratch &xs = c.exact;
     ExactTasks et{};
-    et.depth = static_cast<int32_t *>(b_depth.get(sizeof(int32_t) * P));
-    et.ntask = static_cast<uint64_t *>(b_nt.get(sizeof(uint64_t) * P));
-    et.toff = static_cast<uint64_t *>(b_off.get(sizeof(uint64_t) * P));
-    et.top_nodes = static_cast<int64_t *>(b_top.get(sizeof(int64_t) * P));
-    et.opt = static_cast<int64_t *>(b_opt.get(sizeof(int64_t) * P));
-    et.istar = static_cast<int64_t *>(b_ist.get(sizeof(int64_t) * P));
-    et.state = static_cast<uint8_t *>(b_state.get(P));
-    et.bx = static_cast<int32_t *>(b_bx.get(sizeof(int32_t) * P * kMaxExactCells));
-    et.running = static_cast<unsigned long long *>(b_run.get(sizeof(unsigned long long) * P));
+    et.depth = static_cast<int32_t *>(xs.depth.get(sizeof(int32_t) * P));
+    et.ntask = static_cast<uint64_t *>(xs.nt.get(sizeof(uint64_t) * P));
+    et.toff = static_cast<uint64_t *>(xs.off.get(sizeof(uint64_t) * P));
+    et.top_nodes = static_cast<int64_t *>(xs.top.get(sizeof(int64_t) * P));
+    et.opt = static_cast<int64_t *>(xs.opt.get(sizeof(int64_t) * P));
+    et.istar = static_cast<int64_t *>(xs.ist.get(sizeof(int64_t) * P));
+    et.state = static_cast<uint8_t *>(xs.state.get(P));
+    et.bx = static_cast<int32_t *>(xs.bx.get(sizeof(int32_t) * P * kMaxExactCells));
+    et.running = static_cast<unsigned long long *>(xs.run.get(sizeof(unsigned long long) * P));
     // ~2^21 tasks in flight at most; at least a few thousand per plan when few plans
     const uint64_t budget_tasks = uint64_t{1} << 21;
     static const uint64_t target_env = [] {
@@ -741,25 +767,7 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
     }
     cuda_ok(h2d(et.toff, off.data(), sizeof(uint64_t) * P, s), "H2D");
     cuda_ok(h2d(et.state, state.data(), P, s), "H2D");
-    // per-task arrays, double-buffered for the splitting rounds
-    struct TaskBufs {
-        DBuf plan, td, path, g, lb, m, inc, vis, nodes, cap, done, nch;
-        void bind(ExactTasks &e, uint64_t n) {
-            e.plan = static_cast<uint32_t *>(plan.get(sizeof(uint32_t) * n));
-            e.tdepth = static_cast<uint8_t *>(td.get(n));
-            e.path = static_cast<int32_t *>(path.get(sizeof(int32_t) * n * kTaskDepthMax));
-            e.g = static_cast<int64_t *>(g.get(sizeof(int64_t) * n));
-            e.lb = static_cast<int64_t *>(lb.get(sizeof(int64_t) * n));
-            e.m = static_cast<int64_t *>(m.get(sizeof(int64_t) * n));
-            e.inc = static_cast<int64_t *>(inc.get(sizeof(int64_t) * n));
-            e.vis = static_cast<uint8_t *>(vis.get(n));
-            e.nodes = static_cast<int64_t *>(nodes.get(sizeof(int64_t) * n));
-            e.capped = static_cast<uint8_t *>(cap.get(n));
-            e.done = static_cast<uint8_t *>(done.get(n));
-            e.nchild = static_cast<uint32_t *>(nch.get(sizeof(uint32_t) * n));
-        }
-    };
-    TaskBufs bufs[2];
+    TaskBufs *bufs = c.exact.bufs;
     int cur = 0;
     if (total) {
         bufs[cur].bind(et, total);
@@ -805,8 +813,7 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
             const uint64_t ntot = newoff[total];
             ExactTasks ne = et;
             bufs[cur ^ 1].bind(ne, ntot);
-            DBuf d_off;
-            uint64_t *d_newoff = d_off.upload(newoff, s);
+            uint64_t *d_newoff = xs.newoff.upload(newoff, s);
             cuda_ok(launch_exact_split(c.tables, view, src, prm, et, ne, d_newoff, total, c.sm_count, s, &c.launches),
                     "exact split");
             for (uint64_t i = 0; i < P; ++i) {  // per-plan ranges in the new list
@@ -1604,6 +1611,8 @@ int oserve_gpu_kv_plan(oserve_gpu_ctx *ctx, int n_inflight, const oserve_infligh
         in.dev_id = b[4].upload(dev_id, s);
         in.src_reps = src->num_replicas;
         in.dst_reps = dst->num_replicas;
+        in.n_src_devs = static_cast<int>(sdev.size());
+        in.n_dst_devs = static_cast<int>(ddev.size());
         in.src_off = b[5].upload(soff, s);
         in.src_devs = b[6].upload(sdev, s);
         in.dst_off = b[7].upload(doff, s);

@@ -229,6 +229,7 @@ struct KvPlanIn {
     const int32_t *machine;      // [slots]
     const int32_t *dev_id;       // [slots]
     int src_reps, dst_reps;
+    int n_src_devs, n_dst_devs;  // lengths of src_devs / dst_devs
     const int32_t *src_off;      // [src_reps+1] into src_devs
     const int32_t *src_devs;     // device slots
     const int32_t *dst_off;

@@ -1729,7 +1729,6 @@ __global__ void __launch_bounds__(256) k_switch_cost(SwitchDeps d, SwitchOut o) 
     __shared__ unsigned long long wbytes[8];
     __shared__ int wstatus[8];
     const int pair = blockIdx.x;
-    const int ND = d.num_devices;
     const int deps[2] = {0, pair + 1};
     // ---- layouts (switchplan.cpp:40-63): one slice per device slot ----
     for (int i = threadIdx.x; i < 2 * kSwMaxDev; i += blockDim.x) {
@@ -1858,44 +1857,94 @@ __device__ __forceinline__ KvPick kv_warp_min(KvPick p) {
     return p;
 }
 
-__global__ void __launch_bounds__(32) k_kv_plan(KvPlanIn in) {
+// One warp.  The slot tables (inbound loads, the link-load matrix, machines,
+// replica device lists) are staged in shared memory when they fit (the
+// common case: <= ~150 device slots), so each request's selections are
+// shared-memory reductions; request fields are prefetched 32 at a time, one
+// per lane, and broadcast by shuffles; results are written back coalesced
+// by the owning lane.
+__global__ void __launch_bounds__(32) k_kv_plan(KvPlanIn in, int use_smem) {
+    extern __shared__ __align__(16) unsigned char kv_smem[];
     const int lane = threadIdx.x;
     constexpr int kNone = 0x7fffffff;
-    int rr = 0;
-    for (int q = 0; q < in.n; ++q) {
-        if (in.gen[q] <= in.threshold || in.dst_reps == 0) {
-            if (lane == 0) in.kind[q] = 0;  // drained
-            continue;
+    const int NS = in.num_slots;
+    const int nsd = in.n_src_devs, ndd = in.n_dst_devs;
+    uint64_t *inbound = in.inbound, *load = in.load;
+    const int32_t *machine = in.machine, *src_off = in.src_off, *src_devs = in.src_devs, *dst_off = in.dst_off,
+                  *dst_devs = in.dst_devs;
+    if (use_smem) {
+        uint64_t *sl = reinterpret_cast<uint64_t *>(kv_smem);
+        uint64_t *si = sl + static_cast<size_t>(NS) * NS;
+        int32_t *sm = reinterpret_cast<int32_t *>(si + NS);
+        int32_t *so = sm + NS, *sd = so + in.src_reps + 1, *to = sd + nsd, *td = to + in.dst_reps + 1;
+        for (int i = lane; i < NS * NS; i += 32) sl[i] = in.load[i];
+        for (int i = lane; i < NS; i += 32) {
+            si[i] = 0;
+            sm[i] = in.machine[i];
         }
-        const int trep = rr % in.dst_reps;
-        ++rr;
-        // target: least inbound-loaded device of the target replica, lowest id on ties
-        KvPick t{~0ull, 2, kNone};
-        for (int p = in.dst_off[trep] + lane; p < in.dst_off[trep + 1]; p += 32) {
-            const KvPick c{in.inbound[in.dst_devs[p]], 0, in.dst_devs[p]};
-            if (kv_less(c, t)) t = c;
-        }
-        t = kv_warp_min(t);
-        const int target = t.slot == kNone ? in.none_slot : t.slot;
-        // source: intra-machine first, then least load toward target, then lowest id
-        const int srep = in.srcrep[q];
-        KvPick b{~0ull, 2, kNone};
-        for (int p = in.src_off[srep] + lane; p < in.src_off[srep + 1]; p += 32) {
-            const int slot = in.src_devs[p];
-            const bool intra = in.machine[slot] >= 0 && in.machine[slot] == in.machine[target];
-            const KvPick c{in.load[static_cast<size_t>(slot) * in.num_slots + target], intra ? 0 : 1, slot};
-            if (kv_less(c, b)) b = c;
-        }
-        b = kv_warp_min(b);
-        const int best = b.slot == kNone ? in.none_slot : b.slot;
-        if (lane == 0) {
-            in.load[static_cast<size_t>(best) * in.num_slots + target] += in.kv[q];
-            in.inbound[target] += in.kv[q];
-            in.kind[q] = 1;
-            in.mig_src[q] = in.dev_id[best];
-            in.mig_dst[q] = in.dev_id[target];
-        }
+        for (int i = lane; i <= in.src_reps; i += 32) so[i] = in.src_off[i];
+        for (int i = lane; i < nsd; i += 32) sd[i] = in.src_devs[i];
+        for (int i = lane; i <= in.dst_reps; i += 32) to[i] = in.dst_off[i];
+        for (int i = lane; i < ndd; i += 32) td[i] = in.dst_devs[i];
         __syncwarp();
+        load = sl;
+        inbound = si;
+        machine = sm;
+        src_off = so;
+        src_devs = sd;
+        dst_off = to;
+        dst_devs = td;
+    }
+    int trep = 0;
+    for (int base = 0; base < in.n; base += 32) {
+        const int q = base + lane;
+        const bool has = q < in.n;
+        const int64_t my_gen = has ? in.gen[q] : 0;
+        const uint64_t my_kv = has ? in.kv[q] : 0;
+        const int my_sr = has ? in.srcrep[q] : 0;
+        int my_kind = 0, my_src = 0, my_dst = 0;
+        const int cnt = in.n - base < 32 ? in.n - base : 32;
+        for (int b = 0; b < cnt; ++b) {
+            const int64_t gq = __shfl_sync(0xffffffffu, my_gen, b);
+            if (gq <= in.threshold || in.dst_reps == 0) continue;  // drained
+            const uint64_t kvq = __shfl_sync(0xffffffffu, my_kv, b);
+            const int srq = __shfl_sync(0xffffffffu, my_sr, b);
+            // target: least inbound-loaded device of the target replica, lowest id on ties
+            KvPick t{~0ull, 2, kNone};
+            for (int p = dst_off[trep] + lane; p < dst_off[trep + 1]; p += 32) {
+                const KvPick c{inbound[dst_devs[p]], 0, dst_devs[p]};
+                if (kv_less(c, t)) t = c;
+            }
+            t = kv_warp_min(t);
+            trep = trep + 1 == in.dst_reps ? 0 : trep + 1;
+            const int target = t.slot == kNone ? in.none_slot : t.slot;
+            // source: intra-machine first, then least load toward target, then lowest id
+            KvPick bsel{~0ull, 2, kNone};
+            const int mt = machine[target];
+            for (int p = src_off[srq] + lane; p < src_off[srq + 1]; p += 32) {
+                const int slot = src_devs[p];
+                const bool intra = machine[slot] >= 0 && machine[slot] == mt;
+                const KvPick c{load[static_cast<size_t>(slot) * NS + target], intra ? 0 : 1, slot};
+                if (kv_less(c, bsel)) bsel = c;
+            }
+            bsel = kv_warp_min(bsel);
+            const int best = bsel.slot == kNone ? in.none_slot : bsel.slot;
+            if (lane == 0) {
+                load[static_cast<size_t>(best) * NS + target] += kvq;
+                inbound[target] += kvq;
+            }
+            if (lane == b) {
+                my_kind = 1;
+                my_src = best;
+                my_dst = target;
+            }
+            __syncwarp();
+        }
+        if (has) {
+            in.kind[q] = my_kind;
+            in.mig_src[q] = my_kind ? in.dev_id[my_src] : 0;
+            in.mig_dst[q] = my_kind ? in.dev_id[my_dst] : 0;
+        }
     }
 }
 
@@ -2129,7 +2178,17 @@ int sort_keys(uint64_t *keys, uint64_t *tmp_keys, int n, void **temp, size_t *te
 int launch_kv_plan(const KvPlanIn &in, void *stream, uint64_t *launches) {
     cudaGetLastError();
     if (in.n == 0) return 0;
-    k_kv_plan<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(in);
+    const size_t NS = static_cast<size_t>(in.num_slots);
+    const size_t smem = sizeof(uint64_t) * (NS * NS + NS) +
+                        sizeof(int32_t) * (NS + in.src_reps + 1 + in.dst_reps + 1 + in.n_src_devs + in.n_dst_devs);
+    int use = smem <= 200 * 1024;
+    if (use && smem > 48 * 1024) {
+        if (cudaFuncSetAttribute(k_kv_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess) {
+            cudaGetLastError();
+            use = 0;
+        }
+    }
+    k_kv_plan<<<1, 32, use ? smem : 0, static_cast<cudaStream_t>(stream)>>>(in, use);
     if (launches) ++*launches;
     return check(cudaGetLastError());
 }
