@@ -31,6 +31,9 @@
 #ifndef OSERVE_K1_MINB
 #define OSERVE_K1_MINB 4  // CTAs of 256 threads per SM the register budget must allow (64 regs; measured 5% faster than 3)
 #endif
+#ifndef OSERVE_K1_MINB_1
+#define OSERVE_K1_MINB_1 OSERVE_K1_MINB  // one replica per lane (KPL = 1)
+#endif
 
 namespace oserve_gpu {
 
@@ -259,7 +262,7 @@ __host__ __device__ constexpr size_t group_scratch_bytes(int J, int RMAX, int KP
 }
 
 template <int G, int KPL, bool SMEM>
-__global__ void __launch_bounds__(256, OSERVE_K1_MINB) k_plan_eval(ShapeTables t, SpaceTables sp, KeyLayout key,
+__global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_MINB) k_plan_eval(ShapeTables t, SpaceTables sp, KeyLayout key,
                                                                    PlanSource src, PlanOutputs out, SolveParams prm,
                                                                    int skip_exact) {
     using Grp = Group<G, KPL>;

@@ -273,6 +273,15 @@ def test_gpu_matches_reference_goldens(cuda, name):
         st = g.exhaustive() if name.startswith("cfg1") else g.round(w.space_mode, w.space_sizes)
         assert st.throughput == gr["objective"]
         assert [[r.device_ids, r.tp, r.pp] for r in st.deployment.replicas] == gr["deployment"]
+        if "local_rank" in gr:
+            assert (st.partition_index, st.local_rank, st.sum_pp) == \
+                (gr["partition_index"], gr["local_rank"], gr["sum_pp"])
+        if "all_objective_sha256" in gr:  # every plan of the space, full size (oracle/gen_rounds_full.py)
+            import hashlib
+            obj, _ = g.evaluate_ranks(0, plans)
+            assert int(obj.sum()) == gr["objective_sum"]
+            assert hashlib.sha256(np.ascontiguousarray(obj, dtype="<i8").tobytes()).hexdigest() == \
+                gr["all_objective_sha256"]
 
 
 def test_gpu_switch_matches_reference_goldens(cuda):
