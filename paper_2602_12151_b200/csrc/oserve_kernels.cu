@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "oserve_internal.h"
@@ -146,6 +147,11 @@ __global__ void k_normalize_rows(ShapeTables t) {
 }
 
 // ------------------------------------------------------- plan resolution --
+__device__ __forceinline__ uint64_t div_small(uint64_t a, uint64_t b) {
+    if ((a >> 32) == 0 && (b >> 32) == 0) return static_cast<uint32_t>(a) / static_cast<uint32_t>(b);
+    return a / b;
+}
+
 // Largest p with prefix[p] <= g (skips empty partitions automatically).
 __device__ __forceinline__ int64_t find_partition(const SpaceTables &sp, uint64_t g) {
     int64_t lo = 0, hi = sp.num_parts - 1;
@@ -158,7 +164,7 @@ __device__ __forceinline__ int64_t find_partition(const SpaceTables &sp, uint64_
 }
 
 __device__ __forceinline__ uint64_t shard_rank(const PlanSource &src, uint64_t li) {
-    const uint64_t c = li / src.chunk;
+    const uint64_t c = div_small(li, src.chunk);
     return (c * static_cast<uint64_t>(src.world) + static_cast<uint64_t>(src.rank)) * src.chunk + (li - c * src.chunk);
 }
 
@@ -174,6 +180,50 @@ __device__ __forceinline__ uint64_t source_rank(const PlanSource &src, uint64_t 
         else hi = mid - 1;
     }
     return __ldg(src.range_start + lo) + (b - __ldg(src.range_prefix + lo));
+}
+
+// source_rank with the current rank range cached (consecutive launch-local
+// indices stay inside one range almost always).
+#ifdef OSERVE_K1_STATS
+__device__ unsigned long long g_k1_stats[4];
+#endif
+// Group-uniform K1 state carried across plans (shared memory, written by
+// lane 0 only; read after the next group sync).
+struct K1Carry {
+    uint64_t r_lo, r_hi, r_start;  // current rank range (mode 3)
+    uint64_t cp_lo, cp_hi;         // current partition's plan-rank interval
+    int64_t cpart;
+    uint64_t snap_hi;              // snapshot: prefix digits and partition
+    int64_t snap_part;
+    uint64_t best;                 // group's best key (lane 0 only)
+    uint64_t tk_max;               // worst key kept in the top-K list
+    int tk_idx;                    // its slot (lane 0 only)
+    int lossy;                     // the list dropped a key (lane 0 only)
+};
+// (rlo, rhi, rst): the carried range, read by the caller before any lane
+// of the group may update it.
+__device__ __forceinline__ uint64_t source_rank_cached(const PlanSource &src, uint64_t li, K1Carry *c, int gl,
+                                                       uint64_t rlo, uint64_t rhi, uint64_t rst) {
+    if (src.mode == 1) return src.ranks[li];
+    const uint64_t b = shard_rank(src, li);
+    if (src.mode == 0) return b;
+    if (b < rlo || b >= rhi) {
+        int lo = 0, hi = src.num_ranges - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (__ldg(src.range_prefix + mid) <= b) lo = mid;
+            else hi = mid - 1;
+        }
+        rlo = __ldg(src.range_prefix + lo);
+        rhi = lo + 1 < src.num_ranges ? __ldg(src.range_prefix + lo + 1) : ~uint64_t{0};
+        rst = __ldg(src.range_start + lo);
+        if (gl == 0) {
+            c->r_lo = rlo;
+            c->r_hi = rhi;
+            c->r_start = rst;
+        }
+    }
+    return rst + (b - rlo);
 }
 
 // Unrank a non-decreasing pick sequence of length len over [0, q) (lex order).
@@ -205,16 +255,13 @@ __device__ __forceinline__ int32_t quot_small(int64_t m, int64_t u, double inv_u
     return static_cast<int32_t>(q);
 }
 
-__device__ __forceinline__ uint64_t div_small(uint64_t a, uint64_t b) {
-    if ((a >> 32) == 0 && (b >> 32) == 0) return static_cast<uint32_t>(a) / static_cast<uint32_t>(b);
-    return a / b;
-}
 
 // ------------------------------------------------------------------- K1 ---
 // Group of G lanes evaluates one plan; lane gl owns replicas k = gl + G*kk.
 template <int G, int KPL>
 struct Group {
     static constexpr int RMAX = G * KPL;
+    static constexpr int kG = G;
     unsigned mask;
     int gl, base;
     __device__ __forceinline__ Group() {
@@ -256,15 +303,51 @@ struct Group {
     }
 };
 
-__host__ __device__ constexpr size_t group_scratch_bytes(int J, int RMAX, int KPL) {
-    return ((size_t)kTopK * 8 + (size_t)J * RMAX * 4 + (size_t)kMaxJ * KPL * 4 + (size_t)RMAX * 2 + RMAX + 15) &
+// Greedy-prefix reuse (K1): x changes of the exchange since the snapshot,
+// one u32 per change ((cell << 1) | was_increment), 3 slots per move.
+constexpr int kUndo = 96;
+constexpr uint64_t kGroupChunk = 32;  // plans per contiguous group chunk
+
+// Per-group scratch: the fixed-size arrays first (compile-time offsets from
+// one base register), the J-sized assignment x last.
+template <int RMAX, int KPL>
+__host__ __device__ constexpr size_t group_fixed_bytes() {
+    return ((size_t)kTopK * 8 + (size_t)RMAX * 8 + (size_t)kMaxJ * KPL * 4 + (size_t)(RMAX / KPL) * 4 +
+            (size_t)RMAX * 8 + (size_t)kUndo * 4 + sizeof(K1Carry) + (size_t)RMAX * 2 + RMAX + 15) &
            ~size_t(15);
+}
+template <int RMAX, int KPL>
+__host__ __device__ constexpr size_t group_scratch_bytes(int J) {
+    return group_fixed_bytes<RMAX, KPL>() + (((size_t)J * RMAX * 4 + 15) & ~size_t(15));
+}
+
+// Group-uniform unranking of one run of `len` non-decreasing picks over
+// [0, q) with rank rr (same order as unrank_run): the count of each value v
+// is the largest m with rr < C(rem - m + K, K), K = q - v - 1 (the
+// sequences holding >= m copies of v come first); lanes fill the positions.
+template <class Grp>
+__device__ __forceinline__ void unrank_run_group(const Grp &g, uint64_t rr, int len, int q, uint8_t *out) {
+    int rem = len, pos = 0;
+    for (int v = 0; v < q - 1 && rem > 0; ++v) {
+        const int K = q - v - 1;
+        int lo = 0, hi = rem;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (rr < c_binom[rem - mid + K][K]) lo = mid;
+            else hi = mid - 1;
+        }
+        if (lo < rem) rr -= c_binom[rem - lo - 1 + K][K];
+        for (int p = g.gl; p < lo; p += Grp::kG) out[pos + p] = static_cast<uint8_t>(v);
+        pos += lo;
+        rem -= lo;
+    }
+    for (int p = g.gl; p < rem; p += Grp::kG) out[pos + p] = static_cast<uint8_t>(q - 1);
 }
 
 template <int G, int KPL, bool SMEM>
 __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_MINB) k_plan_eval(ShapeTables t, SpaceTables sp, KeyLayout key,
                                                                    PlanSource src, PlanOutputs out, SolveParams prm,
-                                                                   int skip_exact) {
+                                                                   int skip_exact, int gchunk) {
     using Grp = Group<G, KPL>;
     constexpr int RMAX = Grp::RMAX;
     constexpr int GPB = 256 / G;
@@ -318,33 +401,70 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
 
     // ---- per-group scratch ----
     const int gib = threadIdx.x / G;
-    const size_t per_group = group_scratch_bytes(J, RMAX, KPL);
+    const size_t per_group = group_scratch_bytes<RMAX, KPL>(J);
     unsigned char *gs = smem + off + per_group * gib;
     uint64_t *tks = reinterpret_cast<uint64_t *>(gs);                   // [kTopK] top-K candidate list
-    int32_t *xs = reinterpret_cast<int32_t *>(tks + kTopK);             // [J][RMAX] assignment x
-    uint32_t *Am = reinterpret_cast<uint32_t *>(xs + J * RMAX);         // [kMaxJ][KPL] direct-take masks
-    uint16_t *shpS = reinterpret_cast<uint16_t *>(Am + kMaxJ * KPL);    // [RMAX] shape per replica
+    int64_t *snM = reinterpret_cast<int64_t *>(tks + kTopK);            // [KPL][G] snapshot: mrem
+    uint32_t *Am = reinterpret_cast<uint32_t *>(snM + RMAX);            // [kMaxJ][KPL] direct-take masks
+    int32_t *snL = reinterpret_cast<int32_t *>(Am + kMaxJ * KPL);       // [G] snapshot: lam per class lane
+    uint32_t *snH = reinterpret_cast<uint32_t *>(snL + G);              // [KPL][G] snapshot: held
+    uint32_t *snA = snH + RMAX;                                         // [KPL][G] snapshot: A words
+    uint32_t *ulog = snA + RMAX;                                        // [kUndo] exchange x changes
+    K1Carry *cy = reinterpret_cast<K1Carry *>(ulog + kUndo);            // carried lookups / snapshot key
+    uint16_t *shpS = reinterpret_cast<uint16_t *>(cy + 1);              // [RMAX] shape per replica
     uint8_t *pick = reinterpret_cast<uint8_t *>(shpS + RMAX);           // [RMAX] candidate pick per replica
+    int32_t *xs = reinterpret_cast<int32_t *>(gs + group_fixed_bytes<RMAX, KPL>());  // [J][RMAX] assignment x
     unsigned long long *blk_best = reinterpret_cast<unsigned long long *>(smem + off + per_group * GPB);
     __syncthreads();
 
     const Grp g;
     int jw = 1;
     while (jw < J) jw <<= 1;  // scan width over class positions
-    uint64_t best = kNoKey;
     constexpr int TKE = kTopK / G;  // top-K list entries per lane (shared memory)
     for (int e = 0; e < TKE; ++e) tks[g.gl * TKE + e] = kNoKey;
-    uint64_t tk_max = kNoKey;
-    int tk_idx = 0;
-    bool lossy = false;
     const uint64_t ngroups = static_cast<uint64_t>(gridDim.x) * GPB;
 
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * GPB + gib; i < src.count; i += ngroups) {
+    // Each group walks contiguous chunks of `gchunk` plans, so consecutive
+    // plans of a group usually share their partition and every pick but the
+    // last run's: the partition / rank-range lookups are cached, and the
+    // greedy state at the start of the last run (a step boundary) is kept as
+    // a snapshot that the next plan with the same prefix resumes from (the
+    // exchange's x changes since are undone from a log).
+#ifdef OSERVE_K1_GCH1
+    gchunk = 1;
+#endif
+    const uint64_t gch = static_cast<uint64_t>(gchunk > 0 ? gchunk : 1);
+#ifdef OSERVE_K1_STATS
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        printf("K1 stats so far: plans %llu reuse %llu greedy steps %llu moves %llu\n", g_k1_stats[0], g_k1_stats[1],
+               g_k1_stats[2], g_k1_stats[3]);
+    unsigned long long st_plans = 0, st_reuse = 0, st_steps = 0, st_moves = 0;
+#endif
+    if (g.gl == 0) {
+        cy->r_lo = 1;
+        cy->r_hi = 0;
+        cy->cp_lo = 1;
+        cy->cp_hi = 0;
+        cy->cpart = -1;
+        cy->snap_part = -1;
+        cy->best = kNoKey;
+        cy->tk_max = kNoKey;
+        cy->tk_idx = 0;
+        cy->lossy = 0;
+    }
+    // x changes logged since the snapshot; -1: no live snapshot
+    int nlog = -1;
+    g.sync();
+
+    for (uint64_t cb = (static_cast<uint64_t>(blockIdx.x) * GPB + gib) * gch; cb < src.count; cb += ngroups * gch)
+    for (uint64_t i = cb, ce = (cb + gch < src.count ? cb + gch : src.count); i < ce; ++i) {
         // ---- resolve the plan ----
         int R;
         int shp[KPL];
         int64_t part = 0;
-        uint64_t local = 0;
+        uint64_t local = 0, hi = 0;
+        int P = 0;            // first replica of the partition's last run
+        bool reuse = false;   // resume the greedy from the snapshot at P
         const int64_t *lam_src = prm.lambda;
         if (src.mode == 2) {
             const uint64_t li = src.first + i;
@@ -361,20 +481,78 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                 for (int j = 0; j < J; ++j) tot += lam_src[j];
                 if (tot <= prm.exact_demand_limit && R * J <= prm.exact_cell_limit) continue;
             }
+            nlog = -1;
         } else {
-            const uint64_t gr = source_rank(src, src.first + i);
-            part = find_partition(sp, gr);
+            const uint64_t rlo = cy->r_lo, rhi = cy->r_hi, rst = cy->r_start;
+            uint64_t cp_lo = cy->cp_lo;
+            const uint64_t cp_hi = cy->cp_hi;
+            part = cy->cpart;
+            g.sync();  // every lane has read the carry before lane 0 updates it
+            const uint64_t gr = source_rank_cached(src, src.first + i, cy, g.gl, rlo, rhi, rst);
+            if (gr < cp_lo || gr >= cp_hi) {
+                part = find_partition(sp, gr);
+                cp_lo = __ldg(sp.prefix + part);
+                if (g.gl == 0) {
+                    cy->cpart = part;
+                    cy->cp_lo = cp_lo;
+                    cy->cp_hi = __ldg(sp.prefix + part + 1);
+                }
+            }
             if (skip_exact && sp.exact[part]) continue;
-            local = gr - __ldg(sp.prefix + part);
+            local = gr - cp_lo;
             R = sp.R[part];
             const int ro = sp.rep_off[part], runo = sp.run_off[part], nr = sp.nruns[part];
-            for (int ri = g.gl; ri < nr; ri += G) {
-                const uint64_t w = sp.run_weight[runo + ri], c = sp.run_count[runo + ri];
-                uint64_t rr = div_small(local, w);
-                rr = rr - div_small(rr, c) * c;
-                const int q = sp.run_q[runo + ri], len = sp.run_len[runo + ri], st = sp.run_start[runo + ri];
-                if (len == 1) pick[st] = static_cast<uint8_t>(rr);
-                else unrank_run(rr, len, q, pick + st);
+            // the last run with a choice (later runs have one multiset each)
+            int lr = runo + nr - 1;
+            while (lr > runo && sp.run_count[lr] == 1) --lr;
+            P = sp.run_start[lr];
+            const uint64_t lc = sp.run_count[lr];
+            hi = div_small(local, lc);
+            const uint64_t rl = local - hi * lc;  // run lr's own rank (weight 1)
+            reuse = nlog >= 0 && part == cy->snap_part && hi == cy->snap_hi;
+#ifdef OSERVE_K1_NOREUSE
+            reuse = false;
+#endif
+            if (!reuse) {
+                // runs of one replica: lane-parallel; longer runs: group-uniform
+                uint32_t longm[KPL];
+#pragma unroll
+                for (int t = 0; t < KPL; ++t) {
+                    const int ri = g.gl + G * t;
+                    bool lng = false;
+                    if (ri < nr && runo + ri != lr) {
+                        const int len = sp.run_len[runo + ri];
+                        if (len == 1) {
+                            const uint64_t w = sp.run_weight[runo + ri], c = sp.run_count[runo + ri];
+                            uint64_t rr = div_small(local, w);
+                            rr = rr - div_small(rr, c) * c;
+                            pick[sp.run_start[runo + ri]] = static_cast<uint8_t>(rr);
+                        } else {
+                            lng = true;
+                        }
+                    }
+                    longm[t] = g.ballot(lng);
+                }
+#pragma unroll
+                for (int t = 0; t < KPL; ++t) {
+                    while (longm[t]) {
+                        const int ri = __ffs(longm[t]) - 1 + G * t;
+                        longm[t] &= longm[t] - 1;
+                        const uint64_t w = sp.run_weight[runo + ri], c = sp.run_count[runo + ri];
+                        uint64_t rr = div_small(local, w);
+                        rr = rr - div_small(rr, c) * c;
+                        unrank_run_group(g, rr, sp.run_len[runo + ri], sp.run_q[runo + ri],
+                                         pick + sp.run_start[runo + ri]);
+                    }
+                }
+            }
+            {
+                const int len = sp.run_len[lr];
+                if (len == 1) {
+                    if (g.gl == 0) pick[P] = static_cast<uint8_t>(rl);
+                } else {
+                    unrank_run_group(g, rl, len, sp.run_q[lr], pick + P);
+                }
             }
             g.sync();
 #pragma unroll
@@ -384,19 +562,52 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
             }
         }
 
-        // ---- init: lam (lane j holds class j), x = 0 ----
-        int32_t lamr = g.gl < J ? static_cast<int32_t>(lam_src[g.gl]) : 0;
+        // ---- init: lam (lane j holds class j), x = 0 (or the snapshot) ----
+        int32_t lamr;
+        int64_t mrem[KPL];
+        uint32_t held[KPL];
+        uint32_t areg[KPL];  // lane c: A[c] word per ownership slot, built replica by replica
 #pragma unroll
         for (int kk = 0; kk < KPL; ++kk) {
             const int k = g.gl + G * kk;
             if (k < R) shpS[k] = static_cast<uint16_t>(shp[kk]);
         }
-        {
+        if (reuse) {
+            // undo the previous plans' exchange moves (+-1 changes commute)
+            for (int e = g.gl; e < nlog; e += G) {
+                const uint32_t v = ulog[e];
+                if (v != 0xffffffffu) atomicAdd(&xs[v >> 1], (v & 1u) ? -1 : 1);
+            }
+            g.sync();
+            lamr = snL[g.gl];
+#pragma unroll
+            for (int kk = 0; kk < KPL; ++kk) {
+                const int k = g.gl + G * kk;
+                mrem[kk] = snM[kk * G + g.gl];
+                held[kk] = snH[kk * G + g.gl];
+                areg[kk] = snA[kk * G + g.gl];
+                if (k >= P && k < R)
+                    for (int j = 0; j < J; ++j) xs[j * RMAX + k] = 0;
+            }
+        } else {
+            nlog = -1;
+            lamr = g.gl < J ? static_cast<int32_t>(lam_src[g.gl]) : 0;
+#pragma unroll
+            for (int kk = 0; kk < KPL; ++kk) {
+                mrem[kk] = 0;
+                held[kk] = 0;
+                areg[kk] = 0;
+            }
             int4 *xz = reinterpret_cast<int4 *>(xs);
             const int n4 = (J * RMAX) >> 2;  // RMAX is a multiple of 4
             for (int q = g.gl; q < n4; q += G) xz[q] = make_int4(0, 0, 0, 0);
         }
+        if (reuse) nlog = 0;
         g.sync();
+#ifdef OSERVE_K1_STATS
+        ++st_plans;
+        st_reuse += reuse;
+#endif
 
         // ---- greedy_fill (flowassign.cpp:393-406) ----
         // Replicas in order; inside one replica the reference takes
@@ -406,24 +617,33 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
         // is one prefix scan of costs over its order positions (lane = position)
         // plus a ballot for the binding position.  Bit-identical to the
         // sequential fill; no 64-bit division.
-        int64_t mrem[KPL];
-        uint32_t held[KPL];
-        uint32_t areg[KPL];  // lane c: A[c] word per ownership slot, built replica by replica
-#pragma unroll
-        for (int kk = 0; kk < KPL; ++kk) {
-            mrem[kk] = 0;
-            held[kk] = 0;
-            areg[kk] = 0;
-        }
         // shape-run boundaries: bit k set when replica k+1 has another shape
+        // (or starts the last run: the snapshot point is a step boundary)
         uint32_t bnd[KPL];
 #pragma unroll
         for (int kk = 0; kk < KPL; ++kk) {
             const int k = g.gl + G * kk;
-            const bool last = k < R && (k + 1 == R || shpS[k + 1] != shpS[k]);
+            const bool last = k < R && (k + 1 == R || shpS[k + 1] != shpS[k] || k + 1 == P);
             bnd[kk] = g.ballot(last);
         }
-        for (int k = 0; k < R;) {
+        for (int k = reuse ? P : 0; k < R;) {
+#ifdef OSERVE_K1_STATS
+            ++st_steps;
+#endif
+            if (k == P && P > 0 && !reuse) {  // snapshot the prefix state
+                snL[g.gl] = lamr;
+#pragma unroll
+                for (int kk = 0; kk < KPL; ++kk) {
+                    snM[kk * G + g.gl] = mrem[kk];
+                    snH[kk * G + g.gl] = held[kk];
+                    snA[kk * G + g.gl] = areg[kk];
+                }
+                nlog = 0;
+                if (g.gl == 0) {
+                    cy->snap_part = part;
+                    cy->snap_hi = hi;
+                }
+            }
             const int s = shpS[k];
             const int ol = sOlen[s];
             const bool act = g.gl < ol;
@@ -623,7 +843,8 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
             }
             j2 = g.bcast(j2, ogl);
             k2 = g.bcast(k2, ogl);
-            // apply the move
+            // apply the move (logged while a snapshot is live)
+            const bool lg = nlog >= 0 && nlog + 3 <= kUndo;
 #pragma unroll
             for (int kk = 0; kk < KPL; ++kk) {
                 const int k = g.gl + G * kk;
@@ -638,13 +859,24 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                         mrem[kk] += sUnit[s * J + j2];
                         if (nv == 0) held[kk] &= ~(1u << j2);
                     }
+                    if (lg) {
+                        ulog[nlog] = (static_cast<uint32_t>(jf * RMAX + kf) << 1) | 1u;
+                        ulog[nlog + 1] = j2 >= 0 ? static_cast<uint32_t>(j2 * RMAX + kf) << 1 : 0xffffffffu;
+                        if (j2 < 0) ulog[nlog + 2] = 0xffffffffu;
+                    }
                 }
                 if (j2 >= 0 && k == k2) {
                     xs[j2 * RMAX + k2] += 1;
                     mrem[kk] -= sUnit[s * J + j2];
                     held[kk] |= 1u << j2;
+                    if (lg) ulog[nlog + 2] = (static_cast<uint32_t>(j2 * RMAX + k2) << 1) | 1u;
                 }
             }
+            if (lg) nlog += 3;
+            else nlog = -1;
+#ifdef OSERVE_K1_STATS
+            ++st_moves;
+#endif
             if (g.gl == jf) lamr -= 1;
             lam_mask = g.ballot(g.gl < J && lamr > 0);
             g.sync();
@@ -777,12 +1009,15 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
             const uint64_t kv = ((key.obj_max - served) << key.sh_obj) |
                                 (static_cast<uint64_t>(part) << key.sh_part) |
                                 (static_cast<uint64_t>(spp) << key.sh_spp) | local;
-            best = kv < best ? kv : best;
+            if (g.gl == 0 && kv < cy->best) cy->best = kv;
             if (out.topk) {
-                // per-group top-kTopK list, kTopK/G entries per lane (registers)
+                // per-group top-kTopK list, kTopK/G entries per lane (shared memory)
+                const uint64_t tk_max = cy->tk_max;
                 if (kv < tk_max) {
-                    if (tk_max != kNoKey) lossy = true;  // evicts the current worst
-                    if (g.gl == 0) tks[tk_idx] = kv;
+                    if (g.gl == 0) {
+                        if (tk_max != kNoKey) cy->lossy = 1;  // evicts the current worst
+                        tks[cy->tk_idx] = kv;
+                    }
                     g.sync();
                     uint64_t lm = tks[g.gl * TKE];
                     int ls = 0;
@@ -801,10 +1036,13 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                         gm = o > gm ? o : gm;
                     }
                     const int ml = __ffs(g.ballot(lm == gm)) - 1;
-                    tk_idx = ml * TKE + g.bcast(ls, ml);
-                    tk_max = gm;
-                } else {
-                    lossy = true;
+                    const int ti = ml * TKE + g.bcast(ls, ml);
+                    if (g.gl == 0) {
+                        cy->tk_idx = ti;
+                        cy->tk_max = gm;
+                    }
+                } else if (g.gl == 0) {
+                    cy->lossy = 1;
                 }
             }
             if (out.collect && kv <= out.collect_thr && g.gl == 0) {
@@ -818,12 +1056,20 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
         const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * GPB + gib;
         g.sync();
         for (int e = 0; e < TKE; ++e) out.topk[gid * kTopK + g.gl * TKE + e] = tks[g.gl * TKE + e];
-        if (g.gl == 0) out.topk_meta[gid] = lossy ? tk_max : kNoKey;
+        if (g.gl == 0) out.topk_meta[gid] = cy->lossy ? cy->tk_max : kNoKey;
     }
 
+#ifdef OSERVE_K1_STATS
+    if (g.gl == 0) {
+        atomicAdd(&g_k1_stats[0], st_plans);
+        atomicAdd(&g_k1_stats[1], st_reuse);
+        atomicAdd(&g_k1_stats[2], st_steps);
+        atomicAdd(&g_k1_stats[3], st_moves);
+    }
+#endif
     // ---- CTA argmin -> global atomicMin ----
     if (out.best_key) {
-        if (g.gl == 0) blk_best[gib] = best;
+        if (g.gl == 0) blk_best[gib] = cy->best;
         __syncthreads();
         if (threadIdx.x == 0) {
             unsigned long long b = blk_best[0];
@@ -839,7 +1085,7 @@ size_t plan_eval_smem(int S, int J, bool stage) {
     constexpr int GPB = 256 / G;
     size_t shapes = (size_t)S * 8 + (size_t)S * J * 16 + (size_t)S * J * 4 + 2 * (size_t)S * kMaxJ + 2 * (size_t)S;
     shapes = stage ? (shapes + 15) & ~size_t(15) : 0;
-    return shapes + group_scratch_bytes(J, RMAX, KPL) * GPB + GPB * 8;
+    return shapes + group_scratch_bytes<RMAX, KPL>(J) * GPB + GPB * 8;
 }
 
 // Launch geometry of K1 (also used to size the top-K lists).
@@ -878,7 +1124,14 @@ int run_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &
     if (int e = plan_eval_geometry<G, KPL>(t, prm.J, sm_count, src.count, &smem, &stage, &grid)) return e;
     auto kern = stage ? k_plan_eval<G, KPL, true> : k_plan_eval<G, KPL, false>;
     if (grid == 0) return 0;
-    kern<<<static_cast<unsigned>(grid), 256, smem, stream>>>(t, sp, key, src, out, prm, skip_exact);
+    // contiguous plans per group (greedy-prefix reuse), shrunk so every group
+    // gets >= 16 chunks (static assignment: bounds the tail imbalance)
+    constexpr int GPB = 256 / G;
+    const uint64_t groups = grid * GPB;
+    uint64_t gch = src.count / (groups ? groups * 16 : 1);
+    gch = gch < 1 ? 1 : (gch > kGroupChunk ? kGroupChunk : gch);
+    kern<<<static_cast<unsigned>(grid), 256, smem, stream>>>(t, sp, key, src, out, prm, skip_exact,
+                                                               static_cast<int>(gch));
     if (launches) ++*launches;
     return check(cudaGetLastError());
 }
