@@ -19,9 +19,11 @@
 // contraction here, so no tensor-core path.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 #include "oserve_internal.h"
 
@@ -306,7 +308,10 @@ struct Group {
 // Greedy-prefix reuse (K1): x changes of the exchange since the snapshot,
 // one u32 per change ((cell << 1) | was_increment), 3 slots per move.
 constexpr int kUndo = 96;
-constexpr uint64_t kGroupChunk = 32;  // plans per contiguous group chunk
+#ifndef OSERVE_K1_CHUNK
+#define OSERVE_K1_CHUNK 32
+#endif
+constexpr uint64_t kGroupChunk = OSERVE_K1_CHUNK;  // plans per contiguous group chunk
 
 // Per-group scratch: the fixed-size arrays first (compile-time offsets from
 // one base register), the J-sized assignment x last.
@@ -347,7 +352,8 @@ __device__ __forceinline__ void unrank_run_group(const Grp &g, uint64_t rr, int 
 template <int G, int KPL, bool SMEM>
 __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_MINB) k_plan_eval(ShapeTables t, SpaceTables sp, KeyLayout key,
                                                                    PlanSource src, PlanOutputs out, SolveParams prm,
-                                                                   int skip_exact, int gchunk) {
+                                                                   int skip_exact, int gchunk,
+                                                                   unsigned long long *work) {
     using Grp = Group<G, KPL>;
     constexpr int RMAX = Grp::RMAX;
     constexpr int GPB = 256 / G;
@@ -456,7 +462,13 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
     int nlog = -1;
     g.sync();
 
-    for (uint64_t cb = (static_cast<uint64_t>(blockIdx.x) * GPB + gib) * gch; cb < src.count; cb += ngroups * gch)
+    // chunks are handed out dynamically (one atomic per chunk): neighbouring
+    // plans have correlated costs, so a static split leaves a long tail
+    for (;;) {
+    unsigned long long cix = 0;
+    if (g.gl == 0) cix = atomicAdd(work, 1ull);
+    const uint64_t cb = g.bcast(cix, 0) * gch;
+    if (cb >= src.count) break;
     for (uint64_t i = cb, ce = (cb + gch < src.count ? cb + gch : src.count); i < ce; ++i) {
         // ---- resolve the plan ----
         int R;
@@ -1052,6 +1064,7 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
         }
         g.sync();
     }
+    }
     if (out.topk) {
         const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * GPB + gib;
         g.sync();
@@ -1113,6 +1126,25 @@ int plan_eval_geometry(const ShapeTables &t, int J, int sm_count, uint64_t count
     return 0;
 }
 
+// K1's dynamic chunk counter: a ring of zeroed counters per device, one per
+// launch (memset on the launch stream), so launches in flight on other
+// streams never share one.
+unsigned long long *work_counter(cudaStream_t stream) {
+    constexpr int kRing = 256, kDev = 64;
+    static unsigned long long *ring[kDev] = {};
+    static std::atomic<unsigned> next[kDev];
+    static std::mutex mu;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kDev) return nullptr;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!ring[dev] && cudaMalloc(&ring[dev], kRing * 128) != cudaSuccess) return nullptr;
+    }
+    unsigned long long *c = ring[dev] + (next[dev].fetch_add(1) % kRing) * 16;  // one 128-byte line each
+    if (cudaMemsetAsync(c, 0, sizeof(unsigned long long), stream) != cudaSuccess) return nullptr;
+    return c;
+}
+
 template <int G, int KPL>
 int run_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key, const PlanSource &src,
                   const PlanOutputs &out, const SolveParams &prm, int sm_count, int skip_exact,
@@ -1124,14 +1156,15 @@ int run_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &
     if (int e = plan_eval_geometry<G, KPL>(t, prm.J, sm_count, src.count, &smem, &stage, &grid)) return e;
     auto kern = stage ? k_plan_eval<G, KPL, true> : k_plan_eval<G, KPL, false>;
     if (grid == 0) return 0;
-    // contiguous plans per group (greedy-prefix reuse), shrunk so every group
-    // gets >= 16 chunks (static assignment: bounds the tail imbalance)
+    // contiguous plans per group (greedy-prefix reuse), >= 4 chunks per group
     constexpr int GPB = 256 / G;
     const uint64_t groups = grid * GPB;
-    uint64_t gch = src.count / (groups ? groups * 16 : 1);
+    uint64_t gch = src.count / (groups ? groups * 4 : 1);
     gch = gch < 1 ? 1 : (gch > kGroupChunk ? kGroupChunk : gch);
+    unsigned long long *work = work_counter(stream);
+    if (!work) return static_cast<int>(cudaErrorMemoryAllocation);
     kern<<<static_cast<unsigned>(grid), 256, smem, stream>>>(t, sp, key, src, out, prm, skip_exact,
-                                                               static_cast<int>(gch));
+                                                               static_cast<int>(gch), work);
     if (launches) ++*launches;
     return check(cudaGetLastError());
 }

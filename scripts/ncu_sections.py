@@ -4,10 +4,34 @@ of stall samples.  Usage: python scripts/ncu_sections.py <source.csv>"""
 import csv
 import sys
 
-SECTIONS = [("plan resolution helpers", 148, 213), ("Group helpers (scan/ballot/bcast)", 213, 262),
-            ("table staging + scratch", 262, 343), ("resolve/unrank plan", 343, 387), ("init x/lam", 387, 401),
-            ("greedy_fill", 401, 511), ("exchange: A/F init", 511, 583), ("exchange: move loop", 583, 755),
-            ("objective/key/top-K", 755, 886)]
+import os
+
+SRC = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                   "paper_2602_12151_b200", "csrc", "oserve_kernels.cu")
+# section name -> first line containing the marker (sections run to the next marker)
+MARKERS = [("plan resolution helpers", "// ------------------------------------------------------- plan resolution"),
+           ("K1 helpers (Group, unranking)", "// ------------------------------------------------------------------- K1"),
+           ("table staging + scratch", "k_plan_eval(ShapeTables t"),
+           ("resolve/unrank plan", "// ---- resolve the plan ----"),
+           ("init x/lam / snapshot restore", "// ---- init: lam"),
+           ("greedy_fill", "// ---- greedy_fill"),
+           ("exchange: A/F init", "// ---- exchange_improve"),
+           ("exchange: move loop", "        for (;;) {"),
+           ("objective/key/top-K", "// ---- objective, sum_pp, key"),
+           ("(end)", "size_t plan_eval_smem(")]
+
+
+def sections():
+    lines = open(SRC).read().split("\n")
+    out, pos = [], 0
+    for name, m in MARKERS:
+        while pos < len(lines) and m not in lines[pos]:
+            pos += 1
+        out.append((name, pos + 1))
+    return [(out[i][0], out[i][1], out[i + 1][1]) for i in range(len(out) - 1)]
+
+
+SECTIONS = sections()
 
 
 def f(x):
