@@ -149,9 +149,10 @@ __global__ void k_normalize_rows(ShapeTables t) {
 }
 
 // ------------------------------------------------------- plan resolution --
+__device__ __noinline__ uint64_t div64(uint64_t a, uint64_t b) { return a / b; }  // one out-of-line copy
 __device__ __forceinline__ uint64_t div_small(uint64_t a, uint64_t b) {
     if ((a >> 32) == 0 && (b >> 32) == 0) return static_cast<uint32_t>(a) / static_cast<uint32_t>(b);
-    return a / b;
+    return div64(a, b);
 }
 
 // Largest p with prefix[p] <= g (skips empty partitions automatically).
@@ -313,6 +314,25 @@ constexpr int kUndo = 96;
 #endif
 constexpr uint64_t kGroupChunk = OSERVE_K1_CHUNK;  // plans per contiguous group chunk
 
+// Register-array element by a runtime slot index without dynamic indexing
+// (keeps the array in registers): lets the exchange run ONE copy of a body
+// in a non-unrolled slot loop instead of KPL inlined copies (instruction-
+// cache footprint; the K1 loop body is the whole hot path).
+template <int KPL, class T>
+__device__ __forceinline__ T rsel(const T (&a)[KPL], int kk) {
+    T v = a[0];
+#pragma unroll
+    for (int q = 1; q < KPL; ++q)
+        if (kk == q) v = a[q];
+    return v;
+}
+template <int KPL, class T>
+__device__ __forceinline__ void rput(T (&a)[KPL], int kk, T v) {
+#pragma unroll
+    for (int q = 0; q < KPL; ++q)
+        if (kk == q) a[q] = v;
+}
+
 // Per-group scratch: the fixed-size arrays first (compile-time offsets from
 // one base register), the J-sized assignment x last.
 template <int RMAX, int KPL>
@@ -342,10 +362,12 @@ __device__ __forceinline__ void unrank_run_group(const Grp &g, uint64_t rr, int 
             else hi = mid - 1;
         }
         if (lo < rem) rr -= c_binom[rem - lo - 1 + K][K];
+#pragma unroll 1
         for (int p = g.gl; p < lo; p += Grp::kG) out[pos + p] = static_cast<uint8_t>(v);
         pos += lo;
         rem -= lo;
     }
+#pragma unroll 1
     for (int p = g.gl; p < rem; p += Grp::kG) out[pos + p] = static_cast<uint8_t>(q - 1);
 }
 
@@ -586,6 +608,7 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
         }
         if (reuse) {
             // undo the previous plans' exchange moves (+-1 changes commute)
+#pragma unroll 1
             for (int e = g.gl; e < nlog; e += G) {
                 const uint32_t v = ulog[e];
                 if (v != 0xffffffffu) atomicAdd(&xs[v >> 1], (v & 1u) ? -1 : 1);
@@ -598,8 +621,10 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                 mrem[kk] = snM[kk * G + g.gl];
                 held[kk] = snH[kk * G + g.gl];
                 areg[kk] = snA[kk * G + g.gl];
-                if (k >= P && k < R)
+                if (k >= P && k < R) {
+#pragma unroll 1
                     for (int j = 0; j < J; ++j) xs[j * RMAX + k] = 0;
+                }
             }
         } else {
             nlog = -1;
@@ -612,6 +637,7 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
             }
             int4 *xz = reinterpret_cast<int4 *>(xs);
             const int n4 = (J * RMAX) >> 2;  // RMAX is a multiple of 4
+#pragma unroll 1
             for (int q = g.gl; q < n4; q += G) xz[q] = make_int4(0, 0, 0, 0);
         }
         if (reuse) nlog = 0;
@@ -707,6 +733,7 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                 c = min(static_cast<int>(min(cb, 0x7fffffffu)), run_end - k);
             }
             if (act && take) {
+#pragma unroll 1
                 for (int q = 0; q <= c; ++q) xs[j * RMAX + k + q] = take;
             }
             // direct-take bit of (class at this position, replicas k..k+c)
@@ -759,8 +786,8 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
         uint32_t lam_mask = g.ballot(g.gl < J && lamr > 0);
         g.sync();
         // held classes of owned replica kk whose A set minus k is non-empty
-        auto eligible_held = [&](int kk) -> uint32_t {
-            uint32_t el = 0, hb = held[kk];
+        auto eligible_held = [&](uint32_t hb, int kk) -> uint32_t {
+            uint32_t el = 0;
             while (hb) {
                 const int j2 = __ffs(hb) - 1;
                 hb &= hb - 1;
@@ -779,7 +806,8 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
         auto feasible_row = [&](int kk, uint32_t el) -> uint32_t {
             const int k = g.gl + G * kk;
             if (k >= R) return 0u;
-            const int s = shp[kk];
+            const int s = rsel(shp, kk);
+            const int64_t mr = rsel(mrem, kk);
             int64_t e1 = -1, e2 = -1;
             int e1j = -1;
             while (el) {
@@ -802,15 +830,18 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                 lb &= lb - 1;
                 const int64_t u = sUnit[s * J + j];
                 if (u <= 0 || xs[j * RMAX + k] >= sCap[s * J + j]) continue;
-                if (mrem[kk] >= u || (e1j == j ? e2 : e1) >= u - mrem[kk]) f |= 1u << j;
+                if (mr >= u || (e1j == j ? e2 : e1) >= u - mr) f |= 1u << j;
             }
             return f;
         };
         uint32_t F[KPL], E[KPL];
 #pragma unroll
+        for (int kk = 0; kk < KPL; ++kk) F[kk] = E[kk] = 0u;
+#pragma unroll 1
         for (int kk = 0; kk < KPL; ++kk) {
-            E[kk] = g.gl + G * kk < R ? eligible_held(kk) : 0u;
-            F[kk] = feasible_row(kk, E[kk]);
+            const uint32_t e = g.gl + G * kk < R ? eligible_held(rsel(held, kk), kk) : 0u;
+            rput(E, kk, e);
+            rput(F, kk, feasible_row(kk, e));
         }
         for (;;) {
             uint32_t anyF = 0;
@@ -829,25 +860,23 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
             const int ogl = kf & (G - 1);
             int j2 = -1, k2 = -1;
             if (g.gl == ogl) {
+                const int kk = kf / G;
+                const int s = rsel(shp, kk);
+                const int64_t mr = rsel(mrem, kk);
+                const int64_t u = sUnit[s * J + jf];
+                if (mr < u) {
+                    uint32_t hb = rsel(held, kk) & ~(1u << jf);
+                    while (hb && j2 < 0) {
+                        const int jj = __ffs(hb) - 1;
+                        hb &= hb - 1;
+                        if (mr + sUnit[s * J + jj] < u) continue;
 #pragma unroll
-                for (int kk = 0; kk < KPL; ++kk) {
-                    if (g.gl + G * kk != kf) continue;
-                    const int s = shp[kk];
-                    const int64_t u = sUnit[s * J + jf];
-                    if (mrem[kk] < u) {
-                        uint32_t hb = held[kk] & ~(1u << jf);
-                        while (hb && j2 < 0) {
-                            const int jj = __ffs(hb) - 1;
-                            hb &= hb - 1;
-                            if (mrem[kk] + sUnit[s * J + jj] < u) continue;
-#pragma unroll
-                            for (int k3 = 0; k3 < KPL; ++k3) {
-                                uint32_t w = Am[jj * KPL + k3];
-                                if (k3 == kk) w &= ~(1u << g.gl);
-                                if (w && k2 < 0) {
-                                    k2 = __ffs(w) - 1 + G * k3;
-                                    j2 = jj;
-                                }
+                        for (int k3 = 0; k3 < KPL; ++k3) {
+                            uint32_t w = Am[jj * KPL + k3];
+                            if (k3 == kk) w &= ~(1u << g.gl);
+                            if (w && k2 < 0) {
+                                k2 = __ffs(w) - 1 + G * k3;
+                                j2 = jj;
                             }
                         }
                     }
@@ -923,40 +952,41 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
             g.sync();
             // rows whose feasible set must be rebuilt: kf, k2, and rows whose
             // eligible-held set changed (only possible through dirty classes)
-            bool redo[KPL];
-#pragma unroll
+            uint32_t redo = 0;  // bit kk: owned row kk must be rebuilt
+#pragma unroll 1
             for (int kk = 0; kk < KPL; ++kk) {
                 const int k = g.gl + G * kk;
-                redo[kk] = false;
                 if (k >= R) continue;
-                if (k == kf || k == k2) redo[kk] = true;
-                else if ((held[kk] & dirty) && eligible_held(kk) != E[kk]) redo[kk] = true;
-                else F[kk] &= lam_mask;
+                const uint32_t hk = rsel(held, kk);
+                if (k == kf || k == k2) redo |= 1u << kk;
+                else if ((hk & dirty) && eligible_held(hk, kk) != rsel(E, kk)) redo |= 1u << kk;
+                else rput(F, kk, rsel(F, kk) & lam_mask);
             }
             // many rows: every lane rebuilds its own rows (in parallel);
             // few rows: class-parallel rebuild, one row at a time
             int nredo = 0;
 #pragma unroll
-            for (int kk = 0; kk < KPL; ++kk) nredo += __popc(g.ballot(redo[kk]));
+            for (int kk = 0; kk < KPL; ++kk) nredo += __popc(g.ballot((redo >> kk) & 1u));
             if (nredo > 4) {
-#pragma unroll
+#pragma unroll 1
                 for (int kk = 0; kk < KPL; ++kk)
-                    if (redo[kk]) {
-                        E[kk] = eligible_held(kk);
-                        F[kk] = feasible_row(kk, E[kk]);
-                        redo[kk] = false;
+                    if ((redo >> kk) & 1u) {
+                        const uint32_t e = eligible_held(rsel(held, kk), kk);
+                        rput(E, kk, e);
+                        rput(F, kk, feasible_row(kk, e));
                     }
+                redo = 0;
             }
-#pragma unroll
+#pragma unroll 1
             for (int kk = 0; kk < KPL; ++kk) {
-                uint32_t rows = g.ballot(redo[kk]);
+                uint32_t rows = g.ballot((redo >> kk) & 1u);
                 while (rows) {  // class-parallel rebuild, one row at a time
                     const int rgl = __ffs(rows) - 1;
                     rows &= rows - 1;
                     const int r = rgl + G * kk;
                     const int sr = shpS[r];
-                    const int64_t mr = g.bcast(mrem[kk], rgl);
-                    const uint32_t hr = g.bcast(held[kk], rgl);
+                    const int64_t mr = g.bcast(rsel(mrem, kk), rgl);
+                    const uint32_t hr = g.bcast(rsel(held, kk), rgl);
                     const int j = g.gl;
                     bool el = false;
                     if (j < J && ((hr >> j) & 1u)) {
@@ -989,8 +1019,8 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                     }
                     const uint32_t Fr = g.ballot(f);
                     if (g.gl == rgl) {
-                        E[kk] = Er;
-                        F[kk] = Fr;
+                        rput(E, kk, Er);
+                        rput(F, kk, Fr);
                     }
                 }
             }
