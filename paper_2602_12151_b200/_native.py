@@ -432,11 +432,14 @@ class GpuContext:
         keep = A.Keep()
         s, d = A.deployment_desc(src, keep), A.deployment_desc(dst, keep)
         ntr, est = C.c_int(), C.c_double()
-        self._chk(self.lib.oserve_gpu_switch_plan(self.h, C.byref(s), C.byref(d), 0, None, C.byref(ntr),
-                                                  C.byref(est)))
-        cap = ntr.value
-        tr = (A.TransferDesc * max(1, cap))()
-        self._chk(self.lib.oserve_gpu_switch_plan(self.h, C.byref(s), C.byref(d), cap, tr, C.byref(ntr),
-                                                  C.byref(est)))
-        return core.SwitchPlan([core.Transfer(core.ByteRange(t.begin, t.end), t.src, t.dst) for t in tr[:cap]],
+        cap = 4096  # one call in the common case; the count is reported when it does not fit
+        tr = (A.TransferDesc * cap)()
+        st = self.lib.oserve_gpu_switch_plan(self.h, C.byref(s), C.byref(d), cap, tr, C.byref(ntr), C.byref(est))
+        if st == A.ERR_INVALID_ARGUMENT and ntr.value > cap:
+            cap = ntr.value
+            tr = (A.TransferDesc * cap)()
+            st = self.lib.oserve_gpu_switch_plan(self.h, C.byref(s), C.byref(d), cap, tr, C.byref(ntr), C.byref(est))
+        self._chk(st)
+        n = ntr.value
+        return core.SwitchPlan([core.Transfer(core.ByteRange(t.begin, t.end), t.src, t.dst) for t in tr[:n]],
                                est.value)

@@ -784,21 +784,24 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
             for (int kk = 0; kk < KPL; ++kk) Am[g.gl * KPL + kk] = areg[kk];
         }
         uint32_t lam_mask = g.ballot(g.gl < J && lamr > 0);
-        g.sync();
-        // held classes of owned replica kk whose A set minus k is non-empty
-        auto eligible_held = [&](uint32_t hb, int kk) -> uint32_t {
-            uint32_t el = 0;
-            while (hb) {
-                const int j2 = __ffs(hb) - 1;
-                hb &= hb - 1;
-                uint32_t any = 0;
+        // classes whose A set has >= 2 members / exactly 1 member
+        uint32_t M2, M1;
+        {
+            int pc = 0;
 #pragma unroll
-                for (int k2 = 0; k2 < KPL; ++k2) {
-                    uint32_t w = Am[j2 * KPL + k2];
-                    if (k2 == kk) w &= ~(1u << g.gl);
-                    any |= w;
-                }
-                if (any) el |= 1u << j2;
+            for (int kk = 0; kk < KPL; ++kk) pc += __popc(areg[kk]);
+            M2 = g.ballot(g.gl < J && pc >= 2);
+            M1 = g.ballot(g.gl < J && pc == 1);
+        }
+        g.sync();
+        // held classes of owned replica kk whose A set minus k is non-empty:
+        // |A| >= 2, or |A| == 1 and the member is not k itself
+        auto eligible_held = [&](uint32_t hb, int kk) -> uint32_t {
+            uint32_t el = hb & M2, h1 = hb & M1;
+            while (h1) {
+                const int j2 = __ffs(h1) - 1;
+                h1 &= h1 - 1;
+                if (!((Am[j2 * KPL + kk] >> g.gl) & 1u)) el |= 1u << j2;
             }
             return el;
         };
@@ -950,6 +953,15 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
             }
             dirty = g.or_all(dirty);
             g.sync();
+            if (dirty) {  // an A set crossed size 1 or 2: refresh M1 / M2
+                int pc = 0;
+                if (g.gl < J) {
+#pragma unroll
+                    for (int k3 = 0; k3 < KPL; ++k3) pc += __popc(Am[g.gl * KPL + k3]);
+                }
+                M2 = g.ballot(g.gl < J && pc >= 2);
+                M1 = g.ballot(g.gl < J && pc == 1);
+            }
             // rows whose feasible set must be rebuilt: kf, k2, and rows whose
             // eligible-held set changed (only possible through dirty classes)
             uint32_t redo = 0;  // bit kk: owned row kk must be rebuilt
@@ -989,16 +1001,8 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                     const uint32_t hr = g.bcast(rsel(held, kk), rgl);
                     const int j = g.gl;
                     bool el = false;
-                    if (j < J && ((hr >> j) & 1u)) {
-                        uint32_t any = 0;
-#pragma unroll
-                        for (int k3 = 0; k3 < KPL; ++k3) {
-                            uint32_t w = Am[j * KPL + k3];
-                            if (k3 == kk) w &= ~(1u << rgl);
-                            any |= w;
-                        }
-                        el = any != 0;
-                    }
+                    if (j < J && ((hr >> j) & 1u))
+                        el = ((M2 >> j) & 1u) || (((M1 >> j) & 1u) && !((Am[j * KPL + kk] >> rgl) & 1u));
                     const uint32_t Er = g.ballot(el);
                     // top-2 eligible unit: order positions ascend with unit
                     const uint32_t rk1 = el ? static_cast<uint32_t>(sRank[sr * kMaxJ + j]) + 1u : 0u;
