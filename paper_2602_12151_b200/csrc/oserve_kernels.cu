@@ -926,28 +926,57 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
             g.sync();
             // refresh the A bits of rows kf and k2 (lane j = class j)
             uint32_t dirty = 0;
-            for (int q = 0; q < (j2 >= 0 ? 2 : 1); ++q) {
-                const int r = q == 0 ? kf : k2;
+            // apply row r's new direct-take bit p for class j (lane j)
+            auto a_apply = [&](int j, int r, bool p) {
+                const int rgl = r & (G - 1), rkk = r / G;
+                const uint32_t bit = 1u << rgl;
+                const uint32_t old = Am[j * KPL + rkk];
+                if (p != ((old & bit) != 0)) {
+                    int pc = 0;
+#pragma unroll
+                    for (int k3 = 0; k3 < KPL; ++k3) pc += __popc(Am[j * KPL + k3]);
+                    Am[j * KPL + rkk] = p ? (old | bit) : (old & ~bit);
+                    const int pn = pc + (p ? 1 : -1);
+                    if (pc < 2 || pn < 2) dirty |= 1u << j;
+                }
+            };
+            if constexpr (G == 32) {
+                // J <= 16: half h evaluates row (kf, k2)[h]; lane j of the low
+                // half applies both in order (they may share an A word)
+                const int h = g.gl >> 4, j = g.gl & 15;
+                const int r = (h && j2 >= 0) ? k2 : kf;
                 const int rgl = r & (G - 1), rkk = r / G;
                 int64_t mr = 0;
 #pragma unroll
-                for (int kk = 0; kk < KPL; ++kk)
-                    if (kk == rkk) mr = mrem[kk];
-                mr = g.bcast(mr, rgl);
-                if (g.gl < J) {
-                    const int j = g.gl;
+                for (int kk = 0; kk < KPL; ++kk) {
+                    const int64_t v = __shfl_sync(0xffffffffu, mrem[kk], rgl);
+                    if (kk == rkk) mr = v;
+                }
+                bool p = false;
+                if (j < J) {
                     const int sr = shpS[r];
                     const int64_t u = sUnit[sr * J + j];
-                    const bool p = u > 0 && xs[j * RMAX + r] < sCap[sr * J + j] && mr >= u;
-                    const uint32_t bit = 1u << rgl;
-                    const uint32_t old = Am[j * KPL + rkk];
-                    if (p != ((old & bit) != 0)) {
-                        int pc = 0;
+                    p = u > 0 && xs[j * RMAX + r] < sCap[sr * J + j] && mr >= u;
+                }
+                const bool p_hi = __shfl_down_sync(0xffffffffu, p, 16) != 0;
+                if (h == 0 && j < J) {
+                    a_apply(j, kf, p);
+                    if (j2 >= 0) a_apply(j, k2, p_hi);
+                }
+            } else {
+                for (int q = 0; q < (j2 >= 0 ? 2 : 1); ++q) {
+                    const int r = q == 0 ? kf : k2;
+                    const int rgl = r & (G - 1), rkk = r / G;
+                    int64_t mr = 0;
 #pragma unroll
-                        for (int k3 = 0; k3 < KPL; ++k3) pc += __popc(Am[j * KPL + k3]);
-                        Am[j * KPL + rkk] = p ? (old | bit) : (old & ~bit);
-                        const int pn = pc + (p ? 1 : -1);
-                        if (pc < 2 || pn < 2) dirty |= 1u << j;
+                    for (int kk = 0; kk < KPL; ++kk)
+                        if (kk == rkk) mr = mrem[kk];
+                    mr = g.bcast(mr, rgl);
+                    if (g.gl < J) {
+                        const int j = g.gl;
+                        const int sr = shpS[r];
+                        const int64_t u = sUnit[sr * J + j];
+                        a_apply(j, r, u > 0 && xs[j * RMAX + r] < sCap[sr * J + j] && mr >= u);
                     }
                 }
             }
@@ -989,6 +1018,81 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                     }
                 redo = 0;
             }
+            if constexpr (G == 32) {
+                // J <= 16: two rows per step, half h (lanes 16h..16h+15,
+                // lane = class) rebuilds the h-th row of the pair
+                // rows to rebuild as bit r = replica index (G == 32: bit = gl + 32 kk)
+                uint64_t rlo = 0, rhi = 0;
+#pragma unroll
+                for (int kk = 0; kk < KPL; ++kk) {
+                    const uint64_t b = g.ballot((redo >> kk) & 1u);
+                    if (kk < 2) rlo |= b << (32 * kk);
+                    else rhi |= b << (32 * (kk - 2));
+                }
+                const int h = g.gl >> 4, j = g.gl & 15;
+                const uint32_t hm = h ? 0xffff0000u : 0x0000ffffu;
+                auto pop = [&]() -> int {  // next row index, ascending; -1 when none
+                    if (rlo) {
+                        const int r = __ffsll(static_cast<long long>(rlo)) - 1;
+                        rlo &= rlo - 1;
+                        return r;
+                    }
+                    if (KPL > 2 && rhi) {
+                        const int r = 64 + __ffsll(static_cast<long long>(rhi)) - 1;
+                        rhi &= rhi - 1;
+                        return r;
+                    }
+                    return -1;
+                };
+                for (;;) {
+                    const int ra = pop();
+                    if (ra < 0) break;
+                    const int rb = pop();
+                    const int r = (h && rb >= 0) ? rb : ra;  // an idle high half mirrors row a
+                    const int rgl = r & (G - 1), kk = r / G;
+                    int64_t mr = 0;
+                    uint32_t hr = 0;
+#pragma unroll
+                    for (int q = 0; q < KPL; ++q) {
+                        const int64_t v = __shfl_sync(0xffffffffu, mrem[q], rgl);
+                        const uint32_t w = __shfl_sync(0xffffffffu, held[q], rgl);
+                        if (q == kk) {
+                            mr = v;
+                            hr = w;
+                        }
+                    }
+                    const int sr = shpS[r];
+                    bool el = false;
+                    if (j < J && ((hr >> j) & 1u))
+                        el = ((M2 >> j) & 1u) || (((M1 >> j) & 1u) && !((Am[j * KPL + kk] >> rgl) & 1u));
+                    const uint32_t Eb = __ballot_sync(0xffffffffu, el);
+                    const uint32_t rk1 = el ? static_cast<uint32_t>(sRank[sr * kMaxJ + j]) + 1u : 0u;
+                    const uint32_t t1 = __reduce_max_sync(hm, rk1);
+                    const uint32_t t2 = __reduce_max_sync(hm, rk1 == t1 ? 0u : rk1);
+                    int64_t e1 = -1, e2 = -1;
+                    int e1j = -1;
+                    if (t1) {
+                        e1j = sOrder[sr * kMaxJ + t1 - 1];
+                        e1 = sUnit[sr * J + e1j];
+                    }
+                    if (t2) e2 = sUnit[sr * J + sOrder[sr * kMaxJ + t2 - 1]];
+                    bool f = false;
+                    if (j < J && ((lam_mask >> j) & 1u)) {
+                        const int64_t u = sUnit[sr * J + j];
+                        if (u > 0 && xs[j * RMAX + r] < sCap[sr * J + j])
+                            f = mr >= u || (e1j == j ? e2 : e1) >= u - mr;
+                    }
+                    const uint32_t Fb = __ballot_sync(0xffffffffu, f);
+                    if (g.gl == (ra & (G - 1))) {
+                        rput(E, ra / G, Eb & 0xffffu);
+                        rput(F, ra / G, Fb & 0xffffu);
+                    }
+                    if (rb >= 0 && g.gl == (rb & (G - 1))) {
+                        rput(E, rb / G, Eb >> 16);
+                        rput(F, rb / G, Fb >> 16);
+                    }
+                }
+            } else
 #pragma unroll 1
             for (int kk = 0; kk < KPL; ++kk) {
                 uint32_t rows = g.ballot((redo >> kk) & 1u);
