@@ -137,6 +137,9 @@ def main():
          core.model_140gb(), 16, {"mode": "canonical", "sizes": [2, 4, 8]})
     emit("cfg5_low.json", "config 5 at demand-limited load 0.3", 16, core.model_140gb(), 16,
          {"mode": "canonical", "sizes": [2, 4, 8]}, load=0.3)
+    emit("cfg5_full.json", "128-GPU cluster, 16 classes, canonical plan space sizes {2,4,...,128} "
+         "(every power-of-two block)", 16, core.model_140gb(), 16,
+         {"mode": "canonical", "sizes": [2, 4, 8, 16, 32, 64, 128]})
 
     # config 4: temporal, 24 windows on the config-2 cluster
     cl = core.cluster(4, 8)

@@ -63,6 +63,19 @@ def random_instances(seed, count, max_r, max_j, max_lam, max_n=100):
     return out
 
 
+def canonical_sample(ref, name):
+    """3,000 seeded plans of a canonical space through the reference's
+    evaluate_deployment -> plans_<name>.json."""
+    w = workloads.load(name)
+    pr = problem(w)
+    parts, plans = ref.space_info(pr, w.space_mode, w.space_sizes)
+    sample = np.unique(np.random.default_rng(12151).integers(0, plans, 3000)).astype(np.uint64)
+    obj, spp, _ = ref.evaluate_ranks(pr, w.space_mode, sample, w.space_sizes, threads=THREADS)
+    json.dump({"partitions": parts, "plans": plans, "ranks": sample.tolist(), "objective": obj.tolist(),
+               "sum_pp": spp.tolist()}, open(os.path.join(OUT, f"plans_{name}.json"), "w"))
+    return pr
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     ref = Oracle("ref")
@@ -135,20 +148,18 @@ def main():
         json.dump({"partitions": parts, "plans": plans, "all_objective_sha256": objective_digest(obj),
                    "objective_sum": int(obj.sum()), "ranks": sample.tolist(), "objective": obj[sample].tolist(),
                    "sum_pp": spp[sample].tolist()}, open(os.path.join(OUT, f"plans_{name}.json"), "w"))
-    for name in ("cfg3_70b", "cfg3_7b", "cfg5", "cfg5_low"):
+    for name in ("cfg3_70b", "cfg3_7b", "cfg5", "cfg5_low", "cfg5_full"):
+        pr = canonical_sample(ref, name)
         w = workloads.load(name)
-        pr = problem(w)
-        parts, plans = ref.space_info(pr, w.space_mode, w.space_sizes)
-        sample = np.unique(np.random.default_rng(12151).integers(0, plans, 3000)).astype(np.uint64)
-        obj, spp, _ = ref.evaluate_ranks(pr, w.space_mode, sample, w.space_sizes, threads=THREADS)
-        json.dump({"partitions": parts, "plans": plans, "ranks": sample.tolist(), "objective": obj.tolist(),
-                   "sum_pp": spp.tolist()}, open(os.path.join(OUT, f"plans_{name}.json"), "w"))
         if name == "cfg3_70b":
             s = ref.round(pr, w.space_mode, w.space_sizes, threads=THREADS)
             rounds[name] = {"kind": "canonical space through search::evaluate_deployment", "objective": s.throughput,
                             "partitions": s.iterations, "plans": s.plans, "partition_index": s.partition_index,
                             "local_rank": s.local_rank, "sum_pp": s.sum_pp, "deployment": dep_json(s.deployment)}
-    json.dump(rounds, open(os.path.join(OUT, "rounds.json"), "w"), indent=1)
+    rpath = os.path.join(OUT, "rounds.json")  # keep the full-space entries of gen_rounds_full.py
+    merged = json.load(open(rpath)) if os.path.exists(rpath) else {}
+    merged.update(rounds)
+    json.dump(merged, open(rpath, "w"), indent=1)
 
     # ---- search::search (flow-guided heuristic) with its log ----
     srch = []
@@ -296,5 +307,8 @@ if __name__ == "__main__":
         gen_f4(Oracle("ref"))
     elif sys.argv[1:] == ["exact"]:
         gen_exact_budget(Oracle("ref"), Oracle("port"))
+    elif sys.argv[1:2] == ["sample"]:  # python oracle/gen_golden.py sample cfg5_full
+        for nm in sys.argv[2:]:
+            canonical_sample(Oracle("ref"), nm)
     else:
         main()

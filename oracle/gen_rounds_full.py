@@ -9,7 +9,10 @@ tests/golden/rounds.json:
   * an all-plan SHA-256 of the per-plan objectives (little-endian int64 in
     rank order) plus their sum, so the GPU's per-plan path can be checked
     bit-exact over the whole space at full size.
-Usage: python oracle/gen_rounds_full.py [cfg ...]
+Usage: python oracle/gen_rounds_full.py [--port] [cfg ...]
+  --port: use the CPU restatement (oracle/oserve_port.cpp, pinned to the
+  reference by tests/test_oracle.py; ~4x faster) for spaces the reference
+  library would need hours for (config 5-full: 104.7 M plans).
 """
 import json
 import os
@@ -26,8 +29,10 @@ from pyoracle import Oracle  # noqa: E402
 
 
 def main():
-    names = sys.argv[1:] or ["cfg3_7b", "cfg5_low", "cfg5"]
-    ref = Oracle("ref")
+    args = sys.argv[1:]
+    kind = "port" if "--port" in args else "ref"
+    names = [a for a in args if a != "--port"] or ["cfg3_7b", "cfg5_low", "cfg5"]
+    ref = Oracle(kind)
     path = os.path.join(OUT, "rounds.json")
     for name in names:
         w = workloads.load(name)
@@ -46,7 +51,9 @@ def main():
         t2 = time.time()
         assert int(obj.max()) == s.throughput
         rounds = json.load(open(path))
-        rounds[name] = {"kind": "canonical space through search::evaluate_deployment", "objective": s.throughput,
+        rounds[name] = {"kind": "canonical space through search::evaluate_deployment" if kind == "ref" else
+                        "canonical space through the pinned CPU restatement (oracle/oserve_port.cpp)",
+                        "objective": s.throughput,
                         "partitions": s.iterations, "plans": s.plans, "partition_index": s.partition_index,
                         "local_rank": s.local_rank, "sum_pp": s.sum_pp, "deployment": dep_json(s.deployment),
                         "all_objective_sha256": objective_digest(obj), "objective_sum": int(obj.sum()),

@@ -24,12 +24,18 @@ from paper_2602_12151_b200 import workloads  # noqa: E402
 from pyoracle import Oracle, Problem  # noqa: E402
 
 
-def main():
+CONFIGS = (("cfg1", None), ("cfg2", None), ("cfg2_low", None), ("cfg3_70b", 50000), ("cfg3_7b", 50000),
+           ("cfg5", 50000), ("cfg5_low", 20000), ("cfg5_full", 50000))
+
+
+def main(only=()):
     port = Oracle("port")
-    out = {}
+    path = os.path.join(ROOT, "paper_2602_12151_b200", "configs", "work.json")
+    out = json.load(open(path)) if only and os.path.exists(path) else {}
     threads = os.cpu_count() or 1
-    for name, sample in (("cfg1", None), ("cfg2", None), ("cfg2_low", None), ("cfg3_70b", 50000),
-                         ("cfg3_7b", 50000), ("cfg5", 50000), ("cfg5_low", 20000)):
+    for name, sample in CONFIGS:
+        if only and name not in only:
+            continue
         w = workloads.load(name)
         pr = Problem(w.cluster, w.model, w.types, w.lam, w.span_s, w.params)
         parts, plans = port.space_info(pr, w.space_mode, w.space_sizes)
@@ -47,9 +53,9 @@ def main():
                      "stderr": float(wf.std() / np.sqrt(len(wf))), "kind": kind,
                      "cpu_port_seconds": dt, "cpu_threads": threads}
         print(name, out[name])
-    with open(os.path.join(ROOT, "paper_2602_12151_b200", "configs", "work.json"), "w") as f:
+    with open(path, "w") as f:
         json.dump(out, f, indent=1)
 
 
 if __name__ == "__main__":
-    main()
+    main(tuple(sys.argv[1:]))  # python oracle/gen_work.py [cfg ...]  (only those, merged)

@@ -78,7 +78,7 @@ def test_cfg2_every_plan_and_winner(cuda, port):
     assert same_deployment(got.deployment, exp.deployment)
 
 
-@pytest.mark.parametrize("name", ["cfg3_70b", "cfg3_7b", "cfg5", "cfg5_low"])
+@pytest.mark.parametrize("name", ["cfg3_70b", "cfg3_7b", "cfg5", "cfg5_low", "cfg5_full"])
 def test_sampled_plans_large(cuda, port, name):
     w = workloads.load(name)
     g = ctx_for(w)
@@ -249,7 +249,8 @@ def test_topk_round_and_switch_batch(cuda, port, name, K):
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg1_bnb", "cfg2", "cfg2_low", "cfg3_70b", "cfg3_7b", "cfg5", "cfg5_low"])
+@pytest.mark.parametrize("name", ["cfg1", "cfg1_bnb", "cfg2", "cfg2_low", "cfg3_70b", "cfg3_7b", "cfg5", "cfg5_low",
+                                  "cfg5_full"])
 def test_gpu_matches_reference_goldens(cuda, name):
     """GPU per-plan objectives against the REFERENCE's own values (tests/golden,
     generated from the unmodified reference by oracle/gen_golden.py)."""

@@ -118,7 +118,7 @@ def test_ordered_round_matches_golden(port, name):
         (g["objective"], g["partition_index"], g["local_rank"], g["sum_pp"], g["deployment"])
 
 
-@pytest.mark.parametrize("name", ["cfg3_70b", "cfg3_7b", "cfg5", "cfg5_low"])
+@pytest.mark.parametrize("name", ["cfg3_70b", "cfg3_7b", "cfg5", "cfg5_low", "cfg5_full"])
 def test_canonical_plans_match_golden(port, name):
     w = workloads.load(name)
     pr = problem_for(w)
