@@ -16,7 +16,8 @@ One step = one full scheduling round over the whole plan space:
   e2e   : the public C-ABI from host buffers every step — enumerate + upload the
           space tables, upload the workload, K0 cost kernel, K1 with the exact
           top-K (default 1024) of the packed key, all-gather + merge across
-          ranks, K2 switching batch current -> each of the K best, key D2H,
+          ranks, K2 switching batch current -> each of the K best (pairs sharded
+          across ranks, costs all-gathered), key D2H,
           decode, and the full greedy switch plan current -> winner (transfers
           D2H).  "current" is init_uniform (deploysearch.cpp:120-136).
 The reference arm (--impl reference) times the reference's own CPU path
@@ -298,7 +299,21 @@ def run_ours(args, rank, world, local):
             allk = torch.empty(world * K, dtype=torch.int64, device=dev)
             dist.all_gather_into_tensor(allk, d_topk)
             d_topk.copy_(torch.sort(allk).values[:K])
-        sw_est, _ = ctx.switch_cost_keys(current, d_topk.data_ptr(), K)  # K2 batch: current -> K best
+        if world > 1:  # K2 batch sharded: each rank costs K/world of the pairs, then all-gather
+            per = (K + world - 1) // world
+            lo = min(K, rank * per)
+            n = min(K, lo + per) - lo
+            est_l, _ = ctx.switch_cost_keys(current, d_topk.data_ptr() + 8 * lo, n) if n > 0 else ([], [])
+            buf = torch.full((per,), float("nan"), dtype=torch.float64, device=dev)
+            if n:
+                buf[:n] = torch.tensor(est_l, dtype=torch.float64).to(dev, non_blocking=True)
+            alle = torch.empty(world * per, dtype=torch.float64, device=dev)
+            dist.all_gather_into_tensor(alle, buf)
+            sw_est = alle[:K].cpu().tolist()
+            extra_h2d, extra_d2h = 8 * n, 8 * K
+        else:
+            sw_est, _ = ctx.switch_cost_keys(current, d_topk.data_ptr(), K)  # K2 batch: current -> K best
+            extra_h2d = extra_d2h = 0
         k = int(d_topk[0].item())                                  # D2H result key
         st = ctx.decode_key(k)
         plan = ctx.switch_plan(current, st.deployment)             # K2 detail + transfers D2H
@@ -312,8 +327,8 @@ def run_ours(args, rank, world, local):
     e2e_step = statistics.mean(e2e_ms)
     # bytes per step, counted by the C-ABI itself (every cudaMemcpy it issues)
     bytes1 = ctx.copy_bytes()
-    h2d = (bytes1[0] - bytes0[0]) // args.steps
-    d2h = (bytes1[1] - bytes0[1]) // args.steps + 8  # + the key read through torch (.item())
+    h2d = (bytes1[0] - bytes0[0]) // args.steps + extra_h2d
+    d2h = (bytes1[1] - bytes0[1]) // args.steps + 8 + extra_d2h  # + the key read (.item()), sharded K2 results
     assert k == key, "e2e and device-resident rounds disagree"
 
     if rank != 0:
