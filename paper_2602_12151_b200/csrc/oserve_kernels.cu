@@ -1021,27 +1021,25 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
             if constexpr (G == 32) {
                 // J <= 16: two rows per step, half h (lanes 16h..16h+15,
                 // lane = class) rebuilds the h-th row of the pair
-                // rows to rebuild as bit r = replica index (G == 32: bit = gl + 32 kk)
-                uint64_t rlo = 0, rhi = 0;
-#pragma unroll
-                for (int kk = 0; kk < KPL; ++kk) {
-                    const uint64_t b = g.ballot((redo >> kk) & 1u);
-                    if (kk < 2) rlo |= b << (32 * kk);
-                    else rhi |= b << (32 * (kk - 2));
+                // rows to rebuild, one 32-bit word per slot (bit = owner lane)
+                uint32_t r0 = g.ballot(redo & 1u), r1 = 0, r2 = 0, r3 = 0;
+                if (KPL > 1) r1 = g.ballot((redo >> 1) & 1u);
+                if (KPL > 2) {
+                    r2 = g.ballot((redo >> 2) & 1u);
+                    r3 = g.ballot((redo >> 3) & 1u);
                 }
                 const int h = g.gl >> 4, j = g.gl & 15;
                 const uint32_t hm = h ? 0xffff0000u : 0x0000ffffu;
+                auto pop1 = [](uint32_t &w, int base) -> int {
+                    const int r = __ffs(w) - 1 + base;
+                    w &= w - 1;
+                    return r;
+                };
                 auto pop = [&]() -> int {  // next row index, ascending; -1 when none
-                    if (rlo) {
-                        const int r = __ffsll(static_cast<long long>(rlo)) - 1;
-                        rlo &= rlo - 1;
-                        return r;
-                    }
-                    if (KPL > 2 && rhi) {
-                        const int r = 64 + __ffsll(static_cast<long long>(rhi)) - 1;
-                        rhi &= rhi - 1;
-                        return r;
-                    }
+                    if (r0) return pop1(r0, 0);
+                    if (KPL > 1 && r1) return pop1(r1, 32);
+                    if (KPL > 2 && r2) return pop1(r2, 64);
+                    if (KPL > 2 && r3) return pop1(r3, 96);
                     return -1;
                 };
                 for (;;) {
