@@ -224,7 +224,8 @@ struct oserve_gpu_ctx {
     std::vector<ShapeParam> shapes;
     int tables_shapes = -1;  // shapes computed in device tables
     bool tables_dirty = true;
-    DBuf d_param, d_n, d_e, d_lat, d_M, d_unit, d_inv, d_rank, d_cap, d_order, d_olen, d_pp, d_scaled, d_cin, d_cout;
+    DBuf d_param, d_n, d_e, d_lat, d_M, d_unit, d_inv, d_rank, d_pmask, d_cap, d_order, d_olen, d_pp, d_scaled, d_cin,
+        d_cout;
     ShapeTables tables{};
     // space
     Space space;
@@ -331,6 +332,7 @@ void ensure_tables(oserve_gpu_ctx &c) {
     t.cap = static_cast<int32_t *>(c.d_cap.get(sizeof(int32_t) * S * J));
     t.order = static_cast<uint8_t *>(c.d_order.get(S * kMaxJ));
     t.rank = static_cast<uint8_t *>(c.d_rank.get(S * kMaxJ));
+    t.pmask = static_cast<uint16_t *>(c.d_pmask.get(sizeof(uint16_t) * S * kMaxJ));
     t.olen = static_cast<uint8_t *>(c.d_olen.get(S));
     t.scaled = static_cast<uint8_t *>(c.d_scaled.get(S));
     std::vector<uint8_t> pps(S);
@@ -2062,7 +2064,7 @@ int oserve_gpu_plan_detail(oserve_gpu_ctx *ctx, const oserve_deployment *dep, in
 
 // Raw [count][R][J] rows staged as the shape tables of one call (K0b only).
 struct RawRows {
-    DBuf dn, de, dM, du, dc, dord, dol, dpp, dsc, dlat, dinv, drank;
+    DBuf dn, de, dM, du, dc, dord, dol, dpp, dsc, dlat, dinv, drank, dpmask;
     ShapeTables t{};
 };
 
@@ -2100,6 +2102,7 @@ void stage_raw_rows(oserve_gpu_ctx &c, int64_t rows, int J, const int64_t *n, co
     t.cap = static_cast<int32_t *>(rr.dc.get(sizeof(int32_t) * rows * J));
     t.order = static_cast<uint8_t *>(rr.dord.get(rows * kMaxJ));
     t.rank = static_cast<uint8_t *>(rr.drank.get(rows * kMaxJ));
+    t.pmask = static_cast<uint16_t *>(rr.dpmask.get(sizeof(uint16_t) * rows * kMaxJ));
     t.olen = static_cast<uint8_t *>(rr.dol.get(rows));
     t.scaled = static_cast<uint8_t *>(rr.dsc.get(rows));
     t.pp = static_cast<uint8_t *>(rr.dpp.get(rows));

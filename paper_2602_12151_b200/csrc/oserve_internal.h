@@ -44,6 +44,7 @@ struct ShapeTables {
     int32_t *cap;     // [S*J] min(e, n, M/unit), clamped to INT32_MAX (exact while lambda < 2^31)
     uint8_t *order;   // [S*kMaxJ] classes with cap > 0, stable-sorted by unit
     uint8_t *rank;    // [S*kMaxJ] position of class j in order (0xff: not in order)
+    uint16_t *pmask;  // [S*kMaxJ] class mask of order positions 0..p (units ascend along the order)
     uint8_t *olen;    // [S]
     uint8_t *pp;      // [S]
     uint8_t *scaled;  // [S] LCM fallback used

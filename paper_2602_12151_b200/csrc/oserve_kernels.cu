@@ -143,7 +143,14 @@ __global__ void k_normalize_rows(ShapeTables t) {
             t.order[s * kMaxJ + i] = i < ol ? ord[i] : 0;
             t.rank[s * kMaxJ + i] = 0xff;
         }
-        for (int i = 0; i < ol; ++i) t.rank[s * kMaxJ + ord[i]] = static_cast<uint8_t>(i);
+        uint32_t pm = 0;
+        for (int i = 0; i < kMaxJ; ++i) {
+            if (i < ol) {
+                t.rank[s * kMaxJ + ord[i]] = static_cast<uint8_t>(i);
+                pm |= 1u << ord[i];
+            }
+            t.pmask[s * kMaxJ + i] = static_cast<uint16_t>(pm);
+        }
         t.olen[s] = static_cast<uint8_t>(ol);
     }
 }
@@ -390,6 +397,7 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
     const int32_t *sCap = t.cap;
     const uint8_t *sOrder = t.order;
     const uint8_t *sRank = t.rank;
+    const uint16_t *sPmask = t.pmask;
     const uint8_t *sOlen = t.olen;
     const uint8_t *sPP = t.pp;
     size_t off = 0;
@@ -398,7 +406,8 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
         int64_t *U_ = M_ + S;
         double *I_ = reinterpret_cast<double *>(U_ + S * J);
         int32_t *C_ = reinterpret_cast<int32_t *>(I_ + S * J);
-        uint8_t *O_ = reinterpret_cast<uint8_t *>(C_ + S * J);
+        uint16_t *Q_ = reinterpret_cast<uint16_t *>(C_ + S * J);
+        uint8_t *O_ = reinterpret_cast<uint8_t *>(Q_ + S * kMaxJ);
         uint8_t *K_ = O_ + S * kMaxJ;
         uint8_t *L_ = K_ + S * kMaxJ;
         uint8_t *P_ = L_ + S;
@@ -416,9 +425,11 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
         for (int i = threadIdx.x; i < S * kMaxJ; i += blockDim.x) {
             O_[i] = t.order[i];
             K_[i] = t.rank[i];
+            Q_[i] = t.pmask[i];
         }
         sM = M_;
         sRank = K_;
+        sPmask = Q_;
         sUnit = U_;
         sInv = I_;
         sCap = C_;
@@ -710,7 +721,8 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
             }
             const uint64_t used_l = (g.gl == pb) ? excl + static_cast<uint64_t>(take) * static_cast<uint64_t>(u) : csum;
             const uint64_t used = ol ? g.bcast(used_l, pb < ol ? pb : ol - 1) : 0ull;
-            const uint32_t hb = g.or_all(take > 0 ? (1u << j) : 0u);
+            // held classes (low 16 bits) and full classes x == cap (high 16 bits)
+            const uint32_t hb = g.or_all((take > 0 ? (1u << j) : 0u) | (act && take >= capj ? (1u << (j + 16)) : 0u));
             const int64_t mfin = Ms - static_cast<int64_t>(used);
             // run-length step: the next c replicas of the same shape take the
             // identical fill while lam_p - i*take_p >= a_p at every position
@@ -806,9 +818,17 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
             return el;
         };
         // feasible classes of owned replica kk given its eligible held set
+        // feasible classes of owned replica kk given its eligible held set:
+        // j is feasible iff lam_j > 0, x < cap and u_j <= mrem + max(e(j), 0)
+        // (e(j) = largest eligible held unit other than j's own).  Units
+        // ascend along the shape's class order, so for j != e1j that is a
+        // prefix of the order (binary search + prefix mask); e1j is checked
+        // against e2 separately.
         auto feasible_row = [&](int kk, uint32_t el) -> uint32_t {
             const int k = g.gl + G * kk;
             if (k >= R) return 0u;
+            const uint32_t cand = lam_mask & ~(rsel(held, kk) >> 16);
+            if (!cand) return 0u;
             const int s = rsel(shp, kk);
             const int64_t mr = rsel(mrem, kk);
             int64_t e1 = -1, e2 = -1;
@@ -816,24 +836,26 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
             while (el) {
                 const int j2 = __ffs(el) - 1;
                 el &= el - 1;
-                {
-                    const int64_t u2 = sUnit[s * J + j2];
-                    if (u2 > e1) {
-                        e2 = e1;
-                        e1 = u2;
-                        e1j = j2;
-                    } else if (u2 > e2) {
-                        e2 = u2;
-                    }
+                const int64_t u2 = sUnit[s * J + j2];
+                if (u2 > e1) {
+                    e2 = e1;
+                    e1 = u2;
+                    e1j = j2;
+                } else if (u2 > e2) {
+                    e2 = u2;
                 }
             }
-            uint32_t f = 0, lb = lam_mask;
-            while (lb) {
-                const int j = __ffs(lb) - 1;
-                lb &= lb - 1;
-                const int64_t u = sUnit[s * J + j];
-                if (u <= 0 || xs[j * RMAX + k] >= sCap[s * J + j]) continue;
-                if (mr >= u || (e1j == j ? e2 : e1) >= u - mr) f |= 1u << j;
+            const uint64_t T1 = static_cast<uint64_t>(mr) + static_cast<uint64_t>(e1 > 0 ? e1 : 0);
+            int lo = 0, hi = sOlen[s];
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (static_cast<uint64_t>(sUnit[s * J + sOrder[s * kMaxJ + mid]]) <= T1) lo = mid + 1;
+                else hi = mid;
+            }
+            uint32_t f = lo ? (static_cast<uint32_t>(sPmask[s * kMaxJ + lo - 1]) & cand) : 0u;
+            if (e1j >= 0 && ((f >> e1j) & 1u)) {
+                const uint64_t T2 = static_cast<uint64_t>(mr) + static_cast<uint64_t>(e2 > 0 ? e2 : 0);
+                if (static_cast<uint64_t>(sUnit[s * J + e1j]) > T2) f &= ~(1u << e1j);
             }
             return f;
         };
@@ -868,7 +890,7 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                 const int64_t mr = rsel(mrem, kk);
                 const int64_t u = sUnit[s * J + jf];
                 if (mr < u) {
-                    uint32_t hb = rsel(held, kk) & ~(1u << jf);
+                    uint32_t hb = rsel(held, kk) & 0xffffu & ~(1u << jf);
                     while (hb && j2 < 0) {
                         const int jj = __ffs(hb) - 1;
                         hb &= hb - 1;
@@ -894,13 +916,15 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                 const int k = g.gl + G * kk;
                 const int s = shp[kk];
                 if (k == kf) {
-                    xs[jf * RMAX + kf] += 1;
+                    const int32_t xv = xs[jf * RMAX + kf] + 1;
+                    xs[jf * RMAX + kf] = xv;
                     mrem[kk] -= sUnit[s * J + jf];
-                    held[kk] |= 1u << jf;
+                    held[kk] |= (1u << jf) | (xv >= sCap[s * J + jf] ? 1u << (jf + 16) : 0u);
                     if (j2 >= 0) {
                         const int32_t nv = xs[j2 * RMAX + kf] - 1;
                         xs[j2 * RMAX + kf] = nv;
                         mrem[kk] += sUnit[s * J + j2];
+                        held[kk] &= ~(1u << (j2 + 16));  // now below cap
                         if (nv == 0) held[kk] &= ~(1u << j2);
                     }
                     if (lg) {
@@ -910,9 +934,10 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                     }
                 }
                 if (j2 >= 0 && k == k2) {
-                    xs[j2 * RMAX + k2] += 1;
+                    const int32_t xv = xs[j2 * RMAX + k2] + 1;
+                    xs[j2 * RMAX + k2] = xv;
                     mrem[kk] -= sUnit[s * J + j2];
-                    held[kk] |= 1u << j2;
+                    held[kk] |= (1u << j2) | (xv >= sCap[s * J + j2] ? 1u << (j2 + 16) : 0u);
                     if (lg) ulog[nlog + 2] = (static_cast<uint32_t>(j2 * RMAX + k2) << 1) | 1u;
                 }
             }
@@ -1232,7 +1257,7 @@ template <int G, int KPL>
 size_t plan_eval_smem(int S, int J, bool stage) {
     constexpr int RMAX = G * KPL;
     constexpr int GPB = 256 / G;
-    size_t shapes = (size_t)S * 8 + (size_t)S * J * 16 + (size_t)S * J * 4 + 2 * (size_t)S * kMaxJ + 2 * (size_t)S;
+    size_t shapes = (size_t)S * 8 + (size_t)S * J * 16 + (size_t)S * J * 4 + 4 * (size_t)S * kMaxJ + 2 * (size_t)S;
     shapes = stage ? (shapes + 15) & ~size_t(15) : 0;
     return shapes + group_scratch_bytes<RMAX, KPL>(J) * GPB + GPB * 8;
 }
