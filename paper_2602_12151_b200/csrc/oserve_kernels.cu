@@ -1099,11 +1099,11 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                         e1 = sUnit[sr * J + e1j];
                     }
                     if (t2) e2 = sUnit[sr * J + sOrder[sr * kMaxJ + t2 - 1]];
-                    bool f = false;
-                    if (j < J && ((lam_mask >> j) & 1u)) {
+                    bool f = false;  // x < cap: not full; u > 0: in the shape's order
+                    if (j < J && ((lam_mask >> j) & 1u) && !((hr >> (16 + j)) & 1u) &&
+                        sRank[sr * kMaxJ + j] != 0xff) {
                         const int64_t u = sUnit[sr * J + j];
-                        if (u > 0 && xs[j * RMAX + r] < sCap[sr * J + j])
-                            f = mr >= u || (e1j == j ? e2 : e1) >= u - mr;
+                        f = mr >= u || (e1j == j ? e2 : e1) >= u - mr;
                     }
                     const uint32_t Fb = __ballot_sync(0xffffffffu, f);
                     if (g.gl == (ra & (G - 1))) {
