@@ -496,13 +496,23 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
     g.sync();
 
     // chunks are handed out dynamically (one atomic per chunk): neighbouring
-    // plans have correlated costs, so a static split leaves a long tail
+    // plans have correlated costs, so a static split leaves a long tail.
+    // Guided: once fewer than ~2 full chunks per group remain, chunks shrink
+    // to a quarter so the last ones finish together.
+    const uint64_t tail_from = src.count > 2 * ngroups * gch ? src.count - 2 * ngroups * gch : 0;
+    const uint64_t gsmall = gch >= 4 ? gch / 4 : 1;
     for (;;) {
-    unsigned long long cix = 0;
-    if (g.gl == 0) cix = atomicAdd(work, 1ull);
-    const uint64_t cb = g.bcast(cix, 0) * gch;
+    unsigned long long cb = 0;
+    uint64_t csz = gch;
+    if (g.gl == 0) {
+        const unsigned long long seen = *reinterpret_cast<volatile unsigned long long *>(work);
+        if (seen >= tail_from) csz = gsmall;
+        cb = atomicAdd(work, static_cast<unsigned long long>(csz));
+    }
+    cb = g.bcast(cb, 0);
+    csz = g.bcast(csz, 0);
     if (cb >= src.count) break;
-    for (uint64_t i = cb, ce = (cb + gch < src.count ? cb + gch : src.count); i < ce; ++i) {
+    for (uint64_t i = cb, ce = (cb + csz < src.count ? cb + csz : src.count); i < ce; ++i) {
         // ---- resolve the plan ----
         int R;
         int shp[KPL];
