@@ -5,7 +5,7 @@ object (stdout, and --out if given).
 
     python scripts/bench_rows.py --out profiles/round1_rows.json
 
-Rows: f1 search() (GPU-backed driver), f2 exact B&B (config 1-B&B
+Rows: config 4 (24 re-scheduling windows), f1 search() (GPU-backed driver), f2 exact B&B (config 1-B&B
 exhaustive), f3 kv_plan, f4 max_flow / build_network+max_flow+
 extract_assignment / solve_fractional, and the K2 switching batch.  GPU
 times are wall-clock around the public call (host copies included) after
@@ -24,7 +24,7 @@ sys.path.insert(0, os.path.join(ROOT, "oracle"))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from paper_2602_12151_b200 import core, workloads  # noqa: E402
+from paper_2602_12151_b200 import core, orchestrate, workloads  # noqa: E402
 from paper_2602_12151_b200._native import GpuContext  # noqa: E402
 from pyoracle import Oracle, Problem  # noqa: E402
 
@@ -55,6 +55,35 @@ def row(name, gpu_s, ref_s, same, **kw):
 
 def problem(w):
     return Problem(w.cluster, w.model, w.types, w.lam, w.span_s, w.params)
+
+
+def cpu_timeline(ref, w, forecasts, min_gain, threads):
+    """The config-4 window loop on the reference (oracle/_ref): its round over the
+    full space, evaluate_deployment for the keep rule, capacity table +
+    solve_assignment, greedy_plan/estimate_time."""
+    entries, current, prev_lam, prev_x = [], None, None, None
+    for s, lam in enumerate(forecasts):
+        if entries and lam == prev_lam:
+            continue
+        pr = Problem(w.cluster, w.model, w.types, lam, w.span_s, w.params)
+        found = ref.round(pr, w.space_mode, w.space_sizes, threads=threads)
+        chosen = found.deployment
+        if current is not None:
+            keep = ref.evaluate_deployment(pr, current)
+            if float(found.throughput) <= float(keep) * (1.0 + min_gain):
+                chosen = current
+        t = ref.capacity_table(pr, chosen)
+        x = ref.solve_assignment(t.n, t.e, lam).assignment.x
+        same = current is not None and orchestrate._same(chosen, current)
+        if not entries:
+            entries.append((s, chosen.shapes(), x, None))
+        elif not same:
+            plan, _ = ref.switch_plan(w.cluster, w.model.param_bytes, current, chosen)
+            entries.append((s, chosen.shapes(), x, plan.est_seconds))
+        elif x != prev_x:
+            entries.append((s, chosen.shapes(), x, None))
+        current, prev_lam, prev_x = chosen, lam, x
+    return entries
 
 
 def main():
@@ -154,6 +183,19 @@ def main():
     rs, exp = cpu_timed(lambda: [ref.switch_plan(w.cluster, w.model.param_bytes, src, d)[0].est_seconds
                                  for d in deps])
     rows.append(row("K2 switch_cost_batch 1024 pairs (cfg5)", gs, rs, list(est) == exp))
+
+    # config 4: 24 windows of re-scheduling (orchestrate.py loop: full-space round per window, keep
+    # rule, assignment, switch plan) against the same loop over the reference's CPU round
+    w = workloads.load("cfg4")
+    fc, mg = w.raw["forecasts"], w.raw["min_gain"]
+    g = GpuContext(w.cluster, w.model, w.params)
+    gs, tl = timed(lambda: orchestrate.build_adaptive_timeline(g, w.types, fc, w.span_s, mg, w.space_mode,
+                                                                w.space_sizes))
+    got = [(e.span_index, e.deployment.shapes(), e.assignment,
+            None if e.switch is None else e.switch_seconds) for e in tl.entries]
+    rs, exp = cpu_timed(lambda: cpu_timeline(ref, w, fc, mg, threads))
+    rows.append(row("cfg4 temporal: 24 windows (round + keep rule + assignment + switch plan)", gs, rs, got == exp,
+                    rounds=tl.rounds, entries=len(tl.entries), ms_per_round_gpu=round(1e3 * gs / max(1, tl.rounds), 3)))
 
     out = {"device": torch.cuda.get_device_name(0), "host_threads": threads, "rows": rows}
     print(json.dumps(out, indent=1))
