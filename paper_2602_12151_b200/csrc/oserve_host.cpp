@@ -1625,6 +1625,35 @@ int oserve_gpu_kv_plan(oserve_gpu_ctx *ctx, int n_inflight, const oserve_infligh
         in.kind = static_cast<int32_t *>(b[11].get(sizeof(int32_t) * std::max(n_inflight, 1)));
         in.mig_src = static_cast<int32_t *>(b[12].get(sizeof(int32_t) * std::max(n_inflight, 1)));
         in.mig_dst = static_cast<int32_t *>(b[13].get(sizeof(int32_t) * std::max(n_inflight, 1)));
+        // Requests migrating to different target replicas are independent
+        // (disjoint devices): partition them by target replica (round-robin
+        // over the migrated sequence, switchplan.cpp:178-181) for the
+        // warp-per-replica kernel, unless a target replica is empty.
+        bool par = dst->num_replicas > 1;
+        for (int r = 0; r < dst->num_replicas && par; ++r)
+            if (dst->replica_num_devices[r] == 0) par = false;
+        if (par) {  // replicas must not share a device (the state partition relies on it)
+            std::set<int32_t> seen(ddev.begin(), ddev.end());
+            if (seen.size() != ddev.size()) par = false;
+        }
+        DBuf pb[2];
+        if (par) {
+            std::vector<int32_t> goff(dst->num_replicas + 1, 0), greq;
+            int m = 0;
+            for (int q = 0; q < n_inflight; ++q)
+                if (gen[q] > threshold_tokens) ++goff[(m++ % dst->num_replicas) + 1];
+            for (int r = 0; r < dst->num_replicas; ++r) goff[r + 1] += goff[r];
+            greq.resize(static_cast<size_t>(std::max(m, 1)));
+            std::vector<int32_t> fill(goff.begin(), goff.end() - 1);
+            m = 0;
+            for (int q = 0; q < n_inflight; ++q)
+                if (gen[q] > threshold_tokens) greq[fill[m++ % dst->num_replicas]++] = q;
+            in.grp_off = pb[0].upload(goff, s);
+            in.grp_req = pb[1].upload(greq, s);
+            cuda_ok(cudaMemsetAsync(in.kind, 0, sizeof(int32_t) * n_inflight, s), "memset");
+            cuda_ok(cudaMemsetAsync(in.mig_src, 0, sizeof(int32_t) * n_inflight, s), "memset");
+            cuda_ok(cudaMemsetAsync(in.mig_dst, 0, sizeof(int32_t) * n_inflight, s), "memset");
+        }
         cuda_ok(launch_kv_plan(in, s, &ctx->launches), "kv_plan kernel");
         std::vector<int32_t> kind, ms, md;
         download(kind, in.kind, n_inflight, s);

@@ -240,6 +240,10 @@ struct KvPlanIn {
     // outputs
     int32_t *kind;               // [n] 0 drained, 1 migrated
     int32_t *mig_src, *mig_dst;  // [n] device ids
+    // target-replica partition (parallel path): the migrated requests of
+    // target replica r, in order, are grp_req[grp_off[r] .. grp_off[r+1])
+    const int32_t *grp_off;      // [dst_reps+1] or null (sequential kernel)
+    const int32_t *grp_req;
 };
 int launch_kv_plan(const KvPlanIn &in, void *stream, uint64_t *launches);
 

@@ -2408,6 +2408,89 @@ __global__ void __launch_bounds__(32) k_kv_plan(KvPlanIn in, int use_smem) {
     }
 }
 
+// Parallel kv_plan: requests migrating to different target replicas touch
+// disjoint state (the target's devices' inbound loads and the link-load
+// columns of those devices; replicas own disjoint devices), so one warp per
+// target replica walks that replica's requests in order — the same
+// sequence of picks as the sequential fold.  The host falls back to
+// k_kv_plan when a target replica is empty (its pick, device -1, would be
+// shared).  State lives in global memory (volatile: columns of different
+// warps share cache lines).
+__device__ __forceinline__ KvPick kv_min_width(KvPick p, int width) {
+    for (int d = width >> 1; d > 0; d >>= 1) {
+        KvPick o;
+        o.v = __shfl_xor_sync(0xffffffffu, p.v, d);
+        o.cls = __shfl_xor_sync(0xffffffffu, p.cls, d);
+        o.slot = __shfl_xor_sync(0xffffffffu, p.slot, d);
+        if (kv_less(o, p)) p = o;
+    }
+    return p;
+}
+
+__global__ void __launch_bounds__(128) k_kv_plan_par(KvPlanIn in) {
+    const int lane = threadIdx.x & 31;
+    const int r = blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (r >= in.dst_reps) return;
+    constexpr int kNone = 0x7fffffff;
+    const int NS = in.num_slots;
+    volatile uint64_t *load = in.load;
+    volatile uint64_t *inbound = in.inbound;
+    const int d0 = in.dst_off[r], d1 = in.dst_off[r + 1];
+    const int nd = d1 - d0;
+    int wt = 1;
+    while (wt < nd && wt < 32) wt <<= 1;
+    const int g0 = in.grp_off[r], g1 = in.grp_off[r + 1];
+    for (int base = g0; base < g1; base += 32) {
+        const int idx = base + lane;
+        const int my_q = idx < g1 ? in.grp_req[idx] : 0;
+        const uint64_t my_kv = idx < g1 ? in.kv[my_q] : 0;
+        const int my_sr = idx < g1 ? in.srcrep[my_q] : 0;
+        int my_src = 0, my_dst = 0;
+        const int cnt = g1 - base < 32 ? g1 - base : 32;
+        for (int b = 0; b < cnt; ++b) {
+            const uint64_t kvq = __shfl_sync(0xffffffffu, my_kv, b);
+            const int srq = __shfl_sync(0xffffffffu, my_sr, b);
+            KvPick t{~0ull, 2, kNone};
+            for (int p = d0 + lane; p < d1; p += 32) {
+                const int slot = in.dst_devs[p];
+                const KvPick c{inbound[slot], 0, slot};
+                if (kv_less(c, t)) t = c;
+            }
+            t = kv_min_width(t, nd > 32 ? 32 : wt);
+            const int target = __shfl_sync(0xffffffffu, t.slot, 0);  // lanes < width hold the minimum; nd >= 1
+            const int s0 = in.src_off[srq], s1 = in.src_off[srq + 1];
+            const int ns = s1 - s0;
+            int ws = 1;
+            while (ws < ns && ws < 32) ws <<= 1;
+            KvPick bsel{~0ull, 2, kNone};
+            const int mt = in.machine[target];
+            for (int p = s0 + lane; p < s1; p += 32) {
+                const int slot = in.src_devs[p];
+                const bool intra = in.machine[slot] >= 0 && in.machine[slot] == mt;
+                const KvPick c{load[static_cast<size_t>(slot) * NS + target], intra ? 0 : 1, slot};
+                if (kv_less(c, bsel)) bsel = c;
+            }
+            bsel = kv_min_width(bsel, ns > 32 ? 32 : ws);
+            const int bslot = __shfl_sync(0xffffffffu, bsel.slot, 0);
+            const int best = bslot == kNone ? in.none_slot : bslot;
+            if (lane == 0) {
+                load[static_cast<size_t>(best) * NS + target] += kvq;
+                inbound[target] += kvq;
+            }
+            if (lane == b) {
+                my_src = best;
+                my_dst = target;
+            }
+            __syncwarp();
+        }
+        if (idx < g1) {
+            in.kind[my_q] = 1;
+            in.mig_src[my_q] = in.dev_id[my_src];
+            in.mig_dst[my_q] = in.dev_id[my_dst];
+        }
+    }
+}
+
 __global__ void k_topk_check(const uint64_t *meta, int groups, const uint64_t *kth, unsigned int *bad) {
     const uint64_t kk = *kth;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < groups; i += gridDim.x * blockDim.x)
@@ -2638,6 +2721,11 @@ int sort_keys(uint64_t *keys, uint64_t *tmp_keys, int n, void **temp, size_t *te
 int launch_kv_plan(const KvPlanIn &in, void *stream, uint64_t *launches) {
     cudaGetLastError();
     if (in.n == 0) return 0;
+    if (in.grp_off) {  // target-replica parallel path (kind / mig_* pre-zeroed by the caller)
+        k_kv_plan_par<<<(in.dst_reps + 3) / 4, 128, 0, static_cast<cudaStream_t>(stream)>>>(in);
+        if (launches) ++*launches;
+        return check(cudaGetLastError());
+    }
     const size_t NS = static_cast<size_t>(in.num_slots);
     const size_t smem = sizeof(uint64_t) * (NS * NS + NS) +
                         sizeof(int32_t) * (NS + in.src_reps + 1 + in.dst_reps + 1 + in.n_src_devs + in.n_dst_devs);
