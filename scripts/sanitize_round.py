@@ -1,9 +1,11 @@
-"""Small scheduling-round workloads for compute-sanitizer (memcheck / racecheck /
-synccheck): K0a/K0b cost tables, both K1 buckets (one replica per lane, R <= 32,
-and two per lane, R > 32), the exact top-K path and K2 switching — each on a
-slice small enough for the sanitizer's replay.
+"""Small scheduling-round workloads that touch every round kernel: K0a/K0b cost
+tables, both K1 buckets (one replica per lane, R <= 32, and two per lane,
+R > 32), K2 switching batch and the full switch plan — each on a slice small
+enough for a tool's replay.  (compute-sanitizer is closed on the GPU pool, so
+the memory-safety evidence is the parity suite plus the kernels' own bounds
+checks; this script stays as the minimal per-kernel workload.)
 
-  compute-sanitizer --tool memcheck python scripts/sanitize_round.py
+  python scripts/sanitize_round.py
 """
 import os
 import sys
