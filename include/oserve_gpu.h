@@ -40,7 +40,8 @@ typedef enum {
     OSERVE_ERR_LOGIC = 7,              /* std::logic_error (check_constraints)    */
     OSERVE_ERR_UNSUPPORTED = 8,        /* input outside the GPU path's limits     */
     OSERVE_ERR_CUDA = 9,
-    OSERVE_ERR_NO_DEVICE = 10
+    OSERVE_ERR_NO_DEVICE = 10,
+    OSERVE_ERR_NCCL = 11               /* communicator / collective failure        */
 } oserve_status;
 
 /* ---- L0 types (proj/include/oserve/core.hpp:11-95) -------------------- */
@@ -157,6 +158,27 @@ int oserve_gpu_create(int cuda_device, const oserve_cluster_desc *cluster,
                       const oserve_model_desc *model, const oserve_profile *profile,
                       oserve_gpu_ctx **out);
 int oserve_gpu_destroy(oserve_gpu_ctx *ctx);
+
+/* ---- multi-GPU: the plan space sharded over GPUs ---------- */
+
+/* One context over several local devices (one process): each device
+ * evaluates interleaved chunks of the plan order (OSERVE_SHARD_CHUNK) and an
+ * NCCL communicator over the devices (ncclCommInitAll) carries the one
+ * exchange of the round.  oserve_gpu_round / _exhaustive / _best_strategies /
+ * _launch_round_async then all-reduce(MIN) the packed key and
+ * oserve_gpu_round_topk all-gathers the per-device top-K lists; spaces of
+ * fewer than 65,536 plans (OSERVE_SHARD_MIN) and exact-path spaces run whole
+ * on cuda_devices[0].  Every other entry point runs on cuda_devices[0]. */
+int oserve_gpu_create_multi(const int *cuda_devices, int ndev, const oserve_cluster_desc *cluster,
+                            const oserve_model_desc *model, const oserve_profile *profile, oserve_gpu_ctx **out);
+/* One process per GPU: rank 0 makes an id (128 bytes, ncclGetUniqueId) and
+ * shares it out of band; every rank joins its single-device context to the
+ * world (ncclCommInitRank).  The same entry points then shard over the world
+ * and return the global result on every rank. */
+int oserve_nccl_unique_id(void *id_128_bytes);
+int oserve_gpu_join(oserve_gpu_ctx *ctx, const void *id_128_bytes, int rank, int world);
+/* Global rank of the context's first device, world size, local devices. */
+int oserve_gpu_world(const oserve_gpu_ctx *ctx, int *rank, int *world, int *local_devices);
 const char *oserve_gpu_last_error(const oserve_gpu_ctx *ctx);
 const char *oserve_gpu_status_name(int status);
 

@@ -5,6 +5,8 @@ reference oracle oracle/_ref).  Writes paper_2602_12151_b200/configs/cfg*.json;
 those JSON files are the committed inputs of bench.py and the parity tests,
 so nothing downstream needs /root/reference.
 
+Usage: python oracle/gen_configs.py [cfg ...]   (default: every config)
+
 Workload recipe:
   * trace: 200k records, seed 2602, two lognormal families mixed 60/40 —
     short-output (in ~ LogN(ln 2048, .6), out ~ LogN(ln 28, .8)) and
@@ -95,7 +97,11 @@ def main():
         fitted[J] = ref.fit_types(inp, out, J, seed=0)
     prof = core.ProfileParams()
 
+    only = [a if a.endswith(".json") else a + ".json" for a in sys.argv[1:]]
+
     def write(name, cfg):
+        if only and name not in only:
+            return
         with open(os.path.join(OUT, name), "w") as f:
             json.dump(cfg, f, indent=1)
         print("wrote", name, {k: cfg[k] for k in ("lambda",) if k in cfg})
@@ -117,6 +123,8 @@ def main():
         return [int(round(load * s * C)) for s in share], C
 
     def emit(name, desc, machines, model, J, space, load=0.9):
+        if only and name not in only:
+            return
         cl = core.cluster(machines, 8)
         lam, C = lam_for(cl, model, fitted[J], load)
         write(name, dict(base, name=name[:-5], description=desc, cluster=cluster_json(machines, 8),
@@ -140,8 +148,14 @@ def main():
     emit("cfg5_full.json", "128-GPU cluster, 16 classes, canonical plan space sizes {2,4,...,128} "
          "(every power-of-two block)", 16, core.model_140gb(), 16,
          {"mode": "canonical", "sizes": [2, 4, 8, 16, 32, 64, 128]})
+    # 7B-class model on the config-5 cluster: g_min = 1, so plans reach 128
+    # replicas (sizes {1,2,4}: R from 32 to 128)
+    emit("cfg5_7b.json", "128-GPU cluster, 16 classes, 7B-class cost tables, canonical plan space sizes "
+         "{1,2,4} (32-128 replicas per plan)", 16, core.model_14gb(), 16, {"mode": "canonical", "sizes": [1, 2, 4]})
 
     # config 4: temporal, 24 windows on the config-2 cluster
+    if only and "cfg4.json" not in only:
+        return
     cl = core.cluster(4, 8)
     types = fitted[4]
     lab = assign(types, inp, out)

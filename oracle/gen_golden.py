@@ -293,6 +293,70 @@ def gen_exact_budget(ref, port):
     json.dump(cases, open(os.path.join(OUT, "exact_budget.json"), "w"))
 
 
+def gen_wide(ref):
+    """Config 5-7B (g_min = 1, sizes {1,2,4}: 32-128 replicas per plan) ->
+    plans_cfg5_7b.json and wide.json.  The sample is weighted toward plans
+    with R > 64 (rare under uniform sampling): 2,000 plans from partitions
+    with R > 64, 1,000 uniform, plus each R > 64 partition's first plan.
+    wide.json: switching pairs with 128 source replicas (init_uniform -> plans)
+    and capacity table + solve_assignment of R = 96 / 128 plans."""
+    from math import comb
+    name = "cfg5_7b"
+    w = workloads.load(name)
+    pr = problem(w)
+    parts, plans = ref.space_info(pr, w.space_mode, w.space_sizes)
+    # partitions_desc order with parts {4,2,1} (a fours, b twos, c ones); the
+    # blocks of one size share their candidate list (4: 3 strategies, 2: 2,
+    # 1: 1), so a partition holds C(a+2,2) * (b+1) canonical plans
+    struct = []
+    for a in range(32, -1, -1):
+        for b in range((128 - 4 * a) // 2, -1, -1):
+            struct.append((a + b + 128 - 4 * a - 2 * b, comb(a + 2, 2) * (b + 1)))
+    pre = np.cumsum([0] + [c for _, c in struct])
+    assert len(struct) == parts and pre[-1] == plans
+    for i in (0, len(struct) // 2, len(struct) - 1):  # structure check against the harness
+        d, p, l = ref.space_plan(pr, w.space_mode, int(pre[i]), w.space_sizes)
+        assert (p, l, d.replica_count()) == (i, 0, struct[i][0])
+    rng = np.random.default_rng(12151)
+    wide = [i for i, (R, _) in enumerate(struct) if R > 64]
+    wt = np.array([struct[i][1] for i in wide], float)
+    pick = rng.choice(wide, 2000, p=wt / wt.sum())
+    ranks = [int(pre[i] + rng.integers(0, struct[i][1])) for i in pick]
+    ranks += rng.integers(0, plans, 1000).tolist() + [int(pre[i]) for i in wide]
+    ranks = np.unique(np.array(ranks, np.uint64))
+    obj, spp, _ = ref.evaluate_ranks(pr, w.space_mode, ranks, w.space_sizes, threads=THREADS)
+    part_of = np.searchsorted(pre, ranks, side="right") - 1
+    json.dump({"partitions": parts, "plans": plans, "ranks": ranks.tolist(), "objective": obj.tolist(),
+               "sum_pp": spp.tolist(), "R": [struct[p][0] for p in part_of]},
+              open(os.path.join(OUT, f"plans_{name}.json"), "w"))
+    # 128-source switching pairs and R = 96 / 128 assignment details
+    cur = core.canonical_deployment(w.cluster, [1] * 128, [1] * 128)
+    sw, det = [], []
+    # the R = 128 plan (last rank), R = 127 / ~100 partitions, and uniform ranks
+    targets = [plans - 1, int(pre[-3]), int(pre[-40])] + rng.integers(0, plans, 5).tolist()
+    # (every device of the all-ones source holds the whole model, so those
+    # pairs move nothing; R > 64 sources with 2-/4-device replicas do)
+    plan_at = lambda r: ref.space_plan(pr, w.space_mode, int(r), w.space_sizes)[0]
+    pairs = [(cur, plan_at(r), -1, int(r)) for r in targets]
+    for a in wide[::len(wide) // 12][:12]:
+        ra = int(pre[a] + rng.integers(0, struct[a][1]))
+        rb = int(rng.integers(0, plans))
+        pairs += [(plan_at(ra), plan_at(rb), ra, rb), (plan_at(rb), plan_at(ra), rb, ra)]
+    for src, dst, ra, rb in pairs:
+        plan, mx = ref.switch_plan(w.cluster, w.model.param_bytes, src, dst)
+        sw.append({"src_rank": ra, "rank": rb, "src": dep_json(src), "dst": dep_json(dst),
+                   "est_seconds": plan.est_seconds, "max_link_bytes": mx,
+                   "transfers": [[t.range.begin, t.range.end, t.src, t.dst] for t in plan.transfers]})
+    for r in (plans - 1, plans - 2, int(pre[-20]), int(pre[-300])):
+        dep = ref.space_plan(pr, w.space_mode, r, w.space_sizes)[0]
+        t = ref.capacity_table(pr, dep)
+        ll = ref.solve_assignment(t.n, t.e, w.lam)
+        det.append({"rank": r, "deployment": dep_json(dep), "n": t.n, "e": t.e, "x": ll.assignment.x,
+                    "objective": ll.assignment.objective, "M": ll.M, "unit": ll.unit, "used": ll.used,
+                    "evaluate_deployment": ref.evaluate_deployment(pr, dep)})
+    json.dump({"config": name, "switch": sw, "detail": det}, open(os.path.join(OUT, "wide.json"), "w"))
+
+
 def gen_f3(ref):
     json.dump(kv_cases(ref), open(os.path.join(OUT, "kv_plan.json"), "w"))
     w = workloads.load("cfg4")
@@ -307,6 +371,8 @@ if __name__ == "__main__":
         gen_f4(Oracle("ref"))
     elif sys.argv[1:] == ["exact"]:
         gen_exact_budget(Oracle("ref"), Oracle("port"))
+    elif sys.argv[1:] == ["wide"]:
+        gen_wide(Oracle("ref"))
     elif sys.argv[1:2] == ["sample"]:  # python oracle/gen_golden.py sample cfg5_full
         for nm in sys.argv[2:]:
             canonical_sample(Oracle("ref"), nm)

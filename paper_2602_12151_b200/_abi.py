@@ -25,6 +25,7 @@ ERR_LOGIC = 7
 ERR_UNSUPPORTED = 8
 ERR_CUDA = 9
 ERR_NO_DEVICE = 10
+ERR_NCCL = 11
 
 SPACE_ORDERED = 0
 SPACE_CANONICAL = 1
@@ -275,6 +276,7 @@ _EXC = {
     ERR_UNSUPPORTED: core.Unsupported,
     ERR_CUDA: core.CudaError,
     ERR_NO_DEVICE: core.CudaError,
+    ERR_NCCL: core.CudaError,
 }
 
 

@@ -31,6 +31,7 @@ EXPORTS = [
     "oserve_gpu_search", "oserve_gpu_kv_plan", "oserve_forecast_series",
     "oserve_gpu_max_flow_batch", "oserve_gpu_flow_assign_batch", "oserve_gpu_extract_assignment_batch",
     "oserve_gpu_solve_fractional_batch",
+    "oserve_gpu_create_multi", "oserve_nccl_unique_id", "oserve_gpu_join", "oserve_gpu_world",
 ]
 
 _lib = None
@@ -48,6 +49,10 @@ def load_library() -> C.CDLL:
     vp = C.c_void_p
     L.oserve_gpu_create.argtypes = [C.c_int, P(A.ClusterDesc), P(A.ModelDesc), P(A.Profile), P(vp)]
     L.oserve_gpu_destroy.argtypes = [vp]
+    L.oserve_gpu_create_multi.argtypes = [P(C.c_int), C.c_int, P(A.ClusterDesc), P(A.ModelDesc), P(A.Profile), P(vp)]
+    L.oserve_nccl_unique_id.argtypes = [vp]
+    L.oserve_gpu_join.argtypes = [vp, vp, C.c_int, C.c_int]
+    L.oserve_gpu_world.argtypes = [vp, P(C.c_int), P(C.c_int), P(C.c_int)]
     L.oserve_gpu_last_error.argtypes = [vp]
     L.oserve_gpu_last_error.restype = C.c_char_p
     L.oserve_gpu_status_name.restype = C.c_char_p
@@ -115,6 +120,13 @@ def forecast_series(counts: Sequence[Sequence[int]], window: int = 50, alpha: fl
     return A.i64_rows(out, T, J)
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId for oserve_gpu_join (rank 0 makes it)."""
+    buf = C.create_string_buffer(128)
+    A.raise_for(load_library().oserve_nccl_unique_id(buf), "ncclGetUniqueId failed")
+    return buf.raw
+
+
 def shard_count(total: int, rank: int, world: int, chunk: int = SHARD_CHUNK) -> int:
     """Plans of shard `rank` (C++ host logic, no device needed)."""
     return int(load_library().oserve_shard_count(total, chunk, rank, world))
@@ -150,7 +162,11 @@ class GpuContext:
     """
 
     def __init__(self, cluster: core.ClusterSpec, model: core.ModelSpec,
-                 params: Optional[core.ProfileParams] = None, device: int = 0):
+                 params: Optional[core.ProfileParams] = None, device: int = 0,
+                 devices: Optional[Sequence[int]] = None):
+        """`devices` (several CUDA devices of this process): one context over
+        all of them, rounds sharded with an NCCL communicator
+        (oserve_gpu_create_multi); otherwise one device."""
         self.lib = load_library()
         self.cluster, self.model = cluster, model
         self.params = params or core.ProfileParams()
@@ -159,7 +175,13 @@ class GpuContext:
         md = A.model_desc(model)
         pd = A.profile_desc(self.params)
         h = C.c_void_p()
-        st = self.lib.oserve_gpu_create(device, C.byref(cd), C.byref(md), C.byref(pd), C.byref(h))
+        if devices is not None and len(devices) > 1:
+            devs = A._arr(C.c_int, list(devices))
+            st = self.lib.oserve_gpu_create_multi(devs, len(devices), C.byref(cd), C.byref(md), C.byref(pd),
+                                                  C.byref(h))
+        else:
+            dev = devices[0] if devices else device
+            st = self.lib.oserve_gpu_create(dev, C.byref(cd), C.byref(md), C.byref(pd), C.byref(h))
         if st != A.OK:
             A.raise_for(st, f"oserve_gpu_create: {self.lib.oserve_gpu_status_name(st).decode()}")
         self.h = h
@@ -195,6 +217,18 @@ class GpuContext:
 
     def set_shard(self, rank: int, world: int):
         self._chk(self.lib.oserve_gpu_set_shard(self.h, rank, world))
+
+    def join(self, uid: bytes, rank: int, world: int):
+        """Join a multi-process world (one GPU per process): rounds shard over
+        it and the library runs the NCCL exchange (oserve_gpu_join)."""
+        buf = C.create_string_buffer(bytes(uid), 128)
+        self._chk(self.lib.oserve_gpu_join(self.h, buf, int(rank), int(world)))
+
+    def world(self):
+        """(global rank of the first local device, world size, local devices)."""
+        r, w, n = C.c_int(), C.c_int(), C.c_int()
+        self._chk(self.lib.oserve_gpu_world(self.h, C.byref(r), C.byref(w), C.byref(n)))
+        return r.value, w.value, n.value
 
     def set_stream(self, stream_ptr: int):
         self._chk(self.lib.oserve_gpu_set_stream(self.h, C.c_void_p(stream_ptr)))

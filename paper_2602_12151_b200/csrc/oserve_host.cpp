@@ -17,6 +17,8 @@
 // fallback: without a CUDA device every entry point returns
 // OSERVE_ERR_NO_DEVICE.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -33,6 +35,7 @@
 #include <set>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -53,6 +56,61 @@ void cuda_ok(cudaError_t e, const char *what) {
     if (e != cudaSuccess) fail(OSERVE_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 void cuda_ok(int e, const char *what) { cuda_ok(static_cast<cudaError_t>(e), what); }
+
+// NCCL, resolved at run time: a process that already holds a libnccl.so.2
+// (e.g. the one PyTorch ships) shares it; otherwise the system library loads.
+// Only the multi-GPU entry points need it.
+struct Nccl {
+    std::string why;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommInitAll)(ncclComm_t *, int, const int *) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+    bool ok() const { return why.empty(); }
+};
+
+const Nccl &nccl() {
+    static const Nccl n = [] {
+        Nccl r;
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            r.why = std::string("libnccl.so.2 not loadable: ") + dlerror();
+            return r;
+        }
+        auto sym = [&](auto &fp, const char *name) {
+            fp = reinterpret_cast<std::remove_reference_t<decltype(fp)>>(dlsym(h, name));
+            if (!fp && r.why.empty()) r.why = std::string("NCCL symbol missing: ") + name;
+        };
+        sym(r.GetUniqueId, "ncclGetUniqueId");
+        sym(r.CommInitRank, "ncclCommInitRank");
+        sym(r.CommInitAll, "ncclCommInitAll");
+        sym(r.CommDestroy, "ncclCommDestroy");
+        sym(r.AllReduce, "ncclAllReduce");
+        sym(r.AllGather, "ncclAllGather");
+        sym(r.GroupStart, "ncclGroupStart");
+        sym(r.GroupEnd, "ncclGroupEnd");
+        sym(r.GetErrorString, "ncclGetErrorString");
+        return r;
+    }();
+    return n;
+}
+
+const Nccl &nccl_or_fail() {
+    const Nccl &n = nccl();
+    if (!n.ok()) fail(OSERVE_ERR_NCCL, n.why);
+    return n;
+}
+
+void nccl_ok(ncclResult_t r, const char *what) {
+    if (r != ncclSuccess) fail(OSERVE_ERR_NCCL, std::string(what) + ": " + nccl().GetErrorString(r));
+}
 
 // Byte counters of the host<->device copies issued by the current call
 // (bound to the calling context by guarded()).
@@ -77,6 +135,9 @@ cudaError_t d2h(void *dst, const void *src, size_t bytes, cudaStream_t s) {
 struct DBuf {
     void *p = nullptr;
     size_t cap = 0;
+    DBuf() = default;
+    DBuf(const DBuf &) = delete;
+    DBuf &operator=(const DBuf &) = delete;
     ~DBuf() {
         if (p) cudaFree(p);
     }
@@ -239,6 +300,24 @@ struct oserve_gpu_ctx {
     DBuf d_key, d_obj, d_spp, d_x, d_used, d_aborted, d_aborted_n, d_ranks, d_listR, d_listOff, d_listShapes,
         d_listLam, d_sw[12];
     ExactScratch exact;
+    // K1 dynamic-chunk counters of this context (oserve_internal.h WorkRing)
+    DBuf d_ring;
+    WorkRing ring{nullptr, 0, 0};
+    // multi-GPU: this context is local shard 0; `subs` are contexts on the
+    // other local devices (oserve_gpu_create_multi).  comms[i] is local shard
+    // i's NCCL communicator (empty: no communicator); local shard i has global
+    // rank g_rank0 + i of g_world.
+    std::vector<oserve_gpu_ctx *> subs;
+    std::vector<ncclComm_t> comms;
+    int g_rank0 = 0, g_world = 1;
+    uint64_t space_ver = 0, work_ver = 0;             // bumped by build_space / workload or shape changes
+    uint64_t synced_space = ~0ull, synced_work = ~0ull;  // versions a sub last mirrored from the lead
+    DBuf d_mkey, d_mtopk, d_mbest, d_mall, d_mtmp;    // per-shard collective scratch
+
+    oserve_gpu_ctx() = default;
+    oserve_gpu_ctx(const oserve_gpu_ctx &) = delete;
+    oserve_gpu_ctx &operator=(const oserve_gpu_ctx &) = delete;
+    ~oserve_gpu_ctx();
 
     int D() const { return static_cast<int>(dev_sorted.size()); }
     int machine(int d) const {
@@ -250,6 +329,20 @@ struct oserve_gpu_ctx {
         return m < 0 ? 0 : machine_mem[m];
     }
 };
+
+oserve_gpu_ctx::~oserve_gpu_ctx() {
+    for (oserve_gpu_ctx *s : subs) delete s;  // each on its own device
+    subs.clear();
+    cudaSetDevice(device);
+    for (ncclComm_t cm : comms)
+        if (cm && nccl().ok()) nccl().CommDestroy(cm);
+    if (own) {
+        cudaStreamSynchronize(own);
+        cudaStreamDestroy(own);
+    }
+    if (cub_temp) cudaFree(cub_temp);
+    // the DBuf members are freed next, with this context's device current
+}
 
 namespace {
 
@@ -299,6 +392,7 @@ int shape_for(oserve_gpu_ctx &c, int tp, int pp, uint64_t total_mem) {
     c.shapes.push_back(sp);
     c.shape_id.emplace(key, id);
     c.tables_dirty = true;
+    ++c.work_ver;
     return id;
 }
 
@@ -383,6 +477,8 @@ std::vector<Cand> candidates(oserve_gpu_ctx &c, int off, int d, std::vector<int>
     if (out.size() > static_cast<size_t>(kMaxCand)) fail(OSERVE_ERR_UNSUPPORTED, "more than 8 strategy candidates");
     return out;
 }
+
+void upload_space(oserve_gpu_ctx &c, Space &sp);
 
 void build_space(oserve_gpu_ctx &c, Space &sp, int mode, const std::vector<int> &allowed_sizes,
                  const std::vector<std::vector<int>> *explicit_parts) {
@@ -479,8 +575,29 @@ void build_space(oserve_gpu_ctx &c, Space &sp, int mode, const std::vector<int> 
     }
     if (sp.rmax > OSERVE_MAX_REPLICAS) fail(OSERVE_ERR_UNSUPPORTED, "more than 128 replicas per plan");
     sp.prefix.push_back(sp.total);
+    ++c.space_ver;
+    upload_space(c, sp);
+}
 
-    // flatten + upload
+// Host fields of a space (the enumeration), without its device copies.
+void copy_space_host(const Space &a, Space &b) {
+    b.mode = a.mode;
+    b.sizes_key = a.sizes_key;
+    b.max_devices = a.max_devices;
+    b.explicit_partition = a.explicit_partition;
+    b.explicit_sizes = a.explicit_sizes;
+    b.parts = a.parts;
+    b.prefix = a.prefix;
+    b.total = a.total;
+    b.max_count = a.max_count;
+    b.rmax = a.rmax;
+    b.lists = a.lists;
+    b.list_shapes = a.list_shapes;
+}
+
+// Flatten the enumerated space into the device tables of context c (its
+// device and stream); also the R-buckets.
+void upload_space(oserve_gpu_ctx &c, Space &sp) {
     const size_t P = sp.parts.size();
     std::vector<int32_t> R(P), rep_off(P), run_off(P), nruns(P), rep_list, run_start, run_len, run_q;
     std::vector<uint64_t> run_count, run_weight;
@@ -926,7 +1043,7 @@ void launch_round(oserve_gpu_ctx &c, uint64_t *d_key) {
     SolveParams prm = solve_params(c);
     count_h2d(sizeof(int64_t) * c.J);  // the demand vector travels as a kernel parameter
     for_each_k1_launch(c, sp, [&](const PlanSource &ls, int rmax) {
-        cuda_ok(launch_plan_eval(c.tables, sp.view, c.key, ls, out, prm, rmax, c.sm_count, sp.any_exact ? 1 : 0, s,
+        cuda_ok(launch_plan_eval(c.tables, sp.view, c.key, ls, out, prm, rmax, c.sm_count, sp.any_exact ? 1 : 0, &c.ring, s,
                                  &c.launches),
                 "plan kernel");
     });
@@ -946,7 +1063,7 @@ void launch_round(oserve_gpu_ctx &c, uint64_t *d_key) {
             rs.mode = 1;
             rs.count = n_ab;
             rs.ranks = ab;
-            cuda_ok(launch_plan_eval(c.tables, sp.view, c.key, rs, out, prm, sp.rmax, c.sm_count, 0, s, &c.launches),
+            cuda_ok(launch_plan_eval(c.tables, sp.view, c.key, rs, out, prm, sp.rmax, c.sm_count, 0, &c.ring, s, &c.launches),
                     "plan kernel (budget fallback)");
         }
     }
@@ -1039,7 +1156,7 @@ void eval_lists(oserve_gpu_ctx &c, const std::vector<int32_t> &listR, const std:
     }
     SpaceTables none{};
     KeyLayout nk{};
-    cuda_ok(launch_plan_eval(c.tables, none, nk, src, out, prm, rmax, c.sm_count, any_exact ? 1 : 0, s, &c.launches),
+    cuda_ok(launch_plan_eval(c.tables, none, nk, src, out, prm, rmax, c.sm_count, any_exact ? 1 : 0, &c.ring, s, &c.launches),
             "plan kernel");
     if (any_exact) {
         uint64_t *ab = static_cast<uint64_t *>(c.d_aborted.get(sizeof(uint64_t) * n));
@@ -1071,7 +1188,7 @@ void eval_lists(oserve_gpu_ctx &c, const std::vector<int32_t> &listR, const std:
                     o1.x = out.x + li * out.rmax * prm.J;
                     o1.used = out.used + li * out.rmax;
                 }
-                cuda_ok(launch_plan_eval(c.tables, none, nk, one, o1, prm, rmax, c.sm_count, 0, s, &c.launches),
+                cuda_ok(launch_plan_eval(c.tables, none, nk, one, o1, prm, rmax, c.sm_count, 0, &c.ring, s, &c.launches),
                         "plan kernel (budget fallback)");
             }
         }
@@ -1218,7 +1335,7 @@ void round_topk(oserve_gpu_ctx &c, int K, uint64_t *d_keys, uint64_t *d_best) {
             lo.topk = out.topk + goff * kTopK;
             lo.topk_meta = out.topk_meta + goff;
             cuda_ok(launch_plan_eval(c.tables, sp.view, c.key, launches[q].first, lo, prm, launches[q].second,
-                                     c.sm_count, 0, s, &c.launches),
+                                     c.sm_count, 0, &c.ring, s, &c.launches),
                     "plan kernel (top-K)");
             goff += static_cast<size_t>(lgroups[q]);
         }
@@ -1252,7 +1369,7 @@ void round_topk(oserve_gpu_ctx &c, int K, uint64_t *d_keys, uint64_t *d_best) {
             co.best_key = best;
             cuda_ok(cudaMemsetAsync(co.collect_n, 0, sizeof(unsigned), s), "memset");
             for (auto &[ls, rmax] : launches)
-                cuda_ok(launch_plan_eval(c.tables, sp.view, c.key, ls, co, prm, rmax, c.sm_count, 0, s, &c.launches),
+                cuda_ok(launch_plan_eval(c.tables, sp.view, c.key, ls, co, prm, rmax, c.sm_count, 0, &c.ring, s, &c.launches),
                         "plan kernel (threshold collect)");
             unsigned n = 0;
             cuda_ok(d2h(&n, co.collect_n, sizeof(unsigned), s), "D2H");
@@ -1323,6 +1440,187 @@ void switch_cost_keys(oserve_gpu_ctx &c, const oserve_deployment &current, int c
         if (st[i]) fail(OSERVE_ERR_UNSOURCED_FRAGMENT, "required bytes have no source holder");
 }
 
+// ----------------------------------------------------------- multi-GPU ---
+// A context may own several local shards (oserve_gpu_create_multi: itself
+// plus `subs` on the other devices) and/or belong to a multi-process world
+// (oserve_gpu_join).  The sharded round: every local shard evaluates its
+// interleaved chunks of the plan order (the same tables, mirrored from the
+// lead), then one NCCL collective per shard — all-reduce(MIN) of the packed
+// key, or all-gather of the top-K lists — on the shards' streams.
+
+struct DeviceScope {
+    int prev = -1;
+    explicit DeviceScope(int d) {
+        cudaGetDevice(&prev);
+        cuda_ok(cudaSetDevice(d), "cudaSetDevice");
+    }
+    ~DeviceScope() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// Temporarily evaluate as shard (rank, world).
+struct ShardAs {
+    oserve_gpu_ctx &c;
+    int r0, w0;
+    ShardAs(oserve_gpu_ctx &cc, int r, int w) : c(cc), r0(cc.rank), w0(cc.world) {
+        c.rank = r;
+        c.world = w;
+    }
+    ~ShardAs() {
+        c.rank = r0;
+        c.world = w0;
+    }
+};
+
+std::vector<oserve_gpu_ctx *> local_shards(oserve_gpu_ctx &c) {
+    std::vector<oserve_gpu_ctx *> v{&c};
+    v.insert(v.end(), c.subs.begin(), c.subs.end());
+    return v;
+}
+
+// Bring a sub-context's workload, shape registry and space up to the lead's.
+void mirror(oserve_gpu_ctx &lead, oserve_gpu_ctx &s) {
+    DeviceScope ds(s.device);
+    s.opts = lead.opts;
+    s.chunk = lead.chunk;
+    if (s.synced_work != lead.work_ver) {
+        s.J = lead.J;
+        s.cin = lead.cin;
+        s.cout = lead.cout;
+        s.lambda = lead.lambda;
+        s.span = lead.span;
+        s.have_workload = lead.have_workload;
+        s.shapes = lead.shapes;
+        s.shape_id = lead.shape_id;
+        s.tables_dirty = true;
+        s.synced_work = lead.work_ver;
+    }
+    if (lead.space.valid && s.synced_space != lead.space_ver) {
+        s.space.valid = false;
+        copy_space_host(lead.space, s.space);
+        upload_space(s, s.space);
+        s.synced_space = lead.space_ver;
+    }
+}
+
+uint64_t shard_min_plans() {
+    static const uint64_t v = [] {
+        const char *e = getenv("OSERVE_SHARD_MIN");
+        return e ? static_cast<uint64_t>(atoll(e)) : (uint64_t{1} << 16);
+    }();
+    return v;
+}
+
+// Shard the prepared space over the world?  Exact-path (branch-and-bound)
+// spaces and small spaces run whole on the lead device of every rank.
+bool shard_round(oserve_gpu_ctx &c) {
+    if (c.g_world <= 1 || c.comms.empty()) return false;
+    refresh_exact(c, c.space);
+    return !c.space.any_exact && c.space.total >= shard_min_plans();
+}
+
+// K1 over every local shard + all-reduce(MIN) of the key; the global best
+// key lands in d_key (lead device) on the lead's stream.  Asynchronous.
+void sharded_launch_round(oserve_gpu_ctx &c, uint64_t *d_key) {
+    auto sh = local_shards(c);
+    std::vector<uint64_t *> keys(sh.size());
+    for (size_t i = 0; i < sh.size(); ++i) {
+        oserve_gpu_ctx &s = *sh[i];
+        if (i) mirror(c, s);
+        DeviceScope ds(s.device);
+        ShardAs as(s, c.g_rank0 + static_cast<int>(i), c.g_world);
+        keys[i] = i ? static_cast<uint64_t *>(s.d_mkey.get(sizeof(uint64_t))) : d_key;
+        launch_round(s, keys[i]);
+    }
+    const Nccl &n = nccl_or_fail();
+    nccl_ok(n.GroupStart(), "ncclGroupStart");
+    for (size_t i = 0; i < sh.size(); ++i)
+        nccl_ok(n.AllReduce(keys[i], keys[i], 1, ncclUint64, ncclMin, c.comms[i], sh[i]->stream), "ncclAllReduce");
+    nccl_ok(n.GroupEnd(), "ncclGroupEnd");
+}
+
+// The round's key: sharded over the world when it pays, else this context's
+// own shard (set_shard) — or the whole space when it has a communicator.
+void round_key(oserve_gpu_ctx &c, uint64_t *d_key) {
+    if (shard_round(c)) {
+        sharded_launch_round(c, d_key);
+    } else if (!c.comms.empty()) {
+        ShardAs as(c, 0, 1);
+        launch_round(c, d_key);
+    } else {
+        launch_round(c, d_key);
+    }
+}
+
+// Top-K over every local shard (a host thread per device), all-gather of the
+// per-shard lists, merge on the lead: sort world*K keys, keep the K smallest.
+void sharded_topk(oserve_gpu_ctx &c, int K, uint64_t *d_keys, uint64_t *d_best) {
+    auto sh = local_shards(c);
+    for (size_t i = 1; i < sh.size(); ++i) mirror(c, *sh[i]);
+    const size_t W = static_cast<size_t>(c.g_world);
+    std::vector<uint64_t *> lk(sh.size()), all(sh.size());
+    for (size_t i = 0; i < sh.size(); ++i) {
+        DeviceScope ds(sh[i]->device);
+        lk[i] = static_cast<uint64_t *>(sh[i]->d_mtopk.get(sizeof(uint64_t) * K));
+        all[i] = static_cast<uint64_t *>(sh[i]->d_mall.get(sizeof(uint64_t) * K * W));
+    }
+    std::vector<std::exception_ptr> errs(sh.size());
+    std::vector<uint64_t> h2d(sh.size(), 0), d2h(sh.size(), 0);
+    auto work = [&](size_t i) {
+        try {
+            t_h2d = &h2d[i];
+            t_d2h = &d2h[i];
+            cuda_ok(cudaSetDevice(sh[i]->device), "cudaSetDevice");
+            ShardAs as(*sh[i], c.g_rank0 + static_cast<int>(i), c.g_world);
+            round_topk(*sh[i], K, lk[i], nullptr);
+        } catch (...) {
+            errs[i] = std::current_exception();
+        }
+    };
+    {
+        uint64_t *ch = t_h2d, *cd = t_d2h;
+        std::vector<std::thread> th;
+        for (size_t i = 1; i < sh.size(); ++i) th.emplace_back(work, i);
+        work(0);
+        for (auto &t : th) t.join();
+        t_h2d = ch;
+        t_d2h = cd;
+        for (size_t i = 0; i < sh.size(); ++i) {
+            count_h2d(h2d[i]);
+            count_d2h(d2h[i]);
+        }
+        cuda_ok(cudaSetDevice(c.device), "cudaSetDevice");
+    }
+    for (auto &e : errs)
+        if (e) std::rethrow_exception(e);
+    const Nccl &n = nccl_or_fail();
+    nccl_ok(n.GroupStart(), "ncclGroupStart");
+    for (size_t i = 0; i < sh.size(); ++i)
+        nccl_ok(n.AllGather(lk[i], all[i], static_cast<size_t>(K), ncclUint64, c.comms[i], sh[i]->stream),
+                "ncclAllGather");
+    nccl_ok(n.GroupEnd(), "ncclGroupEnd");
+    cudaStream_t s = c.stream;
+    uint64_t *tmp = static_cast<uint64_t *>(c.d_mtmp.get(sizeof(uint64_t) * K * W));
+    cuda_ok(sort_keys(all[0], tmp, static_cast<int>(K * W), &c.cub_temp, &c.cub_temp_bytes, s), "sort");
+    ++c.launches;
+    cuda_ok(cudaMemcpyAsync(d_keys, tmp, sizeof(uint64_t) * K, cudaMemcpyDeviceToDevice, s), "D2D");
+    if (d_best) cuda_ok(cudaMemcpyAsync(d_best, tmp, sizeof(uint64_t), cudaMemcpyDeviceToDevice, s), "D2D");
+    cuda_ok(cudaStreamSynchronize(s), "sync");
+}
+
+void topk_any(oserve_gpu_ctx &c, int K, uint64_t *d_keys, uint64_t *d_best) {
+    if (K < 1 || K > 65536) fail(OSERVE_ERR_INVALID_ARGUMENT, "K must be in [1, 65536]");
+    if (shard_round(c)) {
+        sharded_topk(c, K, d_keys, d_best);
+    } else if (!c.comms.empty()) {
+        ShardAs as(c, 0, 1);
+        round_topk(c, K, d_keys, d_best);
+    } else {
+        round_topk(c, K, d_keys, d_best);
+    }
+}
+
 }  // namespace
 
 // ====================================================================== ABI
@@ -1341,6 +1639,7 @@ const char *oserve_gpu_status_name(int status) {
         case OSERVE_ERR_UNSUPPORTED: return "UNSUPPORTED";
         case OSERVE_ERR_CUDA: return "CUDA";
         case OSERVE_ERR_NO_DEVICE: return "NO_DEVICE";
+        case OSERVE_ERR_NCCL: return "NCCL";
         default: return "UNKNOWN";
     }
 }
@@ -1375,20 +1674,83 @@ int oserve_gpu_create(int cuda_device, const oserve_cluster_desc *cluster, const
         cudaDeviceProp prop{};
         cuda_ok(cudaGetDeviceProperties(&prop, cuda_device), "props");
         c->sm_count = prop.multiProcessorCount;
+        constexpr int kRingSlots = 64;  // one 128-byte line per K1 launch, round robin
+        c->ring.base = static_cast<unsigned long long *>(c->d_ring.get(128 * kRingSlots));
+        c->ring.slots = kRingSlots;
     });
     if (rc != OSERVE_OK) return rc;
     *out = c.release();
     return OSERVE_OK;
 }
 
-int oserve_gpu_destroy(oserve_gpu_ctx *ctx) {
-    if (!ctx) return OSERVE_OK;
-    cudaSetDevice(ctx->device);
-    if (ctx->own) {
-        cudaStreamSynchronize(ctx->own);
-        cudaStreamDestroy(ctx->own);
+int oserve_gpu_create_multi(const int *cuda_devices, int ndev, const oserve_cluster_desc *cluster,
+                            const oserve_model_desc *model, const oserve_profile *profile, oserve_gpu_ctx **out) {
+    if (!out || !cuda_devices || ndev < 1) return OSERVE_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    for (int i = 0; i < ndev; ++i)
+        for (int j = 0; j < i; ++j)
+            if (cuda_devices[i] == cuda_devices[j]) return OSERVE_ERR_INVALID_ARGUMENT;
+    oserve_gpu_ctx *lead = nullptr;
+    int rc = oserve_gpu_create(cuda_devices[0], cluster, model, profile, &lead);
+    if (rc != OSERVE_OK) return rc;
+    std::unique_ptr<oserve_gpu_ctx> own(lead);
+    for (int i = 1; i < ndev; ++i) {
+        oserve_gpu_ctx *s = nullptr;
+        rc = oserve_gpu_create(cuda_devices[i], cluster, model, profile, &s);
+        if (rc != OSERVE_OK) return rc;
+        lead->subs.push_back(s);
     }
-    if (ctx->cub_temp) cudaFree(ctx->cub_temp);
+    if (ndev > 1) {
+        rc = guarded(lead, [&] {
+            const Nccl &n = nccl_or_fail();
+            std::vector<ncclComm_t> comms(ndev, nullptr);
+            nccl_ok(n.CommInitAll(comms.data(), ndev, cuda_devices), "ncclCommInitAll");
+            lead->comms = comms;
+            lead->g_rank0 = 0;
+            lead->g_world = ndev;
+        });
+        if (rc != OSERVE_OK) return rc;
+    }
+    *out = own.release();
+    return OSERVE_OK;
+}
+
+int oserve_nccl_unique_id(void *id) {
+    if (!id) return OSERVE_ERR_INVALID_ARGUMENT;
+    const Nccl &n = nccl();
+    if (!n.ok()) return OSERVE_ERR_NCCL;
+    ncclUniqueId u;
+    if (n.GetUniqueId(&u) != ncclSuccess) return OSERVE_ERR_NCCL;
+    std::memcpy(id, &u, sizeof(u));
+    return OSERVE_OK;
+}
+
+int oserve_gpu_join(oserve_gpu_ctx *ctx, const void *id, int rank, int world) {
+    return guarded(ctx, [&] {
+        if (!id || world < 1 || rank < 0 || rank >= world) fail(OSERVE_ERR_INVALID_ARGUMENT, "bad rank/world");
+        if (!ctx->subs.empty() || !ctx->comms.empty())
+            fail(OSERVE_ERR_INVALID_ARGUMENT, "context already has a communicator");
+        if (world == 1) return;
+        const Nccl &n = nccl_or_fail();
+        ncclUniqueId u;
+        std::memcpy(&u, id, sizeof(u));
+        ncclComm_t cm = nullptr;
+        nccl_ok(n.CommInitRank(&cm, world, u, rank), "ncclCommInitRank");
+        ctx->comms = {cm};
+        ctx->g_rank0 = rank;
+        ctx->g_world = world;
+    });
+}
+
+int oserve_gpu_world(const oserve_gpu_ctx *ctx, int *rank, int *world, int *local_devices) {
+    if (!ctx) return OSERVE_ERR_INVALID_ARGUMENT;
+    if (rank) *rank = ctx->g_rank0;
+    if (world) *world = ctx->g_world;
+    if (local_devices) *local_devices = 1 + static_cast<int>(ctx->subs.size());
+    return OSERVE_OK;
+}
+
+int oserve_gpu_destroy(oserve_gpu_ctx *ctx) {
     delete ctx;
     return OSERVE_OK;
 }
@@ -1444,6 +1806,7 @@ int oserve_gpu_set_workload(oserve_gpu_ctx *ctx, int num_classes, const oserve_c
             co[j] = classes[j].centroid_out;
         }
         ctx->tables_dirty = true;  // every round re-runs the cost kernel (K0) on its workload
+        ++ctx->work_ver;
         ctx->J = num_classes;
         ctx->cin = ci;
         ctx->cout = co;
@@ -1491,7 +1854,7 @@ int oserve_gpu_prepare_space(oserve_gpu_ctx *ctx, const oserve_space_desc *space
 int oserve_gpu_launch_round_async(oserve_gpu_ctx *ctx, uint64_t *d_key) {
     return guarded(ctx, [&] {
         if (!ctx->space.valid) fail(OSERVE_ERR_INVALID_ARGUMENT, "no prepared space");
-        launch_round(*ctx, d_key);
+        round_key(*ctx, d_key);
     });
 }
 
@@ -1506,19 +1869,20 @@ int oserve_gpu_round(oserve_gpu_ctx *ctx, const oserve_space_desc *space, oserve
     return guarded(ctx, [&] {
         prepare(*ctx, *space);
         uint64_t *dk = static_cast<uint64_t *>(ctx->d_key.get(sizeof(uint64_t)));
-        launch_round(*ctx, dk);
+        round_key(*ctx, dk);
         uint64_t key = kNoKey;
         cuda_ok(d2h(&key, dk, sizeof(key), ctx->stream), "D2H");
         cuda_ok(cudaStreamSynchronize(ctx->stream), "sync");
         decode_key(*ctx, key, out);
-        if (key == kNoKey && ctx->world == 1) fail(OSERVE_ERR_MODEL_TOO_LARGE, "round: no feasible deployment");
+        if (key == kNoKey && (ctx->world == 1 || !ctx->comms.empty()))
+            fail(OSERVE_ERR_MODEL_TOO_LARGE, "round: no feasible deployment");
     });
 }
 
 int oserve_gpu_round_topk(oserve_gpu_ctx *ctx, int K, uint64_t *d_keys, uint64_t *d_best) {
     return guarded(ctx, [&] {
         if (!ctx->space.valid) fail(OSERVE_ERR_INVALID_ARGUMENT, "no prepared space");
-        round_topk(*ctx, K, d_keys, d_best);
+        topk_any(*ctx, K, d_keys, d_best);
     });
 }
 
@@ -1728,7 +2092,7 @@ int oserve_gpu_best_strategies(oserve_gpu_ctx *ctx, int num_replicas, const int 
         out->partitions = 1;
         if (sp.total == 0) return;  // a block without candidates: empty choice, objective 0
         uint64_t *dk = static_cast<uint64_t *>(ctx->d_key.get(sizeof(uint64_t)));
-        launch_round(*ctx, dk);
+        round_key(*ctx, dk);
         uint64_t key = kNoKey;
         cuda_ok(d2h(&key, dk, sizeof(key), ctx->stream), "D2H");
         cuda_ok(cudaStreamSynchronize(ctx->stream), "sync");
@@ -1986,7 +2350,7 @@ int oserve_gpu_evaluate_ranks(oserve_gpu_ctx *ctx, uint64_t first, uint64_t coun
         out.sum_pp = static_cast<int32_t *>(ctx->d_spp.get(sizeof(int32_t) * count));
         SolveParams prm = solve_params(*ctx);
         KeyLayout nk{};
-        cuda_ok(launch_plan_eval(ctx->tables, sp.view, nk, src, out, prm, sp.rmax, ctx->sm_count, sp.any_exact, s,
+        cuda_ok(launch_plan_eval(ctx->tables, sp.view, nk, src, out, prm, sp.rmax, ctx->sm_count, sp.any_exact, &ctx->ring, s,
                                  &ctx->launches),
                 "plan kernel");
         if (sp.any_exact) {
@@ -2011,7 +2375,7 @@ int oserve_gpu_evaluate_ranks(oserve_gpu_ctx *ctx, uint64_t first, uint64_t coun
                     PlanOutputs o1 = out;
                     o1.objective = out.objective + (g - first);
                     o1.sum_pp = out.sum_pp + (g - first);
-                    cuda_ok(launch_plan_eval(ctx->tables, sp.view, nk, one, o1, prm, sp.rmax, ctx->sm_count, 0, s,
+                    cuda_ok(launch_plan_eval(ctx->tables, sp.view, nk, one, o1, prm, sp.rmax, ctx->sm_count, 0, &ctx->ring, s,
                                              &ctx->launches),
                             "plan kernel (budget fallback)");
                 }

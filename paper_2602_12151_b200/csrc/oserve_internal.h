@@ -158,6 +158,14 @@ struct SolveParams {
     int64_t node_budget;
 };
 
+// K1 dynamic-chunk counters: `slots` 128-byte lines of device memory owned by
+// one context (one line per launch, round robin, zeroed on the launch stream).
+struct WorkRing {
+    unsigned long long *base;
+    int slots;
+    unsigned next;
+};
+
 // ---- launchers (oserve_kernels.cu) -----------------------------------------
 int launch_cost_tables(const ShapeTables &t, const double *cin, const double *cout, uint32_t num_layers,
                        uint64_t bytes_per_token_kv, double prefill_coeff, double decode_coeff,
@@ -166,7 +174,7 @@ int launch_normalize_rows(const ShapeTables &t, void *stream);
 // Greedy + exchange (heuristic path) over a plan source; returns CUDA status.
 int launch_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key, const PlanSource &src,
                      const PlanOutputs &out, const SolveParams &sp_params, int rmax, int sm_count,
-                     int skip_exact, void *stream, uint64_t *launches);
+                     int skip_exact, WorkRing *ring, void *stream, uint64_t *launches);
 // Exact branch-and-bound path (thread per plan).
 int launch_plan_exact(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key, const PlanSource &src,
                       const PlanOutputs &out, const SolveParams &sp_params, int sm_count, void *stream,

@@ -1297,21 +1297,13 @@ int plan_eval_geometry(const ShapeTables &t, int J, int sm_count, uint64_t count
     return 0;
 }
 
-// K1's dynamic chunk counter: a ring of zeroed counters per device, one per
-// launch (memset on the launch stream), so launches in flight on other
-// streams never share one.
-unsigned long long *work_counter(cudaStream_t stream) {
-    constexpr int kRing = 256, kDev = 64;
-    static unsigned long long *ring[kDev] = {};
-    static std::atomic<unsigned> next[kDev];
-    static std::mutex mu;
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kDev) return nullptr;
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        if (!ring[dev] && cudaMalloc(&ring[dev], kRing * 128) != cudaSuccess) return nullptr;
-    }
-    unsigned long long *c = ring[dev] + (next[dev].fetch_add(1) % kRing) * 16;  // one 128-byte line each
+// K1's dynamic chunk counter: one zeroed 128-byte line per launch, taken
+// from the calling context's ring (WorkRing, owned per context and device;
+// memset on the launch stream, so launches in flight on other streams or
+// from other contexts never share one).
+unsigned long long *work_counter(WorkRing *ring, cudaStream_t stream) {
+    if (!ring || !ring->base || ring->slots <= 0) return nullptr;
+    unsigned long long *c = ring->base + (ring->next++ % static_cast<unsigned>(ring->slots)) * 16;
     if (cudaMemsetAsync(c, 0, sizeof(unsigned long long), stream) != cudaSuccess) return nullptr;
     return c;
 }
@@ -1319,7 +1311,7 @@ unsigned long long *work_counter(cudaStream_t stream) {
 template <int G, int KPL>
 int run_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key, const PlanSource &src,
                   const PlanOutputs &out, const SolveParams &prm, int sm_count, int skip_exact,
-                  cudaStream_t stream, uint64_t *launches) {
+                  WorkRing *ring, cudaStream_t stream, uint64_t *launches) {
     cudaGetLastError();  // clear any stale (non-sticky) error before launching
     size_t smem = 0;
     bool stage = false;
@@ -1332,7 +1324,7 @@ int run_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &
     const uint64_t groups = grid * GPB;
     uint64_t gch = src.count / (groups ? groups * 4 : 1);
     gch = gch < 1 ? 1 : (gch > kGroupChunk ? kGroupChunk : gch);
-    unsigned long long *work = work_counter(stream);
+    unsigned long long *work = work_counter(ring, stream);
     if (!work) return static_cast<int>(cudaErrorMemoryAllocation);
     kern<<<static_cast<unsigned>(grid), 256, smem, stream>>>(t, sp, key, src, out, prm, skip_exact,
                                                                static_cast<int>(gch), work);
@@ -2500,24 +2492,37 @@ __global__ void k_topk_check(const uint64_t *meta, int groups, const uint64_t *k
 }  // namespace
 
 // ------------------------------------------------------------- launchers ---
-static bool g_binom_ready = false;
-
+// c_binom is a __constant__ symbol: one copy per device (per loaded module),
+// so readiness is tracked per device, under a lock (contexts on several
+// devices may be driven from several host threads).
 static int ensure_binom() {
-    if (g_binom_ready) return 0;
-    static uint64_t h[kBinomN][kBinomK];
-    for (int n = 0; n < kBinomN; ++n)
-        for (int k = 0; k < kBinomK; ++k) {
-            unsigned __int128 r = 1;
-            if (k > n) {
-                r = 0;
-            } else {
-                for (int i = 1; i <= k; ++i) r = r * static_cast<unsigned>(n - k + i) / static_cast<unsigned>(i);
-            }
-            h[n][k] = r > ~0ull ? ~0ull : static_cast<uint64_t>(r);
-        }
-    cudaError_t e = cudaMemcpyToSymbol(c_binom, h, sizeof(h));
+    constexpr int kDevMax = 64;
+    static std::mutex mu;
+    static bool ready[kDevMax] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return static_cast<int>(e);
-    g_binom_ready = true;
+    if (dev < 0 || dev >= kDevMax) return static_cast<int>(cudaErrorInvalidDevice);
+    std::lock_guard<std::mutex> lk(mu);
+    if (ready[dev]) return 0;
+    static uint64_t h[kBinomN][kBinomK];
+    static bool filled = false;
+    if (!filled) {
+        for (int n = 0; n < kBinomN; ++n)
+            for (int k = 0; k < kBinomK; ++k) {
+                unsigned __int128 r = 1;
+                if (k > n) {
+                    r = 0;
+                } else {
+                    for (int i = 1; i <= k; ++i) r = r * static_cast<unsigned>(n - k + i) / static_cast<unsigned>(i);
+                }
+                h[n][k] = r > ~0ull ? ~0ull : static_cast<uint64_t>(r);
+            }
+        filled = true;
+    }
+    e = cudaMemcpyToSymbol(c_binom, h, sizeof(h));  // synchronous: visible to every later launch
+    if (e != cudaSuccess) return static_cast<int>(e);
+    ready[dev] = true;
     return 0;
 }
 
@@ -2542,7 +2547,7 @@ int launch_normalize_rows(const ShapeTables &t, void *stream) {
 
 int launch_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key, const PlanSource &src,
                      const PlanOutputs &out, const SolveParams &prm, int rmax, int sm_count, int skip_exact,
-                     void *stream, uint64_t *launches) {
+                     WorkRing *ring, void *stream, uint64_t *launches) {
     if (int e = ensure_binom()) return e;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (src.count == 0) return 0;
@@ -2555,15 +2560,15 @@ int launch_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayou
         const char *e = getenv("OSERVE_K1_G");
         return e && atoi(e) == 16;
     }();
-    if (need <= 8) return run_plan_eval<8, 1>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
-    if (need <= 16) return run_plan_eval<16, 1>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
+    if (need <= 8) return run_plan_eval<8, 1>(t, sp, key, src, out, prm, sm_count, skip_exact, ring, s, launches);
+    if (need <= 16) return run_plan_eval<16, 1>(t, sp, key, src, out, prm, sm_count, skip_exact, ring, s, launches);
     if (prm.J <= 16 && opt16) {
-        if (rmax <= 32) return run_plan_eval<16, 2>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
-        if (rmax <= 64) return run_plan_eval<16, 4>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
+        if (rmax <= 32) return run_plan_eval<16, 2>(t, sp, key, src, out, prm, sm_count, skip_exact, ring, s, launches);
+        if (rmax <= 64) return run_plan_eval<16, 4>(t, sp, key, src, out, prm, sm_count, skip_exact, ring, s, launches);
     }
-    if (rmax <= 32) return run_plan_eval<32, 1>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
-    if (rmax <= 64) return run_plan_eval<32, 2>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
-    if (rmax <= 128) return run_plan_eval<32, 4>(t, sp, key, src, out, prm, sm_count, skip_exact, s, launches);
+    if (rmax <= 32) return run_plan_eval<32, 1>(t, sp, key, src, out, prm, sm_count, skip_exact, ring, s, launches);
+    if (rmax <= 64) return run_plan_eval<32, 2>(t, sp, key, src, out, prm, sm_count, skip_exact, ring, s, launches);
+    if (rmax <= 128) return run_plan_eval<32, 4>(t, sp, key, src, out, prm, sm_count, skip_exact, ring, s, launches);
     return static_cast<int>(cudaErrorInvalidValue);
 }
 

@@ -17,7 +17,7 @@ HEADER = os.path.join(ROOT, "include", "oserve_gpu.h")
 
 def declared_symbols():
     src = open(HEADER).read()
-    return sorted(set(re.findall(r"\b(oserve_(?:gpu|shard|key|forecast)\w*)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(oserve_(?:gpu|shard|key|forecast|nccl)\w*)\s*\(", src)))
 
 
 def test_library_exports_every_declared_symbol():
