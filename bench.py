@@ -10,16 +10,17 @@ on config 5 (128-GPU cluster, 16 request classes, canonical plan space of
 One step = one full scheduling round over the whole plan space:
   value : device-resident inputs; K1 (enumerate/unrank -> cost gather -> assign
           -> objective -> argmin) on every rank's shard, NCCL all-reduce(min) of
-          the packed key, K2 switching cost current -> winner (decoded on the
-          device) — no host round-trip; CUDA events on the launching stream, max
-          over ranks; L2 flushed (256 MiB write) between timed iterations.
+          the packed key (issued by liboserve_gpu on the round's stream), K2
+          switching cost current -> winner (decoded on the device) — no host
+          round-trip; CUDA events on the launching stream, max over ranks; L2
+          flushed (256 MiB write) between timed iterations.
   e2e   : the public C-ABI from host buffers every step — enumerate + upload the
           space tables, upload the workload, K0 cost kernel, K1 with the exact
-          top-K (default 1024) of the packed key, all-gather + merge across
-          ranks, K2 switching batch current -> each of the K best (pairs sharded
-          across ranks, costs all-gathered), key D2H,
-          decode, and the full greedy switch plan current -> winner (transfers
-          D2H).  "current" is init_uniform (deploysearch.cpp:120-136).
+          top-K (default 1024) of the packed key (at N > 1 the library
+          all-gathers and merges the per-rank lists), K2 switching batch
+          current -> each of the K best, key D2H, decode, and the full greedy
+          switch plan current -> winner (transfers D2H).  "current" is
+          init_uniform (deploysearch.cpp:120-136).
 The reference arm (--impl reference) times the reference's own CPU path
 (oracle/_ref: /root/reference/proj compiled unmodified; evaluate_deployment per
 plan, OpenMP over all host threads) on a bounded sample of the same space.
@@ -205,6 +206,118 @@ def run_reference(args, rank, world):
     emit(line)
 
 
+def reference_window_loop(orc, w, forecasts, min_gain, threads):
+    """The config-4 window loop on the reference CPU path (oracle/_ref): its
+    round over the full ordered space (best_strategies per partition), the
+    keep rule's evaluate_deployment, capacity table + solve_assignment and
+    layout + greedy_plan (orchestrate.cpp:109-150).  Returns per-window seconds."""
+    from pyoracle import Problem
+    from paper_2602_12151_b200 import orchestrate
+    secs, current, prev_lam = [], None, None
+    for lam in forecasts:
+        if secs and lam == prev_lam:
+            continue
+        t0 = time.perf_counter()
+        pr = Problem(w.cluster, w.model, w.types, lam, w.span_s, w.params)
+        found = orc.round(pr, w.space_mode, w.space_sizes, threads=threads)
+        chosen = found.deployment
+        if current is not None:
+            keep = orc.evaluate_deployment(pr, current)
+            if float(found.throughput) <= float(keep) * (1.0 + min_gain):
+                chosen = current
+        t = orc.capacity_table(pr, chosen)
+        orc.solve_assignment(t.n, t.e, lam)
+        if current is not None and not orchestrate._same(chosen, current):
+            orc.switch_plan(w.cluster, w.model.param_bytes, current, chosen)
+        secs.append(time.perf_counter() - t0)
+        current, prev_lam = chosen, lam
+    return secs
+
+
+def run_temporal(args, rank, world, local):
+    """Config 4: 24 windows of re-scheduling.  One step = the whole timeline
+    (orchestrate.build_adaptive_timeline, round strategy): per window K0 + K1
+    over the full ordered space (933,333 plans) with the exact top-K (1,024)
+    of the packed key, the K2 switching batch current -> each candidate, the
+    keep rule, the chosen plan's assignment and the greedy switch plan — all
+    through the public API from host buffers (synchronous calls).
+    value: plans evaluated per second over the timeline, timed with CUDA
+    events on the context's stream; e2e: the same step by the host clock."""
+    if rank != 0:
+        return
+    from paper_2602_12151_b200 import orchestrate
+    from paper_2602_12151_b200._native import GpuContext
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    w = workloads.load(args.config)
+    fc, mg = w.raw["forecasts"], w.raw["min_gain"]
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    ctx = GpuContext(w.cluster, w.model, w.params, device=local)
+    ctx.set_stream(stream.cuda_stream)
+    parts, plans = ctx.prepare_space(w.space_mode, w.space_sizes)
+
+    def step():
+        return orchestrate.build_adaptive_timeline(ctx, w.types, fc, w.span_s, mg, w.space_mode, w.space_sizes,
+                                                   topk=args.topk)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    clocks = Clocks(local)
+    clocks.start()
+    launches0 = ctx.launch_count()
+    bytes0 = ctx.copy_bytes()
+    ev_ms, wall_ms, per_window = [], [], []
+    tl = None
+    for _ in range(args.steps):
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        a_.record(stream)
+        tl = step()
+        b_.record(stream)
+        b_.synchronize()
+        wall_ms.append(1e3 * (time.perf_counter() - t0))
+        ev_ms.append(a_.elapsed_time(b_))
+        per_window.append([1e3 * s_.seconds for s_ in tl.stats])
+    clk = clocks.stop()
+    launches = (ctx.launch_count() - launches0) // args.steps
+    bytes1 = ctx.copy_bytes()
+    rounds = tl.rounds
+    ms = statistics.mean(ev_ms)
+    value = rounds * plans / (ms / 1e3)
+    pw = [statistics.median(col) for col in zip(*per_window)]
+    cpu = None
+    if not args.no_cpu:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        from pyoracle import Oracle, available
+        threads = os.cpu_count() or 1
+        kind = "reference" if available("ref") else "port"
+        orc = Oracle("ref" if kind == "reference" else "port")
+        n_win = max(1, min(len(fc), int(args.cpu_seconds)))  # bounded: ~1 s per window on 16 threads
+        secs = reference_window_loop(orc, w, fc[:n_win], mg, threads)
+        cpu = {"value": len(secs) * plans / sum(secs), "unit": "plans/s", "cores": threads, "kind": kind,
+               "sample": f"first {len(secs)} of {rounds} windows of the timeline (reference round over the full "
+                         f"ordered space per window + keep rule + assignment + switch plan, {threads} threads)",
+               "window_ms": [round(1e3 * x_, 1) for x_ in secs],
+               "timeline_s_projected": sum(secs) / len(secs) * rounds}
+    line = {"metric": METRIC, "value": value, "unit": "plans/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": f"{w.name}: {w.description}", "windows": len(fc), "rounds_per_step": rounds,
+                       "plans_per_round": plans, "partitions": parts, "topk": args.topk,
+                       "step": "the whole 24-window timeline"},
+            "timeline_ms": ms, "window_ms_median": [round(x_, 3) for x_ in pw],
+            "e2e": {"value": rounds * plans / (statistics.mean(wall_ms) / 1e3), "unit": "plans/s",
+                    "timeline_ms": statistics.mean(wall_ms),
+                    "h2d_bytes_per_step": (bytes1[0] - bytes0[0]) // args.steps,
+                    "d2h_bytes_per_step": (bytes1[1] - bytes0[1]) // args.steps},
+            "timeline": [{"window": e.window, "deployment": label(e.deployment), "objective": e.objective,
+                          "switch_s": e.switch_seconds, "kept": e.kept} for e in tl.entries],
+            "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk}
+    emit(line)
+
+
 def run_ours(args, rank, world, local):
     from paper_2602_12151_b200._native import GpuContext
     dev = torch.device(f"cuda:{local}")
@@ -214,7 +327,15 @@ def run_ours(args, rank, world, local):
     torch.cuda.set_stream(stream)
     ctx = GpuContext(w.cluster, w.model, w.params, device=local)
     ctx.set_stream(stream.cuda_stream)
-    ctx.set_shard(rank, world)
+    if world > 1:
+        # the library owns the round's collective: rank 0 makes the NCCL id,
+        # every rank joins; rounds then shard over the world inside liboserve_gpu
+        from paper_2602_12151_b200._native import nccl_unique_id
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        ctx.join(bytes(uid.cpu().numpy().tobytes()), rank, world)
     ctx.set_workload(w.types, w.lam, w.span_s)
     parts, plans = ctx.prepare_space(w.space_mode, w.space_sizes)
     g_min = ctx.min_feasible_group()
@@ -232,10 +353,9 @@ def run_ours(args, rank, world, local):
 
     def device_step():
         # enumerate/unrank -> cost gather -> assign -> objective -> shard argmin (K1),
-        # global argmin (NCCL min), switching cost current -> winner (K2, key decoded on device)
+        # global argmin (NCCL all-reduce MIN issued by the library on the same
+        # stream), switching cost current -> winner (K2, key decoded on device)
         ctx.launch_round_async(d_key.data_ptr())
-        if world > 1:
-            dist.all_reduce(d_key, op=dist.ReduceOp.MIN)
         ctx.switch_cost_keys_async(current, d_key.data_ptr(), 1, d_est.data_ptr())
 
     # ---- value: device-resident round, per-step events, L2 flushed between ----
@@ -294,26 +414,10 @@ def run_ours(args, rank, world, local):
         t0 = time.perf_counter()
         ctx.prepare_space(w.space_mode, w.space_sizes)             # enumerate + H2D space tables
         ctx.set_workload(w.types, w.lam, w.span_s)                 # H2D workload; K0 cost kernel in the round
-        ctx.round_topk(K, d_topk.data_ptr())                       # K0 + K1 + top-K (exact) on this shard
-        if world > 1:                                              # global top-K: all-gather + merge
-            allk = torch.empty(world * K, dtype=torch.int64, device=dev)
-            dist.all_gather_into_tensor(allk, d_topk)
-            d_topk.copy_(torch.sort(allk).values[:K])
-        if world > 1:  # K2 batch sharded: each rank costs K/world of the pairs, then all-gather
-            per = (K + world - 1) // world
-            lo = min(K, rank * per)
-            n = min(K, lo + per) - lo
-            est_l, _ = ctx.switch_cost_keys(current, d_topk.data_ptr() + 8 * lo, n) if n > 0 else ([], [])
-            buf = torch.full((per,), float("nan"), dtype=torch.float64, device=dev)
-            if n:
-                buf[:n] = torch.tensor(est_l, dtype=torch.float64).to(dev, non_blocking=True)
-            alle = torch.empty(world * per, dtype=torch.float64, device=dev)
-            dist.all_gather_into_tensor(alle, buf)
-            sw_est = alle[:K].cpu().tolist()
-            extra_h2d, extra_d2h = 8 * n, 8 * K
-        else:
-            sw_est, _ = ctx.switch_cost_keys(current, d_topk.data_ptr(), K)  # K2 batch: current -> K best
-            extra_h2d = extra_d2h = 0
+        ctx.round_topk(K, d_topk.data_ptr())                       # K0 + K1 + exact top-K; at N > 1 the
+                                                                   # library all-gathers + merges the lists
+        sw_est, _ = ctx.switch_cost_keys(current, d_topk.data_ptr(), K)  # K2 batch: current -> K best
+        extra_h2d = extra_d2h = 0
         k = int(d_topk[0].item())                                  # D2H result key
         st = ctx.decode_key(k)
         plan = ctx.switch_plan(current, st.deployment)             # K2 detail + transfers D2H
@@ -356,7 +460,8 @@ def run_ours(args, rank, world, local):
         "config": {"workload": f"{w.name}: {w.description}", "devices": w.cluster.device_count(),
                    "classes": len(w.types), "plans_in_space": plans, "partitions": parts,
                    "space": ("canonical sizes " + str(w.space_sizes)) if w.space_mode else "ordered (reference)",
-                   "parallelism": f"plan space sharded x{world} (interleaved 4096-plan chunks) + NCCL min",
+                   "parallelism": f"plan space sharded x{world} (interleaved 4096-plan chunks); NCCL all-reduce "
+                                  f"MIN / all-gather top-K inside liboserve_gpu (oserve_gpu_join)",
                    "l2": "flushed between timed iterations (256 MiB write outside the events)"},
         "winner": {"objective": state.throughput, "key": key, "partition": state.partition_index,
                    "local_rank": state.local_rank, "deployment": label(state.deployment),
@@ -414,6 +519,8 @@ def main():
     try:
         if args.impl == "reference":
             run_reference(args, rank, world)
+        elif args.config == "cfg4":
+            run_temporal(args, rank, world, local)
         else:
             run_ours(args, rank, world, local)
     finally:

@@ -41,7 +41,8 @@ typedef enum {
     OSERVE_ERR_UNSUPPORTED = 8,        /* input outside the GPU path's limits     */
     OSERVE_ERR_CUDA = 9,
     OSERVE_ERR_NO_DEVICE = 10,
-    OSERVE_ERR_NCCL = 11               /* communicator / collective failure        */
+    OSERVE_ERR_NCCL = 11,              /* communicator / collective failure        */
+    OSERVE_ERR_LCM_OVERFLOW = 12       /* oserve::LcmOverflow        errors.hpp:39 */
 } oserve_status;
 
 /* ---- L0 types (proj/include/oserve/core.hpp:11-95) -------------------- */
@@ -314,6 +315,65 @@ int oserve_gpu_switch_cost_batch(oserve_gpu_ctx *ctx, const oserve_deployment *s
 int oserve_gpu_switch_plan(oserve_gpu_ctx *ctx, const oserve_deployment *src,
                            const oserve_deployment *dst, int capacity, oserve_transfer *transfers,
                            int *num_transfers, double *est_seconds);
+
+/* ---- reference-signature pieces of switching (switchplan.hpp:34, 57, 61) -- */
+
+/* switchplan::ShardLayout::Shard (switchplan.hpp:24-28). */
+typedef struct {
+    int shard_id;
+    uint64_t begin;
+    uint64_t end;
+    int holder;
+} oserve_shard;
+
+/* One entry of ShardLayout::held (device -> sorted ranges), map order. */
+typedef struct {
+    int device;
+    uint64_t begin;
+    uint64_t end;
+} oserve_held_range;
+
+/* One entry of SwitchPlan::link_load (switchplan.hpp:44). */
+typedef struct {
+    int src;
+    int dst;
+    uint64_t bytes;
+} oserve_link_load;
+
+/* Drop-in for switchplan::layout (switchplan.cpp:40-63): the shards of one
+ * deployment for a model of param_bytes (replica-major, stage, slice), one
+ * device thread per shard.  *n_shards = sum tp*pp; OSERVE_ERR_INVALID_ARGUMENT
+ * (count set) when capacity is smaller.  The caller coalesces `held`. */
+int oserve_gpu_layout(oserve_gpu_ctx *ctx, const oserve_deployment *dep, uint64_t param_bytes, int capacity,
+                      oserve_shard *shards, int *n_shards);
+/* Drop-in for switchplan::greedy_plan(const ShardLayout&, const ShardLayout&,
+ * const ClusterSpec&) (switchplan.cpp:65-131) over arbitrary layouts given
+ * as their `held` maps (device ascending, ranges sorted): fragments sorted on
+ * the device, warp per target device, lane per source device.  Transfers in
+ * the reference's order; est_seconds = estimate_time of the plan.  A needed
+ * fragment without holder: OSERVE_ERR_UNSOURCED_FRAGMENT. */
+int oserve_gpu_greedy_plan_layouts(oserve_gpu_ctx *ctx, int n_src, const oserve_held_range *src, int n_dst,
+                                   const oserve_held_range *dst, int capacity, oserve_transfer *transfers,
+                                   int *n_transfers, double *est_seconds);
+/* Drop-in for switchplan::estimate_time (switchplan.cpp:133-140): the
+ * slowest link's bytes / bandwidth over the cluster's link classes. */
+int oserve_gpu_estimate_time(oserve_gpu_ctx *ctx, int n_links, const oserve_link_load *links, double *est_seconds);
+
+/* ---- reference-signature pieces of the assignment (flowassign.hpp:24-28, 122) */
+
+/* flow::normalize (strict != 0; OSERVE_ERR_LCM_OVERFLOW when the LCM exceeds
+ * 2^62) or flow::normalize_or_scale (strict == 0) of `count` rows of J
+ * capacities (flowassign.cpp:22-62), on the device (K0b).  M [count],
+ * units [count][J], scaled [count] (may be NULL). */
+int oserve_gpu_normalize_batch(oserve_gpu_ctx *ctx, int count, int J, const int64_t *n, int strict, int64_t *M,
+                               int64_t *units, int *scaled);
+/* flow::check_constraints (flowassign.cpp:529-551) on `count` instances
+ * [count][R][J]: OSERVE_ERR_LOGIC with the reference's message for the first
+ * violating instance.  Optional per-instance outputs (may be NULL): kind
+ * (0 ok, 1 C1, 2 C2, 3 C3 zero-capacity type, 4 C3 budget), replica, type. */
+int oserve_gpu_check_constraints_batch(oserve_gpu_ctx *ctx, int count, int R, int J, const int64_t *x,
+                                       const int64_t *n, const int64_t *e, const int64_t *lambda, int *kind,
+                                       int *replica, int *type);
 
 /* ---- device-free helpers (host protocol of the multi-GPU round) ------- */
 

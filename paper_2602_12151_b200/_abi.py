@@ -26,6 +26,7 @@ ERR_UNSUPPORTED = 8
 ERR_CUDA = 9
 ERR_NO_DEVICE = 10
 ERR_NCCL = 11
+ERR_LCM_OVERFLOW = 12
 
 SPACE_ORDERED = 0
 SPACE_CANONICAL = 1
@@ -83,6 +84,18 @@ class RoundResult(C.Structure):
 
 class TransferDesc(C.Structure):
     _fields_ = [("begin", C.c_uint64), ("end", C.c_uint64), ("src", C.c_int), ("dst", C.c_int)]
+
+
+class ShardDesc(C.Structure):  # oserve_shard (switchplan::ShardLayout::Shard)
+    _fields_ = [("shard_id", C.c_int), ("begin", C.c_uint64), ("end", C.c_uint64), ("holder", C.c_int)]
+
+
+class HeldRangeDesc(C.Structure):  # oserve_held_range (one ShardLayout::held entry)
+    _fields_ = [("device", C.c_int), ("begin", C.c_uint64), ("end", C.c_uint64)]
+
+
+class LinkLoadDesc(C.Structure):  # oserve_link_load (SwitchPlan::link_load entry)
+    _fields_ = [("src", C.c_int), ("dst", C.c_int), ("bytes", C.c_uint64)]
 
 
 class FlowEdgeDesc(C.Structure):
@@ -277,6 +290,7 @@ _EXC = {
     ERR_CUDA: core.CudaError,
     ERR_NO_DEVICE: core.CudaError,
     ERR_NCCL: core.CudaError,
+    ERR_LCM_OVERFLOW: core.LcmOverflow,
 }
 
 

@@ -32,6 +32,8 @@ EXPORTS = [
     "oserve_gpu_max_flow_batch", "oserve_gpu_flow_assign_batch", "oserve_gpu_extract_assignment_batch",
     "oserve_gpu_solve_fractional_batch",
     "oserve_gpu_create_multi", "oserve_nccl_unique_id", "oserve_gpu_join", "oserve_gpu_world",
+    "oserve_gpu_layout", "oserve_gpu_greedy_plan_layouts", "oserve_gpu_estimate_time",
+    "oserve_gpu_normalize_batch", "oserve_gpu_check_constraints_batch",
 ]
 
 _lib = None
@@ -53,6 +55,14 @@ def load_library() -> C.CDLL:
     L.oserve_nccl_unique_id.argtypes = [vp]
     L.oserve_gpu_join.argtypes = [vp, vp, C.c_int, C.c_int]
     L.oserve_gpu_world.argtypes = [vp, P(C.c_int), P(C.c_int), P(C.c_int)]
+    L.oserve_gpu_layout.argtypes = [vp, P(A.DeploymentDesc), C.c_uint64, C.c_int, P(A.ShardDesc), P(C.c_int)]
+    L.oserve_gpu_greedy_plan_layouts.argtypes = [vp, C.c_int, P(A.HeldRangeDesc), C.c_int, P(A.HeldRangeDesc),
+                                                 C.c_int, P(A.TransferDesc), P(C.c_int), P(C.c_double)]
+    L.oserve_gpu_estimate_time.argtypes = [vp, C.c_int, P(A.LinkLoadDesc), P(C.c_double)]
+    L.oserve_gpu_normalize_batch.argtypes = [vp, C.c_int, C.c_int, P(C.c_int64), C.c_int, P(C.c_int64),
+                                             P(C.c_int64), P(C.c_int)]
+    L.oserve_gpu_check_constraints_batch.argtypes = [vp, C.c_int, C.c_int, C.c_int] + [P(C.c_int64)] * 4 + \
+        [P(C.c_int)] * 3
     L.oserve_gpu_last_error.argtypes = [vp]
     L.oserve_gpu_last_error.restype = C.c_char_p
     L.oserve_gpu_status_name.restype = C.c_char_p
@@ -175,6 +185,7 @@ class GpuContext:
         md = A.model_desc(model)
         pd = A.profile_desc(self.params)
         h = C.c_void_p()
+        self.device = int(devices[0]) if devices else int(device)
         if devices is not None and len(devices) > 1:
             devs = A._arr(C.c_int, list(devices))
             st = self.lib.oserve_gpu_create_multi(devs, len(devices), C.byref(cd), C.byref(md), C.byref(pd),
@@ -461,6 +472,75 @@ class GpuContext:
         return core.KvPlan(list(drained[:nd.value]),
                            [core.KvTransfer(m.request_id, m.kv_bytes, m.src, m.dst) for m in mig[:nm.value]],
                            buf.value)
+
+    # -- reference-signature pieces (switchplan.hpp:34, 57, 61; flowassign.hpp:24-28, 122)
+    def layout_shards(self, dep: core.Deployment, param_bytes: int):
+        """switchplan::layout shards [(shard_id, begin, end, holder)] (K: k_layout)."""
+        keep = A.Keep()
+        d = A.deployment_desc(dep, keep)
+        n = C.c_int()
+        self._chk(self.lib.oserve_gpu_layout(self.h, C.byref(d), int(param_bytes), 0, None, C.byref(n)))
+        buf = (A.ShardDesc * max(1, n.value))()
+        if n.value:
+            self._chk(self.lib.oserve_gpu_layout(self.h, C.byref(d), int(param_bytes), n.value, buf, C.byref(n)))
+        return [(b.shard_id, b.begin, b.end, b.holder) for b in buf[:n.value]]
+
+    def greedy_plan_held(self, src_held, dst_held) -> core.SwitchPlan:
+        """switchplan::greedy_plan over two `held` maps {device: [(begin, end)]}."""
+        def arr(h):
+            items = [(d, b, e) for d in sorted(h) for (b, e) in h[d]]
+            a = (A.HeldRangeDesc * max(1, len(items)))()
+            for i, (d, b, e) in enumerate(items):
+                a[i] = A.HeldRangeDesc(int(d), int(b), int(e))
+            return a, len(items)
+        sa, ns = arr(src_held)
+        da, nd = arr(dst_held)
+        n, est = C.c_int(), C.c_double()
+        self._chk(self.lib.oserve_gpu_greedy_plan_layouts(self.h, ns, sa, nd, da, 0, None, C.byref(n),
+                                                          C.byref(est)))
+        tr = (A.TransferDesc * max(1, n.value))()
+        if n.value:
+            self._chk(self.lib.oserve_gpu_greedy_plan_layouts(self.h, ns, sa, nd, da, n.value, tr, C.byref(n),
+                                                              C.byref(est)))
+        return core.SwitchPlan([core.Transfer(core.ByteRange(t.begin, t.end), t.src, t.dst) for t in tr[:n.value]],
+                               est.value)
+
+    def estimate_time(self, links) -> float:
+        """switchplan::estimate_time over [(src, dst, bytes)] link loads."""
+        a = (A.LinkLoadDesc * max(1, len(links)))()
+        for i, (s_, d_, b) in enumerate(links):
+            a[i] = A.LinkLoadDesc(int(s_), int(d_), int(b))
+        est = C.c_double()
+        self._chk(self.lib.oserve_gpu_estimate_time(self.h, len(links), a, C.byref(est)))
+        return est.value
+
+    def normalize_batch(self, n: np.ndarray, strict: bool):
+        """flow::normalize (strict) / normalize_or_scale per row -> (M, units, scaled)."""
+        n = np.ascontiguousarray(n, dtype=np.int64)
+        cnt, J = n.shape
+        M = np.zeros(cnt, np.int64)
+        U = np.zeros((cnt, J), np.int64)
+        sc = np.zeros(cnt, np.int32)
+        self._chk(self.lib.oserve_gpu_normalize_batch(self.h, cnt, J, _np_ptr(n, C.c_int64), int(strict),
+                                                      _np_ptr(M, C.c_int64), _np_ptr(U, C.c_int64),
+                                                      _np_ptr(sc, C.c_int)))
+        return M, U, sc.astype(bool)
+
+    def check_constraints_batch(self, x: np.ndarray, n: np.ndarray, e: np.ndarray, lam: np.ndarray,
+                                raise_first: bool = True):
+        """flow::check_constraints per instance -> (kind, replica, type) arrays
+        (kind 0 ok, 1 C1, 2 C2, 3 C3 zero-capacity, 4 C3); raises LogicError
+        for the first violation unless raise_first is False."""
+        x, n, e, lam = (np.ascontiguousarray(v, dtype=np.int64) for v in (x, n, e, lam))
+        cnt, R, J = n.shape
+        kind, kk, jj = (np.zeros(cnt, np.int32) for _ in range(3))
+        st = self.lib.oserve_gpu_check_constraints_batch(self.h, cnt, R, J, _np_ptr(x, C.c_int64),
+                                                         _np_ptr(n, C.c_int64), _np_ptr(e, C.c_int64),
+                                                         _np_ptr(lam, C.c_int64), _np_ptr(kind, C.c_int),
+                                                         _np_ptr(kk, C.c_int), _np_ptr(jj, C.c_int))
+        if raise_first or st not in (A.OK, A.ERR_LOGIC):
+            self._chk(st)
+        return kind, kk, jj
 
     def switch_plan(self, src: core.Deployment, dst: core.Deployment) -> core.SwitchPlan:
         keep = A.Keep()

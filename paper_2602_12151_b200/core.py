@@ -43,6 +43,10 @@ class UnsourcedFragment(OServeError):
     pass
 
 
+class LcmOverflow(OServeError):
+    """oserve::LcmOverflow (errors.hpp:39): flow::normalize past 2^62."""
+
+
 class Unsupported(OServeError):
     """Input outside the GPU path's documented limits."""
 

@@ -1640,6 +1640,7 @@ const char *oserve_gpu_status_name(int status) {
         case OSERVE_ERR_CUDA: return "CUDA";
         case OSERVE_ERR_NO_DEVICE: return "NO_DEVICE";
         case OSERVE_ERR_NCCL: return "NCCL";
+        case OSERVE_ERR_LCM_OVERFLOW: return "LCM_OVERFLOW";
         default: return "UNKNOWN";
     }
 }
@@ -2791,6 +2792,261 @@ int oserve_gpu_switch_plan(oserve_gpu_ctx *ctx, const oserve_deployment *src, co
         if (transfers) {
             for (int i = 0; i < std::min<int>(capacity, static_cast<int>(tr.size())); ++i) transfers[i] = tr[i];
             if (static_cast<int>(tr.size()) > capacity) fail(OSERVE_ERR_INVALID_ARGUMENT, "transfer capacity too small");
+        }
+    });
+}
+
+
+// ---------------------------------------------------------------------------
+// Reference-signature pieces of switching and of the assignment (the C++
+// shim's layout / greedy_plan(ShardLayout...) / estimate_time / normalize /
+// normalize_or_scale / check_constraints).
+
+int oserve_gpu_layout(oserve_gpu_ctx *ctx, const oserve_deployment *dep, uint64_t param_bytes, int capacity,
+                      oserve_shard *shards, int *n_shards) {
+    return guarded(ctx, [&] {
+        if (!dep || !n_shards) fail(OSERVE_ERR_INVALID_ARGUMENT, "layout: null argument");
+        const int R = dep->num_replicas;
+        std::vector<int32_t> rep_off{0}, dev_off, tp, pp, devs;
+        int pos = 0;
+        for (int r = 0; r < R; ++r) {
+            const int nd = dep->replica_num_devices[r];
+            if (dep->tp[r] < 1 || dep->pp[r] < 1) fail(OSERVE_ERR_INVALID_ARGUMENT, "layout: tp and pp must be >= 1");
+            if (static_cast<int64_t>(dep->tp[r]) * dep->pp[r] > nd)
+                fail(OSERVE_ERR_INVALID_ARGUMENT, "layout: replica " + std::to_string(r) + " has fewer than tp*pp devices");
+            std::vector<int> d(dep->device_ids + pos, dep->device_ids + pos + nd);
+            std::sort(d.begin(), d.end());  // devices sorted per replica (switchplan.cpp:45-46)
+            dev_off.push_back(static_cast<int32_t>(devs.size()));
+            devs.insert(devs.end(), d.begin(), d.end());
+            pos += nd;
+            tp.push_back(dep->tp[r]);
+            pp.push_back(dep->pp[r]);
+            rep_off.push_back(rep_off.back() + dep->tp[r] * dep->pp[r]);
+        }
+        const int total = rep_off.back();
+        *n_shards = total;
+        if (total == 0 || !shards) return;  // count query
+        if (capacity < total) fail(OSERVE_ERR_INVALID_ARGUMENT, "layout: shard capacity too small");
+        cudaStream_t s = ctx->stream;
+        DBuf b[8];
+        LayoutIn in{};
+        in.R = R;
+        in.total = total;
+        in.rep_off = b[0].upload(rep_off, s);
+        in.dev_off = b[1].upload(dev_off, s);
+        in.tp = b[2].upload(tp, s);
+        in.pp = b[3].upload(pp, s);
+        in.devs_sorted = b[4].upload(devs, s);
+        in.P = param_bytes;
+        in.begin = static_cast<uint64_t *>(b[5].get(sizeof(uint64_t) * total));
+        in.end = static_cast<uint64_t *>(b[6].get(sizeof(uint64_t) * total));
+        in.holder = static_cast<int32_t *>(b[7].get(sizeof(int32_t) * total));
+        cuda_ok(launch_layout(in, s, &ctx->launches), "layout kernel");
+        std::vector<uint64_t> hb, he;
+        std::vector<int32_t> hh;
+        download(hb, in.begin, total, s);
+        download(he, in.end, total, s);
+        download(hh, in.holder, total, s);
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+        for (int g = 0; g < total; ++g) shards[g] = {g, hb[g], he[g], hh[g]};
+    });
+}
+
+int oserve_gpu_greedy_plan_layouts(oserve_gpu_ctx *ctx, int n_src, const oserve_held_range *src, int n_dst,
+                                   const oserve_held_range *dst, int capacity, oserve_transfer *transfers,
+                                   int *n_transfers, double *est_seconds) {
+    return guarded(ctx, [&] {
+        if (n_src < 0 || n_dst < 0) fail(OSERVE_ERR_INVALID_ARGUMENT, "greedy_plan: negative range count");
+        std::set<int> ids;
+        std::vector<uint64_t> bounds;
+        for (int i = 0; i < n_src; ++i) ids.insert(src[i].device);
+        for (int i = 0; i < n_dst; ++i) ids.insert(dst[i].device);
+        for (const oserve_held_range *v : {src, dst})
+            for (int i = 0, n = (v == src ? n_src : n_dst); i < n; ++i) {
+                if (v[i].end >= (uint64_t{1} << 54)) fail(OSERVE_ERR_UNSUPPORTED, "greedy_plan: byte offsets >= 2^54");
+                bounds.push_back(v[i].begin);
+                bounds.push_back(v[i].end);
+            }
+        if (n_transfers) *n_transfers = 0;
+        if (est_seconds) *est_seconds = 0.0;
+        if (bounds.size() < 2) return;  // cuts.size() < 2: empty plan (:87)
+        if (ids.size() > 256) fail(OSERVE_ERR_UNSUPPORTED, "greedy_plan limited to 256 devices");
+        if (bounds.size() > 16384) fail(OSERVE_ERR_UNSUPPORTED, "greedy_plan limited to 8192 held ranges");
+        std::vector<int32_t> dev_id(ids.begin(), ids.end()), machine;
+        std::map<int, int> slot;
+        for (size_t i = 0; i < dev_id.size(); ++i) {
+            slot[dev_id[i]] = static_cast<int>(i);
+            machine.push_back(ctx->machine(dev_id[i]));
+        }
+        const int ND = static_cast<int>(dev_id.size());
+        auto csr = [&](int n, const oserve_held_range *v, std::vector<int32_t> &off, std::vector<uint64_t> &b,
+                       std::vector<uint64_t> &e) {
+            std::vector<std::vector<std::pair<uint64_t, uint64_t>>> per(ND);
+            for (int i = 0; i < n; ++i) per[slot[v[i].device]].emplace_back(v[i].begin, v[i].end);
+            off.assign(1, 0);
+            for (int t = 0; t < ND; ++t) {
+                for (auto &r : per[t]) {
+                    b.push_back(r.first);
+                    e.push_back(r.second);
+                }
+                off.push_back(static_cast<int32_t>(b.size()));
+            }
+        };
+        std::vector<int32_t> soff, doff;
+        std::vector<uint64_t> sb, se, db, de;
+        csr(n_src, src, soff, sb, se);
+        csr(n_dst, dst, doff, db, de);
+        cudaStream_t s = ctx->stream;
+        DBuf b[14];
+        HeldIn in{};
+        in.num_devices = ND;
+        in.machine = b[0].upload(machine, s);
+        in.src_off = b[1].upload(soff, s);
+        in.dst_off = b[2].upload(doff, s);
+        in.src_b = b[3].upload(sb, s);
+        in.src_e = b[4].upload(se, s);
+        in.dst_b = b[5].upload(db, s);
+        in.dst_e = b[6].upload(de, s);
+        in.nbounds = static_cast<int>(bounds.size());
+        in.bounds = b[7].upload(bounds, s);
+        in.intra_bw = ctx->intra;
+        in.inter_bw = ctx->inter;
+        HeldOut o{};
+        o.max_frags = in.nbounds;
+        o.detail = static_cast<int32_t *>(b[8].get(sizeof(int32_t) * ND * o.max_frags));
+        cuda_ok(cudaMemsetAsync(o.detail, 0xff, sizeof(int32_t) * ND * o.max_frags, s), "memset");
+        o.cuts = static_cast<uint64_t *>(b[9].get(sizeof(uint64_t) * in.nbounds));
+        o.ncuts = static_cast<int32_t *>(b[10].get(sizeof(int32_t)));
+        o.est = static_cast<double *>(b[11].get(sizeof(double)));
+        o.max_bytes = static_cast<unsigned long long *>(b[12].get(sizeof(unsigned long long)));
+        cuda_ok(launch_switch_held(in, o, s, &ctx->launches), "greedy_plan kernel");
+        std::vector<int32_t> detail, nc;
+        std::vector<uint64_t> cuts;
+        std::vector<double> est;
+        download(detail, o.detail, static_cast<size_t>(ND) * o.max_frags, s);
+        download(cuts, o.cuts, in.nbounds, s);
+        download(nc, o.ncuts, 1, s);
+        download(est, o.est, 1, s);
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+        std::vector<oserve_transfer> tr;
+        for (int f = 0; f + 1 < nc[0]; ++f)
+            for (int t = 0; t < ND; ++t) {
+                const int v = detail[static_cast<size_t>(t) * o.max_frags + f];
+                if (v == -2)
+                    fail(OSERVE_ERR_UNSOURCED_FRAGMENT, "bytes [" + std::to_string(cuts[f]) + ", " +
+                                                            std::to_string(cuts[f + 1]) + ") required by device " +
+                                                            std::to_string(dev_id[t]) + " have no source holder");
+                if (v >= 0) tr.push_back({cuts[f], cuts[f + 1], dev_id[v], dev_id[t]});
+            }
+        if (n_transfers) *n_transfers = static_cast<int>(tr.size());
+        if (est_seconds) *est_seconds = est[0];
+        if (transfers) {
+            for (int i = 0; i < std::min<int>(capacity, static_cast<int>(tr.size())); ++i) transfers[i] = tr[i];
+            if (static_cast<int>(tr.size()) > capacity) fail(OSERVE_ERR_INVALID_ARGUMENT, "transfer capacity too small");
+        }
+    });
+}
+
+int oserve_gpu_estimate_time(oserve_gpu_ctx *ctx, int n_links, const oserve_link_load *links, double *est_seconds) {
+    return guarded(ctx, [&] {
+        if (!est_seconds || n_links < 0) fail(OSERVE_ERR_INVALID_ARGUMENT, "estimate_time: bad arguments");
+        *est_seconds = 0.0;
+        if (n_links == 0) return;
+        std::vector<int32_t> ms(n_links), md(n_links);
+        std::vector<uint64_t> by(n_links);
+        for (int i = 0; i < n_links; ++i) {
+            ms[i] = ctx->machine(links[i].src);
+            md[i] = ctx->machine(links[i].dst);
+            by[i] = links[i].bytes;
+        }
+        cudaStream_t s = ctx->stream;
+        DBuf b[4];
+        LinkIn in{};
+        in.n = n_links;
+        in.src_machine = b[0].upload(ms, s);
+        in.dst_machine = b[1].upload(md, s);
+        in.bytes = b[2].upload(by, s);
+        in.intra_bw = ctx->intra;
+        in.inter_bw = ctx->inter;
+        double *d_est = static_cast<double *>(b[3].get(sizeof(double)));
+        cuda_ok(launch_link_time(in, d_est, s, &ctx->launches), "estimate_time kernel");
+        cuda_ok(d2h(est_seconds, d_est, sizeof(double), s), "D2H");
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+    });
+}
+
+int oserve_gpu_normalize_batch(oserve_gpu_ctx *ctx, int count, int J, const int64_t *n, int strict, int64_t *M,
+                               int64_t *units, int *scaled) {
+    return guarded(ctx, [&] {
+        if (count <= 0) return;
+        if (J < 1) fail(OSERVE_ERR_INVALID_ARGUMENT, "normalize: empty row");
+        if (J > OSERVE_MAX_CLASSES) fail(OSERVE_ERR_UNSUPPORTED, "normalize: rows limited to 16 entries");
+        const int64_t cells = static_cast<int64_t>(count) * J;
+        for (int64_t i = 0; i < cells; ++i)
+            if (n[i] < 0) fail(OSERVE_ERR_INVALID_ARGUMENT, "normalize: negative capacity");
+        RawRows rr;
+        stage_raw_rows(*ctx, count, J, n, n, rr);  // K0b: checked LCM, 2^62 fallback
+        cudaStream_t s = ctx->stream;
+        std::vector<int64_t> hM, hu;
+        std::vector<uint8_t> hs;
+        download(hM, rr.t.M, count, s);
+        download(hu, rr.t.unit, cells, s);
+        download(hs, rr.t.scaled, count, s);
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+        for (int i = 0; i < count; ++i) {
+            if (strict && hs[i]) fail(OSERVE_ERR_LCM_OVERFLOW, "normalize: LCM exceeds 2^62");
+            if (M) M[i] = hM[i];
+            if (scaled) scaled[i] = hs[i];
+        }
+        if (units) std::copy(hu.begin(), hu.end(), units);
+    });
+}
+
+int oserve_gpu_check_constraints_batch(oserve_gpu_ctx *ctx, int count, int R, int J, const int64_t *x,
+                                       const int64_t *n, const int64_t *e, const int64_t *lambda, int *kind,
+                                       int *replica, int *type) {
+    return guarded(ctx, [&] {
+        if (count <= 0) return;
+        if (R < 1 || J < 1) fail(OSERVE_ERR_INVALID_ARGUMENT, "check_constraints: empty instance");
+        if (J > OSERVE_MAX_CLASSES) fail(OSERVE_ERR_UNSUPPORTED, "check_constraints: J limited to 16");
+        const int64_t rows = static_cast<int64_t>(count) * R;
+        for (int64_t i = 0; i < rows * J; ++i)
+            if (n[i] < 0) fail(OSERVE_ERR_INVALID_ARGUMENT, "normalize: negative capacity");
+        RawRows rr;
+        stage_raw_rows(*ctx, rows, J, n, e, rr);  // normalize_or_scale per row (K0b)
+        cudaStream_t s = ctx->stream;
+        DBuf b[6];
+        CheckIn in{};
+        in.count = count;
+        in.R = R;
+        in.J = J;
+        in.x = b[0].upload(x, static_cast<size_t>(rows) * J, s);
+        in.e = rr.t.e;
+        in.lambda = b[1].upload(lambda, static_cast<size_t>(count) * J, s);
+        in.t = rr.t;
+        in.kind = static_cast<int32_t *>(b[2].get(sizeof(int32_t) * count));
+        in.k = static_cast<int32_t *>(b[3].get(sizeof(int32_t) * count));
+        in.j = static_cast<int32_t *>(b[4].get(sizeof(int32_t) * count));
+        cuda_ok(launch_check(in, s, &ctx->launches), "check_constraints kernel");
+        std::vector<int32_t> hk, hr, hj;
+        download(hk, in.kind, count, s);
+        download(hr, in.k, count, s);
+        download(hj, in.j, count, s);
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+        for (int i = 0; i < count; ++i) {
+            if (kind) kind[i] = hk[i];
+            if (replica) replica[i] = hr[i];
+            if (type) type[i] = hj[i];
+        }
+        for (int i = 0; i < count; ++i) {
+            const std::string k = std::to_string(hr[i]), j = std::to_string(hj[i]);
+            switch (hk[i]) {  // flowassign.cpp:529-551 messages
+                case 1: fail(OSERVE_ERR_LOGIC, "C1 violated for type " + j);
+                case 2: fail(OSERVE_ERR_LOGIC, "C2 violated at replica " + k + ", type " + j);
+                case 3: fail(OSERVE_ERR_LOGIC, "C3 violated at replica " + k + ": zero-capacity type " + j + " assigned");
+                case 4: fail(OSERVE_ERR_LOGIC, "C3 violated at replica " + k);
+                default: break;
+            }
         }
     });
 }

@@ -301,6 +301,56 @@ struct LpBatch {
 int launch_simplex(const LpBatch &b, void *stream, uint64_t *launches);
 size_t simplex_tableau_doubles(int R, int J);
 
+// Reference-signature helpers of the C++ shim (oserve_aux.cu).
+// switchplan::layout: shard g of replica r (g - rep_off[r] = stage * tp + slice).
+struct LayoutIn {
+    int R, total;                 // replicas, shards (sum of tp * pp)
+    const int32_t *rep_off;       // [R+1] first shard of each replica
+    const int32_t *dev_off;       // [R] first device of each replica in devs_sorted
+    const int32_t *tp, *pp;
+    const int32_t *devs_sorted;   // device ids, ascending within each replica
+    uint64_t P;
+    uint64_t *begin, *end;        // [total]
+    int32_t *holder;              // [total]
+};
+int launch_layout(const LayoutIn &in, void *stream, uint64_t *launches);
+// switchplan::greedy_plan over two ShardLayouts: per device slot (ascending
+// id) its held ranges, CSR.
+struct HeldIn {
+    int num_devices;
+    const int32_t *machine;               // [slots] machine index or -1
+    const int32_t *src_off, *dst_off;     // [slots+1]
+    const uint64_t *src_b, *src_e, *dst_b, *dst_e;
+    int nbounds;                          // every begin/end of both layouts (unsorted)
+    const uint64_t *bounds;
+    double intra_bw, inter_bw;
+};
+struct HeldOut {
+    int32_t *detail;                  // [slots * max_frags] source slot per (target, fragment); -1 none, -2 unsourced
+    int max_frags;
+    uint64_t *cuts;                   // [nbounds] sorted unique boundaries
+    int32_t *ncuts;
+    double *est;
+    unsigned long long *max_bytes;
+};
+int launch_switch_held(const HeldIn &in, const HeldOut &o, void *stream, uint64_t *launches);
+// switchplan::estimate_time over link loads.
+struct LinkIn {
+    int n;
+    const int32_t *src_machine, *dst_machine;
+    const uint64_t *bytes;
+    double intra_bw, inter_bw;
+};
+int launch_link_time(const LinkIn &in, double *est, void *stream, uint64_t *launches);
+// flow::check_constraints over `count` instances (normalised rows in t).
+struct CheckIn {
+    int count, R, J;
+    const int64_t *x, *e, *lambda;
+    ShapeTables t;
+    int32_t *kind, *k, *j;  // 0 ok, 1 C1 (j), 2 C2 (k, j), 3 C3 zero-capacity (k, j), 4 C3 (k)
+};
+int launch_check(const CheckIn &in, void *stream, uint64_t *launches);
+
 // Sort n u64 keys ascending on the device (CUB radix sort); temp is reused.
 int sort_keys(uint64_t *keys, uint64_t *tmp_keys, int n, void **temp, size_t *temp_bytes, void *stream);
 // Groups whose list dropped a key better than `kth` (0 => the lists are exact).

@@ -45,6 +45,40 @@ def solve_assignment_batch(n: Sequence, e: Sequence, lam: Sequence,
                             used[i].tolist()) for i in range(len(obj))]
 
 
+@dataclass
+class NormalizedRow:
+    """flow::NormalizedRow (flowassign.hpp:16-20)."""
+    M: int
+    units: List[int]
+    scaled: bool = False
+
+
+def normalize(n_row: Sequence[int]) -> NormalizedRow:
+    """flow::normalize (flowassign.cpp:31-46) on the device (K0b); raises
+    core.LcmOverflow when the LCM exceeds 2^62."""
+    if not len(n_row):
+        return NormalizedRow(1, [], False)
+    M, U, sc = _gpu(None).normalize_batch(np.asarray([list(n_row)]), strict=True)
+    return NormalizedRow(int(M[0]), U[0].tolist(), bool(sc[0]))
+
+
+def normalize_or_scale(n_row: Sequence[int]) -> NormalizedRow:
+    """flow::normalize_or_scale (flowassign.cpp:48-62) on the device (K0b)."""
+    if not len(n_row):
+        return NormalizedRow(1, [], False)
+    M, U, sc = _gpu(None).normalize_batch(np.asarray([list(n_row)]), strict=False)
+    return NormalizedRow(int(M[0]), U[0].tolist(), bool(sc[0]))
+
+
+def check_constraints(a: core.AssignmentMatrix, table: core.CapacityTable, lam: Sequence[int]) -> None:
+    """flow::check_constraints (flowassign.cpp:529-551) on the device: raises
+    core.LogicError naming the first violated constraint (C1, C2 or C3)."""
+    if not table.n:
+        return
+    _gpu(None).check_constraints_batch(np.asarray([a.x]), np.asarray([table.n]), np.asarray([table.e]),
+                                       np.asarray([list(lam)]))
+
+
 # ---- flow-network formulation ------------------------------------------------
 INT64_MAX = (1 << 63) - 1
 

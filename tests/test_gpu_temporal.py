@@ -95,3 +95,46 @@ def test_cfg4_timeline_file_is_the_references(cuda):
                                        min_gain=w.raw["min_gain"], strategy="search", seed=0, search_max_iters=150)
     text = open(os.path.join(ROOT, "tests", "golden", "timeline_cfg4_ref.json")).read()
     assert json_io.dumps(json_io.timeline_json(tl, w.span_s)) == text
+
+
+def test_cfg4_topk_switch_batch_per_window(cuda, port):
+    """every window keeps the exact top-K (1,024) plans
+    and costs current -> each of them (K2 key mode); the timeline is the same
+    as the plain round's, the batch equals the explicit-deployment K2 and the
+    greedy_plan + estimate_time of the CPU oracle on sampled pairs, and the
+    chosen pair's plan is the batch's entry for the winner."""
+    import numpy as np
+    w = workloads.load("cfg4")
+    fc = w.raw["forecasts"]
+    g = GpuContext(w.cluster, w.model, w.params)
+    K = 1024
+    tl = orchestrate.build_adaptive_timeline(g, w.types, fc, w.span_s, w.raw["min_gain"], w.space_mode, w.space_sizes,
+                                             topk=K)
+    base = orchestrate.build_adaptive_timeline(GpuContext(w.cluster, w.model, w.params), w.types, fc, w.span_s,
+                                               w.raw["min_gain"], w.space_mode, w.space_sizes)
+    assert [(e.span_index, e.deployment.shapes(), e.assignment, e.switch_seconds) for e in tl.entries] == \
+        [(e.span_index, e.deployment.shapes(), e.assignment, e.switch_seconds) for e in base.entries]
+    assert len(tl.stats) >= 2 and all(len(s.candidate_keys) == K for s in tl.stats)
+    rng = np.random.default_rng(4)
+    current = None
+    checked = 0
+    by_window = {e.window: e for e in tl.entries}
+    for st in tl.stats:
+        g.set_workload(w.types, fc[st.window], w.span_s)
+        g.prepare_space(w.space_mode, w.space_sizes)
+        if current is not None:
+            assert len(st.candidate_switch_seconds) == K
+            deps = [g.decode_key(k).deployment for k in st.candidate_keys]
+            est_x, _ = g.switch_cost_batch(current, deps)
+            assert st.candidate_switch_seconds == est_x
+            for i in rng.integers(0, K, 8):
+                plan, _ = port.switch_plan(w.cluster, w.model.param_bytes, current, deps[i])
+                assert st.candidate_switch_seconds[i] == plan.est_seconds
+                checked += 1
+            e = by_window.get(st.window)
+            if e is not None and e.switch is not None and not e.kept:
+                assert e.switch_seconds == st.candidate_switch_seconds[0]  # chosen = top-1 candidate
+        e = by_window.get(st.window)
+        if e is not None:
+            current = e.deployment
+    assert checked > 0
