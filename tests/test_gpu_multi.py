@@ -36,7 +36,8 @@ def test_eight_shards_on_one_gpu_cover_the_space(cuda, name):
     keys = []
     for r in range(8):
         g.set_shard(r, 8)
-        g.launch_round_async(d.data_ptr())
+        g.launch_round_async(d.data_ptr())  # on the context's own stream
+        torch.cuda.synchronize()
         keys.append(int(d.item()) & ((1 << 64) - 1))
     g.set_shard(0, 1)
     assert min(keys) == full
