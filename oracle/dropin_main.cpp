@@ -380,7 +380,10 @@ int main(int argc, char **argv) {
         const double t_ref = secs(t0);
         t0 = std::chrono::steady_clock::now();
         auto gpu = adaptive_windows<true>(c32, m, t4, lams, 40);
-        const double t_gpu = secs(t0);
+        const double t_gpu_cold = secs(t0);  // includes context creation + first kernel loads
+        t0 = std::chrono::steady_clock::now();
+        gpu = adaptive_windows<true>(c32, m, t4, lams, 40);
+        const double t_gpu = secs(t0);  // cached contexts (a long-running scheduler's steady state)
         for (size_t w = 0; w < lams.size(); ++w) {
             EXPECT(ref[w].chosen == gpu[w].chosen && ref[w].found == gpu[w].found, "orchestrate window: chosen");
             EXPECT(ref[w].x == gpu[w].x, "orchestrate window: assignment_for");
@@ -388,8 +391,23 @@ int main(int argc, char **argv) {
                    "orchestrate window: switch plan");
         }
         std::printf("orchestrate windows (4 x search(max_iters=40) + keep + assignment + switch, D=32, J=4): "
-                    "reference %.3f s, GPU through the shim %.3f s\n",
-                    t_ref, t_gpu);
+                    "reference %.3f s, GPU through the shim %.3f s (first call, cold contexts %.3f s)\n",
+                    t_ref, t_gpu, t_gpu_cold);
+        // search() alone on the config-2 shape, warm: the reference vs the shim
+        TraceSpan span{0, lams[0]};
+        search::SearchOptions so;
+        so.seed = 3;
+        t0 = std::chrono::steady_clock::now();
+        auto sa = search::search(c32, m, t4, span, 60.0, cost::ProfileParams{}, so);
+        const double ts_ref = secs(t0);
+        oserve_gpu::search::search(c32, m, t4, span, 60.0, cost::ProfileParams{}, so);
+        t0 = std::chrono::steady_clock::now();
+        auto sb = oserve_gpu::search::search(c32, m, t4, span, 60.0, cost::ProfileParams{}, so);
+        const double ts_gpu = secs(t0);
+        EXPECT(sa.throughput == sb.throughput && sa.deployment == sb.deployment && sa.iterations == sb.iterations,
+               "search::search (D=32)");
+        std::printf("search::search D=32 J=4 seed 3 (%d iterations): reference %.4f s, GPU through the shim %.4f s\n",
+                    sa.iterations, ts_ref, ts_gpu);
     }
     // search::search one for one (the SPEC's schedule path), log rows included
     for (auto lam : {std::vector<int64_t>{700, 300}, std::vector<int64_t>{5000, 40}}) {

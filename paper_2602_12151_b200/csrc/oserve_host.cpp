@@ -214,8 +214,7 @@ struct Space {
     std::vector<std::vector<Cand>> lists;      // candidate lists
     std::vector<std::vector<int>> list_shapes; // shape id per candidate
     // device copies
-    DBuf d_prefix, d_R, d_rep_off, d_run_off, d_nruns, d_exact, d_rep_list, d_run_start, d_run_len, d_run_q,
-        d_run_count, d_run_weight, d_cl_n, d_cl_shape;
+    DBuf d_tables, d_exact;  // every table in one allocation (one H2D copy), exact flags
     SpaceTables view{};
     std::vector<uint8_t> exact;  // per partition, for the current workload
     bool any_exact = false;
@@ -225,7 +224,7 @@ struct Space {
         int rmax = 0;
         uint64_t total = 0;
         std::vector<uint64_t> start, prefix;
-        DBuf d_start, d_prefix;
+        const uint64_t *d_start = nullptr, *d_prefix = nullptr;  // inside Space::d_tables
     };
     Bucket buckets[2];
     bool use_buckets = false;
@@ -285,6 +284,11 @@ struct oserve_gpu_ctx {
     std::vector<ShapeParam> shapes;
     int tables_shapes = -1;  // shapes computed in device tables
     bool tables_dirty = true;
+    uint64_t tables_ver = 0;  // bumped whenever K0 recomputes the tables
+    // host copies of the shape tables (plan_detail), valid for host_tables_ver
+    std::vector<int64_t> h_n, h_e, h_M, h_unit;
+    std::vector<double> h_lat;
+    uint64_t host_tables_ver = ~0ull;
     DBuf d_param, d_n, d_e, d_lat, d_M, d_unit, d_inv, d_rank, d_pmask, d_cap, d_order, d_olen, d_pp, d_scaled, d_cin,
         d_cout;
     ShapeTables tables{};
@@ -443,6 +447,7 @@ void ensure_tables(oserve_gpu_ctx &c) {
     c.tables = t;
     c.tables_shapes = S;
     c.tables_dirty = false;
+    ++c.tables_ver;
 }
 
 SolveParams solve_params(const oserve_gpu_ctx &c) {
@@ -579,6 +584,21 @@ void build_space(oserve_gpu_ctx &c, Space &sp, int mode, const std::vector<int> 
     upload_space(c, sp);
 }
 
+// Several host arrays staged into one device allocation with one H2D copy
+// (16-byte aligned offsets): per-partition callers (search -> best_strategies)
+// would otherwise pay one copy per table.
+struct Packer {
+    std::vector<unsigned char> h;
+    template <class T>
+    size_t add(const std::vector<T> &v) {
+        const size_t off = (h.size() + 15) & ~size_t(15);
+        h.resize(off + v.size() * sizeof(T));
+        if (!v.empty()) std::memcpy(h.data() + off, v.data(), v.size() * sizeof(T));
+        return off;
+    }
+    const unsigned char *upload(DBuf &d, cudaStream_t s) { return d.upload(h.data(), h.size(), s); }
+};
+
 // Host fields of a space (the enumeration), without its device copies.
 void copy_space_host(const Space &a, Space &b) {
     b.mode = a.mode;
@@ -652,27 +672,40 @@ void upload_space(oserve_gpu_ctx &c, Space &sp) {
         b.total += part.count;
     }
     sp.use_buckets = sp.buckets[0].total > 0 && sp.buckets[1].total > 0;
-    if (sp.use_buckets) {
-        for (auto &b : sp.buckets) {
-            b.d_start.upload(b.start, s);
-            b.d_prefix.upload(b.prefix, s);
+    Packer pk;
+    size_t o_bs[2] = {0, 0}, o_bp[2] = {0, 0};
+    if (sp.use_buckets)
+        for (int q = 0; q < 2; ++q) {
+            o_bs[q] = pk.add(sp.buckets[q].start);
+            o_bp[q] = pk.add(sp.buckets[q].prefix);
         }
-    }
+    const size_t o_prefix = pk.add(sp.prefix), o_R = pk.add(R), o_rep_off = pk.add(rep_off),
+                 o_run_off = pk.add(run_off), o_nruns = pk.add(nruns), o_rep_list = pk.add(rep_list),
+                 o_run_start = pk.add(run_start), o_run_len = pk.add(run_len), o_run_q = pk.add(run_q),
+                 o_run_count = pk.add(run_count), o_run_weight = pk.add(run_weight), o_cl_n = pk.add(cl_n),
+                 o_cl_shape = pk.add(cl_shape);
+    const unsigned char *base = pk.upload(sp.d_tables, s);
+    auto at = [&](size_t o) { return static_cast<const void *>(base + o); };
+    if (sp.use_buckets)
+        for (int q = 0; q < 2; ++q) {
+            sp.buckets[q].d_start = static_cast<const uint64_t *>(at(o_bs[q]));
+            sp.buckets[q].d_prefix = static_cast<const uint64_t *>(at(o_bp[q]));
+        }
     SpaceTables v{};
     v.num_parts = static_cast<int64_t>(P);
-    v.prefix = sp.d_prefix.upload(sp.prefix, s);
-    v.R = sp.d_R.upload(R, s);
-    v.rep_off = sp.d_rep_off.upload(rep_off, s);
-    v.run_off = sp.d_run_off.upload(run_off, s);
-    v.nruns = sp.d_nruns.upload(nruns, s);
-    v.rep_list = sp.d_rep_list.upload(rep_list, s);
-    v.run_start = sp.d_run_start.upload(run_start, s);
-    v.run_len = sp.d_run_len.upload(run_len, s);
-    v.run_q = sp.d_run_q.upload(run_q, s);
-    v.run_count = sp.d_run_count.upload(run_count, s);
-    v.run_weight = sp.d_run_weight.upload(run_weight, s);
-    v.cl_n = sp.d_cl_n.upload(cl_n, s);
-    v.cl_shape = sp.d_cl_shape.upload(cl_shape, s);
+    v.prefix = static_cast<const uint64_t *>(at(o_prefix));
+    v.R = static_cast<const int32_t *>(at(o_R));
+    v.rep_off = static_cast<const int32_t *>(at(o_rep_off));
+    v.run_off = static_cast<const int32_t *>(at(o_run_off));
+    v.nruns = static_cast<const int32_t *>(at(o_nruns));
+    v.rep_list = static_cast<const int32_t *>(at(o_rep_list));
+    v.run_start = static_cast<const int32_t *>(at(o_run_start));
+    v.run_len = static_cast<const int32_t *>(at(o_run_len));
+    v.run_q = static_cast<const int32_t *>(at(o_run_q));
+    v.run_count = static_cast<const uint64_t *>(at(o_run_count));
+    v.run_weight = static_cast<const uint64_t *>(at(o_run_weight));
+    v.cl_n = static_cast<const uint8_t *>(at(o_cl_n));
+    v.cl_shape = static_cast<const uint16_t *>(at(o_cl_shape));
     sp.view = v;
     sp.valid = true;
 }
@@ -807,8 +840,8 @@ void for_each_k1_launch(oserve_gpu_ctx &c, Space &sp, F &&fn) {
             src.rank = c.rank;
             src.world = c.world;
             src.chunk = c.chunk;
-            src.range_start = static_cast<const uint64_t *>(b.d_start.p);
-            src.range_prefix = static_cast<const uint64_t *>(b.d_prefix.p);
+            src.range_start = b.d_start;
+            src.range_prefix = b.d_prefix;
             src.num_ranges = static_cast<int>(b.start.size());
             fn(src, b.rmax);
         }
@@ -1132,10 +1165,14 @@ void eval_lists(oserve_gpu_ctx &c, const std::vector<int32_t> &listR, const std:
     PlanSource src{};
     src.mode = 2;
     src.count = n;
-    src.list_R = c.d_listR.upload(listR, s);
-    src.list_off = c.d_listOff.upload(listOff, s);
-    src.list_shapes = c.d_listShapes.upload(shapes, s);
-    if (lam_per_plan) src.list_lambda = c.d_listLam.upload(*lam_per_plan, s);
+    Packer pk;  // the plan lists in one H2D copy
+    const size_t oR = pk.add(listR), oO = pk.add(listOff), oS = pk.add(shapes);
+    const size_t oL = lam_per_plan ? pk.add(*lam_per_plan) : 0;
+    const unsigned char *base = pk.upload(c.d_listR, s);
+    src.list_R = reinterpret_cast<const int32_t *>(base + oR);
+    src.list_off = reinterpret_cast<const int32_t *>(base + oO);
+    src.list_shapes = reinterpret_cast<const int32_t *>(base + oS);
+    if (lam_per_plan) src.list_lambda = reinterpret_cast<const int64_t *>(base + oL);
     PlanOutputs out{};
     out.objective = static_cast<int64_t *>(c.d_obj.get(sizeof(int64_t) * n));
     out.rmax = std::max(rmax, 1);
@@ -2429,17 +2466,21 @@ int oserve_gpu_plan_detail(oserve_gpu_ctx *ctx, const oserve_deployment *dep, in
         std::vector<int32_t> listR{R}, listOff{0}, shapes(ids.begin(), ids.end());
         std::vector<int64_t> obj, xs, us;
         eval_lists(*ctx, listR, listOff, shapes, nullptr, R, obj, &xs, &us, solve_params(*ctx));
-        // shape rows (n, e, latency, M, unit) straight from the device tables
+        // shape rows (n, e, latency, M, unit) from the device tables (host
+        // copies refreshed once per K0 run)
         const int S = ctx->tables.num_shapes;
-        std::vector<int64_t> hn, he, hM, hu;
-        std::vector<double> hl;
-        cudaStream_t s = ctx->stream;
-        download(hn, ctx->tables.n, S * J, s);
-        download(he, ctx->tables.e, S * J, s);
-        download(hl, ctx->tables.latency, S * J, s);
-        download(hM, ctx->tables.M, S, s);
-        download(hu, ctx->tables.unit, S * J, s);
-        cuda_ok(cudaStreamSynchronize(s), "sync");
+        if (ctx->host_tables_ver != ctx->tables_ver) {
+            cudaStream_t s = ctx->stream;
+            download(ctx->h_n, ctx->tables.n, S * J, s);
+            download(ctx->h_e, ctx->tables.e, S * J, s);
+            download(ctx->h_lat, ctx->tables.latency, S * J, s);
+            download(ctx->h_M, ctx->tables.M, S, s);
+            download(ctx->h_unit, ctx->tables.unit, S * J, s);
+            cuda_ok(cudaStreamSynchronize(s), "sync");
+            ctx->host_tables_ver = ctx->tables_ver;
+        }
+        const auto &hn = ctx->h_n, &he = ctx->h_e, &hM = ctx->h_M, &hu = ctx->h_unit;
+        const auto &hl = ctx->h_lat;
         for (int k = 0; k < R; ++k) {
             const int sh = ids[k];
             for (int j = 0; j < J; ++j) {

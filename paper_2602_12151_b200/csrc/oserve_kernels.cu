@@ -21,6 +21,8 @@
 
 #include <atomic>
 #include <cstdint>
+#include <map>
+#include <tuple>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -378,7 +380,14 @@ __device__ __forceinline__ void unrank_run_group(const Grp &g, uint64_t rr, int 
     for (int p = g.gl; p < rem; p += Grp::kG) out[pos + p] = static_cast<uint8_t>(q - 1);
 }
 
-template <int G, int KPL, bool SMEM>
+// K1 variants: the round (best key only; plan sources 0/1/3), the top-K
+// round (+ per-group key lists, threshold collect) and the general kernel
+// (explicit shape lists, per-plan objective / sum_pp / x / used).  The round
+// kernel carries no per-plan output code: its hot loop is the whole kernel,
+// and cold code inside it still costs instruction-cache lines.
+enum K1Variant { kK1Round = 0, kK1TopK = 1, kK1General = 2 };
+
+template <int G, int KPL, bool SMEM, int V>
 __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_MINB) k_plan_eval(ShapeTables t, SpaceTables sp, KeyLayout key,
                                                                    PlanSource src, PlanOutputs out, SolveParams prm,
                                                                    int skip_exact, int gchunk,
@@ -386,6 +395,8 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
     using Grp = Group<G, KPL>;
     constexpr int RMAX = Grp::RMAX;
     constexpr int GPB = 256 / G;
+    constexpr bool kGeneral = V == kK1General;
+    constexpr bool kLists = V != kK1Round;  // top-K lists / threshold collect
     extern __shared__ __align__(16) unsigned char smem[];
     const int S = t.num_shapes, J = prm.J;
 
@@ -460,7 +471,8 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
     int jw = 1;
     while (jw < J) jw <<= 1;  // scan width over class positions
     constexpr int TKE = kTopK / G;  // top-K list entries per lane (shared memory)
-    for (int e = 0; e < TKE; ++e) tks[g.gl * TKE + e] = kNoKey;
+    if (kLists)
+        for (int e = 0; e < TKE; ++e) tks[g.gl * TKE + e] = kNoKey;
     const uint64_t ngroups = static_cast<uint64_t>(gridDim.x) * GPB;
 
     // Each group walks contiguous chunks of `gchunk` plans, so consecutive
@@ -521,7 +533,7 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
         int P = 0;            // first replica of the partition's last run
         bool reuse = false;   // resume the greedy from the snapshot at P
         const int64_t *lam_src = prm.lambda;
-        if (src.mode == 2) {
+        if (kGeneral && src.mode == 2) {
             const uint64_t li = src.first + i;
             R = src.list_R[li];
             const int32_t *ls = src.list_shapes + src.list_off[li];
@@ -1175,9 +1187,9 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
             if (g.gl + G * kk < R) spp += sPP[shp[kk]];
         served = g.sum(served);
         spp = g.sum(spp);
-        if (out.objective && g.gl == 0) out.objective[i] = served;
-        if (out.sum_pp && g.gl == 0) out.sum_pp[i] = static_cast<int32_t>(spp);
-        if (out.x) {
+        if (kGeneral && out.objective && g.gl == 0) out.objective[i] = served;
+        if (kGeneral && out.sum_pp && g.gl == 0) out.sum_pp[i] = static_cast<int32_t>(spp);
+        if (kGeneral && out.x) {
 #pragma unroll
             for (int kk = 0; kk < KPL; ++kk) {
                 const int k = g.gl + G * kk;
@@ -1193,7 +1205,7 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                                 (static_cast<uint64_t>(part) << key.sh_part) |
                                 (static_cast<uint64_t>(spp) << key.sh_spp) | local;
             if (g.gl == 0 && kv < cy->best) cy->best = kv;
-            if (out.topk) {
+            if (kLists && out.topk) {
                 // per-group top-kTopK list, kTopK/G entries per lane (shared memory)
                 const uint64_t tk_max = cy->tk_max;
                 if (kv < tk_max) {
@@ -1228,7 +1240,7 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                     cy->lossy = 1;
                 }
             }
-            if (out.collect && kv <= out.collect_thr && g.gl == 0) {
+            if (kLists && out.collect && kv <= out.collect_thr && g.gl == 0) {
                 const unsigned slot = atomicAdd(out.collect_n, 1u);
                 if (slot < out.collect_cap) out.collect[slot] = kv;
             }
@@ -1236,7 +1248,7 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
         g.sync();
     }
     }
-    if (out.topk) {
+    if (kLists && out.topk) {
         const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * GPB + gib;
         g.sync();
         for (int e = 0; e < TKE; ++e) out.topk[gid * kTopK + g.gl * TKE + e] = tks[g.gl * TKE + e];
@@ -1273,19 +1285,37 @@ size_t plan_eval_smem(int S, int J, bool stage) {
 }
 
 // Launch geometry of K1 (also used to size the top-K lists).
-template <int G, int KPL>
+template <int G, int KPL, int V = kK1Round>
 int plan_eval_geometry(const ShapeTables &t, int J, int sm_count, uint64_t count, size_t *smem_out, bool *stage_out,
                        uint64_t *grid_out) {
     const bool stage = plan_eval_smem<G, KPL>(t.num_shapes, J, true) <= 160 * 1024;
     const size_t smem = plan_eval_smem<G, KPL>(t.num_shapes, J, stage);
-    auto kern = stage ? k_plan_eval<G, KPL, true> : k_plan_eval<G, KPL, false>;
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        if (e != cudaSuccess) return static_cast<int>(e);
-    }
+    auto kern = stage ? k_plan_eval<G, KPL, true, V> : k_plan_eval<G, KPL, false, V>;
+    // occupancy per (device, kernel, smem), computed once: the attribute and
+    // occupancy queries are host API calls that a per-partition caller (search
+    // -> best_strategies) would otherwise pay on every launch
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void *, size_t>, int> occ;
+    int dev = 0;
+    if (cudaError_t e = cudaGetDevice(&dev)) return static_cast<int>(e);
     int per_sm = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
-    if (e != cudaSuccess) return static_cast<int>(e);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        const auto key = std::make_tuple(dev, reinterpret_cast<const void *>(kern), smem);
+        auto it = occ.find(key);
+        if (it != occ.end()) {
+            per_sm = it->second;
+        } else {
+            if (smem > 48 * 1024) {
+                cudaError_t e =
+                    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+                if (e != cudaSuccess) return static_cast<int>(e);
+            }
+            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
+            if (e != cudaSuccess) return static_cast<int>(e);
+            occ.emplace(key, per_sm);
+        }
+    }
     if (per_sm < 1) return static_cast<int>(cudaErrorInvalidConfiguration);
     constexpr int GPB = 256 / G;
     uint64_t need = (count + GPB - 1) / GPB;
@@ -1308,16 +1338,16 @@ unsigned long long *work_counter(WorkRing *ring, cudaStream_t stream) {
     return c;
 }
 
-template <int G, int KPL>
-int run_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key, const PlanSource &src,
+template <int G, int KPL, int V>
+int run_plan_eval_v(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key, const PlanSource &src,
                   const PlanOutputs &out, const SolveParams &prm, int sm_count, int skip_exact,
                   WorkRing *ring, cudaStream_t stream, uint64_t *launches) {
     cudaGetLastError();  // clear any stale (non-sticky) error before launching
     size_t smem = 0;
     bool stage = false;
     uint64_t grid = 0;
-    if (int e = plan_eval_geometry<G, KPL>(t, prm.J, sm_count, src.count, &smem, &stage, &grid)) return e;
-    auto kern = stage ? k_plan_eval<G, KPL, true> : k_plan_eval<G, KPL, false>;
+    if (int e = plan_eval_geometry<G, KPL, V>(t, prm.J, sm_count, src.count, &smem, &stage, &grid)) return e;
+    auto kern = stage ? k_plan_eval<G, KPL, true, V> : k_plan_eval<G, KPL, false, V>;
     if (grid == 0) return 0;
     // contiguous plans per group (greedy-prefix reuse), >= 4 chunks per group
     constexpr int GPB = 256 / G;
@@ -1330,6 +1360,21 @@ int run_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &
                                                                static_cast<int>(gch), work);
     if (launches) ++*launches;
     return check(cudaGetLastError());
+}
+
+// The variant a launch needs: per-plan outputs or explicit lists -> general;
+// key lists -> top-K; otherwise the round kernel.
+template <int G, int KPL>
+int run_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key, const PlanSource &src,
+                  const PlanOutputs &out, const SolveParams &prm, int sm_count, int skip_exact, WorkRing *ring,
+                  cudaStream_t stream, uint64_t *launches) {
+    if (src.mode == 2 || out.objective || out.sum_pp || out.x || out.used)
+        return run_plan_eval_v<G, KPL, kK1General>(t, sp, key, src, out, prm, sm_count, skip_exact, ring, stream,
+                                                   launches);
+    if (out.topk || out.collect)
+        return run_plan_eval_v<G, KPL, kK1TopK>(t, sp, key, src, out, prm, sm_count, skip_exact, ring, stream,
+                                                launches);
+    return run_plan_eval_v<G, KPL, kK1Round>(t, sp, key, src, out, prm, sm_count, skip_exact, ring, stream, launches);
 }
 
 // ------------------------------------------------------------------- K4 ---
@@ -2686,13 +2731,15 @@ int k1_groups(int rmax, int J, int sm_count, const ShapeTables &t, uint64_t coun
     const char *env = getenv("OSERVE_K1_G");
     const bool opt16 = env && atoi(env) == 16;
     int e = 0, gpb = 0;
-    if (need <= 8) e = plan_eval_geometry<8, 1>(t, J, sm_count, count, &smem, &stage, &grid), gpb = 32;
-    else if (need <= 16) e = plan_eval_geometry<16, 1>(t, J, sm_count, count, &smem, &stage, &grid), gpb = 16;
-    else if (J <= 16 && opt16 && rmax <= 32) e = plan_eval_geometry<16, 2>(t, J, sm_count, count, &smem, &stage, &grid), gpb = 16;
-    else if (J <= 16 && opt16 && rmax <= 64) e = plan_eval_geometry<16, 4>(t, J, sm_count, count, &smem, &stage, &grid), gpb = 16;
-    else if (rmax <= 32) e = plan_eval_geometry<32, 1>(t, J, sm_count, count, &smem, &stage, &grid), gpb = 8;
-    else if (rmax <= 64) e = plan_eval_geometry<32, 2>(t, J, sm_count, count, &smem, &stage, &grid), gpb = 8;
-    else e = plan_eval_geometry<32, 4>(t, J, sm_count, count, &smem, &stage, &grid), gpb = 8;
+    // (sizes the top-K lists: the top-K variant's geometry)
+    constexpr int V = kK1TopK;
+    if (need <= 8) e = plan_eval_geometry<8, 1, V>(t, J, sm_count, count, &smem, &stage, &grid), gpb = 32;
+    else if (need <= 16) e = plan_eval_geometry<16, 1, V>(t, J, sm_count, count, &smem, &stage, &grid), gpb = 16;
+    else if (J <= 16 && opt16 && rmax <= 32) e = plan_eval_geometry<16, 2, V>(t, J, sm_count, count, &smem, &stage, &grid), gpb = 16;
+    else if (J <= 16 && opt16 && rmax <= 64) e = plan_eval_geometry<16, 4, V>(t, J, sm_count, count, &smem, &stage, &grid), gpb = 16;
+    else if (rmax <= 32) e = plan_eval_geometry<32, 1, V>(t, J, sm_count, count, &smem, &stage, &grid), gpb = 8;
+    else if (rmax <= 64) e = plan_eval_geometry<32, 2, V>(t, J, sm_count, count, &smem, &stage, &grid), gpb = 8;
+    else e = plan_eval_geometry<32, 4, V>(t, J, sm_count, count, &smem, &stage, &grid), gpb = 8;
     if (e) return -1;
     return static_cast<int>(grid) * gpb;
 }
