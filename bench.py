@@ -167,6 +167,17 @@ def cpu_reference_sample(w: workloads.Workload, plans: int, target_s: float, thr
     return n2 / t, kind, n2, t
 
 
+def cpu_model() -> str:
+    """lscpu "Model name" of the host, from /proc/cpuinfo."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -200,6 +211,7 @@ def run_reference(args, rank, world):
             "config": {"workload": f"{w.name}: {w.description}", "plans_in_space": plans, "partitions": parts,
                        "per_step_sample_plans": per_step},
             "cpu_baseline": {"value": value, "unit": "plans/s", "cores": threads, "kind": kind,
+                             "cpu_model": cpu_model(),
                              "sample": f"{per_step} uniform random plans of {plans} per step "
                                        f"(evaluate_deployment each, OpenMP dynamic,4 over {threads} threads)"},
             "e2e": {"value": value, "unit": "plans/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -441,17 +453,28 @@ def run_ours(args, rank, world, local):
     work = load_work(args.config)
     props = torch.cuda.get_device_properties(dev)
     sm_max = clk.get("sm_max_mhz") or 1965.0
-    peak = props.multi_processor_count * 128 * sm_max * 1e6  # lane-ops/s per GPU
+    nominal = props.multi_processor_count * 128 * sm_max * 1e6  # lane-ops/s per GPU (4 SMSPs x 32 lanes x clock)
+    measured = measured_int_peak()
+    peak = measured or nominal
     achieved = work["mean_work"] * OPS_PER_CELL * (plans / world) / (k_ms / 1e3)
     traffic = profile_traffic(args.config)
+    executed = k1_executed(args.config)  # ncu thread-instructions of one round's K1 launches
+    if executed:
+        executed = dict(executed, lane_ops_per_s=executed["thread_inst_per_round"] / world / (k_ms / 1e3))
+        executed["frac_of_peak"] = executed["lane_ops_per_s"] / peak
     cpu = None
     if world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
         rate, kind, n, t = cpu_reference_sample(w, plans, args.cpu_seconds, threads)
+        # the serial run (parallel = false, 1 thread) beside the parallel one
+        rate1, _, n1, t1 = cpu_reference_sample(w, plans, max(2.0, args.cpu_seconds / 3), 1)
         cpu = {"value": rate, "unit": "plans/s", "cores": threads, "kind": kind,
                "sample": f"{n} uniform random plans of {plans} ({t:.1f} s; evaluate_deployment each, "
                          f"OpenMP dynamic,4 over {threads} host threads)",
-               "round_latency_s_projected": plans / rate}
+               "round_latency_s_projected": plans / rate, "cpu_model": cpu_model(),
+               "serial": {"value": rate1, "unit": "plans/s", "cores": 1,
+                          "sample": f"{n1} uniform random plans ({t1:.1f} s, one thread)",
+                          "round_latency_s_projected": plans / rate1}}
     line = {
         "metric": METRIC, "value": value, "unit": "plans/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "round_latency_ms": ms_per_step,
@@ -472,6 +495,11 @@ def run_ours(args, rank, world, local):
                 "winner_switch_est_seconds": plan.est_seconds, "winner_switch_transfers": len(plan.transfers)},
         "roofline": {"bound": "issue", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tlane-op/s",
                      "frac": achieved / peak, "traffic": traffic,
+                     "peak_kind": ("measured integer issue peak (profiles/round2_int_peak.json: u64 adds, "
+                                   "IADD3+IADD3.X)") if measured else "nominal SMs x 128 lanes x clock",
+                     "peak_nominal": nominal / 1e12,
+                     "achieved_convention": "SURVEY §8d: algorithmic cell-ops per plan x 8 lane-ops",
+                     "executed_ncu": executed,
                      "kernel": "k_plan_eval (K1)", "kernel_ms": k_ms,
                      "work_per_plan": work["mean_work"], "work_kind": work["kind"],
                      "ops_per_cell": OPS_PER_CELL},
@@ -489,6 +517,28 @@ def label(dep: core.Deployment) -> str:
         k = (r.device_count(), r.tp, r.pp)
         groups[k] = groups.get(k, 0) + 1
     return "+".join(f"{c}x(d{d},tp{t},pp{p})" for (d, t, p), c in sorted(groups.items()))
+
+
+def measured_int_peak():
+    """Measured integer issue peak of this B200 (scripts/int_peak.cu): the
+    best of the integer-add kernels, lane-ops/s; None if not measured."""
+    p = os.path.join(ROOT, "profiles", "round2_int_peak.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    return max(d.get("int_add_lane_ops_per_s", 0.0), d.get("add64_lane_ops_per_s", 0.0)) or None
+
+
+def k1_executed(name):
+    """ncu thread-instructions executed by one round's K1 launches
+    (profiles/round2_k1_ncu.json, the same build's capture)."""
+    p = os.path.join(ROOT, "profiles", "round2_k1_ncu.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    return d.get(name)
 
 
 def profile_traffic(name):

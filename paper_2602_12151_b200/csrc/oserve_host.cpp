@@ -941,11 +941,26 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
         // Phase A in rounds: tasks over the round's node cap are split into
         // their children (preorder kept) and rerun; the last round runs with
         // the full budget.
-        constexpr int kRounds = 6;
-        constexpr int64_t kRoundCap = 1 << 15;
+        // Round r caps each task at cap0 * growth^r nodes: a task over the
+        // cap wastes the nodes it ran before it is split, so the caps start
+        // small and grow (most tasks finish in the first round).
+        static const int kRounds = [] {
+            const char *e = getenv("OSERVE_EXACT_ROUNDS");
+            return e ? atoi(e) : 6;
+        }();
+        static const int64_t kCap0 = [] {
+            const char *e = getenv("OSERVE_EXACT_CAP0");
+            return e ? static_cast<int64_t>(atoll(e)) : int64_t{1} << 15;
+        }();
+        static const int kGrowth = [] {
+            const char *e = getenv("OSERVE_EXACT_GROWTH");
+            return e ? atoi(e) : 1;
+        }();
+        int64_t round_cap = kCap0;
         for (int round = 0;; ++round) {
             const bool last = round == kRounds || total > (uint64_t{1} << 24);
-            et.phase_cap = last ? prm.node_budget : kRoundCap;
+            et.phase_cap = last ? prm.node_budget : round_cap;
+            round_cap = std::min<int64_t>(round_cap * kGrowth, int64_t{1} << 22);
             cuda_ok(launch_exact_task_pass(2, c.tables, view, src, prm, et, total, c.sm_count, s, &c.launches),
                     "exact task pass 2");
             cuda_ok(launch_exact_plan_pass(4, c.tables, view, key, src, eo, prm, et, c.sm_count, s, &c.launches),
@@ -953,6 +968,21 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
             cuda_ok(launch_exact_task_pass(0, c.tables, view, src, prm, et, total, c.sm_count, s, &c.launches),
                     "exact task pass 0");
             lap("phaseA round");
+            if (dbg) {
+                std::vector<int64_t> nd;
+                std::vector<uint8_t> cp;
+                download(nd, et.nodes, total, s);
+                download(cp, et.capped, total, s);
+                cuda_ok(cudaStreamSynchronize(s), "sync");
+                int64_t sum = 0, ncap = 0;
+                for (uint64_t q = 0; q < total; ++q) {
+                    sum += nd[q];
+                    ncap += cp[q];
+                }
+                std::fprintf(stderr, "[exact]   round %d cap %lld: nodes %lld, capped tasks %lld of %llu\n", round,
+                             static_cast<long long>(et.phase_cap), static_cast<long long>(sum),
+                             static_cast<long long>(ncap), static_cast<unsigned long long>(total));
+            }
             if (last) break;
             cuda_ok(launch_exact_task_pass(3, c.tables, view, src, prm, et, total, c.sm_count, s, &c.launches),
                     "exact task pass 3");
@@ -1003,7 +1033,7 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
                     sum += nodes[q];
                     ++nv;
                 }
-            std::fprintf(stderr, "[exact] tasks %llu visited %lld, phase-A nodes sum %lld max %lld\n",
+            std::fprintf(stderr, "[exact] tasks %llu visited %lld, phase-A nodes sum (final tasks) %lld max %lld\n",
                          static_cast<unsigned long long>(total), static_cast<long long>(nv),
                          static_cast<long long>(sum), static_cast<long long>(mx));
         }

@@ -350,9 +350,20 @@ __host__ __device__ constexpr size_t group_fixed_bytes() {
             (size_t)RMAX * 8 + (size_t)kUndo * 4 + sizeof(K1Carry) + (size_t)RMAX * 2 + RMAX + 15) &
            ~size_t(15);
 }
-template <int RMAX, int KPL>
+// Warp-wide groups (G = 32, the large configs) size the assignment x as
+// [kMaxJ][RMAX] whatever J is, so a group's scratch — hence every group and
+// the shape rows after them — sits at a compile-time offset in shared memory.
+// Narrow groups (small plans) keep x at [J][RMAX] and the rows first: there
+// the shared-memory footprint, i.e. occupancy, matters more.
+template <int G>
+__host__ __device__ constexpr bool fixed_layout() {
+    return G == 32;
+}
+template <int G, int KPL>
 __host__ __device__ constexpr size_t group_scratch_bytes(int J) {
-    return group_fixed_bytes<RMAX, KPL>() + (((size_t)J * RMAX * 4 + 15) & ~size_t(15));
+    constexpr int RMAX = G * KPL;
+    return group_fixed_bytes<RMAX, KPL>() +
+           (((size_t)(fixed_layout<G>() ? kMaxJ : J) * RMAX * 4 + 15) & ~size_t(15));
 }
 
 // Group-uniform unranking of one run of `len` non-decreasing picks over
@@ -380,6 +391,18 @@ __device__ __forceinline__ void unrank_run_group(const Grp &g, uint64_t rr, int 
     for (int p = g.gl; p < rem; p += Grp::kG) out[pos + p] = static_cast<uint8_t>(q - 1);
 }
 
+// One shape's tables in K1's shared memory (fixed class stride kMaxJ).
+struct alignas(16) ShapeRow {
+    int64_t unit[kMaxJ];
+    double inv[kMaxJ];
+    int64_t M;
+    int32_t cap[kMaxJ];
+    uint16_t pmask[kMaxJ];
+    uint8_t order[kMaxJ];
+    uint8_t rank[kMaxJ];
+    uint8_t olen, pp;
+};
+
 // K1 variants: the round (best key only; plan sources 0/1/3), the top-K
 // round (+ per-group key lists, threshold collect) and the general kernel
 // (explicit shape lists, per-plan objective / sum_pp / x / used).  The round
@@ -400,59 +423,76 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
     extern __shared__ __align__(16) unsigned char smem[];
     const int S = t.num_shapes, J = prm.J;
 
-    // ---- shape tables (SoA): staged in shared memory, or read from global
-    // (L1-cached) when they do not fit (solve_batch: one row per instance) ----
-    const int64_t *sM = t.M;
-    const int64_t *sUnit = t.unit;
-    const double *sInv = t.inv_unit;
-    const int32_t *sCap = t.cap;
-    const uint8_t *sOrder = t.order;
-    const uint8_t *sRank = t.rank;
-    const uint16_t *sPmask = t.pmask;
-    const uint8_t *sOlen = t.olen;
-    const uint8_t *sPP = t.pp;
-    size_t off = 0;
+    // ---- shape tables: staged in shared memory as one fixed-stride row per
+    // shape at the start of the dynamic shared window (every field at a
+    // compile-time offset from a compile-time base: no table pointers held
+    // in, or rematerialised into, registers), or read from the global SoA
+    // tables (L1-cached) when they do not fit (solve_batch: a row per instance)
+    // layout (fixed): GPB group scratch blocks, the CTA's best keys, the
+    // shape rows; (narrow groups) the shape rows, then the groups and keys
+    constexpr bool kFixed = fixed_layout<G>();
+    const size_t per_group = group_scratch_bytes<G, KPL>(kFixed ? kMaxJ : J);
+    const size_t rows_off = kFixed ? ((per_group * GPB + GPB * 8 + 15) & ~size_t(15)) : 0;
+    const size_t groups_off = kFixed ? 0 : static_cast<size_t>(S) * sizeof(ShapeRow);
+    const ShapeRow *rows = reinterpret_cast<const ShapeRow *>(smem + rows_off);
+    auto tUnit = [&](int sh, int j) -> int64_t {
+        if constexpr (SMEM) return rows[sh].unit[j];
+        else return t.unit[sh * J + j];
+    };
+    auto tInv = [&](int sh, int j) -> double {
+        if constexpr (SMEM) return rows[sh].inv[j];
+        else return t.inv_unit[sh * J + j];
+    };
+    auto tCap = [&](int sh, int j) -> int32_t {
+        if constexpr (SMEM) return rows[sh].cap[j];
+        else return t.cap[sh * J + j];
+    };
+    auto tOrder = [&](int sh, int p) -> int {
+        if constexpr (SMEM) return rows[sh].order[p];
+        else return t.order[sh * kMaxJ + p];
+    };
+    auto tRank = [&](int sh, int j) -> int {
+        if constexpr (SMEM) return rows[sh].rank[j];
+        else return t.rank[sh * kMaxJ + j];
+    };
+    auto tPmask = [&](int sh, int p) -> uint32_t {
+        if constexpr (SMEM) return rows[sh].pmask[p];
+        else return t.pmask[sh * kMaxJ + p];
+    };
+    auto tM = [&](int sh) -> int64_t {
+        if constexpr (SMEM) return rows[sh].M;
+        else return t.M[sh];
+    };
+    auto tOlen = [&](int sh) -> int {
+        if constexpr (SMEM) return rows[sh].olen;
+        else return t.olen[sh];
+    };
+    auto tPP = [&](int sh) -> int {
+        if constexpr (SMEM) return rows[sh].pp;
+        else return t.pp[sh];
+    };
     if constexpr (SMEM) {
-        int64_t *M_ = reinterpret_cast<int64_t *>(smem);
-        int64_t *U_ = M_ + S;
-        double *I_ = reinterpret_cast<double *>(U_ + S * J);
-        int32_t *C_ = reinterpret_cast<int32_t *>(I_ + S * J);
-        uint16_t *Q_ = reinterpret_cast<uint16_t *>(C_ + S * J);
-        uint8_t *O_ = reinterpret_cast<uint8_t *>(Q_ + S * kMaxJ);
-        uint8_t *K_ = O_ + S * kMaxJ;
-        uint8_t *L_ = K_ + S * kMaxJ;
-        uint8_t *P_ = L_ + S;
-        off = (reinterpret_cast<uintptr_t>(P_ + S) - reinterpret_cast<uintptr_t>(smem) + 15) & ~size_t(15);
-        for (int i = threadIdx.x; i < S; i += blockDim.x) {
-            M_[i] = t.M[i];
-            L_[i] = t.olen[i];
-            P_[i] = t.pp[i];
-        }
-        for (int i = threadIdx.x; i < S * J; i += blockDim.x) {
-            U_[i] = t.unit[i];
-            I_[i] = t.inv_unit[i];
-            C_[i] = t.cap[i];
-        }
+        ShapeRow *w = reinterpret_cast<ShapeRow *>(smem + rows_off);
         for (int i = threadIdx.x; i < S * kMaxJ; i += blockDim.x) {
-            O_[i] = t.order[i];
-            K_[i] = t.rank[i];
-            Q_[i] = t.pmask[i];
+            const int sh = i / kMaxJ, j = i - sh * kMaxJ;
+            const bool in = j < J;
+            w[sh].unit[j] = in ? t.unit[sh * J + j] : 0;
+            w[sh].inv[j] = in ? t.inv_unit[sh * J + j] : 0.0;
+            w[sh].cap[j] = in ? t.cap[sh * J + j] : 0;
+            w[sh].order[j] = t.order[i];
+            w[sh].rank[j] = t.rank[i];
+            w[sh].pmask[j] = t.pmask[i];
         }
-        sM = M_;
-        sRank = K_;
-        sPmask = Q_;
-        sUnit = U_;
-        sInv = I_;
-        sCap = C_;
-        sOrder = O_;
-        sOlen = L_;
-        sPP = P_;
+        for (int i = threadIdx.x; i < S; i += blockDim.x) {
+            w[i].M = t.M[i];
+            w[i].olen = t.olen[i];
+            w[i].pp = t.pp[i];
+        }
     }
 
     // ---- per-group scratch ----
     const int gib = threadIdx.x / G;
-    const size_t per_group = group_scratch_bytes<RMAX, KPL>(J);
-    unsigned char *gs = smem + off + per_group * gib;
+    unsigned char *gs = smem + groups_off + per_group * gib;
     uint64_t *tks = reinterpret_cast<uint64_t *>(gs);                   // [kTopK] top-K candidate list
     int64_t *snM = reinterpret_cast<int64_t *>(tks + kTopK);            // [KPL][G] snapshot: mrem
     uint32_t *Am = reinterpret_cast<uint32_t *>(snM + RMAX);            // [kMaxJ][KPL] direct-take masks
@@ -463,8 +503,8 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
     K1Carry *cy = reinterpret_cast<K1Carry *>(ulog + kUndo);            // carried lookups / snapshot key
     uint16_t *shpS = reinterpret_cast<uint16_t *>(cy + 1);              // [RMAX] shape per replica
     uint8_t *pick = reinterpret_cast<uint8_t *>(shpS + RMAX);           // [RMAX] candidate pick per replica
-    int32_t *xs = reinterpret_cast<int32_t *>(gs + group_fixed_bytes<RMAX, KPL>());  // [J][RMAX] assignment x
-    unsigned long long *blk_best = reinterpret_cast<unsigned long long *>(smem + off + per_group * GPB);
+    int32_t *xs = reinterpret_cast<int32_t *>(gs + group_fixed_bytes<RMAX, KPL>());  // [kMaxJ][RMAX] assignment x
+    unsigned long long *blk_best = reinterpret_cast<unsigned long long *>(smem + groups_off + per_group * GPB);
     __syncthreads();
 
     const Grp g;
@@ -716,16 +756,16 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                 }
             }
             const int s = shpS[k];
-            const int ol = sOlen[s];
+            const int ol = tOlen(s);
             const bool act = g.gl < ol;
-            const int j = act ? sOrder[s * kMaxJ + g.gl] : 0;
+            const int j = act ? tOrder(s, g.gl) : 0;
             const int32_t lamp = g.bcast(lamr, j);
-            const int64_t Ms = sM[s];
+            const int64_t Ms = tM(s);
             int64_t u = 1;
             int32_t a = 0, capj = 0;
             if (act) {
-                u = sUnit[s * J + j];
-                capj = sCap[s * J + j];
+                u = tUnit(s, j);
+                capj = tCap(s, j);
                 a = min(capj, lamp);
             }
             const uint64_t cost = static_cast<uint64_t>(a) * static_cast<uint64_t>(u);
@@ -739,7 +779,7 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
             int32_t take = 0;
             if (act) {
                 if (g.gl < pb) take = a;
-                else if (g.gl == pb) take = quot_small(Ms - static_cast<int64_t>(excl), u, sInv[s * J + j]);
+                else if (g.gl == pb) take = quot_small(Ms - static_cast<int64_t>(excl), u, tInv(s, j));
             }
             const uint64_t used_l = (g.gl == pb) ? excl + static_cast<uint64_t>(take) * static_cast<uint64_t>(u) : csum;
             const uint64_t used = ol ? g.bcast(used_l, pb < ol ? pb : ol - 1) : 0ull;
@@ -772,7 +812,7 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
             }
             // direct-take bit of (class at this position, replicas k..k+c)
             const bool abit = act && take < capj && mfin >= u;
-            const int rp = g.gl < J ? sRank[s * kMaxJ + g.gl] : 0xff;
+            const int rp = g.gl < J ? tRank(s, g.gl) : 0xff;
             const int src_p = rp < G ? rp : 0;
             const int32_t tk = g.bcast(take, src_p);
             const bool ab = g.bcast(abit ? 1 : 0, src_p) != 0;
@@ -858,7 +898,7 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
             while (el) {
                 const int j2 = __ffs(el) - 1;
                 el &= el - 1;
-                const int64_t u2 = sUnit[s * J + j2];
+                const int64_t u2 = tUnit(s, j2);
                 if (u2 > e1) {
                     e2 = e1;
                     e1 = u2;
@@ -868,16 +908,16 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                 }
             }
             const uint64_t T1 = static_cast<uint64_t>(mr) + static_cast<uint64_t>(e1 > 0 ? e1 : 0);
-            int lo = 0, hi = sOlen[s];
+            int lo = 0, hi = tOlen(s);
             while (lo < hi) {
                 const int mid = (lo + hi) >> 1;
-                if (static_cast<uint64_t>(sUnit[s * J + sOrder[s * kMaxJ + mid]]) <= T1) lo = mid + 1;
+                if (static_cast<uint64_t>(tUnit(s, tOrder(s, mid))) <= T1) lo = mid + 1;
                 else hi = mid;
             }
-            uint32_t f = lo ? (static_cast<uint32_t>(sPmask[s * kMaxJ + lo - 1]) & cand) : 0u;
+            uint32_t f = lo ? (static_cast<uint32_t>(tPmask(s, lo - 1)) & cand) : 0u;
             if (e1j >= 0 && ((f >> e1j) & 1u)) {
                 const uint64_t T2 = static_cast<uint64_t>(mr) + static_cast<uint64_t>(e2 > 0 ? e2 : 0);
-                if (static_cast<uint64_t>(sUnit[s * J + e1j]) > T2) f &= ~(1u << e1j);
+                if (static_cast<uint64_t>(tUnit(s, e1j)) > T2) f &= ~(1u << e1j);
             }
             return f;
         };
@@ -903,34 +943,32 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                 const uint32_t b = g.ballot((F[kk] >> jf) & 1u);
                 if (b) kf = __ffs(b) - 1 + G * kk;
             }
-            // owner of kf picks the move
-            const int ogl = kf & (G - 1);
+            // the move at (jf, kf): direct when mrem >= unit, else the first
+            // held class j2 asc of kf (j2 != jf, mrem + unit[j2] >= unit[jf])
+            // whose A set minus kf is non-empty, and its first replica k2 —
+            // class-parallel (lane = j2), kf's state broadcast by its owner
+            const int ogl = kf & (G - 1), okk = kf / G;
+            const int64_t mr_f = g.bcast(rsel(mrem, okk), ogl);
+            const uint32_t hb_f = g.bcast(rsel(held, okk), ogl) & 0xffffu & ~(1u << jf);
+            const int s_f = shpS[kf];
+            const int64_t u_f = tUnit(s_f, jf);
             int j2 = -1, k2 = -1;
-            if (g.gl == ogl) {
-                const int kk = kf / G;
-                const int s = rsel(shp, kk);
-                const int64_t mr = rsel(mrem, kk);
-                const int64_t u = sUnit[s * J + jf];
-                if (mr < u) {
-                    uint32_t hb = rsel(held, kk) & 0xffffu & ~(1u << jf);
-                    while (hb && j2 < 0) {
-                        const int jj = __ffs(hb) - 1;
-                        hb &= hb - 1;
-                        if (mr + sUnit[s * J + jj] < u) continue;
+            if (mr_f < u_f && hb_f) {
+                int kc = -1;
+                if (((hb_f >> g.gl) & 1u) && mr_f + tUnit(s_f, g.gl) >= u_f) {
 #pragma unroll
-                        for (int k3 = 0; k3 < KPL; ++k3) {
-                            uint32_t w = Am[jj * KPL + k3];
-                            if (k3 == kk) w &= ~(1u << g.gl);
-                            if (w && k2 < 0) {
-                                k2 = __ffs(w) - 1 + G * k3;
-                                j2 = jj;
-                            }
-                        }
+                    for (int k3 = KPL - 1; k3 >= 0; --k3) {
+                        uint32_t w = Am[g.gl * KPL + k3];
+                        if (k3 == okk) w &= ~(1u << ogl);
+                        if (w) kc = __ffs(w) - 1 + G * k3;
                     }
                 }
+                const uint32_t cb = g.ballot(kc >= 0);
+                if (cb) {
+                    j2 = __ffs(cb) - 1;
+                    k2 = g.bcast(kc, j2);
+                }
             }
-            j2 = g.bcast(j2, ogl);
-            k2 = g.bcast(k2, ogl);
             // apply the move (logged while a snapshot is live)
             const bool lg = nlog >= 0 && nlog + 3 <= kUndo;
 #pragma unroll
@@ -940,12 +978,12 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                 if (k == kf) {
                     const int32_t xv = xs[jf * RMAX + kf] + 1;
                     xs[jf * RMAX + kf] = xv;
-                    mrem[kk] -= sUnit[s * J + jf];
-                    held[kk] |= (1u << jf) | (xv >= sCap[s * J + jf] ? 1u << (jf + 16) : 0u);
+                    mrem[kk] -= tUnit(s, jf);
+                    held[kk] |= (1u << jf) | (xv >= tCap(s, jf) ? 1u << (jf + 16) : 0u);
                     if (j2 >= 0) {
                         const int32_t nv = xs[j2 * RMAX + kf] - 1;
                         xs[j2 * RMAX + kf] = nv;
-                        mrem[kk] += sUnit[s * J + j2];
+                        mrem[kk] += tUnit(s, j2);
                         held[kk] &= ~(1u << (j2 + 16));  // now below cap
                         if (nv == 0) held[kk] &= ~(1u << j2);
                     }
@@ -958,8 +996,8 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                 if (j2 >= 0 && k == k2) {
                     const int32_t xv = xs[j2 * RMAX + k2] + 1;
                     xs[j2 * RMAX + k2] = xv;
-                    mrem[kk] -= sUnit[s * J + j2];
-                    held[kk] |= (1u << j2) | (xv >= sCap[s * J + j2] ? 1u << (j2 + 16) : 0u);
+                    mrem[kk] -= tUnit(s, j2);
+                    held[kk] |= (1u << j2) | (xv >= tCap(s, j2) ? 1u << (j2 + 16) : 0u);
                     if (lg) ulog[nlog + 2] = (static_cast<uint32_t>(j2 * RMAX + k2) << 1) | 1u;
                 }
             }
@@ -1002,8 +1040,8 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                 bool p = false;
                 if (j < J) {
                     const int sr = shpS[r];
-                    const int64_t u = sUnit[sr * J + j];
-                    p = u > 0 && xs[j * RMAX + r] < sCap[sr * J + j] && mr >= u;
+                    const int64_t u = tUnit(sr, j);
+                    p = u > 0 && xs[j * RMAX + r] < tCap(sr, j) && mr >= u;
                 }
                 const bool p_hi = __shfl_down_sync(0xffffffffu, p, 16) != 0;
                 if (h == 0 && j < J) {
@@ -1022,8 +1060,8 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                     if (g.gl < J) {
                         const int j = g.gl;
                         const int sr = shpS[r];
-                        const int64_t u = sUnit[sr * J + j];
-                        a_apply(j, r, u > 0 && xs[j * RMAX + r] < sCap[sr * J + j] && mr >= u);
+                        const int64_t u = tUnit(sr, j);
+                        a_apply(j, r, u > 0 && xs[j * RMAX + r] < tCap(sr, j) && mr >= u);
                     }
                 }
             }
@@ -1111,20 +1149,20 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                     if (j < J && ((hr >> j) & 1u))
                         el = ((M2 >> j) & 1u) || (((M1 >> j) & 1u) && !((Am[j * KPL + kk] >> rgl) & 1u));
                     const uint32_t Eb = __ballot_sync(0xffffffffu, el);
-                    const uint32_t rk1 = el ? static_cast<uint32_t>(sRank[sr * kMaxJ + j]) + 1u : 0u;
+                    const uint32_t rk1 = el ? static_cast<uint32_t>(tRank(sr, j)) + 1u : 0u;
                     const uint32_t t1 = __reduce_max_sync(hm, rk1);
                     const uint32_t t2 = __reduce_max_sync(hm, rk1 == t1 ? 0u : rk1);
                     int64_t e1 = -1, e2 = -1;
                     int e1j = -1;
                     if (t1) {
-                        e1j = sOrder[sr * kMaxJ + t1 - 1];
-                        e1 = sUnit[sr * J + e1j];
+                        e1j = tOrder(sr, t1 - 1);
+                        e1 = tUnit(sr, e1j);
                     }
-                    if (t2) e2 = sUnit[sr * J + sOrder[sr * kMaxJ + t2 - 1]];
+                    if (t2) e2 = tUnit(sr, tOrder(sr, t2 - 1));
                     bool f = false;  // x < cap: not full; u > 0: in the shape's order
                     if (j < J && ((lam_mask >> j) & 1u) && !((hr >> (16 + j)) & 1u) &&
-                        sRank[sr * kMaxJ + j] != 0xff) {
-                        const int64_t u = sUnit[sr * J + j];
+                        tRank(sr, j) != 0xff) {
+                        const int64_t u = tUnit(sr, j);
                         f = mr >= u || (e1j == j ? e2 : e1) >= u - mr;
                     }
                     const uint32_t Fb = __ballot_sync(0xffffffffu, f);
@@ -1154,20 +1192,20 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                         el = ((M2 >> j) & 1u) || (((M1 >> j) & 1u) && !((Am[j * KPL + kk] >> rgl) & 1u));
                     const uint32_t Er = g.ballot(el);
                     // top-2 eligible unit: order positions ascend with unit
-                    const uint32_t rk1 = el ? static_cast<uint32_t>(sRank[sr * kMaxJ + j]) + 1u : 0u;
+                    const uint32_t rk1 = el ? static_cast<uint32_t>(tRank(sr, j)) + 1u : 0u;
                     const uint32_t t1 = __reduce_max_sync(g.mask, rk1);
                     const uint32_t t2 = __reduce_max_sync(g.mask, rk1 == t1 ? 0u : rk1);
                     int64_t e1 = -1, e2 = -1;
                     int e1j = -1;
                     if (t1) {
-                        e1j = sOrder[sr * kMaxJ + t1 - 1];
-                        e1 = sUnit[sr * J + e1j];
+                        e1j = tOrder(sr, t1 - 1);
+                        e1 = tUnit(sr, e1j);
                     }
-                    if (t2) e2 = sUnit[sr * J + sOrder[sr * kMaxJ + t2 - 1]];
+                    if (t2) e2 = tUnit(sr, tOrder(sr, t2 - 1));
                     bool f = false;
                     if (j < J && ((lam_mask >> j) & 1u)) {
-                        const int64_t u = sUnit[sr * J + j];
-                        if (u > 0 && xs[j * RMAX + r] < sCap[sr * J + j])
+                        const int64_t u = tUnit(sr, j);
+                        if (u > 0 && xs[j * RMAX + r] < tCap(sr, j))
                             f = mr >= u || (e1j == j ? e2 : e1) >= u - mr;
                     }
                     const uint32_t Fr = g.ballot(f);
@@ -1184,7 +1222,7 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
         uint32_t spp = 0;
 #pragma unroll
         for (int kk = 0; kk < KPL; ++kk)
-            if (g.gl + G * kk < R) spp += sPP[shp[kk]];
+            if (g.gl + G * kk < R) spp += tPP(shp[kk]);
         served = g.sum(served);
         spp = g.sum(spp);
         if (kGeneral && out.objective && g.gl == 0) out.objective[i] = served;
@@ -1196,7 +1234,7 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                 if (k < R) {
                     for (int j = 0; j < J; ++j)
                         out.x[(i * out.rmax + k) * J + j] = xs[j * RMAX + k];
-                    if (out.used) out.used[i * out.rmax + k] = sM[shp[kk]] - mrem[kk];
+                    if (out.used) out.used[i * out.rmax + k] = tM(shp[kk]) - mrem[kk];
                 }
             }
         }
@@ -1277,11 +1315,9 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
 
 template <int G, int KPL>
 size_t plan_eval_smem(int S, int J, bool stage) {
-    constexpr int RMAX = G * KPL;
     constexpr int GPB = 256 / G;
-    size_t shapes = (size_t)S * 8 + (size_t)S * J * 16 + (size_t)S * J * 4 + 4 * (size_t)S * kMaxJ + 2 * (size_t)S;
-    shapes = stage ? (shapes + 15) & ~size_t(15) : 0;
-    return shapes + group_scratch_bytes<RMAX, KPL>(J) * GPB + GPB * 8;
+    const size_t shapes = stage ? (size_t)S * sizeof(ShapeRow) : 0;
+    return ((group_scratch_bytes<G, KPL>(J) * GPB + GPB * 8 + 15) & ~size_t(15)) + shapes;
 }
 
 // Launch geometry of K1 (also used to size the top-K lists).
@@ -1306,10 +1342,23 @@ int plan_eval_geometry(const ShapeTables &t, int J, int sm_count, uint64_t count
         if (it != occ.end()) {
             per_sm = it->second;
         } else {
-            if (smem > 48 * 1024) {
-                cudaError_t e =
-                    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            // the dynamic shared-memory limit only ever rises, once per
+            // (device, kernel), to the device's opt-in maximum: a lowered
+            // limit would invalidate launches cached at larger sizes
+            static std::map<std::pair<int, const void *>, bool> raised;
+            const auto rk = std::make_pair(dev, reinterpret_cast<const void *>(kern));
+            if (smem > 48 * 1024 && !raised[rk]) {
+                int optin = 0;
+                cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
                 if (e != cudaSuccess) return static_cast<int>(e);
+                e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+                if (e != cudaSuccess) return static_cast<int>(e);
+                raised[rk] = true;
+            }
+            if (smem > 48 * 1024) {
+                int optin = 0;
+                cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+                if (smem > static_cast<size_t>(optin)) return static_cast<int>(cudaErrorInvalidValue);
             }
             cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
             if (e != cudaSuccess) return static_cast<int>(e);
