@@ -235,8 +235,10 @@ struct Space {
 // Per-task arrays of the frontier-parallel exact path (double-buffered for
 // the splitting rounds; kept in the context so repeated rounds reuse them).
 struct TaskBufs {
-    DBuf plan, td, path, g, lb, m, inc, vis, nodes, cap, done, nch;
+    DBuf plan, td, path, g, lb, m, inc, vis, nodes, cap, done, nch, al, am;
     void bind(ExactTasks &e, uint64_t n) {
+        e.aL = static_cast<int32_t *>(al.get(sizeof(int32_t) * n));
+        e.amask = static_cast<uint32_t *>(am.get(sizeof(uint32_t) * n));
         e.plan = static_cast<uint32_t *>(plan.get(sizeof(uint32_t) * n));
         e.tdepth = static_cast<uint8_t *>(td.get(n));
         e.path = static_cast<int32_t *>(path.get(sizeof(int32_t) * n * kTaskDepthMax));
@@ -248,12 +250,12 @@ struct TaskBufs {
         e.nodes = static_cast<int64_t *>(nodes.get(sizeof(int64_t) * n));
         e.capped = static_cast<uint8_t *>(cap.get(n));
         e.done = static_cast<uint8_t *>(done.get(n));
-        e.nchild = static_cast<uint32_t *>(nch.get(sizeof(uint32_t) * n));
+        e.nchild = static_cast<uint32_t *>(nch.get(sizeof(uint32_t) * (n + 1)));  // + the scan's trailing 0
     }
 };
 
 struct ExactScratch {
-    DBuf depth, nt, off, top, opt, ist, state, bx, run, ranks, newoff;
+    DBuf depth, nt, off, top, opt, ist, state, bx, run, ranks, newoff, fetch, topn, ubn, anycap, scan, grow, psum;
     TaskBufs bufs[2];
 };
 
@@ -895,6 +897,10 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
     et.state = static_cast<uint8_t *>(xs.state.get(P));
     et.bx = static_cast<int32_t *>(xs.bx.get(sizeof(int32_t) * P * kMaxExactCells));
     et.running = static_cast<unsigned long long *>(xs.run.get(sizeof(unsigned long long) * P));
+    et.fetch = static_cast<unsigned long long *>(xs.fetch.get(sizeof(unsigned long long)));
+    et.topn = static_cast<unsigned long long *>(xs.topn.get(sizeof(unsigned long long) * P));
+    et.ubn = static_cast<unsigned long long *>(xs.ubn.get(sizeof(unsigned long long) * P));
+    et.anycap = static_cast<uint8_t *>(xs.anycap.get(P));
     // ~2^21 tasks in flight at most; at least a few thousand per plan when few plans
     const uint64_t budget_tasks = uint64_t{1} << 21;
     static const uint64_t target_env = [] {
@@ -903,41 +909,139 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
     }();
     et.target = target_env ? target_env : std::max<uint64_t>(64, std::min<uint64_t>(4096, budget_tasks / P));
     et.max_tasks = et.target * 8;
-    cuda_ok(launch_exact_plan_pass(0, c.tables, view, key, src, eo, prm, et, c.sm_count, s, &c.launches),
-            "exact plan pass 0");
-    std::vector<uint64_t> nt;
-    std::vector<uint8_t> state;
-    download(nt, et.ntask, P, s);
-    download(state, et.state, P, s);
-    cuda_ok(cudaStreamSynchronize(s), "sync");
-    std::vector<uint64_t> off(P);
-    uint64_t total = 0;
-    for (uint64_t i = 0; i < P; ++i) {
-        if (state[i] == 1 && total + nt[i] > 4 * budget_tasks) state[i] = 2;  // task buffers full
-        off[i] = total;
-        if (state[i] == 1) total += nt[i];
-    }
-    cuda_ok(h2d(et.toff, off.data(), sizeof(uint64_t) * P, s), "H2D");
-    cuda_ok(h2d(et.state, state.data(), P, s), "H2D");
+    static const bool bfs = [] {
+        const char *e = getenv("OSERVE_EXACT_BFS");
+        return !e || atoi(e) != 0;
+    }();
+    static const bool dbg = getenv("OSERVE_DEBUG_EXACT") != nullptr;
     TaskBufs *bufs = c.exact.bufs;
     int cur = 0;
+    uint64_t total = 0;
+    std::vector<uint8_t> state;
+    auto lap = [&](const char *what) {
+        if (!dbg) return;
+        static auto t0 = std::chrono::steady_clock::now();
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+        const auto t1 = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[exact] %-14s %8.1f ms  (plans %llu, tasks %llu)\n", what,
+                     std::chrono::duration<double, std::milli>(t1 - t0).count(), static_cast<unsigned long long>(P),
+                     static_cast<unsigned long long>(total));
+        t0 = t1;
+    };
+    uint32_t *d_newoff = nullptr;
+    // Rebuild the task list from et.nchild (children of split tasks in
+    // preorder, others copied): device scan, split, per-plan ranges.  False
+    // when nothing was split.
+    auto rebuild = [&]() -> bool {
+        cuda_ok(cudaMemsetAsync(et.nchild + total, 0, sizeof(uint32_t), s), "memset");
+        d_newoff = static_cast<uint32_t *>(xs.newoff.get(sizeof(uint32_t) * (total + 1)));
+        cuda_ok(launch_exact_rescan(et, total, d_newoff, P, &c.cub_temp, &c.cub_temp_bytes, s, &c.launches),
+                "exact rescan");
+        uint32_t ntot32 = 0;
+        cuda_ok(d2h(&ntot32, d_newoff + total, sizeof(uint32_t), s), "D2H");
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+        const uint64_t ntot = ntot32;
+        if (ntot == total) return false;
+        ExactTasks ne = et;
+        bufs[cur ^ 1].bind(ne, ntot);
+        cuda_ok(launch_exact_split(c.tables, view, src, prm, et, ne, d_newoff, total, c.sm_count, s, &c.launches),
+                "exact split");
+        cuda_ok(launch_exact_ranges(et, d_newoff, P, s, &c.launches), "exact ranges");
+        et = ne;
+        cur ^= 1;
+        total = ntot;
+        return true;
+    };
+    if (bfs) {
+        // Frontier built on the device: one root task per exact-path plan,
+        // then level by level every task of a plan still below the target
+        // count becomes the branches of its root's first decision (preorder
+        // kept), unless that would pass the plan's task cap.
+        cuda_ok(launch_exact_plan_pass(10, c.tables, view, key, src, eo, prm, et, c.sm_count, s, &c.launches),
+                "exact plan pass 10");
+        download(state, et.state, P, s);
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+        std::vector<uint64_t> off(P, 0);
+        std::vector<uint32_t> plan_h;
+        for (uint64_t i = 0; i < P; ++i) {
+            off[i] = plan_h.size();
+            if (state[i] == 1) plan_h.push_back(static_cast<uint32_t>(i));
+        }
+        total = plan_h.size();
+        if (total) {
+            bufs[cur].bind(et, total);
+            cuda_ok(h2d(et.toff, off.data(), sizeof(uint64_t) * P, s), "H2D");
+            cuda_ok(h2d(et.plan, plan_h.data(), sizeof(uint32_t) * total, s), "H2D");
+            cuda_ok(cudaMemsetAsync(et.tdepth, 0, total, s), "memset");
+            cuda_ok(cudaMemsetAsync(et.done, 0, total, s), "memset");
+            cuda_ok(cudaMemsetAsync(et.capped, 0, total, s), "memset");
+            et.grow = static_cast<uint8_t *>(xs.grow.get(P));
+            et.plan_sum = static_cast<uint32_t *>(xs.psum.get(sizeof(uint32_t) * P));
+            std::vector<uint64_t> n_h(P, 0);
+            for (uint64_t i = 0; i < P; ++i) n_h[i] = state[i] == 1 ? 1 : 0;
+            std::vector<uint8_t> grow(P, 0);
+            std::vector<uint32_t> psum;
+            for (int level = 1; level <= 6; ++level) {
+                bool any = false;
+                for (uint64_t i = 0; i < P; ++i) {
+                    grow[i] = state[i] == 1 && n_h[i] < et.target;
+                    any = any || grow[i];
+                }
+                if (!any) break;
+                auto children = [&]() {
+                    cuda_ok(h2d(et.grow, grow.data(), P, s), "H2D");
+                    cuda_ok(cudaMemsetAsync(et.plan_sum, 0, sizeof(uint32_t) * P, s), "memset");
+                    cuda_ok(launch_exact_task_pass(9, c.tables, view, src, prm, et, total, c.sm_count, s,
+                                                   &c.launches),
+                            "exact task pass 9");
+                };
+                children();
+                download(psum, et.plan_sum, P, s);
+                cuda_ok(cudaStreamSynchronize(s), "sync");
+                bool redo = false;
+                uint64_t tot_new = 0;
+                for (uint64_t i = 0; i < P; ++i) {
+                    if (grow[i] && psum[i] > et.max_tasks) {  // keep this plan at the previous level
+                        grow[i] = 0;
+                        redo = true;
+                    }
+                    tot_new += grow[i] ? psum[i] : n_h[i];
+                }
+                if (tot_new > 4 * budget_tasks) {  // task buffers full: stop growing
+                    std::fill(grow.begin(), grow.end(), 0);
+                    redo = true;
+                }
+                if (redo) children();
+                for (uint64_t i = 0; i < P; ++i)
+                    if (grow[i]) n_h[i] = psum[i];
+                if (!rebuild()) break;
+            }
+        }
+        lap("frontier");
+    } else {
+        cuda_ok(launch_exact_plan_pass(0, c.tables, view, key, src, eo, prm, et, c.sm_count, s, &c.launches),
+                "exact plan pass 0");
+        std::vector<uint64_t> nt;
+        download(nt, et.ntask, P, s);
+        download(state, et.state, P, s);
+        cuda_ok(cudaStreamSynchronize(s), "sync");
+        std::vector<uint64_t> off(P);
+        for (uint64_t i = 0; i < P; ++i) {
+            if (state[i] == 1 && total + nt[i] > 4 * budget_tasks) state[i] = 2;  // task buffers full
+            off[i] = total;
+            if (state[i] == 1) total += nt[i];
+        }
+        cuda_ok(h2d(et.toff, off.data(), sizeof(uint64_t) * P, s), "H2D");
+        cuda_ok(h2d(et.state, state.data(), P, s), "H2D");
+        if (total) {
+            bufs[cur].bind(et, total);
+            lap("pass0");
+            cuda_ok(launch_exact_plan_pass(1, c.tables, view, key, src, eo, prm, et, c.sm_count, s, &c.launches),
+                    "exact plan pass 1");
+            lap("emit");
+        }
+    }
     if (total) {
-        bufs[cur].bind(et, total);
-        static const bool dbg = getenv("OSERVE_DEBUG_EXACT") != nullptr;
-        auto lap = [&](const char *what) {
-            if (!dbg) return;
-            static auto t0 = std::chrono::steady_clock::now();
-            cuda_ok(cudaStreamSynchronize(s), "sync");
-            const auto t1 = std::chrono::steady_clock::now();
-            std::fprintf(stderr, "[exact] %-14s %8.1f ms  (plans %llu, tasks %llu)\n", what,
-                         std::chrono::duration<double, std::milli>(t1 - t0).count(),
-                         static_cast<unsigned long long>(P), static_cast<unsigned long long>(total));
-            t0 = t1;
-        };
-        lap("pass0");
-        cuda_ok(launch_exact_plan_pass(1, c.tables, view, key, src, eo, prm, et, c.sm_count, s, &c.launches),
-                "exact plan pass 1");
-        lap("emit");
         // Phase A in rounds: tasks over the round's node cap are split into
         // their children (preorder kept) and rerun; the last round runs with
         // the full budget.
@@ -986,33 +1090,28 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
             if (last) break;
             cuda_ok(launch_exact_task_pass(3, c.tables, view, src, prm, et, total, c.sm_count, s, &c.launches),
                     "exact task pass 3");
-            std::vector<uint32_t> nch;
-            download(nch, et.nchild, total, s);
-            cuda_ok(cudaStreamSynchronize(s), "sync");
-            std::vector<uint64_t> newoff(total + 1, 0);
-            for (uint64_t q = 0; q < total; ++q) newoff[q + 1] = newoff[q] + nch[q];
-            if (newoff[total] == total) break;  // nothing capped: phase A complete
-            const uint64_t ntot = newoff[total];
-            ExactTasks ne = et;
-            bufs[cur ^ 1].bind(ne, ntot);
-            uint64_t *d_newoff = xs.newoff.upload(newoff, s);
-            cuda_ok(launch_exact_split(c.tables, view, src, prm, et, ne, d_newoff, total, c.sm_count, s, &c.launches),
-                    "exact split");
-            for (uint64_t i = 0; i < P; ++i) {  // per-plan ranges in the new list
-                if (state[i] != 1) continue;
-                const uint64_t a0 = newoff[off[i]], a1 = newoff[off[i] + nt[i]];
-                off[i] = a0;
-                nt[i] = a1 - a0;
-            }
-            cuda_ok(h2d(et.toff, off.data(), sizeof(uint64_t) * P, s), "H2D");
-            cuda_ok(h2d(et.ntask, nt.data(), sizeof(uint64_t) * P, s), "H2D");
-            cuda_ok(cudaStreamSynchronize(s), "sync");
-            et = ne;
-            cur ^= 1;
-            total = ntot;
+            if (!rebuild()) break;  // nothing capped: phase A complete
         }
-        cuda_ok(launch_exact_plan_pass(2, c.tables, view, key, src, eo, prm, et, c.sm_count, s, &c.launches),
-                "exact plan pass 2");
+        static const bool par_replay = [] {
+            const char *e = getenv("OSERVE_EXACT_REPLAY");
+            return !e || atoi(e) != 0;
+        }();
+        if (par_replay) {  // parallel replay of the top (see exact_replay_task)
+            cuda_ok(launch_exact_plan_pass(6, c.tables, view, key, src, eo, prm, et, c.sm_count, s, &c.launches),
+                    "exact plan pass 6");
+            cuda_ok(launch_exact_task_pass(6, c.tables, view, src, prm, et, total, c.sm_count, s, &c.launches),
+                    "exact task pass 6");
+            uint64_t *tmp = static_cast<uint64_t *>(xs.scan.get(sizeof(uint64_t) * 2 * total));
+            cuda_ok(launch_alive_scan(et, total, tmp, &c.cub_temp, &c.cub_temp_bytes, c.sm_count, s, &c.launches),
+                    "alive scan");
+            cuda_ok(launch_exact_task_pass(7, c.tables, view, src, prm, et, total, c.sm_count, s, &c.launches),
+                    "exact task pass 7");
+            cuda_ok(launch_exact_plan_pass(8, c.tables, view, key, src, eo, prm, et, c.sm_count, s, &c.launches),
+                    "exact plan pass 8");
+        } else {
+            cuda_ok(launch_exact_plan_pass(2, c.tables, view, key, src, eo, prm, et, c.sm_count, s, &c.launches),
+                    "exact plan pass 2");
+        }
         lap("top replay");
         cuda_ok(launch_exact_task_pass(1, c.tables, view, src, prm, et, total, c.sm_count, s, &c.launches),
                 "exact task pass 1");
@@ -1033,6 +1132,32 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
                     sum += nodes[q];
                     ++nv;
                 }
+            {  // per plan: phase-A nodes of all its tasks, final state, top nodes
+                std::vector<uint64_t> toff, ntk;
+                std::vector<uint8_t> st2;
+                std::vector<int64_t> topn;
+                std::vector<unsigned long long> run;
+                download(toff, et.toff, P, s);
+                download(ntk, et.ntask, P, s);
+                download(st2, et.state, P, s);
+                download(topn, et.top_nodes, P, s);
+                download(run, et.running, P, s);
+                cuda_ok(cudaStreamSynchronize(s), "sync");
+                for (uint64_t i = 0; i < P; ++i) {
+                    if (st2[i] == 0) continue;
+                    int64_t a = 0, v = 0;
+                    for (uint64_t q = toff[i]; q < toff[i] + ntk[i] && q < total; ++q) {
+                        a += nodes[q];
+                        if (vis[q]) v += nodes[q];
+                    }
+                    if (a > 1000000)
+                        std::fprintf(stderr, "[exact]   plan %llu state %d tasks %llu phase-A nodes %lld (visited %lld) "
+                                     "top %lld running %llu\n",
+                                     static_cast<unsigned long long>(i), st2[i], static_cast<unsigned long long>(ntk[i]),
+                                     static_cast<long long>(a), static_cast<long long>(v), static_cast<long long>(topn[i]),
+                                     static_cast<unsigned long long>(run[i]));
+                }
+            }
             std::fprintf(stderr, "[exact] tasks %llu visited %lld, phase-A nodes sum (final tasks) %lld max %lld\n",
                          static_cast<unsigned long long>(total), static_cast<long long>(nv),
                          static_cast<long long>(sum), static_cast<long long>(mx));

@@ -148,7 +148,26 @@ struct ExactTasks {
     uint32_t *nchild;     // tasks this one becomes in the next round
     uint64_t target;      // desired tasks per plan
     uint64_t max_tasks;   // cap per plan
+    unsigned long long *fetch;  // task counter of the thread-per-task passes
+    // parallel top replay: per task the shared-prefix length and own / ancestor
+    // alive bits; per plan the top-node count, phase-A upper bound, capped flag
+    int32_t *aL;
+    uint32_t *amask;
+    unsigned long long *topn, *ubn;
+    uint8_t *anycap;
+    // device-built frontier: per plan, grow this level / children summed
+    uint8_t *grow;
+    uint32_t *plan_sum;
 };
+// Exclusive scan of the tasks' child counts (nchild[n] = 0) and the per-plan
+// ranges of the list it describes.
+int launch_exact_rescan(const ExactTasks &et, uint64_t n, uint32_t *newoff, uint64_t plans, void **temp,
+                        size_t *temp_bytes, void *stream, uint64_t *launches);
+int launch_exact_ranges(const ExactTasks &et, const uint32_t *newoff, uint64_t plans, void *stream,
+                        uint64_t *launches);
+// Ancestor-alive masks of the replay (inclusive scan over the tasks).
+int launch_alive_scan(const ExactTasks &et, uint64_t total, uint64_t *tmp, void **temp, size_t *temp_bytes,
+                      int sm_count, void *stream, uint64_t *launches);
 
 struct SolveParams {
     int J;
@@ -192,7 +211,7 @@ int launch_exact_task_pass(int pass, const ShapeTables &t, const SpaceTables &sp
 // Split capped tasks into their children: `nt` receives the new list at the
 // exclusive-scan offsets `newoff` of et.nchild.
 int launch_exact_split(const ShapeTables &t, const SpaceTables &sp, const PlanSource &src, const SolveParams &prm,
-                       const ExactTasks &et, const ExactTasks &nt, const uint64_t *newoff, uint64_t total_tasks,
+                       const ExactTasks &et, const ExactTasks &nt, const uint32_t *newoff, uint64_t total_tasks,
                        int sm_count, void *stream, uint64_t *launches);
 
 // Switching cost (K2).

@@ -30,6 +30,7 @@
 #include "oserve_internal.h"
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #define OSERVE_MAX_REPLICAS_DEV 128
 
@@ -433,7 +434,7 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
     constexpr bool kFixed = fixed_layout<G>();
     const size_t per_group = group_scratch_bytes<G, KPL>(kFixed ? kMaxJ : J);
     const size_t rows_off = kFixed ? ((per_group * GPB + GPB * 8 + 15) & ~size_t(15)) : 0;
-    const size_t groups_off = kFixed ? 0 : static_cast<size_t>(S) * sizeof(ShapeRow);
+    const size_t groups_off = (kFixed || !SMEM) ? 0 : static_cast<size_t>(S) * sizeof(ShapeRow);
     const ShapeRow *rows = reinterpret_cast<const ShapeRow *>(smem + rows_off);
     auto tUnit = [&](int sh, int j) -> int64_t {
         if constexpr (SMEM) return rows[sh].unit[j];
@@ -1540,18 +1541,29 @@ __device__ __forceinline__ void exact_emit(const ShapeTables &t, const KeyLayout
 // leaves into bx.
 template <bool TRACK>
 __device__ void exact_dfs(const ShapeTables &t, ExactState &st, int k, int pos, int64_t count, int64_t &best,
-                          int64_t cap, int64_t &nodes, bool &capped, int32_t *bx) {
+                          int64_t cap, int64_t &nodes, bool &capped, int32_t *bx, unsigned long long *ctr = nullptr,
+                          int64_t ctr_limit = 0) {
     const int R = st.R, J = st.J;
     int fk[kMaxExactCells + 1], fpos[kMaxExactCells + 1], fj[kMaxExactCells + 1];
     int64_t fv[kMaxExactCells + 1];
     int depth = 0;
     bool calling = true;
     capped = false;
+    int64_t flushed = 0;
     while (true) {
         if (calling) {
             if (++nodes > cap) {
                 capped = true;
-                return;
+                break;
+            }
+            if (ctr && (nodes & 255) == 0) {  // shared node total (phase B): stop once it passes the limit
+                const unsigned long long tot =
+                    atomicAdd(ctr, static_cast<unsigned long long>(nodes - flushed)) + (nodes - flushed);
+                flushed = nodes;
+                if (tot > static_cast<unsigned long long>(ctr_limit)) {
+                    capped = true;
+                    break;
+                }
             }
             if (k == R) {
                 if (count > best) {
@@ -1594,7 +1606,7 @@ __device__ void exact_dfs(const ShapeTables &t, ExactState &st, int k, int pos, 
             continue;  // call dfs(k, pos+1)
         }
         // return into the frame on top of the stack
-        if (depth == 0) return;
+        if (depth == 0) break;
         const int d = depth - 1;
         const int kk = fk[d], j = fj[d];
         const int64_t u = t.unit[st.shp[kk] * J + j];
@@ -1617,6 +1629,7 @@ __device__ void exact_dfs(const ShapeTables &t, ExactState &st, int k, int pos, 
         pos = fpos[d] + 1;
         calling = true;
     }
+    if (ctr && nodes != flushed) atomicAdd(ctr, static_cast<unsigned long long>(nodes - flushed));
 }
 
 // Warp-cooperative exact_dfs: all 32 lanes carry the identical DFS state and
@@ -1851,9 +1864,15 @@ __device__ uint64_t exact_top(const ShapeTables &t, ExactState &st, int cut, uin
                 } else if (MODE == 1) {
                     const uint64_t q = base + ti;
                     et.plan[q] = plan;
-                    et.tdepth[q] = static_cast<uint8_t>(depth | (k == R && depth < cut ? 0x80 : 0));
+                    // a task's root is always the node right after its depth-th
+                    // decision — also when the walk reached k == R above the cut:
+                    // the pass-through calls down to that leaf are the task's
+                    // (the reference's dfs(k + 1, 0) calls count as nodes), not
+                    // skipped by a leaf flag
+                    et.tdepth[q] = static_cast<uint8_t>(depth);
                     for (int a = 0; a < depth; ++a) et.path[q * kTaskDepthMax + a] = static_cast<int32_t>(fv[a]);
                     et.done[q] = 0;
+                    et.capped[q] = 0;  // (pass 4 reads m of tasks that ran: done or capped)
                     ++ti;
                 } else {
                     const uint64_t q = base + ti;
@@ -1933,6 +1952,84 @@ __device__ uint64_t exact_top(const ShapeTables &t, ExactState &st, int cut, uin
     return ti;
 }
 
+// Parallel replay of the top of the tree (replaces the per-plan preorder
+// walk exact_top<2>).  With the exact prefix-maximum incumbents inc[q] of
+// the tasks (plan pass 6: the exclusive prefix max of m, the optimum and the
+// task holding the first optimal leaf), an internal top node is checked with
+// the incumbent of the first task below it, so it is alive iff count +
+// min(lam_total, bound) > inc[first task].  Task q enters (first) the nodes
+// at depths c+1 .. d-1 of its path (c: decisions shared with task q-1); pass
+// 6 writes their alive bits and c, a scan combines (keep the previous task's
+// bits 0..c, add the new ones) into each task's ancestor-alive mask, and pass
+// 7 marks the visited tasks (every ancestor alive), adds each visited new
+// node's calls (the node and its pass-through dfs(k+1, 0) calls) to the
+// plan's top-node count and the visited tasks' phase-A counts to its upper
+// bound.
+__device__ __forceinline__ int exact_shared_prefix(const ExactTasks &et, uint64_t q, uint64_t i, int d) {
+    if (q <= et.toff[i]) return -1;
+    const int32_t *path = et.path + q * kTaskDepthMax;
+    const int32_t *pp = et.path + (q - 1) * kTaskDepthMax;
+    const int dp = et.tdepth[q - 1] & 0x7f;
+    int c = 0;
+    while (c < d && c < dp && pp[c] == path[c]) ++c;
+    return c;
+}
+
+__device__ void exact_replay_task(int pass, const ShapeTables &t, ExactState &st, const ExactTasks &et, uint64_t q,
+                                  uint64_t i) {
+    const int R = st.R, J = st.J;
+    const int32_t *path = et.path + q * kTaskDepthMax;
+    const int d = et.tdepth[q] & 0x7f;
+    const int c = exact_shared_prefix(et, q, i, d);
+    const int64_t inc = et.inc[q];
+    const uint32_t anc = pass == 7 ? et.amask[q] : 0u;
+    uint32_t own = 0;
+    int64_t top = 0;
+    int k = 0, pos = 0;
+    int64_t count = 0;
+    for (int e = 0; e < d; ++e) {
+        int64_t calls = 1;
+        while (k < R && pos == t.olen[st.shp[k]]) {
+            ++k;
+            pos = 0;
+            ++calls;
+        }
+        if (k >= R) break;
+        if (e > c) {
+            if (pass == 6) {
+                int64_t lt = 0;
+                for (int j = 0; j < J; ++j) lt += st.lam[j];
+                int64_t bound = suffix_bound(t, st, k, pos, st.lam, st.mrem[k]);
+                for (int k2 = k + 1; k2 < R; ++k2) bound += suffix_bound(t, st, k2, 0, st.lam, t.M[st.shp[k2]]);
+                if (count + (lt < bound ? lt : bound) > inc) own |= 1u << e;
+            } else {
+                const uint32_t need = e ? ((2u << (e - 1)) - 1u) : 0u;  // ancestors 0..e-1
+                if ((anc & need) == need) top += calls;
+            }
+        }
+        const int s = st.shp[k];
+        const int j = t.order[s * kMaxJ + pos];
+        const int64_t u = t.unit[s * J + j];
+        const int64_t v = path[e];
+        st.x[k * J + j] = static_cast<int32_t>(v);
+        st.lam[j] -= v;
+        st.mrem[k] -= v * u;
+        count += v;
+        ++pos;
+    }
+    if (pass == 6) {
+        et.aL[q] = c;
+        et.amask[q] = own;
+        return;
+    }
+    const uint32_t need = d ? ((2u << (d - 1)) - 1u) : 0u;
+    const bool vis = (anc & need) == need;
+    et.vis[q] = vis ? 1 : 0;
+    if (top) atomicAdd(et.topn + i, static_cast<unsigned long long>(top));
+    if (vis) atomicAdd(et.ubn + i, static_cast<unsigned long long>(et.nodes[q]));
+    if (et.capped[q]) et.anycap[i] = 1;
+}
+
 // Per-plan passes: 0 choose the cut depth and count tasks, 1 emit tasks,
 // 2 exact replay of the top, 3 finish (abort decision or outputs).
 __global__ void __launch_bounds__(128) k_exact_plan(int pass, ShapeTables t, SpaceTables sp, KeyLayout key,
@@ -1965,19 +2062,57 @@ __global__ void __launch_bounds__(128) k_exact_plan(int pass, ShapeTables t, Spa
             et.state[i] = ok ? 1 : 2;
             continue;
         }
+        if (pass == 10) {  // device-built frontier: one root task per exact-path plan
+            et.depth[i] = ex ? 0 : -1;
+            et.ntask[i] = ex ? 1 : 0;
+            et.state[i] = ex ? 1 : 0;
+            continue;
+        }
         if (!ex || et.state[i] == 0) continue;
         if (pass == 1) {
             if (et.state[i] == 1)
                 exact_top<1>(t, st, et.depth[i], et.max_tasks, et, et.toff[i], static_cast<uint32_t>(i), tn, opt, istar);
             continue;
         }
+        if (pass == 6) {  // exact incumbents: exclusive prefix max of m; optimum; last rise
+            if (et.state[i] != 1) continue;
+            int64_t run = -1, ist = -1;
+            for (uint64_t q = et.toff[i]; q < et.toff[i] + et.ntask[i]; ++q) {
+                et.inc[q] = run;
+                if (et.m[q] > run) {
+                    run = et.m[q];
+                    ist = static_cast<int64_t>(q);
+                }
+            }
+            et.opt[i] = run;
+            et.istar[i] = ist;
+            et.topn[i] = 0;
+            et.ubn[i] = 0;
+            et.anycap[i] = 0;
+            continue;
+        }
+        if (pass == 8) {  // after the replay: certify (upper bound) or count exactly in phase B
+            if (et.state[i] != 1) continue;
+            if (et.anycap[i]) {  // phase A hit the budget somewhere: sequential DFS
+                et.state[i] = 2;
+                continue;
+            }
+            const unsigned long long tn = et.topn[i];
+            et.top_nodes[i] = static_cast<int64_t>(tn);
+            et.running[i] = tn;
+            if (tn + et.ubn[i] > static_cast<unsigned long long>(prm.node_budget)) et.state[i] = 3;
+            continue;
+        }
         if (pass == 4) {  // lb = exclusive prefix max of the tasks' dives; finished tasks: m = max(m, lb)
             if (et.state[i] != 1) continue;
+            // (a task that ran — finished or capped — holds in m a real leaf
+            // of its subtree or its own lb, both <= the incumbent after it)
             int64_t run = -1;
             for (uint64_t q = et.toff[i]; q < et.toff[i] + et.ntask[i]; ++q) {
                 et.lb[q] = run;
                 if (et.done[q] && et.m[q] < run) et.m[q] = run;
                 run = et.g[q] > run ? et.g[q] : run;
+                if ((et.done[q] || et.capped[q]) && et.m[q] > run) run = et.m[q];
             }
             continue;
         }
@@ -2028,7 +2163,11 @@ __global__ void __launch_bounds__(128) k_exact_task(int pass, ShapeTables t, Spa
     for (uint64_t q = w0; q < total; q += nw) {
         const uint64_t i = et.plan[q];
         const uint8_t ps = et.state[i];
-        if ((pass == 0 || pass == 2 || pass == 3) && ps != 1) continue;
+        if (pass == 3 && ps != 1) {  // not split (every task needs its child count for the rescan)
+            if (lane == 0) et.nchild[q] = 1;
+            continue;
+        }
+        if ((pass == 0 || pass == 2) && ps != 1) continue;
         if ((pass == 0 || pass == 2) && et.done[q]) continue;
         if (pass == 1) {
             if (ps == 1 && static_cast<int64_t>(q) != et.istar[i]) continue;  // certified: only the winner's leaf
@@ -2085,6 +2224,88 @@ __global__ void __launch_bounds__(128) k_exact_task(int pass, ShapeTables t, Spa
                                       prm.node_budget);
         }
         __syncwarp();
+    }
+}
+
+// Per-task passes 0 and 1 with a thread per task (tasks fetched one at a
+// time from a counter, so a long task does not hold up a warp's others):
+// the exact path's instances are small (R*J <= exact_cell_limit, 20 by
+// default), where a warp-cooperative bound leaves most lanes idle.
+__global__ void __launch_bounds__(128) k_exact_task_thr(int pass, ShapeTables t, SpaceTables sp, PlanSource src,
+                                                        SolveParams prm, ExactTasks et, uint64_t total,
+                                                        unsigned long long *fetch) {
+    for (;;) {
+        const uint64_t q = atomicAdd(fetch, 1ull);
+        if (q >= total) break;
+        const uint64_t i = et.plan[q];
+        const uint8_t ps = et.state[i];
+        if (pass == 0 && (ps != 1 || et.done[q])) continue;
+        if (pass == 1) {
+            if (ps == 1 && static_cast<int64_t>(q) != et.istar[i]) continue;
+            if (ps != 1 && (ps != 3 || !et.vis[q])) continue;
+        }
+        if (pass == 9 && ps != 1) {
+            et.nchild[q] = 1;
+            continue;
+        }
+        if ((pass == 6 || pass == 7) && ps != 1) continue;
+        ExactState st;
+        int64_t part;
+        uint64_t local, gr;
+        const int64_t *lam_src;
+        exact_setup(t, sp, src, prm, i, st, part, local, gr, lam_src);
+        const uint8_t td = et.tdepth[q];
+        if (pass == 6 || pass == 7) {
+            exact_replay_task(pass, t, st, et, q, i);
+            continue;
+        }
+        if (pass == 9) {  // frontier expansion: the root's first decision's branches, growing plans only
+            uint32_t nc = 1;
+            const int dq = td & 0x7f;
+            if (et.grow[i] && dq < kTaskDepthMax - 1) {
+                int k, pos;
+                int64_t count;
+                exact_restore(t, st, et.path + q * kTaskDepthMax, dq, false, k, pos, count);
+                while (k < st.R && pos == t.olen[st.shp[k]]) {
+                    ++k;
+                    pos = 0;
+                }
+                if (k < st.R) {
+                    const int s = st.shp[k];
+                    const int j = t.order[s * kMaxJ + pos];
+                    const int64_t u = t.unit[s * st.J + j];
+                    int64_t hi = t.cap[s * st.J + j];
+                    if (st.lam[j] < hi) hi = st.lam[j];
+                    if (hi * u > st.mrem[k]) hi = quot_small(st.mrem[k], u, t.inv_unit[s * st.J + j]);
+                    nc = static_cast<uint32_t>(hi + 1);
+                }
+            }
+            et.nchild[q] = nc;
+            atomicAdd(et.plan_sum + i, nc);
+            continue;
+        }
+        int k, pos;
+        int64_t count;
+        exact_restore(t, st, et.path + q * kTaskDepthMax, td & 0x7f, (td & 0x80) != 0, k, pos, count);
+        int64_t nodes = 0;
+        bool capped;
+        if (pass == 0) {
+            int64_t best = et.lb[q];
+            exact_dfs<false>(t, st, k, pos, count, best, et.phase_cap, nodes, capped, nullptr);
+            et.m[q] = best;
+            et.nodes[q] = nodes;
+            et.capped[q] = capped ? 1 : 0;
+            et.done[q] = capped ? 0 : 1;
+        } else {
+            int64_t best = et.inc[q];
+            unsigned long long *ctr = ps == 3 ? et.running + i : nullptr;
+            if (static_cast<int64_t>(q) == et.istar[i])
+                exact_dfs<true>(t, st, k, pos, count, best, prm.node_budget + 1, nodes, capped,
+                                et.bx + i * kMaxExactCells, ctr, prm.node_budget);
+            else
+                exact_dfs<false>(t, st, k, pos, count, best, prm.node_budget + 1, nodes, capped, nullptr, ctr,
+                                 prm.node_budget);
+        }
     }
 }
 
@@ -2668,7 +2889,7 @@ int launch_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayou
 
 // Thread per task: copy it to the new list, or write its children (the
 // branches v = hi .. 0 of its first decision node, in preorder).
-__global__ void __launch_bounds__(128) k_exact_split(ExactTasks et, ExactTasks nt, const uint64_t *newoff,
+__global__ void __launch_bounds__(128) k_exact_split(ExactTasks et, ExactTasks nt, const uint32_t *newoff,
                                                      uint64_t total) {
     for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
          q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -2697,8 +2918,47 @@ __global__ void __launch_bounds__(128) k_exact_split(ExactTasks et, ExactTasks n
     }
 }
 
+__global__ void k_exact_ranges(ExactTasks et, const uint32_t *newoff, uint64_t plans) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < plans;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        if (et.state[i] != 1) continue;  // only frontier plans hold tasks
+        const uint64_t a = newoff[et.toff[i]], b = newoff[et.toff[i] + et.ntask[i]];
+        et.toff[i] = a;
+        et.ntask[i] = b - a;
+    }
+}
+
+// newoff[0..n] = exclusive prefix sum of nchild[0..n) (nchild[n] must be 0),
+// then the per-plan task ranges of the new list.
+int launch_exact_rescan(const ExactTasks &et, uint64_t n, uint32_t *newoff, uint64_t plans, void **temp,
+                        size_t *temp_bytes, void *stream, uint64_t *launches) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    size_t need = 0;
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, need, et.nchild, newoff, static_cast<int>(n + 1), s);
+    if (e != cudaSuccess) return static_cast<int>(e);
+    if (need > *temp_bytes) {
+        if (*temp) cudaFree(*temp);
+        e = cudaMalloc(temp, need);
+        if (e != cudaSuccess) return static_cast<int>(e);
+        *temp_bytes = need;
+    }
+    e = cub::DeviceScan::ExclusiveSum(*temp, need, et.nchild, newoff, static_cast<int>(n + 1), s);
+    if (e != cudaSuccess) return static_cast<int>(e);
+    if (launches) ++*launches;
+    return 0;
+}
+
+int launch_exact_ranges(const ExactTasks &et, const uint32_t *newoff, uint64_t plans, void *stream,
+                        uint64_t *launches) {
+    if (plans == 0) return 0;
+    k_exact_ranges<<<static_cast<unsigned>((plans + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+        et, newoff, plans);
+    if (launches) ++*launches;
+    return check(cudaGetLastError());
+}
+
 int launch_exact_split(const ShapeTables &t, const SpaceTables &sp, const PlanSource &src, const SolveParams &prm,
-                       const ExactTasks &et, const ExactTasks &nt, const uint64_t *newoff, uint64_t total_tasks,
+                       const ExactTasks &et, const ExactTasks &nt, const uint32_t *newoff, uint64_t total_tasks,
                        int sm_count, void *stream, uint64_t *launches) {
     (void)t;
     (void)sp;
@@ -2732,6 +2992,53 @@ int launch_plan_exact(const ShapeTables &t, const SpaceTables &sp, const KeyLayo
     return check(cudaGetLastError());
 }
 
+// (L, own) scan of the replay: keep the previous task's alive bits 0..L,
+// add the task's own bits (associative: see exact_replay_task)
+struct AliveOp {
+    __device__ __forceinline__ uint64_t operator()(uint64_t a, uint64_t b) const {
+        const int la = static_cast<int>(static_cast<int32_t>(a >> 32)), lb = static_cast<int>(static_cast<int32_t>(b >> 32));
+        const uint32_t keep = lb >= 0 ? ((2u << lb) - 1u) : 0u;
+        const uint32_t own = (static_cast<uint32_t>(a) & keep) | static_cast<uint32_t>(b);
+        const int l = la < lb ? la : lb;
+        return (static_cast<uint64_t>(static_cast<uint32_t>(l)) << 32) | own;
+    }
+};
+
+__global__ void k_alive_pack(const int32_t *L, const uint32_t *own, uint64_t *packed, uint64_t n) {
+    for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
+         q += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        packed[q] = (static_cast<uint64_t>(static_cast<uint32_t>(L[q])) << 32) | own[q];
+}
+__global__ void k_alive_unpack(const uint64_t *packed, uint32_t *mask, uint64_t n) {
+    for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
+         q += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        mask[q] = static_cast<uint32_t>(packed[q]);
+}
+
+// Ancestor-alive masks of all tasks (inclusive scan of the packed (L, own)).
+int launch_alive_scan(const ExactTasks &et, uint64_t total, uint64_t *tmp, void **temp, size_t *temp_bytes,
+                      int sm_count, void *stream, uint64_t *launches) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (total == 0) return 0;
+    const uint64_t grid = std::min<uint64_t>((total + 255) / 256, static_cast<uint64_t>(sm_count) * 8);
+    uint64_t *out = tmp + total;  // tmp holds 2 * total
+    k_alive_pack<<<static_cast<unsigned>(grid), 256, 0, s>>>(et.aL, et.amask, tmp, total);
+    size_t need = 0;
+    cudaError_t e = cub::DeviceScan::InclusiveScan(nullptr, need, tmp, out, AliveOp(), static_cast<int>(total), s);
+    if (e != cudaSuccess) return static_cast<int>(e);
+    if (need > *temp_bytes) {
+        if (*temp) cudaFree(*temp);
+        e = cudaMalloc(temp, need);
+        if (e != cudaSuccess) return static_cast<int>(e);
+        *temp_bytes = need;
+    }
+    e = cub::DeviceScan::InclusiveScan(*temp, need, tmp, out, AliveOp(), static_cast<int>(total), s);
+    if (e != cudaSuccess) return static_cast<int>(e);
+    k_alive_unpack<<<static_cast<unsigned>(grid), 256, 0, s>>>(out, et.amask, total);
+    if (launches) *launches += 3;
+    return check(cudaGetLastError());
+}
+
 int launch_exact_plan_pass(int pass, const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key,
                            const PlanSource &src, const PlanOutputs &out, const SolveParams &prm,
                            const ExactTasks &et, int sm_count, void *stream, uint64_t *launches) {
@@ -2753,6 +3060,23 @@ int launch_exact_task_pass(int pass, const ShapeTables &t, const SpaceTables &sp
                            void *stream, uint64_t *launches) {
     cudaGetLastError();
     if (total_tasks == 0) return 0;
+    static const int thr = [] {
+        const char *e = getenv("OSERVE_EXACT_THR");
+        return e ? atoi(e) : 1;
+    }();
+    if (((thr && (pass == 0 || pass == 1)) || pass >= 6) && et.fetch) {
+        // thread per task, dynamic fetch (counter zeroed on the stream)
+        if (cudaError_t e = cudaMemsetAsync(et.fetch, 0, sizeof(unsigned long long), static_cast<cudaStream_t>(stream)))
+            return static_cast<int>(e);
+        const int block = 128;
+        uint64_t grid = (total_tasks + block - 1) / block;
+        const uint64_t cap = static_cast<uint64_t>(sm_count) * 16;
+        if (grid > cap) grid = cap;
+        k_exact_task_thr<<<static_cast<unsigned>(grid), block, 0, static_cast<cudaStream_t>(stream)>>>(
+            pass, t, sp, src, prm, et, total_tasks, et.fetch);
+        if (launches) ++*launches;
+        return check(cudaGetLastError());
+    }
     const int block = 128;  // 4 warps, warp per task
     const uint64_t cap = static_cast<uint64_t>(sm_count) * 16;
     uint64_t grid = (total_tasks * 32 + block - 1) / block;
