@@ -909,10 +909,6 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
     }();
     et.target = target_env ? target_env : std::max<uint64_t>(64, std::min<uint64_t>(4096, budget_tasks / P));
     et.max_tasks = et.target * 8;
-    static const bool bfs = [] {
-        const char *e = getenv("OSERVE_EXACT_BFS");
-        return !e || atoi(e) != 0;
-    }();
     static const bool dbg = getenv("OSERVE_DEBUG_EXACT") != nullptr;
     TaskBufs *bufs = c.exact.bufs;
     int cur = 0;
@@ -952,7 +948,7 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
         total = ntot;
         return true;
     };
-    if (bfs) {
+    {
         // Frontier built on the device: one root task per exact-path plan,
         // then level by level every task of a plan still below the target
         // count becomes the branches of its root's first decision (preorder
@@ -1018,28 +1014,6 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
             }
         }
         lap("frontier");
-    } else {
-        cuda_ok(launch_exact_plan_pass(0, c.tables, view, key, src, eo, prm, et, c.sm_count, s, &c.launches),
-                "exact plan pass 0");
-        std::vector<uint64_t> nt;
-        download(nt, et.ntask, P, s);
-        download(state, et.state, P, s);
-        cuda_ok(cudaStreamSynchronize(s), "sync");
-        std::vector<uint64_t> off(P);
-        for (uint64_t i = 0; i < P; ++i) {
-            if (state[i] == 1 && total + nt[i] > 4 * budget_tasks) state[i] = 2;  // task buffers full
-            off[i] = total;
-            if (state[i] == 1) total += nt[i];
-        }
-        cuda_ok(h2d(et.toff, off.data(), sizeof(uint64_t) * P, s), "H2D");
-        cuda_ok(h2d(et.state, state.data(), P, s), "H2D");
-        if (total) {
-            bufs[cur].bind(et, total);
-            lap("pass0");
-            cuda_ok(launch_exact_plan_pass(1, c.tables, view, key, src, eo, prm, et, c.sm_count, s, &c.launches),
-                    "exact plan pass 1");
-            lap("emit");
-        }
     }
     if (total) {
         // Phase A in rounds: tasks over the round's node cap are split into
@@ -1054,12 +1028,25 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
         }();
         static const int64_t kCap0 = [] {
             const char *e = getenv("OSERVE_EXACT_CAP0");
-            return e ? static_cast<int64_t>(atoll(e)) : int64_t{1} << 15;
+            return e ? static_cast<int64_t>(atoll(e)) : int64_t{1} << 13;
         }();
         static const int kGrowth = [] {
             const char *e = getenv("OSERVE_EXACT_GROWTH");
-            return e ? atoi(e) : 1;
+            return e ? atoi(e) : 4;
         }();
+        // the replay of the top: exact incumbents, visited tasks and top-node
+        // counts (see exact_replay_task)
+        auto replay = [&]() {
+            cuda_ok(launch_exact_plan_pass(6, c.tables, view, key, src, eo, prm, et, c.sm_count, s, &c.launches),
+                    "exact plan pass 6");
+            cuda_ok(launch_exact_task_pass(6, c.tables, view, src, prm, et, total, c.sm_count, s, &c.launches),
+                    "exact task pass 6");
+            uint64_t *tmp = static_cast<uint64_t *>(xs.scan.get(sizeof(uint64_t) * 2 * total));
+            cuda_ok(launch_alive_scan(et, total, tmp, &c.cub_temp, &c.cub_temp_bytes, c.sm_count, s, &c.launches),
+                    "alive scan");
+            cuda_ok(launch_exact_task_pass(7, c.tables, view, src, prm, et, total, c.sm_count, s, &c.launches),
+                    "exact task pass 7");
+        };
         int64_t round_cap = kCap0;
         for (int round = 0;; ++round) {
             const bool last = round == kRounds || total > (uint64_t{1} << 24);
@@ -1072,46 +1059,14 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
             cuda_ok(launch_exact_task_pass(0, c.tables, view, src, prm, et, total, c.sm_count, s, &c.launches),
                     "exact task pass 0");
             lap("phaseA round");
-            if (dbg) {
-                std::vector<int64_t> nd;
-                std::vector<uint8_t> cp;
-                download(nd, et.nodes, total, s);
-                download(cp, et.capped, total, s);
-                cuda_ok(cudaStreamSynchronize(s), "sync");
-                int64_t sum = 0, ncap = 0;
-                for (uint64_t q = 0; q < total; ++q) {
-                    sum += nd[q];
-                    ncap += cp[q];
-                }
-                std::fprintf(stderr, "[exact]   round %d cap %lld: nodes %lld, capped tasks %lld of %llu\n", round,
-                             static_cast<long long>(et.phase_cap), static_cast<long long>(sum),
-                             static_cast<long long>(ncap), static_cast<unsigned long long>(total));
-            }
             if (last) break;
             cuda_ok(launch_exact_task_pass(3, c.tables, view, src, prm, et, total, c.sm_count, s, &c.launches),
                     "exact task pass 3");
             if (!rebuild()) break;  // nothing capped: phase A complete
         }
-        static const bool par_replay = [] {
-            const char *e = getenv("OSERVE_EXACT_REPLAY");
-            return !e || atoi(e) != 0;
-        }();
-        if (par_replay) {  // parallel replay of the top (see exact_replay_task)
-            cuda_ok(launch_exact_plan_pass(6, c.tables, view, key, src, eo, prm, et, c.sm_count, s, &c.launches),
-                    "exact plan pass 6");
-            cuda_ok(launch_exact_task_pass(6, c.tables, view, src, prm, et, total, c.sm_count, s, &c.launches),
-                    "exact task pass 6");
-            uint64_t *tmp = static_cast<uint64_t *>(xs.scan.get(sizeof(uint64_t) * 2 * total));
-            cuda_ok(launch_alive_scan(et, total, tmp, &c.cub_temp, &c.cub_temp_bytes, c.sm_count, s, &c.launches),
-                    "alive scan");
-            cuda_ok(launch_exact_task_pass(7, c.tables, view, src, prm, et, total, c.sm_count, s, &c.launches),
-                    "exact task pass 7");
-            cuda_ok(launch_exact_plan_pass(8, c.tables, view, key, src, eo, prm, et, c.sm_count, s, &c.launches),
-                    "exact plan pass 8");
-        } else {
-            cuda_ok(launch_exact_plan_pass(2, c.tables, view, key, src, eo, prm, et, c.sm_count, s, &c.launches),
-                    "exact plan pass 2");
-        }
+        replay();  // the exact incumbents, visited tasks and top-node counts (see exact_replay_task)
+        cuda_ok(launch_exact_plan_pass(8, c.tables, view, key, src, eo, prm, et, c.sm_count, s, &c.launches),
+                "exact plan pass 8");
         lap("top replay");
         cuda_ok(launch_exact_task_pass(1, c.tables, view, src, prm, et, total, c.sm_count, s, &c.launches),
                 "exact task pass 1");

@@ -1838,122 +1838,8 @@ __device__ __forceinline__ int64_t exact_dive(const ShapeTables &t, const ExactS
     return count;
 }
 
-// Preorder walk of the tree above the cut.  MODE 0: count tasks (stop past
-// cap); 1: emit tasks; 2: exact replay (visited flags, entering incumbents,
-// top-node count).
-template <int MODE>
-__device__ uint64_t exact_top(const ShapeTables &t, ExactState &st, int cut, uint64_t cap, const ExactTasks &et,
-                              uint64_t base, uint32_t plan, int64_t &top_nodes, int64_t &opt, int64_t &istar) {
-    const int R = st.R, J = st.J;
-    int fk[kTaskDepthMax], fpos[kTaskDepthMax], fj[kTaskDepthMax];
-    int64_t fv[kTaskDepthMax];
-    bool falive[kTaskDepthMax];
-    int depth = 0, k = 0, pos = 0;
-    int64_t count = 0, inc = -1;
-    bool calling = true, vis = true;
-    uint64_t ti = 0;
-    top_nodes = 0;
-    istar = -1;
-    while (true) {
-        if (calling) {
-            const bool boundary = MODE == 2 ? (k == R || (ti < cap && depth == (et.tdepth[base + ti] & 0x7f)))
-                                            : (depth == cut || k == R);
-            if (boundary) {  // task boundary
-                if (MODE == 0) {
-                    if (++ti > cap) return ti;
-                } else if (MODE == 1) {
-                    const uint64_t q = base + ti;
-                    et.plan[q] = plan;
-                    // a task's root is always the node right after its depth-th
-                    // decision — also when the walk reached k == R above the cut:
-                    // the pass-through calls down to that leaf are the task's
-                    // (the reference's dfs(k + 1, 0) calls count as nodes), not
-                    // skipped by a leaf flag
-                    et.tdepth[q] = static_cast<uint8_t>(depth);
-                    for (int a = 0; a < depth; ++a) et.path[q * kTaskDepthMax + a] = static_cast<int32_t>(fv[a]);
-                    et.done[q] = 0;
-                    et.capped[q] = 0;  // (pass 4 reads m of tasks that ran: done or capped)
-                    ++ti;
-                } else {
-                    const uint64_t q = base + ti;
-                    et.vis[q] = vis ? 1 : 0;
-                    et.inc[q] = inc;
-                    if (et.m[q] > inc) {
-                        inc = et.m[q];
-                        istar = static_cast<int64_t>(q);
-                    }
-                    ++ti;
-                }
-                calling = false;
-                continue;
-            }
-            if (MODE == 2 && vis) ++top_nodes;
-            const int s = st.shp[k];
-            if (pos == t.olen[s]) {
-                ++k;
-                pos = 0;
-                continue;
-            }
-            bool alive = true;
-            if (MODE == 2) {
-                alive = false;
-                if (vis) {
-                    int64_t lam_total = 0;
-                    for (int j = 0; j < J; ++j) lam_total += st.lam[j];
-                    int64_t bound = suffix_bound(t, st, k, pos, st.lam, st.mrem[k]);
-                    for (int k2 = k + 1; k2 < R; ++k2) bound += suffix_bound(t, st, k2, 0, st.lam, t.M[st.shp[k2]]);
-                    alive = count + (lam_total < bound ? lam_total : bound) > inc;
-                }
-            }
-            const int j = t.order[s * kMaxJ + pos];
-            const int64_t u = t.unit[s * J + j];
-            int64_t hi = t.cap[s * J + j];
-            if (st.lam[j] < hi) hi = st.lam[j];
-            if (hi * u > st.mrem[k]) hi = quot_small(st.mrem[k], u, t.inv_unit[s * J + j]);
-            fk[depth] = k;
-            fpos[depth] = pos;
-            fj[depth] = j;
-            fv[depth] = hi;
-            falive[depth] = alive;
-            ++depth;
-            st.x[k * J + j] = static_cast<int32_t>(hi);
-            st.lam[j] -= hi;
-            st.mrem[k] -= hi * u;
-            count += hi;
-            pos = pos + 1;
-            vis = alive;
-            continue;
-        }
-        if (depth == 0) break;
-        const int d = depth - 1;
-        const int kk = fk[d], j = fj[d];
-        const int64_t u = t.unit[st.shp[kk] * J + j];
-        int64_t v = fv[d];
-        count -= v;
-        st.mrem[kk] += v * u;
-        st.lam[j] += v;
-        st.x[kk * J + j] = 0;
-        if (v == 0) {
-            --depth;
-            continue;
-        }
-        v -= 1;
-        fv[d] = v;
-        st.x[kk * J + j] = static_cast<int32_t>(v);
-        st.lam[j] -= v;
-        st.mrem[kk] -= v * u;
-        count += v;
-        k = kk;
-        pos = fpos[d] + 1;
-        vis = falive[d];
-        calling = true;
-    }
-    opt = inc;
-    return ti;
-}
-
-// Parallel replay of the top of the tree (replaces the per-plan preorder
-// walk exact_top<2>).  With the exact prefix-maximum incumbents inc[q] of
+// Parallel replay of the top of the tree (round 1 walked it on one thread
+// per plan, in preorder).  With the exact prefix-maximum incumbents inc[q] of
 // the tasks (plan pass 6: the exclusive prefix max of m, the optimum and the
 // task holding the first optimal leaf), an internal top node is checked with
 // the incumbent of the first task below it, so it is alive iff count +
@@ -2037,31 +1923,10 @@ __global__ void __launch_bounds__(128) k_exact_plan(int pass, ShapeTables t, Spa
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < src.count;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         ExactState st;
-        int64_t part, tn, opt, istar;
+        int64_t part;
         uint64_t local, gr;
         const int64_t *lam_src;
         const bool ex = exact_setup(t, sp, src, prm, i, st, part, local, gr, lam_src);
-        if (pass == 0) {
-            if (!ex) {
-                et.depth[i] = -1;
-                et.ntask[i] = 0;
-                et.state[i] = 0;
-                continue;
-            }
-            int chosen = 1;
-            uint64_t n = exact_top<0>(t, st, 1, et.max_tasks, et, 0, 0, tn, opt, istar);
-            for (int d = 2; d <= 6 && n < et.target; ++d) {  // initial cut; phase A splits deeper
-                const uint64_t n2 = exact_top<0>(t, st, d, et.max_tasks, et, 0, 0, tn, opt, istar);
-                if (n2 > et.max_tasks) break;
-                n = n2;
-                chosen = d;
-            }
-            const bool ok = n <= et.max_tasks;
-            et.depth[i] = chosen;
-            et.ntask[i] = ok ? n : 0;
-            et.state[i] = ok ? 1 : 2;
-            continue;
-        }
         if (pass == 10) {  // device-built frontier: one root task per exact-path plan
             et.depth[i] = ex ? 0 : -1;
             et.ntask[i] = ex ? 1 : 0;
@@ -2069,11 +1934,6 @@ __global__ void __launch_bounds__(128) k_exact_plan(int pass, ShapeTables t, Spa
             continue;
         }
         if (!ex || et.state[i] == 0) continue;
-        if (pass == 1) {
-            if (et.state[i] == 1)
-                exact_top<1>(t, st, et.depth[i], et.max_tasks, et, et.toff[i], static_cast<uint32_t>(i), tn, opt, istar);
-            continue;
-        }
         if (pass == 6) {  // exact incumbents: exclusive prefix max of m; optimum; last rise
             if (et.state[i] != 1) continue;
             int64_t run = -1, ist = -1;
@@ -2116,27 +1976,6 @@ __global__ void __launch_bounds__(128) k_exact_plan(int pass, ShapeTables t, Spa
             }
             continue;
         }
-        if (pass == 2) {
-            if (et.state[i] != 1) continue;
-            bool capped = false;
-            for (uint64_t q = et.toff[i]; q < et.toff[i] + et.ntask[i]; ++q) capped = capped || et.capped[q];
-            if (capped) {  // phase A hit the budget somewhere: sequential DFS
-                et.state[i] = 2;
-                continue;
-            }
-            exact_top<2>(t, st, et.depth[i], et.ntask[i], et, et.toff[i], static_cast<uint32_t>(i), tn, opt, istar);
-            et.top_nodes[i] = tn;
-            et.opt[i] = opt;
-            et.istar[i] = istar;
-            et.running[i] = static_cast<unsigned long long>(tn);
-            // phase A visits a superset of the sequential nodes below each task
-            // (its incumbent is never stronger), so top + sum(A) bounds the count
-            int64_t ub = tn;
-            for (uint64_t q = et.toff[i]; q < et.toff[i] + et.ntask[i]; ++q)
-                if (et.vis[q]) ub += et.nodes[q];
-            if (ub > prm.node_budget) et.state[i] = 3;
-            continue;
-        }
         // pass 3: finish
         const uint8_t ps = et.state[i];
         if (ps != 1 && ps != 3) continue;
@@ -2151,86 +1990,14 @@ __global__ void __launch_bounds__(128) k_exact_plan(int pass, ShapeTables t, Spa
     }
 }
 
-// Per-task passes, warp per task: 0 phase A (best leaf seeded with lb, node
-// count), 1 phase B (exact replay from the entering incumbent: the first
-// optimal leaf of the istar task; node counts into the plan's running total
-// when phase A's upper bound did not certify the plan).
-__global__ void __launch_bounds__(128) k_exact_task(int pass, ShapeTables t, SpaceTables sp, PlanSource src,
-                                                    SolveParams prm, ExactTasks et, uint64_t total) {
-    const int lane = threadIdx.x & 31;
-    const uint64_t w0 = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-    for (uint64_t q = w0; q < total; q += nw) {
-        const uint64_t i = et.plan[q];
-        const uint8_t ps = et.state[i];
-        if (pass == 3 && ps != 1) {  // not split (every task needs its child count for the rescan)
-            if (lane == 0) et.nchild[q] = 1;
-            continue;
-        }
-        if ((pass == 0 || pass == 2) && ps != 1) continue;
-        if ((pass == 0 || pass == 2) && et.done[q]) continue;
-        if (pass == 1) {
-            if (ps == 1 && static_cast<int64_t>(q) != et.istar[i]) continue;  // certified: only the winner's leaf
-            if (ps != 1 && (ps != 3 || !et.vis[q])) continue;
-        }
-        ExactState st;
-        int64_t part;
-        uint64_t local, gr;
-        const int64_t *lam_src;
-        exact_setup(t, sp, src, prm, i, st, part, local, gr, lam_src);
-        const uint8_t td = et.tdepth[q];
-        int k, pos;
-        int64_t count;
-        exact_restore(t, st, et.path + q * kTaskDepthMax, td & 0x7f, (td & 0x80) != 0, k, pos, count);
-        int64_t nodes = 0;
-        bool capped;
-        if (pass == 2) {  // greedy dive of the task: a leaf, so a lower bound of its best
-            if (lane == 0) et.g[q] = exact_dive(t, st, k, pos, count);
-        } else if (pass == 3) {  // children count for the next round
-            uint32_t nc = 1;
-            if (et.capped[q] && et.phase_cap < prm.node_budget && (td & 0x7f) < kTaskDepthMax - 1) {
-                while (k < st.R && pos == t.olen[st.shp[k]]) {
-                    ++k;
-                    pos = 0;
-                }
-                if (k < st.R) {
-                    const int s = st.shp[k];
-                    const int j = t.order[s * kMaxJ + pos];
-                    const int64_t u = t.unit[s * st.J + j];
-                    int64_t hi = t.cap[s * st.J + j];
-                    if (st.lam[j] < hi) hi = st.lam[j];
-                    if (hi * u > st.mrem[k]) hi = quot_small(st.mrem[k], u, t.inv_unit[s * st.J + j]);
-                    nc = static_cast<uint32_t>(hi + 1);
-                }
-            }
-            if (lane == 0) et.nchild[q] = nc;
-        } else if (pass == 0) {
-            int64_t best = et.lb[q];
-            exact_dfs_warp<false>(t, st, k, pos, count, best, et.phase_cap, nodes, capped, nullptr, nullptr, 0);
-            if (lane == 0) {
-                et.m[q] = best;
-                et.nodes[q] = nodes;
-                et.capped[q] = capped ? 1 : 0;
-                et.done[q] = capped ? 0 : 1;
-            }
-        } else {
-            int64_t best = et.inc[q];
-            unsigned long long *ctr = ps == 3 ? et.running + i : nullptr;
-            if (static_cast<int64_t>(q) == et.istar[i])
-                exact_dfs_warp<true>(t, st, k, pos, count, best, prm.node_budget + 1, nodes, capped,
-                                     et.bx + i * kMaxExactCells, ctr, prm.node_budget);
-            else
-                exact_dfs_warp<false>(t, st, k, pos, count, best, prm.node_budget + 1, nodes, capped, nullptr, ctr,
-                                      prm.node_budget);
-        }
-        __syncwarp();
-    }
-}
-
-// Per-task passes 0 and 1 with a thread per task (tasks fetched one at a
-// time from a counter, so a long task does not hold up a warp's others):
-// the exact path's instances are small (R*J <= exact_cell_limit, 20 by
-// default), where a warp-cooperative bound leaves most lanes idle.
+// Per-task passes, a thread per task (tasks fetched one at a time from a
+// counter, so a long task does not hold up a warp's others; the exact path's
+// instances are small — R*J <= exact_cell_limit, 20 by default — where a
+// warp-cooperative bound leaves most lanes idle): 0 phase A (best leaf seeded
+// with lb, node count, capped at phase_cap), 1 phase B (exact replay from the
+// entering incumbent: the first optimal leaf of the istar task; node counts
+// into the plan's running total for uncertified plans), 2 greedy dive,
+// 3 children of capped tasks, 6 / 7 top replay, 9 frontier children.
 __global__ void __launch_bounds__(128) k_exact_task_thr(int pass, ShapeTables t, SpaceTables sp, PlanSource src,
                                                         SolveParams prm, ExactTasks et, uint64_t total,
                                                         unsigned long long *fetch) {
@@ -2239,7 +2006,15 @@ __global__ void __launch_bounds__(128) k_exact_task_thr(int pass, ShapeTables t,
         if (q >= total) break;
         const uint64_t i = et.plan[q];
         const uint8_t ps = et.state[i];
-        if (pass == 0 && (ps != 1 || et.done[q])) continue;
+        if (pass == 3) {  // children count for the next round: capped tasks only
+            const uint8_t td3 = et.tdepth[q];
+            if (ps != 1 || !et.capped[q] || et.phase_cap >= prm.node_budget ||
+                (td3 & 0x7f) >= kTaskDepthMax - 1) {
+                et.nchild[q] = 1;
+                continue;
+            }
+        }
+        if ((pass == 0 || pass == 2) && (ps != 1 || et.done[q])) continue;
         if (pass == 1) {
             if (ps == 1 && static_cast<int64_t>(q) != et.istar[i]) continue;
             if (ps != 1 && (ps != 3 || !et.vis[q])) continue;
@@ -2248,7 +2023,13 @@ __global__ void __launch_bounds__(128) k_exact_task_thr(int pass, ShapeTables t,
             et.nchild[q] = 1;
             continue;
         }
-        if ((pass == 6 || pass == 7) && ps != 1) continue;
+        if ((pass == 6 || pass == 7) && ps != 1) {
+            if (pass == 6) {  // not a frontier plan's task: neutral scan element
+                et.aL[q] = -1;
+                et.amask[q] = 0;
+            }
+            continue;
+        }
         ExactState st;
         int64_t part;
         uint64_t local, gr;
@@ -2289,6 +2070,28 @@ __global__ void __launch_bounds__(128) k_exact_task_thr(int pass, ShapeTables t,
         exact_restore(t, st, et.path + q * kTaskDepthMax, td & 0x7f, (td & 0x80) != 0, k, pos, count);
         int64_t nodes = 0;
         bool capped;
+        if (pass == 2) {  // greedy dive of the task: a leaf, so a lower bound of its best
+            et.g[q] = exact_dive(t, st, k, pos, count);
+            continue;
+        }
+        if (pass == 3) {
+            uint32_t nc = 1;
+            while (k < st.R && pos == t.olen[st.shp[k]]) {
+                ++k;
+                pos = 0;
+            }
+            if (k < st.R) {
+                const int s = st.shp[k];
+                const int j = t.order[s * kMaxJ + pos];
+                const int64_t u = t.unit[s * st.J + j];
+                int64_t hi = t.cap[s * st.J + j];
+                if (st.lam[j] < hi) hi = st.lam[j];
+                if (hi * u > st.mrem[k]) hi = quot_small(st.mrem[k], u, t.inv_unit[s * st.J + j]);
+                nc = static_cast<uint32_t>(hi + 1);
+            }
+            et.nchild[q] = nc;
+            continue;
+        }
         if (pass == 0) {
             int64_t best = et.lb[q];
             exact_dfs<false>(t, st, k, pos, count, best, et.phase_cap, nodes, capped, nullptr);
@@ -3060,29 +2863,15 @@ int launch_exact_task_pass(int pass, const ShapeTables &t, const SpaceTables &sp
                            void *stream, uint64_t *launches) {
     cudaGetLastError();
     if (total_tasks == 0) return 0;
-    static const int thr = [] {
-        const char *e = getenv("OSERVE_EXACT_THR");
-        return e ? atoi(e) : 1;
-    }();
-    if (((thr && (pass == 0 || pass == 1)) || pass >= 6) && et.fetch) {
-        // thread per task, dynamic fetch (counter zeroed on the stream)
-        if (cudaError_t e = cudaMemsetAsync(et.fetch, 0, sizeof(unsigned long long), static_cast<cudaStream_t>(stream)))
-            return static_cast<int>(e);
-        const int block = 128;
-        uint64_t grid = (total_tasks + block - 1) / block;
-        const uint64_t cap = static_cast<uint64_t>(sm_count) * 16;
-        if (grid > cap) grid = cap;
-        k_exact_task_thr<<<static_cast<unsigned>(grid), block, 0, static_cast<cudaStream_t>(stream)>>>(
-            pass, t, sp, src, prm, et, total_tasks, et.fetch);
-        if (launches) ++*launches;
-        return check(cudaGetLastError());
-    }
-    const int block = 128;  // 4 warps, warp per task
+    // thread per task, dynamic fetch (counter zeroed on the stream)
+    if (cudaError_t e = cudaMemsetAsync(et.fetch, 0, sizeof(unsigned long long), static_cast<cudaStream_t>(stream)))
+        return static_cast<int>(e);
+    const int block = 128;
+    uint64_t grid = (total_tasks + block - 1) / block;
     const uint64_t cap = static_cast<uint64_t>(sm_count) * 16;
-    uint64_t grid = (total_tasks * 32 + block - 1) / block;
     if (grid > cap) grid = cap;
-    k_exact_task<<<static_cast<unsigned>(grid), block, 0, static_cast<cudaStream_t>(stream)>>>(pass, t, sp, src, prm,
-                                                                                               et, total_tasks);
+    k_exact_task_thr<<<static_cast<unsigned>(grid), block, 0, static_cast<cudaStream_t>(stream)>>>(
+        pass, t, sp, src, prm, et, total_tasks, et.fetch);
     if (launches) ++*launches;
     return check(cudaGetLastError());
 }
