@@ -254,6 +254,12 @@ struct TaskBufs {
     }
 };
 
+// Raw [count][R][J] rows staged as the shape tables of one call (K0b only).
+struct RawRows {
+    DBuf dn, de, dM, du, dc, dord, dol, dpp, dsc, dlat, dinv, drank, dpmask;
+    ShapeTables t{};
+};
+
 struct ExactScratch {
     DBuf depth, nt, off, top, opt, ist, state, bx, run, ranks, newoff, fetch, topn, ubn, anycap, scan, grow, psum;
     TaskBufs bufs[2];
@@ -306,6 +312,10 @@ struct oserve_gpu_ctx {
     DBuf d_key, d_obj, d_spp, d_x, d_used, d_aborted, d_aborted_n, d_ranks, d_listR, d_listOff, d_listShapes,
         d_listLam, d_sw[12];
     ExactScratch exact;
+    // per-call device scratch of the batch entry points, kept across calls
+    // (a cudaMalloc / cudaFree pair per buffer per call otherwise)
+    RawRows raw;
+    DBuf sc_kv[16], sc_fa[10], sc_mf[20], sc_lp[7], sc_sw[14], sc_aux[8];
     // K1 dynamic-chunk counters of this context (oserve_internal.h WorkRing)
     DBuf d_ring;
     WorkRing ring{nullptr, 0, 0};
@@ -2112,7 +2122,7 @@ int oserve_gpu_kv_plan(oserve_gpu_ctx *ctx, int n_inflight, const oserve_infligh
             sr[q] = inflight[q].source_replica;
         }
         cudaStream_t s = ctx->stream;
-        DBuf b[14];
+        DBuf *b = ctx->sc_kv;
         KvPlanIn in{};
         in.n = n_inflight;
         in.gen = b[0].upload(gen, s);
@@ -2148,7 +2158,7 @@ int oserve_gpu_kv_plan(oserve_gpu_ctx *ctx, int n_inflight, const oserve_infligh
             std::set<int32_t> seen(ddev.begin(), ddev.end());
             if (seen.size() != ddev.size()) par = false;
         }
-        DBuf pb[2];
+        DBuf *pb = ctx->sc_kv + 14;
         if (par) {
             std::vector<int32_t> goff(dst->num_replicas + 1, 0), greq;
             int m = 0;
@@ -2607,12 +2617,6 @@ int oserve_gpu_plan_detail(oserve_gpu_ctx *ctx, const oserve_deployment *dep, in
     });
 }
 
-// Raw [count][R][J] rows staged as the shape tables of one call (K0b only).
-struct RawRows {
-    DBuf dn, de, dM, du, dc, dord, dol, dpp, dsc, dlat, dinv, drank, dpmask;
-    ShapeTables t{};
-};
-
 void validate_raw(int count, int R, int J, const int64_t *n, const int64_t *lambda) {
     if (J < 1 || J > OSERVE_MAX_CLASSES) fail(OSERVE_ERR_UNSUPPORTED, "classes must be in [1, 16]");
     if (R < 1 || R > OSERVE_MAX_REPLICAS) fail(OSERVE_ERR_UNSUPPORTED, "replicas must be in [1, 128]");
@@ -2691,7 +2695,7 @@ int oserve_gpu_solve_batch(oserve_gpu_ctx *ctx, int count, int R, int J, const i
         validate_raw(count, R, J, n, lambda);
         const int64_t rows = static_cast<int64_t>(count) * R;
         cudaStream_t s = ctx->stream;
-        RawRows rr;
+        RawRows &rr = ctx->raw;
         stage_raw_rows(*ctx, rows, J, n, e, rr);
         std::vector<int> all(count);
         std::iota(all.begin(), all.end(), 0);
@@ -2725,13 +2729,13 @@ int flow_assign_impl(oserve_gpu_ctx *ctx, int count, int R, int J, const int64_t
         validate_raw(count, R, J, n, lambda);
         const int64_t rows = static_cast<int64_t>(count) * R;
         cudaStream_t s = ctx->stream;
-        RawRows rr;
+        RawRows &rr = ctx->raw;
         stage_raw_rows(*ctx, rows, J, n, e, rr);
         // K6b: network, push-relabel, rounded chain flows, warm greedy + exchange
         size_t n32 = 0, n64 = 0, n8 = 0;
         flow_assign_workspace(R, J, count, &n32, &n64, &n8);
         const int m = J + 2 * R * J + 2 * R;
-        DBuf w32, w64, w8, dlam, dx, dobj, dval, dflow, dst;
+        DBuf &w32 = ctx->sc_fa[0], &w64 = ctx->sc_fa[1], &w8 = ctx->sc_fa[2], &dlam = ctx->sc_fa[3], &dx = ctx->sc_fa[4], &dobj = ctx->sc_fa[5], &dval = ctx->sc_fa[6], &dflow = ctx->sc_fa[7], &dst = ctx->sc_fa[8];
         FlowAssignBatch fb{};
         fb.count = count;
         fb.R = R;
@@ -2745,7 +2749,7 @@ int flow_assign_impl(oserve_gpu_ctx *ctx, int count, int R, int J, const int64_t
         fb.value = static_cast<int64_t *>(dval.get(sizeof(int64_t) * count));
         fb.edge_flow = edge_flow ? static_cast<int64_t *>(dflow.get(sizeof(int64_t) * count * m)) : nullptr;
         fb.status = static_cast<int32_t *>(dst.get(sizeof(int32_t) * count));
-        DBuf dfin;
+        DBuf &dfin = ctx->sc_fa[9];
         if (flow_in) fb.flow_in = dfin.upload(flow_in, static_cast<size_t>(count) * m, s);
         cuda_ok(launch_flow_assign(rr.t, fb, s, &ctx->launches), "flow assign kernel");
         std::vector<int64_t> hx, hobj, hval, hflow;
@@ -2832,7 +2836,7 @@ int oserve_gpu_max_flow_batch(oserve_gpu_ctx *ctx, int count, const int *num_nod
             cap[i] = edges[edge_offset[0] + i].cap;
         }
         cudaStream_t s = ctx->stream;
-        DBuf b[20];
+        DBuf *b = ctx->sc_mf;
         MaxFlowBatch mb{};
         mb.count = count;
         mb.num_nodes = b[0].upload(nn, s);
@@ -2876,7 +2880,7 @@ int oserve_gpu_solve_fractional_batch(oserve_gpu_ctx *ctx, int count, int R, int
         const int chunk = static_cast<int>(std::min<size_t>(count, std::max<size_t>(1, budget / per)));
         const int nv = R * J;
         cudaStream_t s = ctx->stream;
-        DBuf dn, de, dl, dt, df, dobj, dst;
+        DBuf &dn = ctx->sc_lp[0], &de = ctx->sc_lp[1], &dl = ctx->sc_lp[2], &dt = ctx->sc_lp[3], &df = ctx->sc_lp[4], &dobj = ctx->sc_lp[5], &dst = ctx->sc_lp[6];
         for (int c0 = 0; c0 < count; c0 += chunk) {
             const int cn = std::min(chunk, count - c0);
             LpBatch lb{};
@@ -2979,7 +2983,7 @@ int oserve_gpu_layout(oserve_gpu_ctx *ctx, const oserve_deployment *dep, uint64_
         if (total == 0 || !shards) return;  // count query
         if (capacity < total) fail(OSERVE_ERR_INVALID_ARGUMENT, "layout: shard capacity too small");
         cudaStream_t s = ctx->stream;
-        DBuf b[8];
+        DBuf *b = ctx->sc_aux;
         LayoutIn in{};
         in.R = R;
         in.total = total;
@@ -3048,7 +3052,7 @@ int oserve_gpu_greedy_plan_layouts(oserve_gpu_ctx *ctx, int n_src, const oserve_
         csr(n_src, src, soff, sb, se);
         csr(n_dst, dst, doff, db, de);
         cudaStream_t s = ctx->stream;
-        DBuf b[14];
+        DBuf *b = ctx->sc_sw;
         HeldIn in{};
         in.num_devices = ND;
         in.machine = b[0].upload(machine, s);
@@ -3111,7 +3115,7 @@ int oserve_gpu_estimate_time(oserve_gpu_ctx *ctx, int n_links, const oserve_link
             by[i] = links[i].bytes;
         }
         cudaStream_t s = ctx->stream;
-        DBuf b[4];
+        DBuf *b = ctx->sc_aux;
         LinkIn in{};
         in.n = n_links;
         in.src_machine = b[0].upload(ms, s);
@@ -3135,7 +3139,7 @@ int oserve_gpu_normalize_batch(oserve_gpu_ctx *ctx, int count, int J, const int6
         const int64_t cells = static_cast<int64_t>(count) * J;
         for (int64_t i = 0; i < cells; ++i)
             if (n[i] < 0) fail(OSERVE_ERR_INVALID_ARGUMENT, "normalize: negative capacity");
-        RawRows rr;
+        RawRows &rr = ctx->raw;
         stage_raw_rows(*ctx, count, J, n, n, rr);  // K0b: checked LCM, 2^62 fallback
         cudaStream_t s = ctx->stream;
         std::vector<int64_t> hM, hu;
@@ -3163,10 +3167,10 @@ int oserve_gpu_check_constraints_batch(oserve_gpu_ctx *ctx, int count, int R, in
         const int64_t rows = static_cast<int64_t>(count) * R;
         for (int64_t i = 0; i < rows * J; ++i)
             if (n[i] < 0) fail(OSERVE_ERR_INVALID_ARGUMENT, "normalize: negative capacity");
-        RawRows rr;
+        RawRows &rr = ctx->raw;
         stage_raw_rows(*ctx, rows, J, n, e, rr);  // normalize_or_scale per row (K0b)
         cudaStream_t s = ctx->stream;
-        DBuf b[6];
+        DBuf *b = ctx->sc_aux;
         CheckIn in{};
         in.count = count;
         in.R = R;
