@@ -292,11 +292,12 @@ struct Group {
     __device__ __forceinline__ T bcast(T v, int src) const { return __shfl_sync(mask, v, src, G); }
     __device__ __forceinline__ uint32_t sum(uint32_t v) const { return __reduce_add_sync(mask, v); }
     __device__ __forceinline__ uint32_t or_all(uint32_t v) const { return __reduce_or_sync(mask, v); }
-    // inclusive prefix sum of u64, saturating at `sat` (sat + sat must not overflow)
-    __device__ __forceinline__ uint64_t scan_sat64(uint64_t v, uint64_t sat, int width) const {
+    // inclusive prefix sum of u64 over the first W lanes, saturating at `sat`
+    // (sat + sat must not overflow)
+    template <int W>
+    __device__ __forceinline__ uint64_t scan_sat64(uint64_t v, uint64_t sat) const {
 #pragma unroll
-        for (int d = 1; d < G; d <<= 1) {
-            if (d >= width) break;
+        for (int d = 1; d < W; d <<= 1) {
             const uint64_t o = __shfl_up_sync(mask, v, d, G);
             if (gl >= d) {
                 v += o;
@@ -509,8 +510,6 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
     __syncthreads();
 
     const Grp g;
-    int jw = 1;
-    while (jw < J) jw <<= 1;  // scan width over class positions
     constexpr int TKE = kTopK / G;  // top-K list entries per lane (shared memory)
     if (kLists)
         for (int e = 0; e < TKE; ++e) tks[g.gl * TKE + e] = kNoKey;
@@ -770,7 +769,8 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_M
                 a = min(capj, lamp);
             }
             const uint64_t cost = static_cast<uint64_t>(a) * static_cast<uint64_t>(u);
-            const uint64_t csum = g.scan_sat64(cost, static_cast<uint64_t>(Ms) + 1, jw);
+            // (over min(G, 16) >= J lanes: positions past the shape's order add 0)
+            const uint64_t csum = g.template scan_sat64<(G < kMaxJ ? G : kMaxJ)>(cost, static_cast<uint64_t>(Ms) + 1);
             // exclusive prefix from the previous lane: unsaturated up to the
             // binding position (csum - cost is not, once saturated)
             uint64_t excl = __shfl_up_sync(g.mask, csum, 1, G);
