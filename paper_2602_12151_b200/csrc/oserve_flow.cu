@@ -40,6 +40,34 @@ __global__ void __launch_bounds__(128) k_max_flow(MaxFlowBatch b) {
     PrGraph pg;
     pg.n = n;
     pg.m = static_cast<int>(m);
+    if (b.interleave) {
+        const int64_t G = b.count;
+        for (int64_t i = 0; i < m; ++i) {
+            b.il_from[i * G + g] = b.from[e0 + i];
+            b.il_to[i * G + g] = b.to[e0 + i];
+            b.il_cap[i * G + g] = b.cap[e0 + i];
+        }
+        pg.from = {b.il_from + g, G};
+        pg.to = {b.il_to + g, G};
+        pg.cap = {b.il_cap + g, G};
+        pg.res = {b.res + g, G};
+        pg.arc_to = {b.arc_to + g, G};
+        pg.adj = {b.adj + g, G};
+        pg.excess = {b.excess + g, G};
+        pg.adj_off = {b.adj_off + g, G};
+        pg.height = {b.height + g, G};
+        pg.cur = {b.cur + g, G};
+        pg.fifo = {b.fifo + g, G};
+        pg.active = {b.active + g, G};
+        if (!pr_build(pg)) {
+            b.status[g] = 1;  // negative capacity
+            return;
+        }
+        b.value[g] = pr_run(pg, b.source[g], b.sink[g]);
+        for (int64_t i = 0; i < m; ++i) b.flow[e0 + i] = b.il_cap[i * G + g] - b.res[2 * i * G + g];
+        b.status[g] = 0;
+        return;
+    }
     pg.from = {b.from + e0, 1};
     pg.to = {b.to + e0, 1};
     pg.cap = {b.cap + e0, 1};
@@ -181,16 +209,19 @@ void flow_assign_workspace(int R, int J, int64_t count, size_t *i32, size_t *i64
 
 // ------------------------------------------------------------------- K7 ---
 // Tableau row r, column c of instance i at tab[i * rows * cols + r * cols + c].
+// SMEM: the whole tableau lives in shared memory (small instances; else in
+// the instance's HBM slab).
+template <bool SMEM>
 __global__ void __launch_bounds__(512) k_simplex(LpBatch b) {
     extern __shared__ double sm[];
     const int i = blockIdx.x;
     const int R = b.R, J = b.J;
     const int nvars = R * J, nrows = nvars + J + R, ncols = nvars + nrows + 1;
     const double eps = 1e-9;
-    double *t = b.tab + static_cast<int64_t>(i) * (nrows + 1) * ncols;
+    double *t = SMEM ? sm + 2 * nrows + 1 : b.tab + static_cast<int64_t>(i) * (nrows + 1) * ncols;
     double *fcol = sm;                                           // [nrows + 1]
     double *ratio = fcol + (nrows + 1);                          // [nrows]
-    int *basis = reinterpret_cast<int *>(ratio + nrows);         // [nrows]
+    int *basis = reinterpret_cast<int *>(SMEM ? t + static_cast<int64_t>(nrows + 1) * ncols : ratio + nrows);  // [nrows]
     int *misc = basis + nrows;                                   // [4]
     const int64_t *n = b.n + static_cast<int64_t>(i) * nvars;
     const int64_t *e = b.e + static_cast<int64_t>(i) * nvars;
@@ -267,14 +298,16 @@ __global__ void __launch_bounds__(512) k_simplex(LpBatch b) {
         for (int c = threadIdx.x; c < ncols; c += blockDim.x) prow[c] = __ddiv_rn(prow[c], p);
         __syncthreads();
         // eliminate: t[r][c] -= f_r * t[pr][c], f_r read before the row changes
-        const int64_t cells = static_cast<int64_t>(nrows + 1) * ncols;
-        for (int64_t q = threadIdx.x; q < cells; q += blockDim.x) {
-            const int r = static_cast<int>(q / ncols);
-            if (r == pr) continue;
-            const double f = fcol[r];
-            if (fabs(f) < eps) continue;
-            const int c = static_cast<int>(q - static_cast<int64_t>(r) * ncols);
-            t[q] = __dsub_rn(t[q], __dmul_rn(f, prow[c]));
+        // (warp per row, lanes over the columns)
+        {
+            const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+            for (int r = warp; r <= nrows; r += nw) {
+                if (r == pr) continue;
+                const double f = fcol[r];
+                if (fabs(f) < eps) continue;
+                double *row = t + static_cast<int64_t>(r) * ncols;
+                for (int c = lane; c < ncols; c += 32) row[c] = __dsub_rn(row[c], __dmul_rn(f, prow[c]));
+            }
         }
         __syncthreads();
         if (threadIdx.x == 0) basis[pr] = pc;
@@ -306,14 +339,18 @@ size_t simplex_tableau_doubles(int R, int J) {
 int launch_simplex(const LpBatch &b, void *stream, uint64_t *launches) {
     cudaGetLastError();
     if (b.count == 0) return 0;
-    const int nvars = b.R * b.J, nrows = nvars + b.J + b.R;
-    const size_t smem = sizeof(double) * (2 * nrows + 1) + sizeof(int) * (nrows + 4);
+    const int nvars = b.R * b.J, nrows = nvars + b.J + b.R, ncols = nvars + nrows + 1;
+    const size_t small = sizeof(double) * (2 * nrows + 1) + sizeof(int) * (nrows + 4);
+    const size_t whole = sizeof(double) * (2 * nrows + 1 + static_cast<size_t>(nrows + 1) * ncols) +
+                         sizeof(int) * (nrows + 4);
+    const bool in_smem = whole <= 96 * 1024;  // two instances per SM at least
+    const size_t smem = in_smem ? whole : small;
+    auto kern = in_smem ? k_simplex<true> : k_simplex<false>;
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(k_simplex, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (e != cudaSuccess) return check(e);
     }
-    k_simplex<<<b.count, 512, smem, static_cast<cudaStream_t>(stream)>>>(b);
+    kern<<<b.count, in_smem ? 256 : 512, smem, static_cast<cudaStream_t>(stream)>>>(b);
     if (launches) ++*launches;
     return check(cudaGetLastError());
 }

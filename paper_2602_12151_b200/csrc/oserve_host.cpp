@@ -2847,15 +2847,34 @@ int oserve_gpu_max_flow_batch(oserve_gpu_ctx *ctx, int count, const int *num_nod
         mb.cap = b[5].upload(cap, s);
         mb.source = b[6].upload(src, s);
         mb.sink = b[7].upload(snk, s);
-        mb.res = static_cast<int64_t *>(b[8].get(sizeof(int64_t) * 2 * E));
-        mb.excess = static_cast<int64_t *>(b[9].get(sizeof(int64_t) * N));
-        mb.arc_to = static_cast<int32_t *>(b[10].get(sizeof(int32_t) * 2 * E));
-        mb.adj = static_cast<int32_t *>(b[11].get(sizeof(int32_t) * 2 * E));
-        mb.adj_off = static_cast<int32_t *>(b[12].get(sizeof(int32_t) * (N + count)));
-        mb.height = static_cast<int32_t *>(b[13].get(sizeof(int32_t) * N));
-        mb.cur = static_cast<int32_t *>(b[14].get(sizeof(int32_t) * N));
-        mb.fifo = static_cast<int32_t *>(b[15].get(sizeof(int32_t) * N));
-        mb.active = static_cast<uint8_t *>(b[16].get(N));
+        // graphs of similar size: interleaved workspace padded to the largest
+        // (coalesced across a warp's graphs); very uneven batches stay packed
+        int64_t n_max = 0, m_max = 0;
+        for (int g = 0; g < count; ++g) {
+            n_max = std::max<int64_t>(n_max, num_nodes[g]);
+            m_max = std::max<int64_t>(m_max, eoff[g + 1] - eoff[g]);
+        }
+        const bool il = count >= 32 && m_max * count <= 4 * std::max<int64_t>(E, 1) + 64 * count &&
+                        (n_max + 1) * count <= 4 * (N + count) + 64 * count;
+        const int64_t We = il ? m_max * count : E, Wn = il ? n_max * count : N,
+                      Wo = il ? (n_max + 1) * count : N + count;
+        mb.interleave = il ? 1 : 0;
+        mb.n_max = static_cast<int>(n_max);
+        mb.m_max = static_cast<int>(m_max);
+        mb.res = static_cast<int64_t *>(b[8].get(sizeof(int64_t) * 2 * We));
+        mb.excess = static_cast<int64_t *>(b[9].get(sizeof(int64_t) * Wn));
+        mb.arc_to = static_cast<int32_t *>(b[10].get(sizeof(int32_t) * 2 * We));
+        mb.adj = static_cast<int32_t *>(b[11].get(sizeof(int32_t) * 2 * We));
+        mb.adj_off = static_cast<int32_t *>(b[12].get(sizeof(int32_t) * Wo));
+        mb.height = static_cast<int32_t *>(b[13].get(sizeof(int32_t) * Wn));
+        mb.cur = static_cast<int32_t *>(b[14].get(sizeof(int32_t) * Wn));
+        mb.fifo = static_cast<int32_t *>(b[15].get(sizeof(int32_t) * Wn));
+        mb.active = static_cast<uint8_t *>(b[16].get(Wn));
+        if (il) {
+            mb.il_from = static_cast<int32_t *>(ctx->sc_aux[5].get(sizeof(int32_t) * We));
+            mb.il_to = static_cast<int32_t *>(ctx->sc_aux[6].get(sizeof(int32_t) * We));
+            mb.il_cap = static_cast<int64_t *>(ctx->sc_aux[7].get(sizeof(int64_t) * We));
+        }
         mb.flow = static_cast<int64_t *>(b[17].get(sizeof(int64_t) * E));
         mb.value = static_cast<int64_t *>(b[18].get(sizeof(int64_t) * count));
         mb.status = static_cast<int32_t *>(b[19].get(sizeof(int32_t) * count));

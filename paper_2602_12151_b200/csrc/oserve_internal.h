@@ -288,6 +288,13 @@ struct MaxFlowBatch {
     uint8_t *active;
     int64_t *flow, *value;
     int32_t *status;
+    // interleaved workspace (graphs of similar size): element q of graph g
+    // at [q * count + g], sized for the largest graph (n_max, m_max); the
+    // edge lists are copied in (il_from / il_to / il_cap) so every access of
+    // a warp's 32 graphs is one coalesced line
+    int interleave, n_max, m_max;
+    int32_t *il_from, *il_to;
+    int64_t *il_cap;
 };
 int launch_max_flow(const MaxFlowBatch &b, void *stream, uint64_t *launches);
 
