@@ -1462,6 +1462,38 @@ __device__ int64_t suffix_bound(const ShapeTables &t, const ExactState &st, int 
     return cnt;
 }
 
+// The pruning test of ExactSolver::dfs (flowassign.cpp:351-354): count +
+// min(lam_total, bound) <= best, bound = greedy_suffix of replica k from pos
+// plus greedy_suffix of every later replica from 0.  lam_total is passed in
+// (count + lam_total is the same at every node: each branch moves v from lam
+// to count), and since the bound's terms are non-negative the sum stops as
+// soon as it clears best - count.
+__device__ __forceinline__ bool exact_pruned(const ShapeTables &t, const ExactState &st, int k, int pos,
+                                             int64_t count, int64_t lam_total, int64_t best) {
+    if (count + lam_total <= best) return true;
+    const int64_t need = best - count;  // pruned iff bound <= need
+    if (need < 0) return false;
+    int64_t acc = 0;
+    for (int kk = k; kk < st.R; ++kk) {
+        const int s = st.shp[kk];
+        const int ol = t.olen[s];
+        int64_t mr = kk == k ? st.mrem[k] : t.M[s];
+        for (int i = kk == k ? pos : 0; i < ol; ++i) {
+            const int j = t.order[s * kMaxJ + i];
+            const int64_t u = t.unit[s * st.J + j];
+            int64_t tk = t.cap[s * st.J + j];
+            if (st.lam[j] < tk) tk = st.lam[j];
+            if (tk * u > mr) tk = quot_small(mr, u, t.inv_unit[s * st.J + j]);
+            if (tk > 0) {
+                acc += tk;
+                if (acc > need) return false;
+                mr -= tk * u;
+            }
+        }
+    }
+    return true;
+}
+
 // Resolve plan i of a source into an ExactState; false if it does not take
 // the exact path.
 __device__ __forceinline__ bool exact_setup(const ShapeTables &t, const SpaceTables &sp, const PlanSource &src,
@@ -1534,102 +1566,205 @@ __device__ __forceinline__ void exact_emit(const ShapeTables &t, const KeyLayout
     }
 }
 
-// Subtree DFS of the reference's ExactSolver::dfs (flowassign.cpp:330-369)
-// from the node (k, pos) with `count` assigned above it and incumbent `best`:
-// the same node counting, bound, descending branch order and strictly-better
-// leaf rule.  Stops (capped) after `cap` nodes.  TRACK copies improving
-// leaves into bx.
-template <bool TRACK>
-__device__ void exact_dfs(const ShapeTables &t, ExactState &st, int k, int pos, int64_t count, int64_t &best,
-                          int64_t cap, int64_t &nodes, bool &capped, int32_t *bx, unsigned long long *ctr = nullptr,
-                          int64_t ctr_limit = 0) {
+// The plan's decisions flattened: position p is the p-th (replica, order
+// slot) pair in DFS order, so a DFS frame is just its position and the
+// stack is x[p].  meta[p] = class | replica << 8 | first-of-replica << 16 |
+// adv << 24, adv = the nodes entered from the decision before p to p itself:
+// the reference's pass-through dfs(k + 1, 0) calls at replica ends (one per
+// replica end crossed, empty replicas included) plus p's own node; meta[D]
+// holds the leaf's adv.  T is int32_t when every value fits (each cap * unit
+// <= M < 2^30 and count + lam_total < 2^30), else int64_t.
+template <typename T>
+struct ExactFlat {
+    int D;
+    uint32_t meta[kMaxExactCells + 1];
+    T u[kMaxExactCells], cap[kMaxExactCells], x[kMaxExactCells], mr_at[kMaxExactCells];
+    double inv[kMaxExactCells];
+    T lam[kMaxJ];
+    T M[kMaxExactCells];  // per replica
+};
+
+// The plan's flat decision table and the restored path; false if T cannot
+// hold the plan's values.
+template <typename T>
+__device__ __forceinline__ bool exact_flatten(const ShapeTables &t, const ExactState &st, int64_t conserved,
+                                              ExactFlat<T> &f) {
     const int R = st.R, J = st.J;
-    int fk[kMaxExactCells + 1], fpos[kMaxExactCells + 1], fj[kMaxExactCells + 1];
-    int64_t fv[kMaxExactCells + 1];
-    int depth = 0;
-    bool calling = true;
+    if (sizeof(T) == 4 && conserved >= (int64_t{1} << 30)) return false;
+    int p = 0, kprev = 0;
+    for (int k = 0; k < R; ++k) {
+        const int s = st.shp[k];
+        const int64_t Mk = t.M[s];
+        if (sizeof(T) == 4 && Mk >= (int64_t{1} << 30)) return false;
+        f.M[k] = static_cast<T>(Mk);
+        for (int i = 0; i < t.olen[s]; ++i, ++p) {
+            const int j = t.order[s * kMaxJ + i];
+            const int64_t u = t.unit[s * J + j], cp = t.cap[s * J + j];
+            if (sizeof(T) == 4 && cp * u > Mk) return false;
+            const uint32_t adv = 1u + static_cast<uint32_t>(k - kprev);
+            f.meta[p] = static_cast<uint32_t>(j) | (static_cast<uint32_t>(k) << 8) | ((i == 0 ? 1u : 0u) << 16) |
+                        (adv << 24);
+            kprev = k;
+            f.u[p] = static_cast<T>(u);
+            f.cap[p] = static_cast<T>(cp);
+            f.inv[p] = t.inv_unit[s * J + j];
+            f.x[p] = static_cast<T>(st.x[k * J + j]);
+        }
+    }
+    f.D = p;
+    f.meta[p] = (1u + static_cast<uint32_t>(R - kprev)) << 24;
+    for (int j = 0; j < J; ++j) f.lam[j] = static_cast<T>(st.lam[j]);
+    return true;
+}
+
+// The pruning test on the flat table (exact_pruned's rule): prune iff
+// count + min(lam_total, bound) <= best, the bound summed from position p
+// with the current replica's budget mr.
+template <typename T>
+__device__ __forceinline__ bool flat_pruned(const ExactFlat<T> &f, int p, T mr, T count, T conserved, T best) {
+    if (conserved <= best) return true;
+    const T need = best - count;
+    if (need < 0) return false;
+    T acc = 0, m = mr;
+    for (int q = p; q < f.D; ++q) {
+        const uint32_t mt = f.meta[q];
+        if (q > p && (mt & 0x10000u)) m = f.M[(mt >> 8) & 0xff];
+        const T u = f.u[q];
+        T tk = f.cap[q];
+        const T l = f.lam[mt & 0xff];
+        if (l < tk) tk = l;
+        if (tk * u > m) tk = static_cast<T>(quot_small(m, u, f.inv[q]));
+        if (tk > 0) {
+            acc += tk;
+            if (acc > need) return false;
+            m -= tk * u;
+        }
+    }
+    return true;
+}
+
+// The DFS from position p (entered with e nodes: the task root and its
+// pass-through chain).
+template <bool TRACK, typename T>
+__device__ void exact_dfs_flat(ExactFlat<T> &f, const ExactState &st, int p, int64_t e, int64_t count64,
+                               int64_t &best64, int64_t cap, int64_t &nodes, bool &capped, int32_t *bx,
+                               unsigned long long *ctr, int64_t ctr_limit, int64_t conserved64) {
+    const int R = st.R, J = st.J, D = f.D;
+    const int p0 = p;
+    T count = static_cast<T>(count64), best = static_cast<T>(best64);
+    const T conserved = static_cast<T>(conserved64);
+    T mr = p < D ? static_cast<T>(st.mrem[(f.meta[p] >> 8) & 0xff]) : T(0);
     capped = false;
-    int64_t flushed = 0;
-    while (true) {
+    int64_t flushed = 0, next_flush = 256;
+    bool calling = true;
+    nodes += e;
+    for (;;) {
         if (calling) {
-            if (++nodes > cap) {
+            if (nodes > cap) {
                 capped = true;
                 break;
             }
-            if (ctr && (nodes & 255) == 0) {  // shared node total (phase B): stop once it passes the limit
+            if (ctr && nodes >= next_flush) {  // shared node total (phase B): stop once it passes the limit
                 const unsigned long long tot =
                     atomicAdd(ctr, static_cast<unsigned long long>(nodes - flushed)) + (nodes - flushed);
                 flushed = nodes;
+                next_flush = nodes + 256;
                 if (tot > static_cast<unsigned long long>(ctr_limit)) {
                     capped = true;
                     break;
                 }
             }
-            if (k == R) {
+            if (p == D) {  // leaf
                 if (count > best) {
                     best = count;
-                    if (TRACK)
-                        for (int c = 0; c < R * J; ++c) bx[c] = st.x[c];
+                    if (TRACK) {
+                        for (int c = 0; c < R * J; ++c) bx[c] = 0;
+                        for (int q = 0; q < D; ++q) {
+                            const uint32_t mt = f.meta[q];
+                            bx[((mt >> 8) & 0xff) * J + (mt & 0xff)] = static_cast<int32_t>(f.x[q]);
+                        }
+                    }
                 }
                 calling = false;
                 continue;
             }
-            const int s = st.shp[k];
-            if (pos == t.olen[s]) {
-                ++k;
-                pos = 0;
-                continue;  // tail call dfs(k+1, 0)
-            }
-            int64_t lam_total = 0;
-            for (int j = 0; j < J; ++j) lam_total += st.lam[j];
-            int64_t bound = suffix_bound(t, st, k, pos, st.lam, st.mrem[k]);
-            for (int k2 = k + 1; k2 < R; ++k2) bound += suffix_bound(t, st, k2, 0, st.lam, t.M[st.shp[k2]]);
-            if (count + (lam_total < bound ? lam_total : bound) <= best) {
+            if (flat_pruned(f, p, mr, count, conserved, best)) {
                 calling = false;
                 continue;
             }
-            const int j = t.order[s * kMaxJ + pos];
-            const int64_t u = t.unit[s * J + j];
-            int64_t hi = t.cap[s * J + j];
-            if (st.lam[j] < hi) hi = st.lam[j];
-            if (hi * u > st.mrem[k]) hi = quot_small(st.mrem[k], u, t.inv_unit[s * J + j]);
-            fk[depth] = k;
-            fpos[depth] = pos;
-            fj[depth] = j;
-            fv[depth] = hi;
-            ++depth;
-            st.x[k * J + j] = static_cast<int32_t>(hi);
-            st.lam[j] -= hi;
-            st.mrem[k] -= hi * u;
+            const uint32_t mt = f.meta[p];
+            const int j = mt & 0xff;
+            const T u = f.u[p];
+            T hi = f.cap[p];
+            if (f.lam[j] < hi) hi = f.lam[j];
+            if (hi * u > mr) hi = static_cast<T>(quot_small(mr, u, f.inv[p]));
+            f.mr_at[p] = mr;
+            f.x[p] = hi;
+            f.lam[j] -= hi;
+            mr -= hi * u;
             count += hi;
-            pos = pos + 1;
-            continue;  // call dfs(k, pos+1)
-        }
-        // return into the frame on top of the stack
-        if (depth == 0) break;
-        const int d = depth - 1;
-        const int kk = fk[d], j = fj[d];
-        const int64_t u = t.unit[st.shp[kk] * J + j];
-        int64_t v = fv[d];
-        count -= v;
-        st.mrem[kk] += v * u;
-        st.lam[j] += v;
-        st.x[kk * J + j] = 0;
-        if (v == 0) {
-            --depth;  // loop exhausted: return from this visit
+            ++p;
+            const uint32_t mn = f.meta[p];
+            if (p < D && (mn & 0x10000u)) mr = f.M[(mn >> 8) & 0xff];
+            nodes += mn >> 24;
             continue;
         }
-        v -= 1;
-        fv[d] = v;
-        st.x[kk * J + j] = static_cast<int32_t>(v);
-        st.lam[j] -= v;
-        st.mrem[kk] -= v * u;
-        count += v;
-        k = kk;
-        pos = fpos[d] + 1;
+        // return into the frame of position p - 1
+        if (p == p0) break;
+        const int q = p - 1;
+        T v = f.x[q];
+        if (v == 0) {
+            p = q;
+            continue;
+        }
+        --v;
+        f.x[q] = v;
+        const uint32_t mt = f.meta[q];
+        f.lam[mt & 0xff] += 1;
+        count -= 1;
+        mr = f.mr_at[q] - v * f.u[q];
+        p = q + 1;
+        const uint32_t mn = f.meta[p];
+        if (p < D && (mn & 0x10000u)) mr = f.M[(mn >> 8) & 0xff];
+        nodes += mn >> 24;
         calling = true;
     }
     if (ctr && nodes != flushed) atomicAdd(ctr, static_cast<unsigned long long>(nodes - flushed));
+    best64 = best;
+}
+
+// Subtree DFS of the reference's ExactSolver::dfs (flowassign.cpp:330-369)
+// from the node (k, pos) with `count` assigned above it and incumbent `best`:
+// the same node counting, bound, descending branch order and strictly-better
+// leaf rule.  Stops (capped) once past `cap` nodes.  TRACK copies improving
+// leaves into bx.  Runs on the flat decision table in 32-bit arithmetic when
+// the plan's values allow it.
+template <bool TRACK>
+__device__ void exact_dfs(const ShapeTables &t, ExactState &st, int k, int pos, int64_t count, int64_t &best,
+                          int64_t cap, int64_t &nodes, bool &capped, int32_t *bx, unsigned long long *ctr = nullptr,
+                          int64_t ctr_limit = 0) {
+    int64_t conserved = count;  // count + lam_total, the same at every node
+    for (int j = 0; j < st.J; ++j) conserved += st.lam[j];
+    // the task root (k, pos) and its pass-through chain: e nodes up to the
+    // first decision (position p) or the leaf (p = D)
+    int64_t e = 1;
+    while (k < st.R && pos == t.olen[st.shp[k]]) {
+        ++k;
+        pos = 0;
+        ++e;
+    }
+    int p = pos;
+    for (int kk = 0; kk < k && kk < st.R; ++kk) p += t.olen[st.shp[kk]];
+    {
+        ExactFlat<int32_t> f;
+        if (exact_flatten(t, st, conserved, f)) {
+            exact_dfs_flat<TRACK>(f, st, p, e, count, best, cap, nodes, capped, bx, ctr, ctr_limit, conserved);
+            return;
+        }
+    }
+    ExactFlat<int64_t> f;
+    exact_flatten(t, st, conserved, f);
+    exact_dfs_flat<TRACK>(f, st, p, e, count, best, cap, nodes, capped, bx, ctr, ctr_limit, conserved);
 }
 
 // Warp-cooperative exact_dfs: all 32 lanes carry the identical DFS state and
@@ -1885,9 +2020,7 @@ __device__ void exact_replay_task(int pass, const ShapeTables &t, ExactState &st
             if (pass == 6) {
                 int64_t lt = 0;
                 for (int j = 0; j < J; ++j) lt += st.lam[j];
-                int64_t bound = suffix_bound(t, st, k, pos, st.lam, st.mrem[k]);
-                for (int k2 = k + 1; k2 < R; ++k2) bound += suffix_bound(t, st, k2, 0, st.lam, t.M[st.shp[k2]]);
-                if (count + (lt < bound ? lt : bound) > inc) own |= 1u << e;
+                if (!exact_pruned(t, st, k, pos, count, lt, inc)) own |= 1u << e;
             } else {
                 const uint32_t need = e ? ((2u << (e - 1)) - 1u) : 0u;  // ancestors 0..e-1
                 if ((anc & need) == need) top += calls;
