@@ -23,6 +23,7 @@
 #include <cstdint>
 #include <map>
 #include <tuple>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -1573,16 +1574,38 @@ __device__ __forceinline__ void exact_emit(const ShapeTables &t, const KeyLayout
 // the reference's pass-through dfs(k + 1, 0) calls at replica ends (one per
 // replica end crossed, empty replicas included) plus p's own node; meta[D]
 // holds the leaf's adv.  T is int32_t when every value fits (each cap * unit
-// <= M < 2^30 and count + lam_total < 2^30), else int64_t.
+// <= M < 2^30 and count + lam_total < 2^20), else int64_t.
 template <typename T>
 struct ExactFlat {
+    using Inv = typename std::conditional<sizeof(T) == 4, float, double>::type;
     int D;
+    // per position, slot D included so a pair of positions can be read
+    // ahead of the q + 1 < D test
     uint32_t meta[kMaxExactCells + 1];
-    T u[kMaxExactCells], cap[kMaxExactCells], x[kMaxExactCells], mr_at[kMaxExactCells];
-    double inv[kMaxExactCells];
+    T u[kMaxExactCells + 1], cap[kMaxExactCells + 1], mres[kMaxExactCells + 1];  // mres: M if first of replica, else -1
+    Inv inv[kMaxExactCells + 1];
+    T x[kMaxExactCells], mr_at[kMaxExactCells];
     T lam[kMaxJ];
     T M[kMaxExactCells];  // per replica
 };
+
+// floor(m / u) for the take of a position (m < take * u, so the quotient is
+// below the take): FP32 reciprocal and a remainder correction on the 32-bit
+// table (quotients < 2^20 there: at most 2 off), quot_small on the 64-bit one.
+__device__ __forceinline__ int32_t flat_quot(int32_t m, int32_t u, float inv) {
+    int32_t q = __float2int_rz(__int2float_rn(m) * inv);
+    int32_t r = m - q * u;
+    while (r < 0) {
+        --q;
+        r += u;
+    }
+    while (r >= u) {
+        ++q;
+        r -= u;
+    }
+    return q;
+}
+__device__ __forceinline__ int64_t flat_quot(int64_t m, int64_t u, double inv) { return quot_small(m, u, inv); }
 
 // The plan's flat decision table and the restored path; false if T cannot
 // hold the plan's values.
@@ -1590,7 +1613,7 @@ template <typename T>
 __device__ __forceinline__ bool exact_flatten(const ShapeTables &t, const ExactState &st, int64_t conserved,
                                               ExactFlat<T> &f) {
     const int R = st.R, J = st.J;
-    if (sizeof(T) == 4 && conserved >= (int64_t{1} << 30)) return false;
+    if (sizeof(T) == 4 && conserved >= (int64_t{1} << 20)) return false;
     int p = 0, kprev = 0;
     for (int k = 0; k < R; ++k) {
         const int s = st.shp[k];
@@ -1607,37 +1630,52 @@ __device__ __forceinline__ bool exact_flatten(const ShapeTables &t, const ExactS
             kprev = k;
             f.u[p] = static_cast<T>(u);
             f.cap[p] = static_cast<T>(cp);
-            f.inv[p] = t.inv_unit[s * J + j];
+            f.mres[p] = i == 0 ? static_cast<T>(Mk) : T(-1);
+            f.inv[p] = static_cast<typename ExactFlat<T>::Inv>(t.inv_unit[s * J + j]);
             f.x[p] = static_cast<T>(st.x[k * J + j]);
         }
     }
     f.D = p;
     f.meta[p] = (1u + static_cast<uint32_t>(R - kprev)) << 24;
+    f.u[p] = 1;
+    f.cap[p] = 0;
+    f.mres[p] = -1;
+    f.inv[p] = 1;
     for (int j = 0; j < J; ++j) f.lam[j] = static_cast<T>(st.lam[j]);
     return true;
 }
 
 // The pruning test on the flat table (exact_pruned's rule): prune iff
 // count + min(lam_total, bound) <= best, the bound summed from position p
-// with the current replica's budget mr.
+// with the current replica's budget mr.  Two positions per step, their
+// table entries loaded together.
 template <typename T>
 __device__ __forceinline__ bool flat_pruned(const ExactFlat<T> &f, int p, T mr, T count, T conserved, T best) {
     if (conserved <= best) return true;
     const T need = best - count;
     if (need < 0) return false;
     T acc = 0, m = mr;
-    for (int q = p; q < f.D; ++q) {
-        const uint32_t mt = f.meta[q];
-        if (q > p && (mt & 0x10000u)) m = f.M[(mt >> 8) & 0xff];
-        const T u = f.u[q];
-        T tk = f.cap[q];
-        const T l = f.lam[mt & 0xff];
-        if (l < tk) tk = l;
-        if (tk * u > m) tk = static_cast<T>(quot_small(m, u, f.inv[q]));
+    for (int q = p; q < f.D; q += 2) {
+        const uint32_t ma = f.meta[q], mb = f.meta[q + 1];
+        const T ua = f.u[q], ub = f.u[q + 1], ca = f.cap[q], cb = f.cap[q + 1];
+        const T ra = f.mres[q], rb = f.mres[q + 1];
+        const T la = f.lam[ma & 0xff], lb = f.lam[mb & 0xff];
+        if (q > p && ra >= 0) m = ra;
+        T tk = la < ca ? la : ca;
+        if (tk * ua > m) tk = flat_quot(m, ua, f.inv[q]);
         if (tk > 0) {
             acc += tk;
             if (acc > need) return false;
-            m -= tk * u;
+            m -= tk * ua;
+        }
+        if (q + 1 >= f.D) break;
+        if (rb >= 0) m = rb;
+        tk = lb < cb ? lb : cb;
+        if (tk * ub > m) tk = flat_quot(m, ub, f.inv[q + 1]);
+        if (tk > 0) {
+            acc += tk;
+            if (acc > need) return false;
+            m -= tk * ub;
         }
     }
     return true;
@@ -1697,7 +1735,7 @@ __device__ void exact_dfs_flat(ExactFlat<T> &f, const ExactState &st, int p, int
             const T u = f.u[p];
             T hi = f.cap[p];
             if (f.lam[j] < hi) hi = f.lam[j];
-            if (hi * u > mr) hi = static_cast<T>(quot_small(mr, u, f.inv[p]));
+            if (hi * u > mr) hi = flat_quot(mr, u, f.inv[p]);
             f.mr_at[p] = mr;
             f.x[p] = hi;
             f.lam[j] -= hi;
@@ -1705,7 +1743,7 @@ __device__ void exact_dfs_flat(ExactFlat<T> &f, const ExactState &st, int p, int
             count += hi;
             ++p;
             const uint32_t mn = f.meta[p];
-            if (p < D && (mn & 0x10000u)) mr = f.M[(mn >> 8) & 0xff];
+            if (f.mres[p] >= 0) mr = f.mres[p];
             nodes += mn >> 24;
             continue;
         }
@@ -1725,7 +1763,7 @@ __device__ void exact_dfs_flat(ExactFlat<T> &f, const ExactState &st, int p, int
         mr = f.mr_at[q] - v * f.u[q];
         p = q + 1;
         const uint32_t mn = f.meta[p];
-        if (p < D && (mn & 0x10000u)) mr = f.M[(mn >> 8) & 0xff];
+        if (f.mres[p] >= 0) mr = f.mres[p];
         nodes += mn >> 24;
         calling = true;
     }

@@ -1,6 +1,6 @@
-# exact-path sweep on config 1-B&B: first cap x growth x frontier target
-for cfg in "8192 4 0" "8192 2 0" "4096 2 0" "16384 2 0" "8192 3 0" "8192 4 16384" "8192 2 16384" "4096 4 16384" "2048 4 32768"; do
+# exact-path sweep on config 1-B&B: first cap x growth x rounds
+for cfg in "8192 4 6" "8192 2 10" "8192 1 12" "4096 2 10" "16384 1 10" "4096 1 14" "8192 3 8" "2048 2 12"; do
   set -- $cfg
-  echo "== cap0 $1 growth $2 target $3"
-  OSERVE_EXACT_CAP0=$1 OSERVE_EXACT_GROWTH=$2 OSERVE_EXACT_TARGET=$3 OSERVE_EXACT_ROUNDS=10 timeout 200 python scripts/time_exact.py 2>&1 | grep -E "gpu exhaustive" | tail -1
+  echo "== cap0 $1 growth $2 rounds $3"
+  OSERVE_EXACT_CAP0=$1 OSERVE_EXACT_GROWTH=$2 OSERVE_EXACT_ROUNDS=$3 timeout 200 python scripts/time_exact.py 2>&1 | grep -E "gpu exhaustive" | tail -1
 done
