@@ -205,6 +205,7 @@ def main():
     gen_f3(ref)
     gen_f4(ref)
     gen_exact_budget(ref, Oracle("port"))
+    gen_exact_wide(ref, Oracle("port"))
     print("golden fixtures written to", OUT)
 
 
@@ -293,6 +294,31 @@ def gen_exact_budget(ref, port):
     json.dump(cases, open(os.path.join(OUT, "exact_budget.json"), "w"))
 
 
+def gen_exact_wide(ref, port):
+    """B&B abort boundary on instances whose values need the 64-bit DFS
+    table: large request sizes (row LCMs past 2^30) and, with the demand
+    limit raised, demands past 2^20 -> exact_budget_wide.json."""
+    cases = []
+    sets = [(random_instances(77, 300, 5, 3, 130, max_n=20000), core.SolveOptions()),
+            (random_instances(78, 60, 2, 2, 3_000_000, max_n=100), core.SolveOptions(4_000_000, 20, 8_000_000))]
+    for insts, opts in sets:
+        for n, e, lam in insts:
+            R, J = len(n), len(lam)
+            if R * J > opts.exact_cell_limit or sum(lam) > opts.exact_demand_limit:
+                continue
+            N = port.solve_assignment(n, e, lam, opts).work
+            if N < 30 or N > 4_000_000:
+                continue
+            row = {"n": n, "e": e, "lambda": lam, "nodes": N, "demand_limit": opts.exact_demand_limit,
+                   "budgets": []}
+            for b in (N - 1, N, N // 2):
+                ll = ref.solve_assignment(n, e, lam, core.SolveOptions(opts.exact_demand_limit, 20, b))
+                row["budgets"].append({"budget": b, "x": ll.assignment.x, "objective": ll.assignment.objective})
+            cases.append(row)
+    json.dump(cases, open(os.path.join(OUT, "exact_budget_wide.json"), "w"))
+    print(len(cases), "wide exact cases")
+
+
 def gen_wide(ref):
     """Config 5-7B (g_min = 1, sizes {1,2,4}: 32-128 replicas per plan) ->
     plans_cfg5_7b.json and wide.json.  The sample is weighted toward plans
@@ -371,6 +397,8 @@ if __name__ == "__main__":
         gen_f4(Oracle("ref"))
     elif sys.argv[1:] == ["exact"]:
         gen_exact_budget(Oracle("ref"), Oracle("port"))
+    elif sys.argv[1:] == ["exact_wide"]:
+        gen_exact_wide(Oracle("ref"), Oracle("port"))
     elif sys.argv[1:] == ["wide"]:
         gen_wide(Oracle("ref"))
     elif sys.argv[1:2] == ["sample"]:  # python oracle/gen_golden.py sample cfg5_full

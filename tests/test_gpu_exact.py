@@ -15,6 +15,8 @@ from paper_2602_12151_b200._native import GpuContext
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CASES = json.load(open(os.path.join(ROOT, "tests", "golden", "exact_budget.json")))
+# values that need the 64-bit DFS table: row LCMs past 2^30, demands past 2^20
+WIDE = json.load(open(os.path.join(ROOT, "tests", "golden", "exact_budget_wide.json")))
 
 
 @pytest.fixture(scope="module")
@@ -45,3 +47,13 @@ def test_exact_batch_default_budget(gctx):
             ref = c["budgets"][1] if c["nodes"] <= 8_000_000 else None
             if ref is not None:
                 assert int(obj[i]) == ref["objective"] and x[i].tolist() == ref["x"]
+
+
+@pytest.mark.parametrize("which", [0, 1, 2])
+def test_exact_budget_boundary_wide_values(gctx, which):
+    for c in WIDE:
+        b = c["budgets"][which]
+        gctx.set_solve_options(core.SolveOptions(c["demand_limit"], 20, b["budget"]))
+        x, obj, *_ = gctx.solve_batch(np.asarray([c["n"]]), np.asarray([c["e"]]), np.asarray([c["lambda"]]))
+        assert int(obj[0]) == b["objective"] and x[0].tolist() == b["x"], (c["nodes"], b["budget"])
+    gctx.set_solve_options(core.SolveOptions())

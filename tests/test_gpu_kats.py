@@ -40,6 +40,23 @@ def test_capacity_kats(cuda):
         assert table.latency == k["latency"], k["fixture"]  # FP64, 0 ulp
 
 
+def test_capacity_kats_module(cuda):
+    """The same fixtures through cost.build_capacity_table (cached contexts:
+    each fixture twice, the second a cache hit)."""
+    from paper_2602_12151_b200 import cost
+    for _ in range(2):
+        for k in gold("kats.json")["capacity"]:
+            machines, per = k["cluster"]
+            types = [core.WorkloadType(**t) for t in k["types"]]
+            dep = core.Deployment([core.ReplicaConfig(i, t, p) for i, t, p in k["deployment"]])
+            table = cost.build_capacity_table(dep, types, core.ModelSpec(**k["model"]), core.cluster(machines, per),
+                                              core.ProfileParams(**k["params"]), k["span"])
+            assert table.n == k["n"] and table.e == k["e"] and table.latency == k["latency"], k["fixture"]
+            [t2] = cost.build_capacity_tables([dep], types, core.ModelSpec(**k["model"]),
+                                              core.cluster(machines, per), core.ProfileParams(**k["params"]), k["span"])
+            assert t2.n == table.n and t2.latency == table.latency
+
+
 def test_assignment_kats(cuda):
     g = GpuContext(core.cluster(1, 8), core.model_140gb())
     for k in gold("kats.json")["assignment"]:

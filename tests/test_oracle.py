@@ -83,6 +83,17 @@ def test_solver_matches_reference_goldens(port):
         port.check_constraints(ll.assignment.x, inst["n"], inst["e"], inst["lambda"])
 
 
+@pytest.mark.parametrize("name", ["exact_budget.json", "exact_budget_wide.json"])
+def test_exact_budget_boundary(port, name):
+    """The B&B abort boundary fixtures (reference results at budgets N-1, N,
+    N/2 around the node count N): the restatement reproduces every one."""
+    for c in gold(name):
+        lim = c.get("demand_limit", 400)
+        for b in c["budgets"]:
+            ll = port.solve_assignment(c["n"], c["e"], c["lambda"], core.SolveOptions(lim, 20, b["budget"]))
+            assert ll.assignment.objective == b["objective"] and ll.assignment.x == b["x"], (c["nodes"], b)
+
+
 def test_check_constraints_detects_violations(port):
     n, e = [[80, 50]], [[80, 50]]
     with pytest.raises(core.LogicError):
