@@ -156,7 +156,7 @@ def kv_arrays(drained, nd: int, mig, nm: int, buffer_bytes: int):
     """kv_plan outputs as numpy: drained ids [nd], migrated rows [nm, 4] =
     (request_id, kv_bytes, src, dst), buffer bytes."""
     import numpy as np
-    d = np.ctypeslib.as_array(drained, shape=(max(1, nd),))[:nd].copy()
+    d = np.ctypeslib.as_array(drained)[:nd].copy()
     rec = np.dtype([("request_id", "<i8"), ("kv_bytes", "<u8"), ("src", "<i4"), ("dst", "<i4")])
     raw = np.frombuffer(mig, dtype=rec, count=nm) if nm else np.zeros(0, rec)
     m = np.stack([raw["request_id"], raw["kv_bytes"].astype(np.int64), raw["src"], raw["dst"]], axis=1) \

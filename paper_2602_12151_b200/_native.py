@@ -461,8 +461,11 @@ class GpuContext:
         reqs = A.inflight_arr(inflight, keep)
         tr, ntr = A.transfer_arr(carry, keep)
         n = len(inflight)
-        drained = (C.c_int64 * max(1, n))()
-        mig = (A.KvTransferDesc * max(1, n))()
+        # output buffers kept across calls (results are copied out below)
+        bufs = getattr(self, "_kv_bufs", None)
+        if bufs is None or bufs[0] < n:
+            bufs = self._kv_bufs = (max(1, n), (C.c_int64 * max(1, n))(), (A.KvTransferDesc * max(1, n))())
+        drained, mig = bufs[1], bufs[2]
         nd, nm, buf = C.c_int(), C.c_int(), C.c_uint64()
         self._chk(self.lib.oserve_gpu_kv_plan(self.h, n, reqs, threshold_tokens, C.byref(s), C.byref(d),
                                               float(headroom), ntr, tr, drained, C.byref(nd), mig, C.byref(nm),

@@ -2066,6 +2066,14 @@ int oserve_gpu_kv_plan(oserve_gpu_ctx *ctx, int n_inflight, const oserve_infligh
                        const oserve_transfer *carry, int64_t *drained, int *n_drained, oserve_kv_transfer *migrated,
                        int *n_migrated, uint64_t *buffer_bytes) {
     return guarded(ctx, [&] {
+        static const bool dbg = getenv("OSERVE_DEBUG_KV") != nullptr;
+        auto t0 = std::chrono::steady_clock::now();
+        auto lap = [&](const char *what) {
+            if (!dbg) return;
+            const auto t1 = std::chrono::steady_clock::now();
+            std::fprintf(stderr, "[kv] %-10s %7.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+            t0 = t1;
+        };
         if (headroom < 0.0 || headroom > 0.5) fail(OSERVE_ERR_INVALID_ARGUMENT, "kv_plan: headroom must be in [0, 0.5]");
         for (int q = 0; q < n_inflight; ++q) {
             const auto &r = inflight[q];
@@ -2074,6 +2082,7 @@ int oserve_gpu_kv_plan(oserve_gpu_ctx *ctx, int n_inflight, const oserve_infligh
                 fail(OSERVE_ERR_INVALID_ARGUMENT, "kv_plan: request " + std::to_string(r.request_id) +
                                                       " names unknown source replica");
         }
+        lap("validate");
         // device slots: cluster devices plus any id of the deployments / carry, ascending
         std::set<int> ids(ctx->dev_sorted.begin(), ctx->dev_sorted.end());
         auto add = [&](const oserve_deployment &d) {
@@ -2110,43 +2119,11 @@ int oserve_gpu_kv_plan(oserve_gpu_ctx *ctx, int n_inflight, const oserve_infligh
         std::vector<int32_t> soff, sdev, doff, ddev;
         flat(*src, soff, sdev);
         flat(*dst, doff, ddev);
+        lap("slots");
         std::vector<uint64_t> load(static_cast<size_t>(NS) * NS, 0);
         for (int i = 0; i < n_carry; ++i)  // SwitchPlan::link_load from its transfers
             load[static_cast<size_t>(slot[carry[i].src]) * NS + slot[carry[i].dst]] += carry[i].end - carry[i].begin;
-        std::vector<int64_t> gen(n_inflight);
-        std::vector<uint64_t> kv(n_inflight);
-        std::vector<int32_t> sr(n_inflight);
-        for (int q = 0; q < n_inflight; ++q) {
-            gen[q] = inflight[q].generated_tokens;
-            kv[q] = inflight[q].kv_bytes;
-            sr[q] = inflight[q].source_replica;
-        }
-        cudaStream_t s = ctx->stream;
-        DBuf *b = ctx->sc_kv;
-        KvPlanIn in{};
-        in.n = n_inflight;
-        in.gen = b[0].upload(gen, s);
-        in.kv = b[1].upload(kv, s);
-        in.srcrep = b[2].upload(sr, s);
-        in.threshold = threshold_tokens;
-        in.num_slots = NS;
-        in.none_slot = slot.count(-1) ? slot[-1] : -1;
-        in.machine = b[3].upload(machine, s);
-        in.dev_id = b[4].upload(dev_id, s);
-        in.src_reps = src->num_replicas;
-        in.dst_reps = dst->num_replicas;
-        in.n_src_devs = static_cast<int>(sdev.size());
-        in.n_dst_devs = static_cast<int>(ddev.size());
-        in.src_off = b[5].upload(soff, s);
-        in.src_devs = b[6].upload(sdev, s);
-        in.dst_off = b[7].upload(doff, s);
-        in.dst_devs = b[8].upload(ddev, s);
-        in.load = b[9].upload(load, s);
-        in.inbound = static_cast<uint64_t *>(b[10].get(sizeof(uint64_t) * NS));
-        cuda_ok(cudaMemsetAsync(in.inbound, 0, sizeof(uint64_t) * NS, s), "memset");
-        in.kind = static_cast<int32_t *>(b[11].get(sizeof(int32_t) * std::max(n_inflight, 1)));
-        in.mig_src = static_cast<int32_t *>(b[12].get(sizeof(int32_t) * std::max(n_inflight, 1)));
-        in.mig_dst = static_cast<int32_t *>(b[13].get(sizeof(int32_t) * std::max(n_inflight, 1)));
+        lap("load");
         // Requests migrating to different target replicas are independent
         // (disjoint devices): partition them by target replica (round-robin
         // over the migrated sequence, switchplan.cpp:178-181) for the
@@ -2158,43 +2135,110 @@ int oserve_gpu_kv_plan(oserve_gpu_ctx *ctx, int n_inflight, const oserve_infligh
             std::set<int32_t> seen(ddev.begin(), ddev.end());
             if (seen.size() != ddev.size()) par = false;
         }
-        DBuf *pb = ctx->sc_kv + 14;
+        cudaStream_t s = ctx->stream;
+        DBuf *b = ctx->sc_kv;
+        KvPlanIn in{};
+        in.n = n_inflight;
+        in.threshold = threshold_tokens;
+        in.num_slots = NS;
+        in.none_slot = slot.count(-1) ? slot[-1] : -1;
+        in.src_reps = src->num_replicas;
+        in.dst_reps = dst->num_replicas;
+        in.n_src_devs = static_cast<int>(sdev.size());
+        in.n_dst_devs = static_cast<int>(ddev.size());
+        in.h_dst_off = doff.data();
+        const int R = dst->num_replicas;
+        std::vector<int32_t> goff, gsr, gpos;  // gpos: group position of the m-th migrated request
+        std::vector<uint64_t> gkv;
+        std::vector<int64_t> gen;
+        std::vector<uint64_t> kv;
+        std::vector<int32_t> sr;
+        int m_tot = 0;
         if (par) {
-            std::vector<int32_t> goff(dst->num_replicas + 1, 0), greq;
-            int m = 0;
-            for (int q = 0; q < n_inflight; ++q)
-                if (gen[q] > threshold_tokens) ++goff[(m++ % dst->num_replicas) + 1];
-            for (int r = 0; r < dst->num_replicas; ++r) goff[r + 1] += goff[r];
-            greq.resize(static_cast<size_t>(std::max(m, 1)));
+            // the m-th migrated request goes to target replica m mod R: group
+            // sizes follow from the count, no per-request division
+            for (int q = 0; q < n_inflight; ++q) m_tot += inflight[q].generated_tokens > threshold_tokens;
+            goff.assign(static_cast<size_t>(R) + 1, 0);
+            for (int r = 0; r < R; ++r) goff[r + 1] = goff[r] + m_tot / R + (r < m_tot % R ? 1 : 0);
+            gkv.resize(static_cast<size_t>(std::max(m_tot, 1)));
+            gsr.resize(gkv.size());
+            gpos.resize(gkv.size());
             std::vector<int32_t> fill(goff.begin(), goff.end() - 1);
-            m = 0;
-            for (int q = 0; q < n_inflight; ++q)
-                if (gen[q] > threshold_tokens) greq[fill[m++ % dst->num_replicas]++] = q;
-            in.grp_off = pb[0].upload(goff, s);
-            in.grp_req = pb[1].upload(greq, s);
-            cuda_ok(cudaMemsetAsync(in.kind, 0, sizeof(int32_t) * n_inflight, s), "memset");
-            cuda_ok(cudaMemsetAsync(in.mig_src, 0, sizeof(int32_t) * n_inflight, s), "memset");
-            cuda_ok(cudaMemsetAsync(in.mig_dst, 0, sizeof(int32_t) * n_inflight, s), "memset");
+            int m = 0, r = 0;
+            for (int q = 0; q < n_inflight; ++q) {
+                if (inflight[q].generated_tokens <= threshold_tokens) continue;
+                const int at = fill[r]++;
+                r = r + 1 == R ? 0 : r + 1;
+                gkv[at] = inflight[q].kv_bytes;
+                gsr[at] = inflight[q].source_replica;
+                gpos[m++] = at;
+            }
+        } else {
+            gen.resize(n_inflight);
+            kv.resize(n_inflight);
+            sr.resize(n_inflight);
+            for (int q = 0; q < n_inflight; ++q) {
+                gen[q] = inflight[q].generated_tokens;
+                kv[q] = inflight[q].kv_bytes;
+                sr[q] = inflight[q].source_replica;
+            }
         }
+        lap("host prep");
+        in.machine = b[3].upload(machine, s);
+        in.dev_id = b[4].upload(dev_id, s);
+        in.src_off = b[5].upload(soff, s);
+        in.src_devs = b[6].upload(sdev, s);
+        in.dst_off = b[7].upload(doff, s);
+        in.dst_devs = b[8].upload(ddev, s);
+        in.load = b[9].upload(load, s);
+        in.inbound = static_cast<uint64_t *>(b[10].get(sizeof(uint64_t) * NS));
+        cuda_ok(cudaMemsetAsync(in.inbound, 0, sizeof(uint64_t) * NS, s), "memset");
+        if (par) {
+            DBuf *pb = ctx->sc_kv + 14;
+            in.grp_off = pb[0].upload(goff, s);
+            in.grp_kv = b[1].upload(gkv, s);
+            in.grp_sr = b[2].upload(gsr, s);
+            in.grp_src = static_cast<int32_t *>(b[12].get(sizeof(int32_t) * gkv.size()));
+            in.grp_dst = static_cast<int32_t *>(b[13].get(sizeof(int32_t) * gkv.size()));
+        } else {
+            in.gen = b[0].upload(gen, s);
+            in.kv = b[1].upload(kv, s);
+            in.srcrep = b[2].upload(sr, s);
+            in.kind = static_cast<int32_t *>(b[11].get(sizeof(int32_t) * std::max(n_inflight, 1)));
+            in.mig_src = static_cast<int32_t *>(b[12].get(sizeof(int32_t) * std::max(n_inflight, 1)));
+            in.mig_dst = static_cast<int32_t *>(b[13].get(sizeof(int32_t) * std::max(n_inflight, 1)));
+        }
+        lap("upload");
         cuda_ok(launch_kv_plan(in, s, &ctx->launches), "kv_plan kernel");
+        if (dbg) cuda_ok(cudaStreamSynchronize(s), "sync");
+        lap("kernel");
         std::vector<int32_t> kind, ms, md;
-        download(kind, in.kind, n_inflight, s);
-        download(ms, in.mig_src, n_inflight, s);
-        download(md, in.mig_dst, n_inflight, s);
+        if (par) {
+            download(ms, in.grp_src, static_cast<size_t>(m_tot), s);
+            download(md, in.grp_dst, static_cast<size_t>(m_tot), s);
+        } else {
+            download(kind, in.kind, n_inflight, s);
+            download(ms, in.mig_src, n_inflight, s);
+            download(md, in.mig_dst, n_inflight, s);
+        }
         cuda_ok(cudaStreamSynchronize(s), "sync");
+        lap("download");
         int nd = 0, nm = 0;
         uint64_t migrated_bytes = 0;
         for (int q = 0; q < n_inflight; ++q) {
-            if (kind[q] == 0) {
+            const bool mig = par ? inflight[q].generated_tokens > threshold_tokens : kind[q] != 0;
+            if (!mig) {
                 drained[nd++] = inflight[q].request_id;
             } else {
-                migrated[nm++] = {inflight[q].request_id, inflight[q].kv_bytes, ms[q], md[q]};
+                const size_t at = par ? static_cast<size_t>(gpos[nm]) : static_cast<size_t>(q);
+                migrated[nm++] = {inflight[q].request_id, inflight[q].kv_bytes, ms[at], md[at]};
                 migrated_bytes += inflight[q].kv_bytes;
             }
         }
         *n_drained = nd;
         *n_migrated = nm;
         *buffer_bytes = static_cast<uint64_t>(std::ceil(static_cast<double>(migrated_bytes) * (1.0 + headroom)));
+        lap("assemble");
     });
 }
 

@@ -268,9 +268,14 @@ struct KvPlanIn {
     int32_t *kind;               // [n] 0 drained, 1 migrated
     int32_t *mig_src, *mig_dst;  // [n] device ids
     // target-replica partition (parallel path): the migrated requests of
-    // target replica r, in order, are grp_req[grp_off[r] .. grp_off[r+1])
+    // target replica r, in order, are entries grp_off[r] .. grp_off[r+1] of
+    // the group-ordered arrays (kv bytes, source replica in; picked source
+    // and target device ids out); kind / mig_* / gen are unused then
     const int32_t *grp_off;      // [dst_reps+1] or null (sequential kernel)
-    const int32_t *grp_req;
+    const uint64_t *grp_kv;
+    const int32_t *grp_sr;
+    int32_t *grp_src, *grp_dst;
+    const int32_t *h_dst_off;    // host copy of dst_off (launch geometry)
 };
 int launch_kv_plan(const KvPlanIn &in, void *stream, uint64_t *launches);
 

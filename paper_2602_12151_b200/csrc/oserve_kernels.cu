@@ -2723,9 +2723,8 @@ __global__ void __launch_bounds__(128) k_kv_plan_par(KvPlanIn in) {
     const int g0 = in.grp_off[r], g1 = in.grp_off[r + 1];
     for (int base = g0; base < g1; base += 32) {
         const int idx = base + lane;
-        const int my_q = idx < g1 ? in.grp_req[idx] : 0;
-        const uint64_t my_kv = idx < g1 ? in.kv[my_q] : 0;
-        const int my_sr = idx < g1 ? in.srcrep[my_q] : 0;
+        const uint64_t my_kv = idx < g1 ? in.grp_kv[idx] : 0;
+        const int my_sr = idx < g1 ? in.grp_sr[idx] : 0;
         int my_src = 0, my_dst = 0;
         const int cnt = g1 - base < 32 ? g1 - base : 32;
         for (int b = 0; b < cnt; ++b) {
@@ -2765,9 +2764,89 @@ __global__ void __launch_bounds__(128) k_kv_plan_par(KvPlanIn in) {
             __syncwarp();
         }
         if (idx < g1) {
-            in.kind[my_q] = 1;
-            in.mig_src[my_q] = in.dev_id[my_src];
-            in.mig_dst[my_q] = in.dev_id[my_dst];
+            in.grp_src[idx] = in.dev_id[my_src];
+            in.grp_dst[idx] = in.dev_id[my_dst];
+        }
+    }
+}
+
+// The lexicographic minimum (cls, v, slot) of the warp's candidates by four
+// 32-bit warp reductions (cls, v's high word, low word, slot) instead of a
+// shuffle tree; returns the winning slot (0x7fffffff when no lane has one).
+__device__ __forceinline__ int kv_pick_redux(const KvPick &p) {
+    const bool valid = p.slot != 0x7fffffff;
+    const unsigned c = valid ? static_cast<unsigned>(p.cls) : 0xffffffffu;
+    const unsigned cm = __reduce_min_sync(0xffffffffu, c);
+    bool in = valid && c == cm;
+    const unsigned hi = in ? static_cast<unsigned>(p.v >> 32) : 0xffffffffu;
+    const unsigned hm = __reduce_min_sync(0xffffffffu, hi);
+    in = in && hi == hm;
+    const unsigned lo = in ? static_cast<unsigned>(p.v) : 0xffffffffu;
+    const unsigned lm = __reduce_min_sync(0xffffffffu, lo);
+    in = in && lo == lm;
+    const unsigned sl = in ? static_cast<unsigned>(p.slot) : 0x7fffffffu;
+    return static_cast<int>(__reduce_min_sync(0xffffffffu, sl));
+}
+
+// k_kv_plan_par with the replica's state in shared memory: a warp (one CTA)
+// per target replica of <= 32 devices holds the inbound loads of those
+// devices and their link-load columns (every source slot -> each of them):
+// the only state its picks read or write, so the request walk never leaves
+// shared memory.  Columns start from the carried plan's loads.
+__global__ void __launch_bounds__(32) k_kv_plan_par_smem(KvPlanIn in, int ndmax) {
+    extern __shared__ __align__(16) unsigned char kv_smem[];
+    const int lane = threadIdx.x, r = blockIdx.x;
+    constexpr int kNone = 0x7fffffff;
+    const int NS = in.num_slots;
+    const int d0 = in.dst_off[r], nd = in.dst_off[r + 1] - d0;
+    uint64_t *inb = reinterpret_cast<uint64_t *>(kv_smem);         // [nd]
+    uint64_t *col = inb + ndmax;                                     // [NS][nd]
+    for (int i = lane; i < nd; i += 32) inb[i] = in.inbound[in.dst_devs[d0 + i]];
+    for (int i = lane; i < NS * nd; i += 32) {
+        const int sl = i / nd, tl = i - sl * nd;
+        col[i] = in.load[static_cast<size_t>(sl) * NS + in.dst_devs[d0 + tl]];
+    }
+    __syncwarp();
+    const int my_tslot = lane < nd ? in.dst_devs[d0 + lane] : kNone;
+    const int g0 = in.grp_off[r], g1 = in.grp_off[r + 1];
+    for (int base = g0; base < g1; base += 32) {
+        const int idx = base + lane;
+        const uint64_t my_kv = idx < g1 ? in.grp_kv[idx] : 0;
+        const int my_sr = idx < g1 ? in.grp_sr[idx] : 0;
+        int my_src = 0, my_dst = 0;
+        const int cnt = g1 - base < 32 ? g1 - base : 32;
+        for (int b = 0; b < cnt; ++b) {
+            const uint64_t kvq = __shfl_sync(0xffffffffu, my_kv, b);
+            const int srq = __shfl_sync(0xffffffffu, my_sr, b);
+            KvPick t{~0ull, 2, kNone};
+            if (lane < nd) t = KvPick{inb[lane], 0, my_tslot};
+            const int target = kv_pick_redux(t);
+            const int tl = __ffs(__ballot_sync(0xffffffffu, my_tslot == target)) - 1;
+            const int s0 = in.src_off[srq], s1 = in.src_off[srq + 1];
+            KvPick bsel{~0ull, 2, kNone};
+            const int mt = __ldg(in.machine + target);
+            for (int p = s0 + lane; p < s1; p += 32) {
+                const int slot = __ldg(in.src_devs + p);
+                const int ms = __ldg(in.machine + slot);
+                const KvPick c{col[slot * nd + tl], (ms >= 0 && ms == mt) ? 0 : 1, slot};
+                if (kv_less(c, bsel)) bsel = c;
+            }
+            const int bslot = kv_pick_redux(bsel);
+            const int best = bslot == kNone ? in.none_slot : bslot;
+            __syncwarp();
+            if (lane == 0) {
+                col[best * nd + tl] += kvq;
+                inb[tl] += kvq;
+            }
+            if (lane == b) {
+                my_src = best;
+                my_dst = target;
+            }
+            __syncwarp();
+        }
+        if (idx < g1) {
+            in.grp_src[idx] = in.dev_id[my_src];
+            in.grp_dst[idx] = in.dev_id[my_dst];
         }
     }
 }
@@ -3106,8 +3185,21 @@ int sort_keys(uint64_t *keys, uint64_t *tmp_keys, int n, void **temp, size_t *te
 int launch_kv_plan(const KvPlanIn &in, void *stream, uint64_t *launches) {
     cudaGetLastError();
     if (in.n == 0) return 0;
-    if (in.grp_off) {  // target-replica parallel path (kind / mig_* pre-zeroed by the caller)
-        k_kv_plan_par<<<(in.dst_reps + 3) / 4, 128, 0, static_cast<cudaStream_t>(stream)>>>(in);
+    if (in.grp_off) {  // target-replica parallel path (group-ordered arrays)
+        int ndmax = 0;
+        for (int r = 0; r < in.dst_reps; ++r) ndmax = std::max(ndmax, in.h_dst_off[r + 1] - in.h_dst_off[r]);
+        const size_t smem = sizeof(uint64_t) * (static_cast<size_t>(ndmax) + static_cast<size_t>(in.num_slots) * ndmax);
+        bool use = ndmax <= 32 && smem <= 96 * 1024;
+        if (use && smem > 48 * 1024 &&
+            cudaFuncSetAttribute(k_kv_plan_par_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024) !=
+                cudaSuccess) {
+            cudaGetLastError();
+            use = false;
+        }
+        if (use)
+            k_kv_plan_par_smem<<<in.dst_reps, 32, smem, static_cast<cudaStream_t>(stream)>>>(in, ndmax);
+        else
+            k_kv_plan_par<<<(in.dst_reps + 3) / 4, 128, 0, static_cast<cudaStream_t>(stream)>>>(in);
         if (launches) ++*launches;
         return check(cudaGetLastError());
     }
