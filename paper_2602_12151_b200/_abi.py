@@ -258,6 +258,34 @@ def deployment_desc(dep: core.Deployment, keep: Keep) -> DeploymentDesc:
     return DeploymentDesc(dep.replica_count(), nd, ids, tp, pp)
 
 
+def deployment_desc_array(deps: Sequence[core.Deployment], keep: Keep):
+    """A DeploymentDesc array for many deployments: the replica fields of all
+    of them packed into four int arrays, the descriptors' pointers filled by
+    numpy offset arithmetic (no per-deployment ctypes arrays)."""
+    import numpy as np
+    n = len(deps)
+    nrep = np.fromiter((len(d.replicas) for d in deps), np.int64, n)
+    reps = [r for d in deps for r in d.replicas]
+    nd = keep(np.fromiter((len(r.device_ids) for r in reps), np.int32, len(reps)))
+    tp = keep(np.fromiter((r.tp for r in reps), np.int32, len(reps)))
+    pp = keep(np.fromiter((r.pp for r in reps), np.int32, len(reps)))
+    ids = keep(np.fromiter((x for r in reps for x in r.device_ids), np.int32, int(nd.sum())))
+    roff = np.zeros(n, np.int64)
+    roff[1:] = np.cumsum(nrep)[:-1]
+    doff = np.zeros(len(reps) + 1, np.int64)
+    doff[1:] = np.cumsum(nd)
+    dt = np.dtype({"names": ["num_replicas", "rnd", "ids", "tp", "pp"],
+                   "formats": ["<i4", "<u8", "<u8", "<u8", "<u8"],
+                   "offsets": [0, 8, 16, 24, 32], "itemsize": C.sizeof(DeploymentDesc)})
+    a = keep(np.zeros(max(1, n), dt))
+    a["num_replicas"][:n] = nrep
+    a["rnd"][:n] = nd.ctypes.data + 4 * roff
+    a["ids"][:n] = ids.ctypes.data + 4 * doff[roff]
+    a["tp"][:n] = tp.ctypes.data + 4 * roff
+    a["pp"][:n] = pp.ctypes.data + 4 * roff
+    return C.cast(a.ctypes.data, C.POINTER(DeploymentDesc))
+
+
 def space_desc(mode: int, sizes: Sequence[int] = (), max_devices: int = 0, keep: Keep = None) -> SpaceDesc:
     keep = keep or Keep()
     sz = keep(_arr(C.c_int, sizes))

@@ -331,9 +331,7 @@ class GpuContext:
 
     def evaluate_deployments(self, deps: Sequence[core.Deployment]) -> List[int]:
         keep = A.Keep()
-        arr = (A.DeploymentDesc * max(1, len(deps)))()
-        for i, d in enumerate(deps):
-            arr[i] = A.deployment_desc(d, keep)
+        arr = A.deployment_desc_array(deps, keep)
         out = (C.c_int64 * max(1, len(deps)))()
         self._chk(self.lib.oserve_gpu_evaluate_deployments(self.h, len(deps), arr, out))
         return list(out[:len(deps)])
@@ -373,9 +371,7 @@ class GpuContext:
     def switch_cost_batch(self, src: core.Deployment, dsts: Sequence[core.Deployment]):
         keep = A.Keep()
         s = A.deployment_desc(src, keep)
-        arr = (A.DeploymentDesc * max(1, len(dsts)))()
-        for i, d in enumerate(dsts):
-            arr[i] = A.deployment_desc(d, keep)
+        arr = A.deployment_desc_array(dsts, keep)
         est = (C.c_double * max(1, len(dsts)))()
         mb = (C.c_uint64 * max(1, len(dsts)))()
         self._chk(self.lib.oserve_gpu_switch_cost_batch(self.h, C.byref(s), len(dsts), arr, est, mb))
@@ -400,8 +396,8 @@ class GpuContext:
         off = keep(np.ascontiguousarray(edge_offset, dtype=np.int64))
         ed = A.flow_edges(edges, keep)
         E = int(off[-1] - off[0]) if G else 0
-        fl = np.zeros(max(1, E), np.int64)
-        val = np.zeros(max(1, G), np.int64)
+        fl = np.empty(max(1, E), np.int64)  # every entry is written
+        val = np.empty(max(1, G), np.int64)
         src = keep(np.ascontiguousarray(sources, dtype=np.int32))
         snk = keep(np.ascontiguousarray(sinks, dtype=np.int32))
         self._chk(self.lib.oserve_gpu_max_flow_batch(self.h, G, _np_ptr(nn, C.c_int), _np_ptr(off, C.c_int64), ed,

@@ -19,6 +19,7 @@
 // touch neighbouring words.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "flow_core.hpp"
@@ -31,6 +32,17 @@ inline int check(cudaError_t e) { return e == cudaSuccess ? 0 : static_cast<int>
 }  // namespace
 
 // ------------------------------------------------------------------ K6a ---
+// Views of graph edges [e0, ...) in the uploaded oserve_flow_edge array.
+__device__ __forceinline__ Strided<const int32_t> mf_from(const MaxFlowBatch &b, int64_t e0) {
+    return {b.edges32 + 4 * e0, 4};
+}
+__device__ __forceinline__ Strided<const int32_t> mf_to(const MaxFlowBatch &b, int64_t e0) {
+    return {b.edges32 + 4 * e0 + 1, 4};
+}
+__device__ __forceinline__ Strided<const int64_t> mf_cap(const MaxFlowBatch &b, int64_t e0) {
+    return {reinterpret_cast<const int64_t *>(b.edges32) + 2 * e0 + 1, 2};
+}
+
 __global__ void __launch_bounds__(128) k_max_flow(MaxFlowBatch b) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= b.count) return;
@@ -42,10 +54,12 @@ __global__ void __launch_bounds__(128) k_max_flow(MaxFlowBatch b) {
     pg.m = static_cast<int>(m);
     if (b.interleave) {
         const int64_t G = b.count;
+        const auto ef = mf_from(b, e0), et = mf_to(b, e0);
+        const auto ec = mf_cap(b, e0);
         for (int64_t i = 0; i < m; ++i) {
-            b.il_from[i * G + g] = b.from[e0 + i];
-            b.il_to[i * G + g] = b.to[e0 + i];
-            b.il_cap[i * G + g] = b.cap[e0 + i];
+            b.il_from[i * G + g] = ef[i];
+            b.il_to[i * G + g] = et[i];
+            b.il_cap[i * G + g] = ec[i];
         }
         pg.from = {b.il_from + g, G};
         pg.to = {b.il_to + g, G};
@@ -68,9 +82,9 @@ __global__ void __launch_bounds__(128) k_max_flow(MaxFlowBatch b) {
         b.status[g] = 0;
         return;
     }
-    pg.from = {b.from + e0, 1};
-    pg.to = {b.to + e0, 1};
-    pg.cap = {b.cap + e0, 1};
+    pg.from = mf_from(b, e0);
+    pg.to = mf_to(b, e0);
+    pg.cap = mf_cap(b, e0);
     pg.res = {b.res + 2 * e0, 1};
     pg.arc_to = {b.arc_to + 2 * e0, 1};
     pg.adj = {b.adj + 2 * e0, 1};
@@ -85,24 +99,93 @@ __global__ void __launch_bounds__(128) k_max_flow(MaxFlowBatch b) {
         return;
     }
     b.value[g] = pr_run(pg, b.source[g], b.sink[g]);
-    for (int64_t i = 0; i < m; ++i) b.flow[e0 + i] = b.cap[e0 + i] - pg.res[2 * i];
+    for (int64_t i = 0; i < m; ++i) b.flow[e0 + i] = pg.cap[i] - pg.res[2 * i];
     b.status[g] = 0;
+}
+
+// Shared-memory bytes of one graph's residual workspace (res, excess: 8 B;
+// arc_to, adj, adj_off, height, cur, fifo: 4 B; active: 1 B).
+__host__ __device__ inline size_t mf_smem_bytes(int n, int m) {
+    return (static_cast<size_t>(16) * m + 8 * n + 8 * m + 8 * m + 4 * (n + 1) + 12 * n + n + 15) & ~size_t(15);
+}
+
+// K6a with the workspace in shared memory: a warp per graph, lane 0 runs the
+// sequential discipline (pr_build / pr_run, stride-1 views into the warp's
+// slice), the warp writes the flows.  Every dependent access of the push /
+// relabel loop is a shared-memory hit instead of an L2 round trip.
+__global__ void __launch_bounds__(256) k_max_flow_smem(MaxFlowBatch b, int per_warp) {
+    extern __shared__ __align__(16) unsigned char mf_smem[];
+    const int wpb = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = blockIdx.x * wpb + w;
+    if (g >= b.count) return;
+    const int n = b.num_nodes[g];
+    const int64_t e0 = b.edge_off[g];
+    const int m = static_cast<int>(b.edge_off[g + 1] - e0);
+    unsigned char *p = mf_smem + static_cast<size_t>(w) * per_warp;
+    int64_t *res = reinterpret_cast<int64_t *>(p);
+    int64_t *excess = res + 2 * m;
+    int32_t *arc_to = reinterpret_cast<int32_t *>(excess + n);
+    int32_t *adj = arc_to + 2 * m;
+    int32_t *adj_off = adj + 2 * m;
+    int32_t *height = adj_off + n + 1;
+    int32_t *cur = height + n;
+    int32_t *fifo = cur + n;
+    uint8_t *active = reinterpret_cast<uint8_t *>(fifo + n);
+    int ok = 1;
+    if (lane == 0) {
+        PrGraph pg;
+        pg.n = n;
+        pg.m = m;
+        pg.from = mf_from(b, e0);
+        pg.to = mf_to(b, e0);
+        pg.cap = mf_cap(b, e0);
+        pg.res = {res, 1};
+        pg.excess = {excess, 1};
+        pg.arc_to = {arc_to, 1};
+        pg.adj = {adj, 1};
+        pg.adj_off = {adj_off, 1};
+        pg.height = {height, 1};
+        pg.cur = {cur, 1};
+        pg.fifo = {fifo, 1};
+        pg.active = {active, 1};
+        ok = pr_build(pg) ? 1 : 0;
+        if (ok) b.value[g] = pr_run(pg, b.source[g], b.sink[g]);
+        b.status[g] = ok ? 0 : 1;  // 1: negative capacity
+    }
+    ok = __shfl_sync(0xffffffffu, ok, 0);
+    __syncwarp();
+    if (ok) {
+        const auto ec = mf_cap(b, e0);
+        for (int i = lane; i < m; i += 32) b.flow[e0 + i] = ec[i] - res[2 * i];
+    }
 }
 
 int launch_max_flow(const MaxFlowBatch &b, void *stream, uint64_t *launches) {
     cudaGetLastError();
     if (b.count == 0) return 0;
-    k_max_flow<<<(b.count + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(b);
+    const size_t per = mf_smem_bytes(b.n_max, b.m_max);
+    if (per <= 48 * 1024) {
+        const int wpb = static_cast<int>(std::min<size_t>(8, std::max<size_t>(1, (96 * 1024) / per)));
+        const size_t smem = per * wpb;
+        if (smem > 48 * 1024 &&  // opt in past the 48 KB default (per device: set on every such launch)
+            cudaFuncSetAttribute(k_max_flow_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024) !=
+                cudaSuccess)
+            return check(cudaGetLastError());
+        k_max_flow_smem<<<(b.count + wpb - 1) / wpb, 32 * wpb, smem, static_cast<cudaStream_t>(stream)>>>(
+            b, static_cast<int>(per));
+    } else {
+        k_max_flow<<<(b.count + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(b);
+    }
     if (launches) ++*launches;
     return check(cudaGetLastError());
 }
 
 // ------------------------------------------------------------------ K6b ---
-__global__ void __launch_bounds__(128) k_flow_assign(ShapeTables t, FlowAssignBatch b) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= b.count) return;
+// One instance: workspace element q at base[q * B] (B = the batch size for
+// the interleaved HBM workspace, 1 for a shared-memory slice).
+__device__ void flow_assign_one(const ShapeTables &t, const FlowAssignBatch &b, int i, int32_t *ws32, int64_t *ws64,
+                                uint8_t *ws8, int64_t B) {
     const int R = b.R, J = b.J;
-    const int64_t B = b.count;
     const int n = net_nodes(R, J), m = net_edges(R, J);
     const int64_t row0 = static_cast<int64_t>(i) * R;
     NetInstance in;
@@ -114,7 +197,7 @@ __global__ void __launch_bounds__(128) k_flow_assign(ShapeTables t, FlowAssignBa
     in.M = {t.M + row0, 1};
     in.lambda = {b.lambda + static_cast<int64_t>(i) * J, 1};
     // interleaved workspace: element q of instance i at [q * B + i]
-    int32_t *from = b.ws_i32 + i;
+    int32_t *from = ws32;
     int32_t *to = from + static_cast<int64_t>(m) * B;
     int32_t *arc_to = to + static_cast<int64_t>(m) * B;
     int32_t *adj = arc_to + static_cast<int64_t>(2 * m) * B;
@@ -122,11 +205,11 @@ __global__ void __launch_bounds__(128) k_flow_assign(ShapeTables t, FlowAssignBa
     int32_t *height = adj_off + static_cast<int64_t>(n + 1) * B;
     int32_t *cur = height + static_cast<int64_t>(n) * B;
     int32_t *fifo = cur + static_cast<int64_t>(n) * B;
-    int64_t *cap = b.ws_i64 + i;
+    int64_t *cap = ws64;
     int64_t *res = cap + static_cast<int64_t>(m) * B;
     int64_t *excess = res + static_cast<int64_t>(2 * m) * B;
     int64_t *mrem = excess + static_cast<int64_t>(n) * B;
-    uint8_t *active = b.ws_u8 + i;
+    uint8_t *active = ws8;
     int64_t *x = b.x + static_cast<int64_t>(i) * R * J;
     if (b.flow_in) {  // extract_assignment of a given flow
         const int64_t *fl = b.flow_in + static_cast<int64_t>(i) * m;
@@ -192,10 +275,54 @@ __global__ void __launch_bounds__(128) k_flow_assign(ShapeTables t, FlowAssignBa
     b.status[i] = 0;
 }
 
+__global__ void __launch_bounds__(128) k_flow_assign(ShapeTables t, FlowAssignBatch b) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= b.count) return;
+    flow_assign_one(t, b, i, b.ws_i32 + i, b.ws_i64 + i, b.ws_u8 + i, b.count);
+}
+
+// Workspace bytes of one instance in shared memory (i64 block first).
+__host__ __device__ inline size_t fa_smem_bytes(int R, int J) {
+    size_t i32, i64, u8;
+    const int64_t n = net_nodes(R, J), m = net_edges(R, J);
+    i32 = static_cast<size_t>(6 * m + (n + 1) + 3 * n);
+    i64 = static_cast<size_t>(3 * m + n + R);
+    u8 = static_cast<size_t>(n);
+    return (8 * i64 + 4 * i32 + u8 + 15) & ~size_t(15);
+}
+
+// K6b with the instance's workspace in shared memory: a warp per instance,
+// lane 0 runs it (the dependent loads of push-relabel and the warm start hit
+// shared memory instead of L2).
+__global__ void __launch_bounds__(256) k_flow_assign_smem(ShapeTables t, FlowAssignBatch b, int per_warp) {
+    extern __shared__ __align__(16) unsigned char fa_smem[];
+    const int wpb = blockDim.x >> 5, w = threadIdx.x >> 5;
+    const int i = blockIdx.x * wpb + w;
+    if (i >= b.count || (threadIdx.x & 31) != 0) return;
+    const int64_t n = net_nodes(b.R, b.J), m = net_edges(b.R, b.J);
+    unsigned char *p = fa_smem + static_cast<size_t>(w) * per_warp;
+    int64_t *ws64 = reinterpret_cast<int64_t *>(p);
+    int32_t *ws32 = reinterpret_cast<int32_t *>(ws64 + (3 * m + n + b.R));
+    uint8_t *ws8 = reinterpret_cast<uint8_t *>(ws32 + (6 * m + (n + 1) + 3 * n));
+    flow_assign_one(t, b, i, ws32, ws64, ws8, 1);
+}
+
 int launch_flow_assign(const ShapeTables &t, const FlowAssignBatch &b, void *stream, uint64_t *launches) {
     cudaGetLastError();
     if (b.count == 0) return 0;
-    k_flow_assign<<<(b.count + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(t, b);
+    const size_t per = fa_smem_bytes(b.R, b.J);
+    if (per <= 48 * 1024) {
+        const int wpb = static_cast<int>(std::min<size_t>(8, std::max<size_t>(1, (96 * 1024) / per)));
+        const size_t smem = per * wpb;
+        if (smem > 48 * 1024 &&
+            cudaFuncSetAttribute(k_flow_assign_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024) !=
+                cudaSuccess)
+            return check(cudaGetLastError());
+        k_flow_assign_smem<<<(b.count + wpb - 1) / wpb, 32 * wpb, smem, static_cast<cudaStream_t>(stream)>>>(
+            t, b, static_cast<int>(per));
+    } else {
+        k_flow_assign<<<(b.count + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(t, b);
+    }
     if (launches) ++*launches;
     return check(cudaGetLastError());
 }

@@ -2871,14 +2871,7 @@ int oserve_gpu_max_flow_batch(oserve_gpu_ctx *ctx, int count, const int *num_nod
         if (eoff[0] != 0) {
             for (auto &v : eoff) v -= edge_offset[0];
         }
-        std::vector<int32_t> from(E), to(E), nn(num_nodes, num_nodes + count), src(source, source + count),
-            snk(sink, sink + count);
-        std::vector<int64_t> cap(E);
-        for (int64_t i = 0; i < E; ++i) {
-            from[i] = edges[edge_offset[0] + i].from;
-            to[i] = edges[edge_offset[0] + i].to;
-            cap[i] = edges[edge_offset[0] + i].cap;
-        }
+        std::vector<int32_t> nn(num_nodes, num_nodes + count), src(source, source + count), snk(sink, sink + count);
         cudaStream_t s = ctx->stream;
         DBuf *b = ctx->sc_mf;
         MaxFlowBatch mb{};
@@ -2886,9 +2879,8 @@ int oserve_gpu_max_flow_batch(oserve_gpu_ctx *ctx, int count, const int *num_nod
         mb.num_nodes = b[0].upload(nn, s);
         mb.edge_off = b[1].upload(eoff, s);
         mb.node_off = b[2].upload(node_off, s);
-        mb.from = b[3].upload(from, s);
-        mb.to = b[4].upload(to, s);
-        mb.cap = b[5].upload(cap, s);
+        static_assert(sizeof(oserve_flow_edge) == 16, "oserve_flow_edge: from, to, cap");
+        mb.edges32 = reinterpret_cast<const int32_t *>(b[3].upload(edges + edge_offset[0], static_cast<size_t>(E), s));
         mb.source = b[6].upload(src, s);
         mb.sink = b[7].upload(snk, s);
         // graphs of similar size: interleaved workspace padded to the largest
@@ -2923,12 +2915,9 @@ int oserve_gpu_max_flow_batch(oserve_gpu_ctx *ctx, int count, const int *num_nod
         mb.value = static_cast<int64_t *>(b[18].get(sizeof(int64_t) * count));
         mb.status = static_cast<int32_t *>(b[19].get(sizeof(int32_t) * count));
         cuda_ok(launch_max_flow(mb, s, &ctx->launches), "max flow kernel");
-        std::vector<int64_t> hf, hv;
-        download(hf, mb.flow, E, s);
-        download(hv, mb.value, count, s);
+        if (E) cuda_ok(d2h(flow, mb.flow, sizeof(int64_t) * E, s), "D2H");
+        cuda_ok(d2h(value, mb.value, sizeof(int64_t) * count, s), "D2H");
         cuda_ok(cudaStreamSynchronize(s), "sync");
-        std::copy(hf.begin(), hf.end(), flow);
-        std::copy(hv.begin(), hv.end(), value);
     });
 }
 

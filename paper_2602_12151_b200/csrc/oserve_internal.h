@@ -285,8 +285,7 @@ struct MaxFlowBatch {
     const int32_t *num_nodes;  // [count]
     const int64_t *edge_off;   // [count+1]
     const int64_t *node_off;   // [count+1] (adj_off uses node_off[g] + g)
-    const int32_t *from, *to;
-    const int64_t *cap;
+    const int32_t *edges32;    // the caller's oserve_flow_edge array as is (from, to, cap: 4 words per edge)
     const int32_t *source, *sink;
     int64_t *res, *excess;
     int32_t *arc_to, *adj, *adj_off, *height, *cur, *fifo;
