@@ -437,7 +437,8 @@ typedef struct {
 } oserve_flow_edge;
 
 /* Drop-in for flow::max_flow (FIFO push-relabel, flowassign.cpp:67-147) over
- * `count` independent graphs, one device thread each: graph g has
+ * `count` independent graphs, each run by one device lane (its workspace in
+ * shared memory when it fits): graph g has
  * num_nodes[g] nodes and edges[edge_offset[g] .. edge_offset[g+1]).  Writes
  * per-edge flows (parallel to `edges`) and the value per graph — the
  * reference's exact flows, not just an equal value.  Bad source/sink or a

@@ -5,7 +5,7 @@ greedy/exchange (K1) or branch-and-bound (K4), batched over raw tables.
 
 The flow-network formulation (flowassign.cpp:67-245, 505-519, 559-645):
 Graph / FlowResult / FlowNetwork mirror the reference types; max_flow runs
-the FIFO push-relabel on the device (K6a, one thread per graph, the
+the FIFO push-relabel on the device (K6a, one lane per graph, the
 reference's per-edge flows), build_network + max_flow + extract_assignment
 run fused per instance (K6b), solve_fractional is the dense simplex (K7).
 build_network's bookkeeping and to_dot's text are host-side."""
