@@ -275,6 +275,35 @@ def gen_f4(ref):
     json.dump({"graphs": graphs, "instances": inst, "lp": lps, "dot": dots}, open(os.path.join(OUT, "flow.json"), "w"))
 
 
+def gen_flow_big(ref):
+    """Graphs and instances past the shared-memory workspace (K6a/K6b HBM
+    paths): a batch of 34 similar graphs (interleaved workspace), a ragged
+    batch (packed workspace) and R=40, J=10 instances -> flow_big.json
+    (per-edge flows as sha256 of their int64 bytes)."""
+    import hashlib
+    rng = np.random.default_rng(2603)
+    digest = lambda fl: hashlib.sha256(np.asarray(fl, "<i8").tobytes()).hexdigest()  # noqa: E731
+
+    def graph(nn, m):
+        edges = [(int(rng.integers(0, nn)), int(rng.integers(0, nn)), int(rng.integers(0, 1000))) for _ in range(m)]
+        value, fl = ref.max_flow(nn, edges, 0, nn - 1)
+        return {"num_nodes": nn, "edges": edges, "source": 0, "sink": nn - 1, "value": value,
+                "flow_sha256": digest(fl)}
+    similar = [graph(nn, int(rng.integers(2 * nn, 3 * nn))) for nn in rng.integers(700, 801, 34).tolist()]
+    ragged = [graph(nn, int(rng.integers(nn, 4 * nn))) for nn in (50, 3000, 100, 1200, 20)]
+    inst = []
+    for _ in range(6):  # R = 40, J = 10
+        n = rng.integers(1, 101, (40, 10))
+        n[rng.random((40, 10)) < 0.125] = 0
+        e = (rng.random((40, 10)) * (n + 1)).astype(np.int64)
+        lam = rng.integers(0, 20001, 10)
+        n, e, lam = n.tolist(), e.tolist(), lam.tolist()
+        x, obj, val, fl = ref.flow_assign(n, e, lam)
+        inst.append({"n": n, "e": e, "lambda": lam, "x": x, "objective": obj, "value": val,
+                     "flow_sha256": digest(fl)})
+    json.dump({"similar": similar, "ragged": ragged, "instances": inst}, open(os.path.join(OUT, "flow_big.json"), "w"))
+
+
 def gen_exact_budget(ref, port):
     """B&B abort boundary: budgets N-1 / N around the reference's node count N
     (counted by the restatement, checked here against the reference)."""
@@ -397,6 +426,8 @@ if __name__ == "__main__":
         gen_f4(Oracle("ref"))
     elif sys.argv[1:] == ["exact"]:
         gen_exact_budget(Oracle("ref"), Oracle("port"))
+    elif sys.argv[1:] == ["flow_big"]:
+        gen_flow_big(Oracle("ref"))
     elif sys.argv[1:] == ["exact_wide"]:
         gen_exact_wide(Oracle("ref"), Oracle("port"))
     elif sys.argv[1:] == ["wide"]:

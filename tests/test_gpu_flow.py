@@ -113,3 +113,33 @@ def test_to_dot_text(cuda):
         net = flow.build_network(d["lambda"], table(d["n"], d["e"]))
         fr = flow.max_flow(net.graph, net.source(), net.sink()) if d["with_flow"] else None
         assert flow.to_dot(net, fr) == d["dot"]
+
+
+BIG = json.load(open(os.path.join(ROOT, "tests", "golden", "flow_big.json")))
+
+
+def _sha(fl):
+    import hashlib
+    return hashlib.sha256(np.asarray(fl, "<i8").tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("batch", ["similar", "ragged"])
+def test_max_flow_past_shared_memory(cuda, batch):
+    """Graphs whose workspace exceeds the shared-memory slice: the HBM kernel,
+    interleaved (34 similar graphs) and packed (a ragged batch)."""
+    gs = BIG[batch]
+    out = flow.max_flow_batch([g(x["num_nodes"], x["edges"]) for x in gs], [x["source"] for x in gs],
+                              [x["sink"] for x in gs])
+    for x, r in zip(gs, out):
+        assert r.value == x["value"] and _sha(r.flow) == x["flow_sha256"]
+
+
+def test_flow_assign_past_shared_memory(cuda):
+    """R = 40, J = 10 instances (workspace past the shared-memory slice)."""
+    gctx = GpuContext(core.cluster(1, 8), core.model_140gb())
+    cs = BIG["instances"]
+    x, obj, val, fl = gctx.flow_assign_batch(np.asarray([c["n"] for c in cs]), np.asarray([c["e"] for c in cs]),
+                                             np.asarray([c["lambda"] for c in cs]), edge_flows=True)
+    for i, c in enumerate(cs):
+        assert x[i].tolist() == c["x"] and int(obj[i]) == c["objective"] and int(val[i]) == c["value"]
+        assert _sha(fl[i]) == c["flow_sha256"]
