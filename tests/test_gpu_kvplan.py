@@ -103,3 +103,20 @@ def test_kv_plan_live_reference_random(cuda, ref):
             a = g.kv_plan(inflight, 40, src, dst, 0.2)
             b = ref.kv_plan(cl, inflight, 40, src, dst, 0.2)
             assert a == b
+
+
+def test_kv_plan_wide_target_replicas(cuda, ref):
+    """Target replicas of more than 32 devices: the replica-parallel kernel
+    keeps its state in HBM (the shared-memory form takes <= 32 devices)."""
+    rng = np.random.default_rng(6)
+    machines = [core.MachineSpec(m, list(range(8 * m, 8 * m + 8)), 80 * core.KGB) for m in range(8)]
+    cl = core.ClusterSpec(machines, 300e9, 25e9)
+    g = GpuContext(cl, core.small_model())
+    for trial in range(3):
+        perm = [int(v) for v in rng.permutation(64)]
+        dst = core.Deployment([core.ReplicaConfig(perm[:40], 8, 5), core.ReplicaConfig(perm[40:], 4, 6)])
+        perm = [int(v) for v in rng.permutation(64)]
+        src = core.Deployment([core.ReplicaConfig(perm[i:i + 4], 1, 4) for i in range(0, 64, 4)])
+        inflight = [core.InflightRequest(q, int(rng.integers(0, 100)), int(rng.integers(1, 1 << 36)),
+                                         int(rng.integers(0, src.replica_count()))) for q in range(4000)]
+        assert g.kv_plan(inflight, 30, src, dst, 0.1) == ref.kv_plan(cl, inflight, 30, src, dst, 0.1)
