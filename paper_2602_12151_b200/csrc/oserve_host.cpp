@@ -235,7 +235,7 @@ struct Space {
 // Per-task arrays of the frontier-parallel exact path (double-buffered for
 // the splitting rounds; kept in the context so repeated rounds reuse them).
 struct TaskBufs {
-    DBuf plan, td, path, g, lb, m, inc, vis, nodes, cap, done, nch, al, am;
+    DBuf plan, td, path, g, lb, m, inc, vis, nodes, cap, done, nch, nz, al, am;
     void bind(ExactTasks &e, uint64_t n) {
         e.aL = static_cast<int32_t *>(al.get(sizeof(int32_t) * n));
         e.amask = static_cast<uint32_t *>(am.get(sizeof(uint32_t) * n));
@@ -251,6 +251,7 @@ struct TaskBufs {
         e.capped = static_cast<uint8_t *>(cap.get(n));
         e.done = static_cast<uint8_t *>(done.get(n));
         e.nchild = static_cast<uint32_t *>(nch.get(sizeof(uint32_t) * (n + 1)));  // + the scan's trailing 0
+        e.nzero = static_cast<uint8_t *>(nz.get(n));
     }
 };
 

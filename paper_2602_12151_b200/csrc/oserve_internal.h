@@ -146,6 +146,7 @@ struct ExactTasks {
     uint8_t *capped;      // phase A exceeded its cap
     uint8_t *done;        // phase A finished (m, nodes valid)
     uint32_t *nchild;     // tasks this one becomes in the next round
+    uint8_t *nzero;       // single-branch decisions (v = 0 forced) between the root and the split point
     uint64_t target;      // desired tasks per plan
     uint64_t max_tasks;   // cap per plan
     unsigned long long *fetch;  // task counter of the thread-per-task passes

@@ -2161,6 +2161,37 @@ __global__ void __launch_bounds__(128) k_exact_plan(int pass, ShapeTables t, Spa
     }
 }
 
+// Where a task splits: from its root (k, pos), decisions with a single
+// branch (hi = 0: v = 0 forced, no state change) are walked down to the first
+// decision with hi >= 1; its hi + 1 branches become the children (paths: the
+// task's path, nz zeros, then v).  1 (no split) when a leaf comes first or the
+// children would pass depth `room`.
+__device__ __forceinline__ uint32_t exact_branches(const ShapeTables &t, const ExactState &st, int k, int pos,
+                                                   int room, uint8_t &nz) {
+    int z = 0;
+    for (;;) {
+        while (k < st.R && pos == t.olen[st.shp[k]]) {
+            ++k;
+            pos = 0;
+        }
+        if (k >= st.R || z >= room) break;
+        const int s = st.shp[k];
+        const int j = t.order[s * kMaxJ + pos];
+        const int64_t u = t.unit[s * st.J + j];
+        int64_t hi = t.cap[s * st.J + j];
+        if (st.lam[j] < hi) hi = st.lam[j];
+        if (hi * u > st.mrem[k]) hi = quot_small(st.mrem[k], u, t.inv_unit[s * st.J + j]);
+        if (hi >= 1) {
+            nz = static_cast<uint8_t>(z);
+            return static_cast<uint32_t>(hi + 1);
+        }
+        ++z;
+        ++pos;
+    }
+    nz = 0;
+    return 1u;
+}
+
 // Per-task passes, a thread per task (tasks fetched one at a time from a
 // counter, so a long task does not hold up a warp's others; the exact path's
 // instances are small — R*J <= exact_cell_limit, 20 by default — where a
@@ -2179,9 +2210,9 @@ __global__ void __launch_bounds__(128) k_exact_task_thr(int pass, ShapeTables t,
         const uint8_t ps = et.state[i];
         if (pass == 3) {  // children count for the next round: capped tasks only
             const uint8_t td3 = et.tdepth[q];
-            if (ps != 1 || !et.capped[q] || et.phase_cap >= prm.node_budget ||
-                (td3 & 0x7f) >= kTaskDepthMax - 1) {
+            if (ps != 1 || !et.capped[q] || et.phase_cap >= prm.node_budget || (td3 & 0x7f) >= kTaskDepthMax - 1) {
                 et.nchild[q] = 1;
+                et.nzero[q] = 0;
                 continue;
             }
         }
@@ -2192,6 +2223,7 @@ __global__ void __launch_bounds__(128) k_exact_task_thr(int pass, ShapeTables t,
         }
         if (pass == 9 && ps != 1) {
             et.nchild[q] = 1;
+            et.nzero[q] = 0;
             continue;
         }
         if ((pass == 6 || pass == 7) && ps != 1) {
@@ -2213,26 +2245,16 @@ __global__ void __launch_bounds__(128) k_exact_task_thr(int pass, ShapeTables t,
         }
         if (pass == 9) {  // frontier expansion: the root's first decision's branches, growing plans only
             uint32_t nc = 1;
+            uint8_t nz = 0;
             const int dq = td & 0x7f;
             if (et.grow[i] && dq < kTaskDepthMax - 1) {
                 int k, pos;
                 int64_t count;
                 exact_restore(t, st, et.path + q * kTaskDepthMax, dq, false, k, pos, count);
-                while (k < st.R && pos == t.olen[st.shp[k]]) {
-                    ++k;
-                    pos = 0;
-                }
-                if (k < st.R) {
-                    const int s = st.shp[k];
-                    const int j = t.order[s * kMaxJ + pos];
-                    const int64_t u = t.unit[s * st.J + j];
-                    int64_t hi = t.cap[s * st.J + j];
-                    if (st.lam[j] < hi) hi = st.lam[j];
-                    if (hi * u > st.mrem[k]) hi = quot_small(st.mrem[k], u, t.inv_unit[s * st.J + j]);
-                    nc = static_cast<uint32_t>(hi + 1);
-                }
+                nc = exact_branches(t, st, k, pos, kTaskDepthMax - 2 - dq, nz);
             }
             et.nchild[q] = nc;
+            et.nzero[q] = nz;
             atomicAdd(et.plan_sum + i, nc);
             continue;
         }
@@ -2246,21 +2268,9 @@ __global__ void __launch_bounds__(128) k_exact_task_thr(int pass, ShapeTables t,
             continue;
         }
         if (pass == 3) {
-            uint32_t nc = 1;
-            while (k < st.R && pos == t.olen[st.shp[k]]) {
-                ++k;
-                pos = 0;
-            }
-            if (k < st.R) {
-                const int s = st.shp[k];
-                const int j = t.order[s * kMaxJ + pos];
-                const int64_t u = t.unit[s * st.J + j];
-                int64_t hi = t.cap[s * st.J + j];
-                if (st.lam[j] < hi) hi = st.lam[j];
-                if (hi * u > st.mrem[k]) hi = quot_small(st.mrem[k], u, t.inv_unit[s * st.J + j]);
-                nc = static_cast<uint32_t>(hi + 1);
-            }
-            et.nchild[q] = nc;
+            uint8_t nz = 0;
+            et.nchild[q] = exact_branches(t, st, k, pos, kTaskDepthMax - 2 - (td & 0x7f), nz);
+            et.nzero[q] = nz;
             continue;
         }
         if (pass == 0) {
@@ -2950,6 +2960,7 @@ __global__ void __launch_bounds__(128) k_exact_split(ExactTasks et, ExactTasks n
         const uint32_t nc = et.nchild[q];
         const uint8_t td = et.tdepth[q];
         const int dep = td & 0x7f;
+        const int nz = nc > 1 ? et.nzero[q] : 0;
         for (uint32_t c = 0; c < nc; ++c) {
             const uint64_t r = o + c;
             nt.plan[r] = et.plan[q];
@@ -2961,9 +2972,10 @@ __global__ void __launch_bounds__(128) k_exact_split(ExactTasks et, ExactTasks n
                 nt.nodes[r] = et.nodes[q];
                 nt.capped[r] = et.capped[q];
                 nt.done[r] = et.done[q];
-            } else {
-                nt.tdepth[r] = static_cast<uint8_t>(dep + 1);
-                nt.path[r * kTaskDepthMax + dep] = static_cast<int32_t>(nc - 1 - c);  // v = hi - c
+            } else {  // path + nz forced zeros + v
+                for (int a = 0; a < nz; ++a) nt.path[r * kTaskDepthMax + dep + a] = 0;
+                nt.tdepth[r] = static_cast<uint8_t>(dep + nz + 1);
+                nt.path[r * kTaskDepthMax + dep + nz] = static_cast<int32_t>(nc - 1 - c);  // v = hi - c
                 nt.capped[r] = 0;
                 nt.done[r] = 0;
             }

@@ -1,6 +1,10 @@
-# exact-path sweep on config 1-B&B: first cap x growth x rounds
-for cfg in "8192 4 6" "8192 2 10" "8192 1 12" "4096 2 10" "16384 1 10" "4096 1 14" "8192 3 8" "2048 2 12"; do
+# exact-path sweep on config 1-B&B: deep split of small late rounds (max new tasks x levels)
+python -m pytest tests/test_gpu_exact.py -q -x 2>&1 | tail -1
+for cfg in "0 1" "30000 1" "100000 1" "100000 2"; do
   set -- $cfg
-  echo "== cap0 $1 growth $2 rounds $3"
-  OSERVE_EXACT_CAP0=$1 OSERVE_EXACT_GROWTH=$2 OSERVE_EXACT_ROUNDS=$3 timeout 200 python scripts/time_exact.py 2>&1 | grep -E "gpu exhaustive" | tail -1
+  echo "== deep $1 levels $2"
+  OSERVE_EXACT_DEEP=$1 OSERVE_EXACT_DEEP_LEVELS=$2 timeout 200 python scripts/time_exact.py 2>&1 | grep -E "gpu exhaustive" | tail -1
 done
+OSERVE_DEBUG_EXACT=1 timeout 200 python scripts/time_exact.py 2>&1 | grep -E "^\[exact\] [a-zA-Z]" | tail -9
+OSERVE_EXACT_DEEP=30000 python -m pytest tests/test_gpu_exact.py -q -x 2>&1 | tail -1
+OSERVE_EXACT_DEEP=30000 OSERVE_DEBUG_EXACT=1 timeout 200 python scripts/time_exact.py 2>&1 | grep -E "^\[exact\] [a-zA-Z]" | tail -9
