@@ -38,6 +38,9 @@
 #ifndef OSERVE_K1_MINB
 #define OSERVE_K1_MINB 4  // CTAs of 256 threads per SM the register budget must allow (64 regs; measured 5% faster than 3)
 #endif
+#ifndef OSERVE_K1_MINB_4
+#define OSERVE_K1_MINB_4 2  // four replicas per lane (KPL = 4, R <= 128): shared memory holds it to 2 CTAs/SM anyway, so no spill at 107 registers (cfg5-7B 63.8 -> 59.0 ms)
+#endif
 #ifndef OSERVE_K1_MINB_1
 #define OSERVE_K1_MINB_1 OSERVE_K1_MINB  // one replica per lane (KPL = 1)
 #endif
@@ -414,7 +417,7 @@ struct alignas(16) ShapeRow {
 enum K1Variant { kK1Round = 0, kK1TopK = 1, kK1General = 2 };
 
 template <int G, int KPL, bool SMEM, int V>
-__global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : OSERVE_K1_MINB) k_plan_eval(ShapeTables t, SpaceTables sp, KeyLayout key,
+__global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : (KPL == 4 ? OSERVE_K1_MINB_4 : OSERVE_K1_MINB)) k_plan_eval(ShapeTables t, SpaceTables sp, KeyLayout key,
                                                                    PlanSource src, PlanOutputs out, SolveParams prm,
                                                                    int skip_exact, int gchunk,
                                                                    unsigned long long *work) {

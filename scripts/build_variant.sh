@@ -15,4 +15,4 @@ $NV $ARCH -O3 -lineinfo -std=c++17 -ccbin /usr/bin/g++ -Xcompiler -fPIC,-ffp-con
     --expt-relaxed-constexpr -I"$CS" "$@" -c "${SRC:-$CS/oserve_kernels.cu}" -o "$out/oserve_kernels.o" 2> "$out/ptxas.log"
 $NV $ARCH -shared -ccbin /usr/bin/g++ -o "$out/liboserve_gpu.so" "$out/oserve_kernels.o" "$CS/oserve_flow.o" \
     "$CS/oserve_aux.o" "$CS/oserve_host.o" -lcudart -ldl
-grep -A2 "k_plan_evalILi32ELi[12]ELb1ELi0" "$out/ptxas.log" | grep -E "registers|spill" | tr '\n' ' '; echo
+grep -A2 "k_plan_evalILi32ELi[124]ELb1ELi0" "$out/ptxas.log" | grep -E "registers|spill" | tr '\n' ' '; echo
