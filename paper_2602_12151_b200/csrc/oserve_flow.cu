@@ -184,7 +184,7 @@ int launch_max_flow(const MaxFlowBatch &b, void *stream, uint64_t *launches) {
 // One instance: workspace element q at base[q * B] (B = the batch size for
 // the interleaved HBM workspace, 1 for a shared-memory slice).
 __device__ void flow_assign_one(const ShapeTables &t, const FlowAssignBatch &b, int i, int32_t *ws32, int64_t *ws64,
-                                uint8_t *ws8, int64_t B) {
+                                uint8_t *ws8, int64_t B, int64_t *xw = nullptr) {
     const int R = b.R, J = b.J;
     const int n = net_nodes(R, J), m = net_edges(R, J);
     const int64_t row0 = static_cast<int64_t>(i) * R;
@@ -210,7 +210,8 @@ __device__ void flow_assign_one(const ShapeTables &t, const FlowAssignBatch &b, 
     int64_t *excess = res + static_cast<int64_t>(2 * m) * B;
     int64_t *mrem = excess + static_cast<int64_t>(n) * B;
     uint8_t *active = ws8;
-    int64_t *x = b.x + static_cast<int64_t>(i) * R * J;
+    int64_t *const xout = b.x + static_cast<int64_t>(i) * R * J;
+    int64_t *x = xw ? xw : xout;  // xw: a shared-memory working copy
     if (b.flow_in) {  // extract_assignment of a given flow
         const int64_t *fl = b.flow_in + static_cast<int64_t>(i) * m;
         for (int k = 0; k < R; ++k) {
@@ -272,6 +273,8 @@ __device__ void flow_assign_one(const ShapeTables &t, const FlowAssignBatch &b, 
     w.x = {x, 1};
     w.mrem = {mrem, B};
     b.objective[i] = warm_solve(w);
+    if (x != xout)
+        for (int c = 0; c < R * J; ++c) xout[c] = x[c];
     b.status[i] = 0;
 }
 
@@ -286,7 +289,7 @@ __host__ __device__ inline size_t fa_smem_bytes(int R, int J) {
     size_t i32, i64, u8;
     const int64_t n = net_nodes(R, J), m = net_edges(R, J);
     i32 = static_cast<size_t>(6 * m + (n + 1) + 3 * n);
-    i64 = static_cast<size_t>(3 * m + n + R);
+    i64 = static_cast<size_t>(3 * m + n + R + R * J);  // + the x working copy
     u8 = static_cast<size_t>(n);
     return (8 * i64 + 4 * i32 + u8 + 15) & ~size_t(15);
 }
@@ -302,9 +305,10 @@ __global__ void __launch_bounds__(256) k_flow_assign_smem(ShapeTables t, FlowAss
     const int64_t n = net_nodes(b.R, b.J), m = net_edges(b.R, b.J);
     unsigned char *p = fa_smem + static_cast<size_t>(w) * per_warp;
     int64_t *ws64 = reinterpret_cast<int64_t *>(p);
-    int32_t *ws32 = reinterpret_cast<int32_t *>(ws64 + (3 * m + n + b.R));
+    int64_t *xw = ws64 + (3 * m + n + b.R);
+    int32_t *ws32 = reinterpret_cast<int32_t *>(xw + b.R * b.J);
     uint8_t *ws8 = reinterpret_cast<uint8_t *>(ws32 + (6 * m + (n + 1) + 3 * n));
-    flow_assign_one(t, b, i, ws32, ws64, ws8, 1);
+    flow_assign_one(t, b, i, ws32, ws64, ws8, 1, xw);
 }
 
 int launch_flow_assign(const ShapeTables &t, const FlowAssignBatch &b, void *stream, uint64_t *launches) {
