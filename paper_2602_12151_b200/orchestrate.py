@@ -72,6 +72,7 @@ def build_adaptive_timeline(ctx: GpuContext, types: Sequence[core.WorkloadType],
     prev_lam: Optional[List[int]] = None
     prev_x: Optional[List[List[int]]] = None
     d_keys = None
+    prepared = False
     if topk and strategy != "search":
         import torch  # device memory for the key list (plumbing)
         d_keys = torch.empty(int(topk), dtype=torch.int64, device=f"cuda:{ctx.device}")
@@ -86,7 +87,9 @@ def build_adaptive_timeline(ctx: GpuContext, types: Sequence[core.WorkloadType],
             found, _ = ctx.search(seed=seed, max_iters=search_max_iters, stale_limit=search_stale_limit,
                                   warm_start=current)
         elif d_keys is not None:
-            ctx.prepare_space(mode, list(sizes))
+            if not prepared:  # the space does not depend on the workload (exact flags and key bits follow it)
+                ctx.prepare_space(mode, list(sizes))
+                prepared = True
             ctx.round_topk(int(topk), d_keys.data_ptr())
             keys = [int(k) & ((1 << 64) - 1) for k in d_keys.cpu().tolist()]
             found = ctx.decode_key(keys[0])
