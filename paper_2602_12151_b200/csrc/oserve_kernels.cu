@@ -806,10 +806,16 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : (KPL == 4 ?
             }
             int c = 0;
             if (run_end > k) {  // same shape follows: how many can take the identical fill
-                uint32_t cb = 0xffffffffu;
-                if (act && take > 0 && g.gl <= pb) cb = static_cast<uint32_t>(lamp - a) / static_cast<uint32_t>(take);
+                // c = min(run length left L, min over positions of (lam_p - a_p) / take_p):
+                // the quotient only matters below L, so divide only then
+                const uint32_t L = static_cast<uint32_t>(run_end - k);
+                uint32_t cb = L;
+                if (act && take > 0 && g.gl <= pb) {
+                    const uint32_t xq = static_cast<uint32_t>(lamp - a), tq = static_cast<uint32_t>(take);
+                    if (static_cast<uint64_t>(L) * tq > xq) cb = xq / tq;
+                }
                 cb = __reduce_min_sync(g.mask, cb);
-                c = min(static_cast<int>(min(cb, 0x7fffffffu)), run_end - k);
+                c = static_cast<int>(cb);
             }
             if (act && take) {
 #pragma unroll 1
