@@ -262,7 +262,7 @@ struct RawRows {
 };
 
 struct ExactScratch {
-    DBuf depth, nt, off, top, opt, ist, state, bx, run, ranks, newoff, fetch, topn, ubn, anycap, scan, grow, psum;
+    DBuf depth, nt, off, top, opt, ist, state, bx, run, ranks, newoff, fetch, topn, ubn, anycap, scan, grow, psum, pmax;
     TaskBufs bufs[2];
 };
 
@@ -918,7 +918,7 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
         const char *e = getenv("OSERVE_EXACT_TARGET");
         return e ? static_cast<uint64_t>(atoll(e)) : 0ull;
     }();
-    et.target = target_env ? target_env : std::max<uint64_t>(64, std::min<uint64_t>(4096, budget_tasks / P));
+    et.target = target_env ? target_env : std::max<uint64_t>(64, std::min<uint64_t>(1024, budget_tasks / P));
     et.max_tasks = et.target * 8;
     static const bool dbg = getenv("OSERVE_DEBUG_EXACT") != nullptr;
     TaskBufs *bufs = c.exact.bufs;
@@ -1032,24 +1032,28 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
         // the full budget.
         // Round r caps each task at cap0 * growth^r nodes: a task over the
         // cap wastes the nodes it ran before it is split, so the caps start
-        // small and grow (most tasks finish in the first round).
+        // small and grow (most tasks finish in the first round).  Small caps
+        // keep each round's longest task short; the rounds themselves are
+        // cheap (device scans for the per-plan prefix maxima, no per-plan
+        // loops): config 1-B&B 1,024 x 2: 13 ms, 8,192 x 4: 36 ms.
         static const int kRounds = [] {
             const char *e = getenv("OSERVE_EXACT_ROUNDS");
-            return e ? atoi(e) : 6;
+            return e ? atoi(e) : 14;
         }();
         static const int64_t kCap0 = [] {
             const char *e = getenv("OSERVE_EXACT_CAP0");
-            return e ? static_cast<int64_t>(atoll(e)) : int64_t{1} << 13;
+            return e ? static_cast<int64_t>(atoll(e)) : int64_t{1} << 10;
         }();
         static const int kGrowth = [] {
             const char *e = getenv("OSERVE_EXACT_GROWTH");
-            return e ? atoi(e) : 4;
+            return e ? atoi(e) : 2;
         }();
         // the replay of the top: exact incumbents, visited tasks and top-node
         // counts (see exact_replay_task)
         auto replay = [&]() {
-            cuda_ok(launch_exact_plan_pass(6, c.tables, view, key, src, eo, prm, et, c.sm_count, s, &c.launches),
-                    "exact plan pass 6");
+            cuda_ok(launch_exact_prefix(6, et, total, P, static_cast<int64_t *>(xs.pmax.get(sizeof(int64_t) * total)),
+                                        &c.cub_temp, &c.cub_temp_bytes, c.sm_count, s, &c.launches),
+                    "exact incumbents");
             cuda_ok(launch_exact_task_pass(6, c.tables, view, src, prm, et, total, c.sm_count, s, &c.launches),
                     "exact task pass 6");
             uint64_t *tmp = static_cast<uint64_t *>(xs.scan.get(sizeof(uint64_t) * 2 * total));
@@ -1065,8 +1069,9 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
             round_cap = std::min<int64_t>(round_cap * kGrowth, int64_t{1} << 22);
             cuda_ok(launch_exact_task_pass(2, c.tables, view, src, prm, et, total, c.sm_count, s, &c.launches),
                     "exact task pass 2");
-            cuda_ok(launch_exact_plan_pass(4, c.tables, view, key, src, eo, prm, et, c.sm_count, s, &c.launches),
-                    "exact plan pass 4");
+            cuda_ok(launch_exact_prefix(4, et, total, P, static_cast<int64_t *>(xs.pmax.get(sizeof(int64_t) * total)),
+                                        &c.cub_temp, &c.cub_temp_bytes, c.sm_count, s, &c.launches),
+                    "exact lower bounds");
             cuda_ok(launch_exact_task_pass(0, c.tables, view, src, prm, et, total, c.sm_count, s, &c.launches),
                     "exact task pass 0");
             lap("phaseA round");

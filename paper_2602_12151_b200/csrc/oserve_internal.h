@@ -199,16 +199,22 @@ int launch_plan_eval(const ShapeTables &t, const SpaceTables &sp, const KeyLayou
 int launch_plan_exact(const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key, const PlanSource &src,
                       const PlanOutputs &out, const SolveParams &sp_params, int sm_count, void *stream,
                       uint64_t *launches);
-// Frontier-parallel exact path: per-plan passes (0 count/choose depth, 1 emit
-// tasks, 4 lower bounds from the dives, 2 replay the top of the tree,
-// 3 finish/emit) and per-task passes (2 greedy dives, 0 phase A subtree
-// maxima, 1 phase B node counts + first optimal leaf).
+// Frontier-parallel exact path: per-plan passes (10 root tasks, 8 certify,
+// 3 finish/emit) and per-task passes (9 frontier children, 2 greedy dives,
+// 0 phase A subtree maxima, 3 split counts, 6/7 top replay, 1 phase B node
+// counts + first optimal leaf).
 int launch_exact_plan_pass(int pass, const ShapeTables &t, const SpaceTables &sp, const KeyLayout &key,
                            const PlanSource &src, const PlanOutputs &out, const SolveParams &prm,
                            const ExactTasks &et, int sm_count, void *stream, uint64_t *launches);
 int launch_exact_task_pass(int pass, const ShapeTables &t, const SpaceTables &sp, const PlanSource &src,
                            const SolveParams &prm, const ExactTasks &et, uint64_t total_tasks, int sm_count,
                            void *stream, uint64_t *launches);
+// Per-plan prefix maxima over the task list as segmented scans: which = 4
+// lower bounds (lb, and m of finished tasks), 6 exact incumbents (inc, opt,
+// istar; resets the replay's per-plan counters).  tmp: [total] int64.
+int launch_exact_prefix(int which, const ExactTasks &et, uint64_t total, uint64_t plans, int64_t *tmp, void **temp,
+                        size_t *temp_bytes, int sm_count, void *stream, uint64_t *launches);
+
 // Split capped tasks into their children: `nt` receives the new list at the
 // exclusive-scan offsets `newoff` of et.nchild.
 int launch_exact_split(const ShapeTables &t, const SpaceTables &sp, const PlanSource &src, const SolveParams &prm,

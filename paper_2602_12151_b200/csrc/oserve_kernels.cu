@@ -2096,8 +2096,10 @@ __device__ void exact_replay_task(int pass, const ShapeTables &t, ExactState &st
     if (et.capped[q]) et.anycap[i] = 1;
 }
 
-// Per-plan passes: 0 choose the cut depth and count tasks, 1 emit tasks,
-// 2 exact replay of the top, 3 finish (abort decision or outputs).
+// Per-plan passes: 10 one root task per exact-path plan, 8 certify after the
+// replay (or count exactly in phase B), 3 finish (abort decision or outputs).
+// The per-plan prefix maxima over the tasks are segmented scans
+// (launch_exact_prefix).
 __global__ void __launch_bounds__(128) k_exact_plan(int pass, ShapeTables t, SpaceTables sp, KeyLayout key,
                                                     PlanSource src, PlanOutputs out, SolveParams prm, ExactTasks et) {
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < src.count;
@@ -2114,23 +2116,6 @@ __global__ void __launch_bounds__(128) k_exact_plan(int pass, ShapeTables t, Spa
             continue;
         }
         if (!ex || et.state[i] == 0) continue;
-        if (pass == 6) {  // exact incumbents: exclusive prefix max of m; optimum; last rise
-            if (et.state[i] != 1) continue;
-            int64_t run = -1, ist = -1;
-            for (uint64_t q = et.toff[i]; q < et.toff[i] + et.ntask[i]; ++q) {
-                et.inc[q] = run;
-                if (et.m[q] > run) {
-                    run = et.m[q];
-                    ist = static_cast<int64_t>(q);
-                }
-            }
-            et.opt[i] = run;
-            et.istar[i] = ist;
-            et.topn[i] = 0;
-            et.ubn[i] = 0;
-            et.anycap[i] = 0;
-            continue;
-        }
         if (pass == 8) {  // after the replay: certify (upper bound) or count exactly in phase B
             if (et.state[i] != 1) continue;
             if (et.anycap[i]) {  // phase A hit the budget somewhere: sequential DFS
@@ -2141,19 +2126,6 @@ __global__ void __launch_bounds__(128) k_exact_plan(int pass, ShapeTables t, Spa
             et.top_nodes[i] = static_cast<int64_t>(tn);
             et.running[i] = tn;
             if (tn + et.ubn[i] > static_cast<unsigned long long>(prm.node_budget)) et.state[i] = 3;
-            continue;
-        }
-        if (pass == 4) {  // lb = exclusive prefix max of the tasks' dives; finished tasks: m = max(m, lb)
-            if (et.state[i] != 1) continue;
-            // (a task that ran — finished or capped — holds in m a real leaf
-            // of its subtree or its own lb, both <= the incumbent after it)
-            int64_t run = -1;
-            for (uint64_t q = et.toff[i]; q < et.toff[i] + et.ntask[i]; ++q) {
-                et.lb[q] = run;
-                if (et.done[q] && et.m[q] < run) et.m[q] = run;
-                run = et.g[q] > run ? et.g[q] : run;
-                if ((et.done[q] || et.capped[q]) && et.m[q] > run) run = et.m[q];
-            }
             continue;
         }
         // pass 3: finish
@@ -2299,6 +2271,65 @@ __global__ void __launch_bounds__(128) k_exact_task_thr(int pass, ShapeTables t,
                 exact_dfs<false>(t, st, k, pos, count, best, prm.node_budget + 1, nodes, capped, nullptr, ctr,
                                  prm.node_budget);
         }
+    }
+}
+
+// Per-plan prefix maxima of the exact path as segmented scans over the task
+// list (tasks of a plan are contiguous; the key is the plan index):
+//  lower bounds: lb[q] = exclusive max over the plan's earlier tasks of
+//    max(dive g, best leaf m of a task that ran); finished tasks m = max(m, lb)
+//  exact incumbents: inc[q] = exclusive max of m; opt = the plan's max; istar
+//    = the first task reaching it (the only one with m > inc and m == opt).
+struct MaxI64 {
+    __device__ __forceinline__ int64_t operator()(int64_t a, int64_t b) const { return a > b ? a : b; }
+};
+
+__global__ void k_exact_lb_vals(ExactTasks et, uint64_t total, int64_t *v) {
+    for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
+         q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const int64_t g = et.g[q];
+        const int64_t m = (et.done[q] || et.capped[q]) ? et.m[q] : -1;
+        v[q] = g > m ? g : m;
+    }
+}
+
+__global__ void k_exact_lb_apply(ExactTasks et, uint64_t total) {
+    for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
+         q += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        if (et.done[q] && et.m[q] < et.lb[q]) et.m[q] = et.lb[q];
+}
+
+__global__ void k_exact_inc_reset(ExactTasks et, uint64_t plans) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < plans;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        if (et.state[i] != 1) continue;
+        et.opt[i] = -1;
+        et.istar[i] = -1;
+        et.topn[i] = 0;
+        et.ubn[i] = 0;
+        et.anycap[i] = 0;
+    }
+}
+
+__global__ void k_exact_opt(ExactTasks et, uint64_t total) {
+    for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
+         q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t i = et.plan[q];
+        if (et.state[i] != 1) continue;
+        if (q + 1 == total || et.plan[q + 1] != i) {
+            const int64_t a = et.inc[q], b = et.m[q];
+            et.opt[i] = a > b ? a : b;
+        }
+    }
+}
+
+__global__ void k_exact_istar(ExactTasks et, uint64_t total) {
+    for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
+         q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t i = et.plan[q];
+        if (et.state[i] != 1) continue;
+        const int64_t m = et.m[q];
+        if (m > et.inc[q] && m == et.opt[i]) et.istar[i] = static_cast<int64_t>(q);
     }
 }
 
@@ -3144,6 +3175,45 @@ int launch_exact_task_pass(int pass, const ShapeTables &t, const SpaceTables &sp
     k_exact_task_thr<<<static_cast<unsigned>(grid), block, 0, static_cast<cudaStream_t>(stream)>>>(
         pass, t, sp, src, prm, et, total_tasks, et.fetch);
     if (launches) ++*launches;
+    return check(cudaGetLastError());
+}
+
+int launch_exact_prefix(int which, const ExactTasks &et, uint64_t total, uint64_t plans, int64_t *tmp, void **temp,
+                        size_t *temp_bytes, int sm_count, void *stream, uint64_t *launches) {
+    cudaGetLastError();
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const unsigned gt = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, static_cast<uint64_t>(sm_count) * 8));
+    const unsigned gp = static_cast<unsigned>(std::min<uint64_t>((plans + 255) / 256, static_cast<uint64_t>(sm_count) * 8));
+    if (which == 6 && plans) k_exact_inc_reset<<<gp, 256, 0, s>>>(et, plans);
+    if (total == 0) return check(cudaGetLastError());
+    const int64_t *in = et.m;
+    int64_t *out = et.inc;
+    if (which == 4) {
+        k_exact_lb_vals<<<gt, 256, 0, s>>>(et, total, tmp);
+        in = tmp;
+        out = et.lb;
+    }
+    size_t need = 0;
+    const uint32_t n = static_cast<uint32_t>(total);
+    cudaError_t e = cub::DeviceScan::ExclusiveScanByKey(nullptr, need, et.plan, in, out, MaxI64(), int64_t{-1}, n,
+                                                        ::cuda::std::equal_to<>(), s);
+    if (e != cudaSuccess) return static_cast<int>(e);
+    if (need > *temp_bytes) {
+        if (*temp) cudaFree(*temp);
+        e = cudaMalloc(temp, need);
+        if (e != cudaSuccess) return static_cast<int>(e);
+        *temp_bytes = need;
+    }
+    e = cub::DeviceScan::ExclusiveScanByKey(*temp, need, et.plan, in, out, MaxI64(), int64_t{-1}, n,
+                                            ::cuda::std::equal_to<>(), s);
+    if (e != cudaSuccess) return static_cast<int>(e);
+    if (which == 4) {
+        k_exact_lb_apply<<<gt, 256, 0, s>>>(et, total);
+    } else {
+        k_exact_opt<<<gt, 256, 0, s>>>(et, total);
+        k_exact_istar<<<gt, 256, 0, s>>>(et, total);
+    }
+    if (launches) *launches += 4;
     return check(cudaGetLastError());
 }
 
