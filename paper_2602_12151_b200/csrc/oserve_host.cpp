@@ -235,7 +235,7 @@ struct Space {
 // Per-task arrays of the frontier-parallel exact path (double-buffered for
 // the splitting rounds; kept in the context so repeated rounds reuse them).
 struct TaskBufs {
-    DBuf plan, td, path, g, lb, m, inc, vis, nodes, cap, done, nch, nz, al, am;
+    DBuf plan, td, path, g, lb, lbr, m, inc, vis, nodes, cap, done, nch, nz, al, am;
     void bind(ExactTasks &e, uint64_t n) {
         e.aL = static_cast<int32_t *>(al.get(sizeof(int32_t) * n));
         e.amask = static_cast<uint32_t *>(am.get(sizeof(uint32_t) * n));
@@ -244,6 +244,7 @@ struct TaskBufs {
         e.path = static_cast<int32_t *>(path.get(sizeof(int32_t) * n * kTaskDepthMax));
         e.g = static_cast<int64_t *>(g.get(sizeof(int64_t) * n));
         e.lb = static_cast<int64_t *>(lb.get(sizeof(int64_t) * n));
+        e.lbran = static_cast<int64_t *>(lbr.get(sizeof(int64_t) * n));
         e.m = static_cast<int64_t *>(m.get(sizeof(int64_t) * n));
         e.inc = static_cast<int64_t *>(inc.get(sizeof(int64_t) * n));
         e.vis = static_cast<uint8_t *>(vis.get(n));
@@ -262,7 +263,7 @@ struct RawRows {
 };
 
 struct ExactScratch {
-    DBuf depth, nt, off, top, opt, ist, state, bx, run, ranks, newoff, fetch, topn, ubn, anycap, scan, grow, psum, pmax;
+    DBuf depth, nt, off, top, opt, ist, state, bx, run, ranks, newoff, fetch, topn, ubn, lbn, anycap, scan, grow, psum, pmax;
     TaskBufs bufs[2];
 };
 
@@ -911,6 +912,7 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
     et.fetch = static_cast<unsigned long long *>(xs.fetch.get(sizeof(unsigned long long)));
     et.topn = static_cast<unsigned long long *>(xs.topn.get(sizeof(unsigned long long) * P));
     et.ubn = static_cast<unsigned long long *>(xs.ubn.get(sizeof(unsigned long long) * P));
+    et.lbn = static_cast<unsigned long long *>(xs.lbn.get(sizeof(unsigned long long) * P));
     et.anycap = static_cast<uint8_t *>(xs.anycap.get(P));
     // ~2^21 tasks in flight at most; at least a few thousand per plan when few plans
     const uint64_t budget_tasks = uint64_t{1} << 21;

@@ -129,7 +129,8 @@ struct ExactTasks {
     int64_t *top_nodes;   // visited nodes above the cut (pass 2)
     int64_t *opt;         // optimum (pass 2)
     int64_t *istar;       // task holding the first optimal leaf (pass 2)
-    uint8_t *state;       // 0 not exact, 1 frontier, 2 sequential fallback, 3 frontier + phase-B counts
+    uint8_t *state;       // 0 not exact, 1 frontier, 2 sequential fallback, 3 frontier + phase-B counts,
+                          // 4 abort proven by exact phase-A counts
     unsigned long long *running;  // phase-B running node total (top + finished task nodes)
     int32_t *bx;          // [plans][kMaxExactCells] first optimal leaf
     int64_t phase_cap;    // phase-A node cap of this round (tasks above it are split)
@@ -139,6 +140,7 @@ struct ExactTasks {
     int32_t *path;        // [tasks][kTaskDepthMax]
     int64_t *g;           // greedy-dive leaf count of the task
     int64_t *lb;          // lower bound of the incumbent entering the task (prefix max of g)
+    int64_t *lbran;       // the lower bound phase A actually ran the task with
     int64_t *m;           // max(best leaf in the subtree, lb)  (phase A)
     int64_t *inc;         // exact incumbent entering the task (pass 2)
     uint8_t *vis;         // task root visited by the sequential DFS (pass 2)
@@ -155,6 +157,7 @@ struct ExactTasks {
     int32_t *aL;
     uint32_t *amask;
     unsigned long long *topn, *ubn;
+    unsigned long long *lbn;  // per plan: exact counts of visited tasks whose phase-A bound was the exact incumbent
     uint8_t *anycap;
     // device-built frontier: per plan, grow this level / children summed
     uint8_t *grow;

@@ -2092,7 +2092,11 @@ __device__ void exact_replay_task(int pass, const ShapeTables &t, ExactState &st
     const bool vis = (anc & need) == need;
     et.vis[q] = vis ? 1 : 0;
     if (top) atomicAdd(et.topn + i, static_cast<unsigned long long>(top));
-    if (vis) atomicAdd(et.ubn + i, static_cast<unsigned long long>(et.nodes[q]));
+    if (vis) {
+        atomicAdd(et.ubn + i, static_cast<unsigned long long>(et.nodes[q]));
+        // entered with the exact incumbent: phase A ran the sequential search itself
+        if (et.lbran[q] == inc) atomicAdd(et.lbn + i, static_cast<unsigned long long>(et.nodes[q]));
+    }
     if (et.capped[q]) et.anycap[i] = 1;
 }
 
@@ -2125,13 +2129,20 @@ __global__ void __launch_bounds__(128) k_exact_plan(int pass, ShapeTables t, Spa
             const unsigned long long tn = et.topn[i];
             et.top_nodes[i] = static_cast<int64_t>(tn);
             et.running[i] = tn;
-            if (tn + et.ubn[i] > static_cast<unsigned long long>(prm.node_budget)) et.state[i] = 3;
+            if (tn + et.lbn[i] > static_cast<unsigned long long>(prm.node_budget)) {
+                // exact counts of a subset of the visited nodes already pass the
+                // budget: the sequential search aborts, no phase-B recount
+                et.running[i] = tn + et.lbn[i];
+                et.state[i] = 4;
+            } else if (tn + et.ubn[i] > static_cast<unsigned long long>(prm.node_budget)) {
+                et.state[i] = 3;
+            }
             continue;
         }
         // pass 3: finish
         const uint8_t ps = et.state[i];
-        if (ps != 1 && ps != 3) continue;
-        if (ps == 3 && et.running[i] > static_cast<unsigned long long>(prm.node_budget)) {
+        if (ps != 1 && ps != 3 && ps != 4) continue;
+        if (ps == 4 || (ps == 3 && et.running[i] > static_cast<unsigned long long>(prm.node_budget))) {
             if (out.aborted) {
                 const unsigned slot2 = atomicAdd(out.aborted_n, 1u);
                 out.aborted[slot2] = gr;
@@ -2256,6 +2267,7 @@ __global__ void __launch_bounds__(128) k_exact_task_thr(int pass, ShapeTables t,
         }
         if (pass == 0) {
             int64_t best = et.lb[q];
+            et.lbran[q] = best;
             exact_dfs<false>(t, st, k, pos, count, best, et.phase_cap, nodes, capped, nullptr);
             et.m[q] = best;
             et.nodes[q] = nodes;
@@ -2307,6 +2319,7 @@ __global__ void k_exact_inc_reset(ExactTasks et, uint64_t plans) {
         et.istar[i] = -1;
         et.topn[i] = 0;
         et.ubn[i] = 0;
+        et.lbn[i] = 0;
         et.anycap[i] = 0;
     }
 }
@@ -3010,6 +3023,7 @@ __global__ void __launch_bounds__(128) k_exact_split(ExactTasks et, ExactTasks n
                 nt.g[r] = et.g[q];
                 nt.m[r] = et.m[q];
                 nt.nodes[r] = et.nodes[q];
+                nt.lbran[r] = et.lbran[q];
                 nt.capped[r] = et.capped[q];
                 nt.done[r] = et.done[q];
             } else {  // path + nz forced zeros + v
