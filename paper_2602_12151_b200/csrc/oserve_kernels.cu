@@ -1603,7 +1603,7 @@ struct ExactFlat {
 // table (quotients < 2^20 there: at most 2 off), quot_small on the 64-bit one.
 __device__ __forceinline__ int32_t flat_quot(int32_t m, int32_t u, float inv) {
     int32_t q = __float2int_rz(__int2float_rn(m) * inv);
-    int32_t r = m - q * u;
+    int64_t r = static_cast<int64_t>(m) - static_cast<int64_t>(q) * u;  // 64-bit: q * u may pass 2^31
     while (r < 0) {
         --q;
         r += u;
