@@ -2083,9 +2083,11 @@ int oserve_gpu_kv_plan(oserve_gpu_ctx *ctx, int n_inflight, const oserve_infligh
             t0 = t1;
         };
         if (headroom < 0.0 || headroom > 0.5) fail(OSERVE_ERR_INVALID_ARGUMENT, "kv_plan: headroom must be in [0, 0.5]");
+        int m_tot = 0;  // migrating requests (also the validation pass)
         for (int q = 0; q < n_inflight; ++q) {
             const auto &r = inflight[q];
             if (r.generated_tokens <= threshold_tokens) continue;
+            ++m_tot;
             if (r.source_replica < 0 || r.source_replica >= src->num_replicas)
                 fail(OSERVE_ERR_INVALID_ARGUMENT, "kv_plan: request " + std::to_string(r.request_id) +
                                                       " names unknown source replica");
@@ -2161,11 +2163,9 @@ int oserve_gpu_kv_plan(oserve_gpu_ctx *ctx, int n_inflight, const oserve_infligh
         std::vector<int64_t> gen;
         std::vector<uint64_t> kv;
         std::vector<int32_t> sr;
-        int m_tot = 0;
         if (par) {
             // the m-th migrated request goes to target replica m mod R: group
             // sizes follow from the count, no per-request division
-            for (int q = 0; q < n_inflight; ++q) m_tot += inflight[q].generated_tokens > threshold_tokens;
             goff.assign(static_cast<size_t>(R) + 1, 0);
             for (int r = 0; r < R; ++r) goff[r + 1] = goff[r] + m_tot / R + (r < m_tot % R ? 1 : 0);
             gkv.resize(static_cast<size_t>(std::max(m_tot, 1)));
