@@ -297,3 +297,25 @@ def test_gpu_switch_matches_reference_goldens(cuda):
         assert [[t.range.begin, t.range.end, t.src, t.dst] for t in plan.transfers] == case["transfers"]
         est, mb = g.switch_cost_batch(src, [dst])
         assert est[0] == case["est_seconds"] and mb[0] == case["max_link_bytes"]
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_exact_path_random_demands(cuda, port, seed):
+    """The branch-and-bound path (every config 1-B&B plan takes it: sum of
+    lambda <= 400) at seeded random demands: every plan's objective against
+    the restatement (node budget, aborts and heuristic fallthrough included)
+    and the exhaustive winner."""
+    w = workloads.load("cfg1_bnb")
+    rng = np.random.default_rng(900 + seed)
+    total = int(rng.integers(40, 401))
+    a = int(rng.integers(0, total + 1))
+    w.lam = [a, total - a][:len(w.lam)] + [0] * max(0, len(w.lam) - 2)
+    g = ctx_for(w)
+    parts, plans = g.prepare_space(w.space_mode, w.space_sizes)
+    obj, spp = g.evaluate_ranks(0, plans)
+    eo, es, _ = port.evaluate_ranks(problem_for(w), w.space_mode, np.arange(plans, dtype=np.uint64), w.space_sizes,
+                                    threads=NCPU)
+    assert np.array_equal(obj, eo) and np.array_equal(spp, es), (w.lam, np.nonzero(obj != eo)[0][:10])
+    got = g.exhaustive()
+    exp = port.exhaustive(problem_for(w))
+    assert got.throughput == exp.throughput and same_deployment(got.deployment, exp.deployment)
