@@ -38,6 +38,18 @@
 #ifndef OSERVE_K1_MINB
 #define OSERVE_K1_MINB 4  // CTAs of 256 threads per SM the register budget must allow (64 regs; measured 5% faster than 3)
 #endif
+// exchange-loop per-slot loops: unrolled for one or two slots per lane (config
+// 5: 105.5 -> 103.9 ms), rolled for four (instruction-cache footprint: config
+// 5-7B 58.9 ms rolled, 61.4 ms unrolled)
+#ifndef OSERVE_K1_XUNROLL
+#define OSERVE_K1_XUNROLL _Pragma("unroll (KPL <= 2 ? KPL : 1)")
+#endif
+#ifndef OSERVE_K1_ZUNROLL  // clearing a resumed replica's J classes (config 5: -0.4%)
+#define OSERVE_K1_ZUNROLL _Pragma("unroll (KPL <= 2 ? 4 : 1)")
+#endif
+#ifndef OSERVE_K1_TUNROLL
+#define OSERVE_K1_TUNROLL _Pragma("unroll 1")
+#endif
 #ifndef OSERVE_K1_MINB_4
 #define OSERVE_K1_MINB_4 2  // four replicas per lane (KPL = 4, R <= 128): shared memory holds it to 2 CTAs/SM anyway, so no spill at 107 registers (cfg5-7B 63.8 -> 59.0 ms)
 #endif
@@ -699,7 +711,7 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : (KPL == 4 ?
                 held[kk] = snH[kk * G + g.gl];
                 areg[kk] = snA[kk * G + g.gl];
                 if (k >= P && k < R) {
-#pragma unroll 1
+OSERVE_K1_ZUNROLL
                     for (int j = 0; j < J; ++j) xs[j * RMAX + k] = 0;
                 }
             }
@@ -818,7 +830,7 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : (KPL == 4 ?
                 c = static_cast<int>(cb);
             }
             if (act && take) {
-#pragma unroll 1
+OSERVE_K1_TUNROLL
                 for (int q = 0; q <= c; ++q) xs[j * RMAX + k + q] = take;
             }
             // direct-take bit of (class at this position, replicas k..k+c)
@@ -935,7 +947,7 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : (KPL == 4 ?
         uint32_t F[KPL], E[KPL];
 #pragma unroll
         for (int kk = 0; kk < KPL; ++kk) F[kk] = E[kk] = 0u;
-#pragma unroll 1
+OSERVE_K1_XUNROLL
         for (int kk = 0; kk < KPL; ++kk) {
             const uint32_t e = g.gl + G * kk < R ? eligible_held(rsel(held, kk), kk) : 0u;
             rput(E, kk, e);
@@ -1090,7 +1102,7 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : (KPL == 4 ?
             // rows whose feasible set must be rebuilt: kf, k2, and rows whose
             // eligible-held set changed (only possible through dirty classes)
             uint32_t redo = 0;  // bit kk: owned row kk must be rebuilt
-#pragma unroll 1
+OSERVE_K1_XUNROLL
             for (int kk = 0; kk < KPL; ++kk) {
                 const int k = g.gl + G * kk;
                 if (k >= R) continue;
@@ -1105,7 +1117,7 @@ __global__ void __launch_bounds__(256, KPL == 1 ? OSERVE_K1_MINB_1 : (KPL == 4 ?
 #pragma unroll
             for (int kk = 0; kk < KPL; ++kk) nredo += __popc(g.ballot((redo >> kk) & 1u));
             if (nredo > 4) {
-#pragma unroll 1
+OSERVE_K1_XUNROLL
                 for (int kk = 0; kk < KPL; ++kk)
                     if ((redo >> kk) & 1u) {
                         const uint32_t e = eligible_held(rsel(held, kk), kk);
