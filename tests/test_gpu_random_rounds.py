@@ -101,3 +101,30 @@ def test_random_problem_every_plan_and_winner(cuda, ref, seed):
     lower = ref.solve_assignment(tref.n, tref.e, lam)
     assert asg.assignment.x == lower.assignment.x
     assert asg.assignment.objective == lower.assignment.objective == got.throughput
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_problem_switching(cuda, ref, seed):
+    """K2 on random clusters / models: est_seconds and max link bytes of the
+    switching batch, and full transfer lists, against the reference's
+    switchplan::layout + greedy_plan + estimate_time (switchplan.cpp:40-140)."""
+    from pyoracle import Problem
+    cl, model, types, lam, params, mode, sizes, plans = draw_case(ref, 100 + seed)
+    pr = Problem(cl, model, types, lam, 60.0, params)
+    g = GpuContext(cl, model, params)
+    g.set_workload(types, lam, 60.0)
+    g.prepare_space(mode, sizes)
+    rng = np.random.default_rng(seed)
+    ranks = rng.integers(0, plans, 48)
+    deps = [ref.space_plan(pr, mode, int(r), sizes)[0] for r in ranks]
+    for src in (deps[0], g.round(mode, sizes).deployment):
+        est, mb = g.switch_cost_batch(src, deps)
+        for d, e, m in zip(deps, est, mb):
+            plan, emax = ref.switch_plan(cl, model.param_bytes, src, d)
+            assert e == plan.est_seconds and m == emax
+        for d in deps[:6]:
+            got = g.switch_plan(src, d)
+            exp, _ = ref.switch_plan(cl, model.param_bytes, src, d)
+            assert got.est_seconds == exp.est_seconds
+            assert [(t.range.begin, t.range.end, t.src, t.dst) for t in got.transfers] == \
+                [(t.range.begin, t.range.end, t.src, t.dst) for t in exp.transfers]
