@@ -263,7 +263,8 @@ struct RawRows {
 };
 
 struct ExactScratch {
-    DBuf depth, nt, off, top, opt, ist, state, bx, run, ranks, newoff, fetch, topn, ubn, lbn, anycap, scan, grow, psum, pmax;
+    DBuf depth, nt, off, top, opt, ist, state, bx, run, ranks, newoff, fetch, topn, ubn, lbn, anycap, scan, grow, psum, pmax,
+        work;
     TaskBufs bufs[2];
 };
 
@@ -914,6 +915,18 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
     et.ubn = static_cast<unsigned long long *>(xs.ubn.get(sizeof(unsigned long long) * P));
     et.lbn = static_cast<unsigned long long *>(xs.lbn.get(sizeof(unsigned long long) * P));
     et.anycap = static_cast<uint8_t *>(xs.anycap.get(P));
+    // Phase A runs every task with a lower bound of its entering incumbent,
+    // so a plan whose tree is far larger than the node budget (the sequential
+    // search aborts after node_budget nodes) would be explored whole: its
+    // phase-A nodes over all rounds are capped at kWorkBudgets x node_budget,
+    // past which the sequential DFS (<= node_budget nodes) decides it.
+    static const int64_t kWorkBudgets = [] {
+        const char *e = getenv("OSERVE_EXACT_WORK");
+        return e ? static_cast<int64_t>(atoll(e)) : int64_t{16};
+    }();
+    et.work = static_cast<unsigned long long *>(xs.work.get(sizeof(unsigned long long) * P));
+    et.work_limit = kWorkBudgets * prm.node_budget;
+    cuda_ok(cudaMemsetAsync(et.work, 0, sizeof(unsigned long long) * P, s), "memset");
     // ~2^21 tasks in flight at most; at least a few thousand per plan when few plans
     const uint64_t budget_tasks = uint64_t{1} << 21;
     static const uint64_t target_env = [] {
@@ -1076,6 +1089,7 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
                     "exact lower bounds");
             cuda_ok(launch_exact_task_pass(0, c.tables, view, src, prm, et, total, c.sm_count, s, &c.launches),
                     "exact task pass 0");
+            cuda_ok(launch_exact_retire(et, P, c.sm_count, s, &c.launches), "exact retire");
             lap("phaseA round");
             if (last) break;
             cuda_ok(launch_exact_task_pass(3, c.tables, view, src, prm, et, total, c.sm_count, s, &c.launches),
@@ -1109,7 +1123,8 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
                 std::vector<uint64_t> toff, ntk;
                 std::vector<uint8_t> st2;
                 std::vector<int64_t> topn;
-                std::vector<unsigned long long> run;
+                std::vector<unsigned long long> run, wk;
+                download(wk, et.work, P, s);
                 download(toff, et.toff, P, s);
                 download(ntk, et.ntask, P, s);
                 download(st2, et.state, P, s);
@@ -1123,12 +1138,12 @@ void run_exact(oserve_gpu_ctx &c, const SpaceTables &view, const KeyLayout &key,
                         a += nodes[q];
                         if (vis[q]) v += nodes[q];
                     }
-                    if (a > 1000000)
+                    if (a > 1000000 || wk[i] > 1000000)
                         std::fprintf(stderr, "[exact]   plan %llu state %d tasks %llu phase-A nodes %lld (visited %lld) "
-                                     "top %lld running %llu\n",
+                                     "top %lld running %llu, all rounds %llu\n",
                                      static_cast<unsigned long long>(i), st2[i], static_cast<unsigned long long>(ntk[i]),
                                      static_cast<long long>(a), static_cast<long long>(v), static_cast<long long>(topn[i]),
-                                     static_cast<unsigned long long>(run[i]));
+                                     static_cast<unsigned long long>(run[i]), wk[i]);
                 }
             }
             std::fprintf(stderr, "[exact] tasks %llu visited %lld, phase-A nodes sum (final tasks) %lld max %lld\n",

@@ -131,6 +131,8 @@ struct ExactTasks {
     int64_t *istar;       // task holding the first optimal leaf (pass 2)
     uint8_t *state;       // 0 not exact, 1 frontier, 2 sequential fallback, 3 frontier + phase-B counts,
                           // 4 abort proven by exact phase-A counts
+    unsigned long long *work;  // phase-A nodes run so far, all rounds (pass 0 adds to it)
+    int64_t work_limit;   // a plan past it leaves the frontier for the sequential fallback
     unsigned long long *running;  // phase-B running node total (top + finished task nodes)
     int32_t *bx;          // [plans][kMaxExactCells] first optimal leaf
     int64_t phase_cap;    // phase-A node cap of this round (tasks above it are split)
@@ -215,6 +217,8 @@ int launch_exact_task_pass(int pass, const ShapeTables &t, const SpaceTables &sp
 // Per-plan prefix maxima over the task list as segmented scans: which = 4
 // lower bounds (lb, and m of finished tasks), 6 exact incumbents (inc, opt,
 // istar; resets the replay's per-plan counters).  tmp: [total] int64.
+// Plans whose phase-A node total passed et.work_limit -> state 2 (sequential).
+int launch_exact_retire(const ExactTasks &et, uint64_t plans, int sm_count, void *stream, uint64_t *launches);
 int launch_exact_prefix(int which, const ExactTasks &et, uint64_t total, uint64_t plans, int64_t *tmp, void **temp,
                         size_t *temp_bytes, int sm_count, void *stream, uint64_t *launches);
 

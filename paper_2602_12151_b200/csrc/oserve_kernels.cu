@@ -25,6 +25,7 @@
 #include <tuple>
 #include <type_traits>
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 #include <mutex>
 
@@ -1959,6 +1960,32 @@ __global__ void __launch_bounds__(128) k_plan_exact(ShapeTables t, SpaceTables s
     }
 }
 
+// Thread per plan: the same sequential DFS on the flat decision table (one
+// thread runs a whole plan's search; the per-node latency of one thread is
+// far below a warp-cooperative node's).
+__global__ void __launch_bounds__(128) k_plan_exact_thr(ShapeTables t, SpaceTables sp, KeyLayout key, PlanSource src,
+                                                        PlanOutputs out, SolveParams prm) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < src.count;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        ExactState st;
+        int64_t part;
+        uint64_t local, gr;
+        const int64_t *lam_src;
+        if (!exact_setup(t, sp, src, prm, i, st, part, local, gr, lam_src)) continue;
+        int64_t best = -1, nodes = 0;
+        bool aborted;
+        exact_dfs<true>(t, st, 0, 0, 0, best, prm.node_budget, nodes, aborted, st.bx);
+        if (aborted) {
+            if (out.aborted) {
+                const unsigned slot2 = atomicAdd(out.aborted_n, 1u);
+                out.aborted[slot2] = gr;
+            }
+            continue;
+        }
+        exact_emit(t, key, out, i, st, st.bx, best, part, local);
+    }
+}
+
 // ---- frontier-parallel exact path -------------------------------------------
 // The sequential DFS's result is decided by two facts (flowassign.cpp:330-369):
 //  * the incumbent when a node is checked equals the best leaf among ALL
@@ -2280,7 +2307,11 @@ __global__ void __launch_bounds__(128) k_exact_task_thr(int pass, ShapeTables t,
         if (pass == 0) {
             int64_t best = et.lb[q];
             et.lbran[q] = best;
-            exact_dfs<false>(t, st, k, pos, count, best, et.phase_cap, nodes, capped, nullptr);
+            // the plan's phase-A nodes over all rounds are bounded: past
+            // work_limit its tasks stop and k_exact_retire hands the plan to
+            // the sequential fallback (trees far past the node budget)
+            exact_dfs<false>(t, st, k, pos, count, best, et.phase_cap, nodes, capped, nullptr, et.work + i,
+                             et.work_limit);
             et.m[q] = best;
             et.nodes[q] = nodes;
             et.capped[q] = capped ? 1 : 0;
@@ -2321,6 +2352,14 @@ __global__ void k_exact_lb_apply(ExactTasks et, uint64_t total) {
     for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
          q += static_cast<uint64_t>(gridDim.x) * blockDim.x)
         if (et.done[q] && et.m[q] < et.lb[q]) et.m[q] = et.lb[q];
+}
+
+// Plans whose phase-A nodes passed work_limit leave the frontier (state 2:
+// the sequential DFS, at most node_budget nodes, decides them).
+__global__ void k_exact_retire(ExactTasks et, uint64_t plans) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < plans;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        if (et.state[i] == 1 && et.work[i] > static_cast<unsigned long long>(et.work_limit)) et.state[i] = 2;
 }
 
 __global__ void k_exact_inc_reset(ExactTasks et, uint64_t plans) {
@@ -3113,12 +3152,20 @@ int launch_plan_exact(const ShapeTables &t, const SpaceTables &sp, const KeyLayo
     cudaGetLastError();
     if (int e = ensure_binom()) return e;
     if (src.count == 0) return 0;
-    const int block = 128;  // 4 warps, warp per plan
+    static const bool warp = [] {
+        const char *e = getenv("OSERVE_EXACT_SEQ");
+        return e && std::strcmp(e, "warp") == 0;
+    }();
+    const int block = 128;
     const uint64_t cap = static_cast<uint64_t>(sm_count) * 16;
-    uint64_t grid = (src.count * 32 + block - 1) / block;
+    uint64_t grid = ((warp ? src.count * 32 : src.count) + block - 1) / block;
     if (grid > cap) grid = cap;
-    k_plan_exact<<<static_cast<unsigned>(grid), block, 0, static_cast<cudaStream_t>(stream)>>>(t, sp, key, src, out,
-                                                                                               prm);
+    if (warp)  // 4 warps, warp per plan
+        k_plan_exact<<<static_cast<unsigned>(grid), block, 0, static_cast<cudaStream_t>(stream)>>>(t, sp, key, src,
+                                                                                                   out, prm);
+    else  // thread per plan
+        k_plan_exact_thr<<<static_cast<unsigned>(grid), block, 0, static_cast<cudaStream_t>(stream)>>>(t, sp, key, src,
+                                                                                                       out, prm);
     if (launches) ++*launches;
     return check(cudaGetLastError());
 }
@@ -3240,6 +3287,15 @@ int launch_exact_prefix(int which, const ExactTasks &et, uint64_t total, uint64_
         k_exact_istar<<<gt, 256, 0, s>>>(et, total);
     }
     if (launches) *launches += 4;
+    return check(cudaGetLastError());
+}
+
+int launch_exact_retire(const ExactTasks &et, uint64_t plans, int sm_count, void *stream, uint64_t *launches) {
+    cudaGetLastError();
+    if (plans == 0) return 0;
+    const unsigned gp = static_cast<unsigned>(std::min<uint64_t>((plans + 255) / 256, static_cast<uint64_t>(sm_count) * 8));
+    k_exact_retire<<<gp, 256, 0, static_cast<cudaStream_t>(stream)>>>(et, plans);
+    if (launches) ++*launches;
     return check(cudaGetLastError());
 }
 

@@ -128,3 +128,27 @@ def test_random_problem_switching(cuda, ref, seed):
             assert got.est_seconds == exp.est_seconds
             assert [(t.range.begin, t.range.end, t.src, t.dst) for t in got.transfers] == \
                 [(t.range.begin, t.range.end, t.src, t.dst) for t in exp.transfers]
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_problem_search(cuda, ref, seed):
+    """search::search (deploysearch.cpp:341-417) on random problems (D <= 32:
+    the reference's best_strategies walks ordered combos): final state and
+    the whole log (ops, acceptances, throughputs) equal the reference's."""
+    from pyoracle import Problem
+    s = 200 + seed
+    while True:
+        cl, model, types, lam, params, mode, sizes, plans = draw_case(ref, s)
+        if cl.device_count() <= 32:
+            break
+        s += 1000
+    pr = Problem(cl, model, types, lam, 60.0, params)
+    g = GpuContext(cl, model, params)
+    g.set_workload(types, lam, 60.0)
+    for sd in (seed, 7 * seed + 1):
+        st, log = g.search(seed=sd, max_iters=200)
+        es, elog = ref.search(pr, seed=sd, max_iters=200)
+        assert (st.throughput, st.iterations, st.stale_iters) == (es.throughput, es.iterations, es.stale_iters)
+        assert [(r.device_ids, r.tp, r.pp) for r in st.deployment.replicas] == \
+            [(r.device_ids, r.tp, r.pp) for r in es.deployment.replicas]
+        assert [list(r) for r in log] == [list(r) for r in elog]
