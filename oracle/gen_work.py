@@ -25,7 +25,7 @@ from pyoracle import Oracle, Problem  # noqa: E402
 
 
 CONFIGS = (("cfg1", None), ("cfg2", None), ("cfg2_low", None), ("cfg3_70b", 50000), ("cfg3_7b", 50000),
-           ("cfg5", 50000), ("cfg5_low", 20000), ("cfg5_full", 50000))
+           ("cfg5", 50000), ("cfg5_low", 20000), ("cfg5_full", 50000), ("cfg5_7b", 20000))
 
 
 def main(only=()):
