@@ -2488,26 +2488,40 @@ int oserve_gpu_search(oserve_gpu_ctx *ctx, const oserve_search_options *opts, os
             ++nlog;
         };
         auto candidate = std::make_unique<oserve_round_result>();
+        // best_strategies is a pure function of the ordered sizes for this
+        // context and workload, and the search revisits the same mutations
+        // again and again while the current deployment stands (the reference
+        // recomputes them): results are memoised per sizes vector, and the
+        // current deployment's classification is redone only when it changes.
+        std::map<std::vector<int>, std::unique_ptr<oserve_round_result>> memo;
+        bool classified = false;
+        std::vector<int> over, under, cur_sizes, cur_pps;
         while (iter < opts->max_iters && stale < opts->stale_limit) {
             ++iter;
             // capacity table + assignment of the current deployment (GPU), classify
             const oserve_plan &cp = current->plan;
             const int R = cp.num_replicas, J = ctx->J;
-            oserve_deployment dd{R, cp.replica_num_devices, cp.device_ids, cp.tp, cp.pp};
-            std::vector<int64_t> M(R), unit(static_cast<size_t>(R) * J), used(R);
-            check_status(oserve_gpu_plan_detail(ctx, &dd, nullptr, nullptr, nullptr, nullptr, M.data(), unit.data(),
-                                                used.data(), nullptr),
-                         ctx);
-            std::vector<int> over, under, cur_sizes, cur_pps;
-            for (int k = 0; k < R; ++k) {
-                int64_t min_unit = std::numeric_limits<int64_t>::max();
-                for (int j = 0; j < J; ++j)
-                    if (unit[k * J + j] > 0) min_unit = std::min(min_unit, unit[k * J + j]);
-                const bool saturated =
-                    min_unit != std::numeric_limits<int64_t>::max() && M[k] - used[k] < min_unit;
-                (saturated ? over : under).push_back(k);
-                cur_sizes.push_back(cp.replica_num_devices[k]);
-                cur_pps.push_back(cp.pp[k]);
+            if (!classified) {
+                oserve_deployment dd{R, cp.replica_num_devices, cp.device_ids, cp.tp, cp.pp};
+                std::vector<int64_t> M(R), unit(static_cast<size_t>(R) * J), used(R);
+                check_status(oserve_gpu_plan_detail(ctx, &dd, nullptr, nullptr, nullptr, nullptr, M.data(), unit.data(),
+                                                    used.data(), nullptr),
+                             ctx);
+                over.clear();
+                under.clear();
+                cur_sizes.clear();
+                cur_pps.clear();
+                for (int k = 0; k < R; ++k) {
+                    int64_t min_unit = std::numeric_limits<int64_t>::max();
+                    for (int j = 0; j < J; ++j)
+                        if (unit[k * J + j] > 0) min_unit = std::min(min_unit, unit[k * J + j]);
+                    const bool saturated =
+                        min_unit != std::numeric_limits<int64_t>::max() && M[k] - used[k] < min_unit;
+                    (saturated ? over : under).push_back(k);
+                    cur_sizes.push_back(cp.replica_num_devices[k]);
+                    cur_pps.push_back(cp.pp[k]);
+                }
+                classified = true;
             }
             Mutation mut;
             bool found = false;
@@ -2523,12 +2537,19 @@ int oserve_gpu_search(oserve_gpu_ctx *ctx, const oserve_search_options *opts, os
                 emit("stale(no-mutation)", false);
                 continue;
             }
-            check_status(oserve_gpu_best_strategies(ctx, static_cast<int>(mut.sizes.size()), mut.sizes.data(),
-                                                    candidate.get()),
-                         ctx);
+            auto hit = memo.find(mut.sizes);
+            if (hit != memo.end()) {
+                *candidate = *hit->second;
+            } else {
+                check_status(oserve_gpu_best_strategies(ctx, static_cast<int>(mut.sizes.size()), mut.sizes.data(),
+                                                        candidate.get()),
+                             ctx);
+                memo.emplace(mut.sizes, std::make_unique<oserve_round_result>(*candidate));
+            }
             const bool accepted = candidate->plan.num_replicas > 0 && candidate->objective > current->objective;
             if (accepted) {
                 std::swap(current, candidate);
+                classified = false;
                 stale = 0;
             } else {
                 ++stale;
