@@ -1960,13 +1960,14 @@ __global__ void __launch_bounds__(128) k_plan_exact(ShapeTables t, SpaceTables s
     }
 }
 
-// Thread per plan: the same sequential DFS on the flat decision table (one
-// thread runs a whole plan's search; the per-node latency of one thread is
-// far below a warp-cooperative node's).
-__global__ void __launch_bounds__(128) k_plan_exact_thr(ShapeTables t, SpaceTables sp, KeyLayout key, PlanSource src,
-                                                        PlanOutputs out, SolveParams prm) {
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < src.count;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+// One thread per plan, alone in its warp (one warp per CTA, so plans spread
+// over the SMs): the same sequential DFS on the flat decision table.  The
+// per-node latency of one thread is far below a warp-cooperative node's, and
+// plans sharing a warp would serialise on their diverging searches.
+__global__ void __launch_bounds__(32) k_plan_exact_thr(ShapeTables t, SpaceTables sp, KeyLayout key, PlanSource src,
+                                                       PlanOutputs out, SolveParams prm) {
+    if (threadIdx.x != 0) return;
+    for (uint64_t i = blockIdx.x; i < src.count; i += gridDim.x) {
         ExactState st;
         int64_t part;
         uint64_t local, gr;
@@ -3156,14 +3157,14 @@ int launch_plan_exact(const ShapeTables &t, const SpaceTables &sp, const KeyLayo
         const char *e = getenv("OSERVE_EXACT_SEQ");
         return e && std::strcmp(e, "warp") == 0;
     }();
-    const int block = 128;
-    const uint64_t cap = static_cast<uint64_t>(sm_count) * 16;
-    uint64_t grid = ((warp ? src.count * 32 : src.count) + block - 1) / block;
+    const int block = warp ? 128 : 32;
+    const uint64_t cap = static_cast<uint64_t>(sm_count) * (warp ? 16 : 64);
+    uint64_t grid = warp ? (src.count * 32 + block - 1) / block : src.count;
     if (grid > cap) grid = cap;
     if (warp)  // 4 warps, warp per plan
         k_plan_exact<<<static_cast<unsigned>(grid), block, 0, static_cast<cudaStream_t>(stream)>>>(t, sp, key, src,
                                                                                                    out, prm);
-    else  // thread per plan
+    else  // a thread (a warp) per plan
         k_plan_exact_thr<<<static_cast<unsigned>(grid), block, 0, static_cast<cudaStream_t>(stream)>>>(t, sp, key, src,
                                                                                                        out, prm);
     if (launches) ++*launches;
